@@ -1,0 +1,398 @@
+// clip.cu — clip factors and clipped sums (north-star subsystems 2-3).
+//
+//   clip_factors : clip_and_sum pass 1 tail + factors (optimizer.hpp:67-98)
+//   clipped sums : clip_and_sum pass 2 (optimizer.hpp:99-114) formed as (scale ⊙ B)^T A from the
+//                  activations and highway gradients — the materialised per-sample gradients are
+//                  not read again. Split-K over samples with a fixed-order reduction, so results
+//                  are deterministic and identical on every replay.
+//   materialised : the reference's own pass 2 over a stored record, in its exact order.
+#include "conv_common.cuh"
+#include "igemm.cuh"
+
+namespace dpg {
+
+// ------------------------------------------------------------------------------------------
+// Clip factors. slab [rows, b]: per-(parameter tile, sample) squared norms; row_param[r] is the
+// parameter index owning row r (rows are in parameter order). Sum rows in order, flag the first
+// non-finite parameter per sample (NumericError, optimizer.hpp:77-83), then
+// norm = sqrt(sq), scale = (float)(C / max(norm, C)), count norm > C.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) clip_factors_kernel(const double* __restrict__ slab,
+                                                           const int32_t* __restrict__ row_param,
+                                                           int rows, int64_t b, double c,
+                                                           double* __restrict__ norms,
+                                                           float* __restrict__ scale,
+                                                           unsigned long long* num_clipped,
+                                                           DeviceErr* err) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int clipped = 0;
+  if (n < b) {
+    double sq = 0.0;
+    int bad = -1;
+    for (int r = 0; r < rows; ++r) {
+      const double v = slab[(int64_t)r * b + n];
+      if (bad < 0 && !isfinite(v)) bad = row_param ? row_param[r] : 0;
+      sq += v;
+    }
+    if (bad >= 0) report_error(err, err_key(ERR_STAGE_NONFINITE, (uint64_t)bad, (uint64_t)n), 0);
+    const double norm = sqrt(sq);
+    const double s = c / (norm < c ? c : norm);  // C / std::max(norm, C)
+    if (norms) norms[n] = norm;
+    scale[n] = (float)s;
+    clipped = norm > c ? 1 : 0;
+  }
+  const int cnt = __syncthreads_count(clipped);
+  if (threadIdx.x == 0 && num_clipped && cnt) atomicAdd(num_clipped, (unsigned long long)cnt);
+}
+
+void launch_clip_factors(dpg_ctx* ctx, const double* slab, const int32_t* row_param, int rows,
+                         int64_t b, double c, double* norms, float* scale, int64_t* num_clipped) {
+  if (num_clipped) DPG_CUDA(cudaMemsetAsync(num_clipped, 0, sizeof(int64_t), ctx->stream));
+  if (b == 0) return;
+  clip_factors_kernel<<<(unsigned)((b + 255) / 256), 256, 0, ctx->stream>>>(
+      slab, row_param, rows, b, c, norms, scale, reinterpret_cast<unsigned long long*>(num_clipped),
+      ctx->dev_err);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// ------------------------------------------------------------------------------------------
+// Split-K reduction: out = [out +] sum_z part[z] (z ascending) — the fold of
+// optimizer.hpp:245-250 when accumulating over virtual steps.
+// ------------------------------------------------------------------------------------------
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int64_t n,
+                                     float* __restrict__ out, int accumulate) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float acc = 0.f;
+  for (int z = 0; z < splits; ++z) acc = __fadd_rn(acc, part[(int64_t)z * n + i]);
+  out[i] = accumulate ? __fadd_rn(out[i], acc) : acc;
+}
+
+static void launch_splitk_reduce(dpg_ctx* ctx, const float* part, int splits, int64_t n, float* out,
+                                 int accumulate) {
+  splitk_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(part, splits, n, out, accumulate);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+struct SplitKStore {
+  float* part;
+  int64_t M, N;
+  template <int TM, int TN>
+  __device__ void store(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+        if (m < M && n < N) part[((int64_t)z * M + m) * N + n] = acc[i][j];
+      }
+  }
+};
+
+// Choose samples per split so that tiles x splits fills the GPU about twice.
+static int pick_splits(int64_t b, int64_t tiles, int64_t per_sample_k) {
+  int64_t want = (2 * kNumSMs + tiles - 1) / tiles;
+  if (want > b) want = b;
+  // keep at least ~64 k-steps per split
+  const int64_t max_by_k = (b * per_sample_k) / 64;
+  if (want > max_by_k) want = max_by_k;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+
+// ------------------------------------------------------------------------------------------
+// Linear weight, mid == 1: S[o, i] = sum_n scale_n * (B[n,o] * A[n,i]) — the reference's
+// association (acc += w * g with g = b * a rounded, optimizer.hpp:107-110), so bit-exact.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) clipped_sum_linear_outer_kernel(
+    const float* __restrict__ acts, int acts_relu, const float* __restrict__ hw,
+    const float* __restrict__ scale, int64_t b, int64_t d, int64_t r, float* __restrict__ sw,
+    int accumulate) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= r * d) return;
+  const int64_t o = e / d, i = e - o * d;
+  float acc = 0.f;
+  for (int64_t n = 0; n < b; ++n) {
+    const float g = __fmul_rn(__ldg(hw + n * r + o), relu_if(__ldg(acts + n * d + i), acts_relu));
+    acc = __fadd_rn(acc, __fmul_rn(__ldg(scale + n), g));
+  }
+  sw[e] = accumulate ? __fadd_rn(sw[e], acc) : acc;
+}
+
+// Linear weight, mid > 1: split-K GEMM over (n, t).
+struct CsLinearProb : SplitKStore {
+  static constexpr bool kAMajorM = true;
+  static constexpr bool kBMajorN = true;
+  static constexpr bool kExact = false;
+  const float* acts;
+  const float* hw;
+  const float* scale;
+  int acts_relu;
+  int64_t K;        // per split: spl * mid
+  int64_t spl, mid, bsz;
+  __device__ float init(int, int64_t, int64_t) const { return 0.f; }
+  __device__ float a(int z, int64_t m, int64_t k) const {
+    const int64_t n = z * spl + k / mid, t = k - (k / mid) * mid;
+    if (n >= bsz) return 0.f;
+    return __ldg(scale + n) * __ldg(hw + (n * mid + t) * M + m);
+  }
+  __device__ float b(int z, int64_t k, int64_t col) const {
+    const int64_t n = z * spl + k / mid, t = k - (k / mid) * mid;
+    if (n >= bsz) return 0.f;
+    return relu_if(__ldg(acts + (n * mid + t) * N + col), acts_relu);
+  }
+  template <int TM, int TN>
+  __device__ void epilogue(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
+    store<TM, TN>(z, m0, n0, tx, ty, acc);
+  }
+};
+
+size_t clipped_sum_ws_linear(int64_t b, int64_t mid, int64_t d, int64_t r) {
+  if (mid == 1) return 0;
+  const int64_t tiles = ((r + 63) / 64) * ((d + 63) / 64);
+  const int splits = pick_splits(b, tiles, mid);
+  return sizeof(float) * (size_t)splits * (size_t)(r * d);
+}
+
+void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw,
+                               const float* scale, int64_t b, int64_t mid, int64_t d, int64_t r,
+                               float* sw, float* sb, int accumulate, void* ws) {
+  (void)sb;  // the bias sum is formed from the per-sample bias record (launch_weighted_sum_...)
+  if (mid == 1) {
+    const int64_t n = r * d;
+    clipped_sum_linear_outer_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+        acts, acts_relu, hw, scale, b, d, r, sw, accumulate);
+    DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
+  const int64_t tiles = ((r + 63) / 64) * ((d + 63) / 64);
+  const int splits = pick_splits(b, tiles, mid);
+  const int64_t spl = (b + splits - 1) / splits;
+  CsLinearProb p;
+  p.part = static_cast<float*>(ws);
+  p.M = r;
+  p.N = d;
+  p.acts = acts;
+  p.hw = hw;
+  p.scale = scale;
+  p.acts_relu = acts_relu;
+  p.K = spl * mid;
+  p.spl = spl;
+  p.mid = mid;
+  p.bsz = b;
+  launch_igemm<64, 64, 16>(ctx, p, splits);
+  launch_splitk_reduce(ctx, p.part, splits, r * d, sw, accumulate);
+}
+
+// ------------------------------------------------------------------------------------------
+// Conv weight: S[oc, k] = sum_{n, p} (scale_n * B[n, oc, p]) * X~[n, k, p] — the conv weight
+// gradient of the clip-scaled highway; split-K over samples.
+// ------------------------------------------------------------------------------------------
+struct CsConvProb : SplitKStore {
+  static constexpr bool kAMajorM = false;
+  static constexpr bool kBMajorN = false;
+  static constexpr bool kExact = false;
+  Im2col xc;
+  const float* hw;
+  const float* scale;
+  int64_t K, spl, P, bsz;
+  __device__ float init(int, int64_t, int64_t) const { return 0.f; }
+  __device__ float a(int z, int64_t m, int64_t k) const {
+    const int64_t q = k / P;
+    const int64_t n = z * spl + q, p = k - q * P;
+    if (n >= bsz) return 0.f;
+    return __ldg(scale + n) * __ldg(hw + (n * M + m) * P + p);
+  }
+  __device__ float b(int z, int64_t k, int64_t col) const {
+    const int64_t q = k / P;
+    const int64_t n = z * spl + q, p = k - q * P;
+    if (n >= bsz) return 0.f;
+    return xc(n, (int)col, (int)p);
+  }
+  template <int TM, int TN>
+  __device__ void epilogue(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
+    store<TM, TN>(z, m0, n0, tx, ty, acc);
+  }
+};
+
+static void cs_conv_tiles(const ConvGeom& g, int& bm, int& bn) {
+  bm = g.oc <= 32 ? 32 : 64;
+  bn = g.K() <= 32 ? 32 : 64;
+}
+
+size_t clipped_sum_ws_conv2d(const ConvGeom& g) {
+  int bm, bn;
+  cs_conv_tiles(g, bm, bn);
+  const int64_t tiles = ((g.oc + bm - 1) / bm) * ((g.K() + bn - 1) / bn);
+  const int splits = pick_splits(g.b, tiles, g.P());
+  return sizeof(float) * (size_t)splits * (size_t)(g.oc * g.K());
+}
+
+void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
+                               const float* scale, const ConvGeom& g, float* sw, float* sb,
+                               int accumulate, void* ws) {
+  (void)sb;
+  int bm, bn;
+  cs_conv_tiles(g, bm, bn);
+  const int64_t tiles = ((g.oc + bm - 1) / bm) * ((g.K() + bn - 1) / bn);
+  const int splits = pick_splits(g.b, tiles, g.P());
+  const int64_t spl = (g.b + splits - 1) / splits;
+  CsConvProb p;
+  p.part = static_cast<float*>(ws);
+  p.M = g.oc;
+  p.N = g.K();
+  p.xc = make_im2col(x, x_relu, g);
+  p.hw = hw;
+  p.scale = scale;
+  p.K = spl * g.P();
+  p.spl = spl;
+  p.P = g.P();
+  p.bsz = g.b;
+  if (bm == 32 && bn == 32) launch_igemm<32, 32, 16>(ctx, p, splits);
+  else if (bm == 32) launch_igemm<32, 64, 16>(ctx, p, splits);
+  else if (bn == 32) launch_igemm<64, 32, 16>(ctx, p, splits);
+  else launch_igemm<64, 64, 16>(ctx, p, splits);
+  launch_splitk_reduce(ctx, p.part, splits, g.oc * g.K(), sw, accumulate);
+}
+
+// ------------------------------------------------------------------------------------------
+// Embedding: summed[v, :] = sum_n scale_n * G_n[v, :], G_n[v] = sum over sample n's duplicates
+// of v in ascending s — exactly the reference's order (grad_sample.hpp:74-80 then
+// optimizer.hpp:107-110), so bit-exact. Stage 1 builds start[n][c] = first sorted position of
+// sample n in vocab chunk c; stage 2 gives each CTA one chunk of kCsRows rows, warps own rows,
+// samples are visited in ascending order.
+// ------------------------------------------------------------------------------------------
+constexpr int kCsRows = 32;
+
+__global__ void embed_chunk_starts_kernel(const int32_t* __restrict__ sorted_v, int64_t t,
+                                          int nchunks, int32_t* __restrict__ starts) {
+  const int64_t n = blockIdx.x;
+  const int32_t* sv = sorted_v + n * t;
+  for (int c = threadIdx.x; c <= nchunks; c += blockDim.x) {
+    const int32_t v = (int32_t)((int64_t)c * kCsRows);
+    int lo = 0, hi = (int)t;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sv[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    starts[n * (nchunks + 1) + c] = lo;
+  }
+}
+
+__global__ void __launch_bounds__(256) clipped_sum_embedding_kernel(
+    const int32_t* __restrict__ sorted_v, const int32_t* __restrict__ sorted_s,
+    const int32_t* __restrict__ starts, const float* __restrict__ hw,
+    const float* __restrict__ scale, int64_t b, int64_t t, int64_t vocab, int64_t dim,
+    int nchunks, float* __restrict__ summed, int accumulate) {
+  extern __shared__ float acc[];  // [kCsRows][dim]
+  const int c = blockIdx.x;
+  const int64_t v0 = (int64_t)c * kCsRows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t i = threadIdx.x; i < kCsRows * dim; i += 256) acc[i] = 0.f;
+  __syncthreads();
+  for (int64_t n = 0; n < b; ++n) {
+    const int j0 = starts[n * (nchunks + 1) + c], j1 = starts[n * (nchunks + 1) + c + 1];
+    if (j0 == j1) continue;
+    const float w = __ldg(scale + n);
+    const int32_t* sv = sorted_v + n * t;
+    const int32_t* ss = sorted_s + n * t;
+    const float* hwn = hw + n * t * dim;
+    for (int j = j0; j < j1;) {
+      const int32_t v = sv[j];
+      int e = j + 1;
+      while (e < j1 && sv[e] == v) ++e;
+      if (((v - v0) & 7) == warp) {
+        float* arow = acc + (v - v0) * dim;
+        for (int64_t d0 = lane; d0 < dim; d0 += 32) {
+          float g = 0.f;
+          for (int q = j; q < e; ++q) g = __fadd_rn(g, __ldg(hwn + (int64_t)ss[q] * dim + d0));
+          arow[d0] = __fadd_rn(arow[d0], __fmul_rn(w, g));
+        }
+      }
+      j = e;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < kCsRows * dim; i += 256) {
+    const int64_t v = v0 + i / dim;
+    if (v >= vocab) break;
+    float* o = summed + v0 * dim + i;
+    *o = accumulate ? __fadd_rn(*o, acc[i]) : acc[i];
+  }
+}
+
+size_t clipped_sum_ws_embedding(int64_t b, int64_t vocab) {
+  const int64_t nchunks = (vocab + kCsRows - 1) / kCsRows;
+  return sizeof(int32_t) * (size_t)(b * (nchunks + 1));
+}
+
+void launch_clipped_sum_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* sorted_s,
+                                  const float* hw, const float* scale, int64_t b, int64_t t,
+                                  int64_t vocab, int64_t dim, float* summed, int accumulate,
+                                  void* ws) {
+  const int nchunks = (int)((vocab + kCsRows - 1) / kCsRows);
+  int32_t* starts = static_cast<int32_t*>(ws);
+  if (b > 0) {
+    embed_chunk_starts_kernel<<<(unsigned)b, 256, 0, ctx->stream>>>(sorted_v, t, nchunks, starts);
+    DPG_LAUNCH_CHECK(ctx);
+  }
+  const size_t smem = sizeof(float) * kCsRows * (size_t)dim;
+  if (smem > 48 * 1024)
+    DPG_CUDA(cudaFuncSetAttribute(clipped_sum_embedding_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  clipped_sum_embedding_kernel<<<(unsigned)nchunks, 256, smem, ctx->stream>>>(
+      sorted_v, sorted_s, starts, hw, scale, b, t, vocab, dim, nchunks, summed, accumulate);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// ------------------------------------------------------------------------------------------
+// Materialised record (reference pass 1 and pass 2 over stored per-sample gradients).
+// ------------------------------------------------------------------------------------------
+constexpr int64_t kSqChunk = 16384;
+
+__global__ void __launch_bounds__(256) sq_materialised_kernel(const float* __restrict__ g,
+                                                              int64_t b, int64_t numel,
+                                                              double* __restrict__ sq_part) {
+  const int64_t n = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * kSqChunk;
+  const int64_t c1 = c0 + kSqChunk < numel ? c0 + kSqChunk : numel;
+  const float* row = g + n * numel;
+  double sq = 0.0;
+  for (int64_t j = c0 + threadIdx.x; j < c1; j += 256) {
+    const double v = (double)__ldg(row + j);
+    sq += v * v;
+  }
+  __shared__ double red[8];
+  const double t = block_sum<256>(sq, red);
+  if (threadIdx.x == 0) sq_part[(int64_t)blockIdx.x * b + n] = t;
+}
+
+int sq_rows_materialised(int64_t numel) { return (int)((numel + kSqChunk - 1) / kSqChunk); }
+
+void launch_sq_materialised(dpg_ctx* ctx, const float* g, int64_t b, int64_t numel,
+                            double* sq_part) {
+  if (b == 0) return;
+  dim3 grid((unsigned)sq_rows_materialised(numel), (unsigned)b);
+  sq_materialised_kernel<<<grid, 256, 0, ctx->stream>>>(g, b, numel, sq_part);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// summed[j] = [summed[j] +] sum_n (float)scale_n * g[n, j], n ascending (optimizer.hpp:106-111)
+__global__ void weighted_sum_kernel(const float* __restrict__ g, const float* __restrict__ scale,
+                                    int64_t b, int64_t numel, float* __restrict__ summed,
+                                    int accumulate) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= numel) return;
+  float acc = 0.f;
+  for (int64_t n = 0; n < b; ++n) acc = __fadd_rn(acc, __fmul_rn(__ldg(scale + n), __ldg(g + n * numel + j)));
+  summed[j] = accumulate ? __fadd_rn(summed[j], acc) : acc;
+}
+
+void launch_weighted_sum_materialised(dpg_ctx* ctx, const float* g, const float* scale, int64_t b,
+                                      int64_t numel, float* summed, int accumulate) {
+  if (numel == 0) return;
+  weighted_sum_kernel<<<(unsigned)((numel + 255) / 256), 256, 0, ctx->stream>>>(g, scale, b, numel, summed, accumulate);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace dpg

@@ -1,0 +1,62 @@
+// dpg_device.cuh — device-side helpers shared by the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dpg_internal.h"
+
+namespace dpg {
+
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
+__device__ __forceinline__ float relu_if(float v, int relu) { return (relu && !(v > 0.f)) ? 0.f : v; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed tree): every thread passes its value, thread 0 gets the total.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* smem /* >= NT/32 */) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = lane < NT / 32 ? smem[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ void report_error(DeviceErr* err, uint64_t key, uint64_t aux) {
+  const unsigned long long old = atomicMin(&err->key, (unsigned long long)key);
+  if (key < old) atomicExch(&err->aux, (unsigned long long)aux);
+}
+
+__device__ __forceinline__ bool error_pending(const DeviceErr* err) {
+  return *(volatile const unsigned long long*)&err->key != ERR_NONE;
+}
+
+// streaming store for write-once outputs (per-sample gradients)
+__device__ __forceinline__ void st_stream4(float* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_stream(float* p, float v) {
+  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+}  // namespace dpg

@@ -1,0 +1,222 @@
+// dpg_internal.h — context, error plumbing and kernel launcher declarations shared by the
+// libdpg.so translation units. Not part of the ABI (include/dpg.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dpg.h"
+
+namespace dpg {
+
+// C++ side of the error contract: thrown inside libdpg, caught at the ABI boundary and turned
+// into a dpg_status (the reference's exception classes, errors.hpp:12-72).
+struct Error : std::runtime_error {
+  dpg_status code;
+  Error(dpg_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void raise(dpg_status c, const std::string& m) { throw Error(c, m); }
+
+#define DPG_CUDA(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      ::dpg::raise(DPG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+#define DPG_NCCL(expr)                                                                  \
+  do {                                                                                  \
+    ncclResult_t r_ = (expr);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      ::dpg::raise(DPG_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_));   \
+  } while (0)
+
+// Device-side error record. Kernels that detect a reference error (non-finite per-sample
+// gradient, out-of-range index / target) atomicMin a 64-bit key so the FIRST offender in the
+// reference's execution order wins: stage (forward < loss < clip), then parameter / layer,
+// then sample.
+enum ErrStage : uint64_t {
+  ERR_STAGE_EMBED_INDEX = 1,  // layers.hpp:425-426 (forward gather)
+  ERR_STAGE_TARGET = 2,       // layers.hpp:905
+  ERR_STAGE_NONFINITE = 3,    // optimizer.hpp:77-83
+};
+__host__ __device__ inline uint64_t err_key(uint64_t stage, uint64_t major, uint64_t sample) {
+  return (stage << 56) | ((major & 0xFFFFFFull) << 32) | (sample & 0xFFFFFFFFull);
+}
+constexpr uint64_t ERR_NONE = ~0ull;
+
+struct DeviceErr {
+  unsigned long long key;  // ERR_NONE when clear
+  unsigned long long aux;  // stage-specific detail (e.g. the raw index bits)
+};
+
+}  // namespace dpg
+
+struct dpg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int64_t launches = 0;
+  dpg::DeviceErr* dev_err = nullptr;  // device
+  dpg::DeviceErr* host_err = nullptr; // pinned mirror
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  bool capturing = false;
+
+  // scratch space for operator-ABI calls (grows outside capture only)
+  void* workspace(size_t bytes);
+
+  // stage profiling (eager launches only): CUDA events on this stream around each stage,
+  // with the stage's algorithmic bytes / flops
+  struct ProfRec {
+    std::string name;
+    double bytes, flops;
+    cudaEvent_t a, b;
+  };
+  struct ProfAgg {
+    double ms = 0, bytes = 0, flops = 0;
+    int64_t count = 0;
+  };
+  bool profiling = false;
+  std::vector<ProfRec> prof_pending;
+  std::map<std::string, ProfAgg> prof_agg;
+  std::vector<cudaEvent_t> event_pool;
+  std::string prof_text;
+};
+
+namespace dpg {
+
+// Error-surfacing helpers (ctx.cpp). Reads the device error record (synchronising the stream),
+// clears it, and throws the matching dpg::Error; `names` maps (stage, major) to a description of
+// the offending layer / parameter in the reference's wording.
+using ErrNamer = std::string (*)(const void* user, uint64_t stage, uint64_t major);
+void throw_device_error(dpg_ctx* ctx, ErrNamer names, const void* user);
+void sync_ctx(dpg_ctx* ctx);
+
+inline void count_launch(dpg_ctx* ctx) { ++ctx->launches; }
+
+// RAII stage timer: records an event pair on ctx->stream when profiling is on (never inside a
+// graph capture). Kernel durations are read back by dpg_ctx_profile_read.
+struct ProfScope {
+  dpg_ctx* ctx;
+  bool on;
+  dpg_ctx::ProfRec rec;
+  ProfScope(dpg_ctx* c, std::string name, double bytes, double flops);
+  ~ProfScope();
+};
+
+std::string& thread_err();
+
+// Run f, converting dpg::Error (and any other exception) into a status + message: no
+// exception crosses the C ABI.
+template <typename F>
+dpg_status guard(dpg_ctx* ctx, F&& f) {
+  try {
+    f();
+    return DPG_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->err = e.what();
+    thread_err() = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    thread_err() = e.what();
+    return DPG_ERR_INTERNAL;
+  }
+}
+
+#define DPG_LAUNCH_CHECK(ctx)                                                            \
+  do {                                                                                   \
+    ::dpg::count_launch(ctx);                                                            \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess)                                                               \
+      ::dpg::raise(DPG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------
+// Kernel launchers (implemented in the .cu files). All asynchronous on ctx->stream.
+// Norm partials: `sq_part` is a [rows, b] double slab; a launcher writes `sq_rows(...)`
+// consecutive rows starting at sq_part (row-major, stride b).
+// ---------------------------------------------------------------------------------------
+
+struct ConvGeom {
+  int64_t b, ic, h, w, oc, kh, kw, stride, pad, oh, ow;
+  int64_t K() const { return ic * kh * kw; }
+  int64_t P() const { return oh * ow; }
+};
+
+// rules.cu — per-sample gradients
+int sq_rows_linear(int64_t mid, int64_t d, int64_t r);
+int sq_rows_conv2d(const ConvGeom& g);
+int sq_rows_embedding(int64_t vocab, int64_t dim);
+void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw, int64_t b,
+                      int64_t mid, int64_t d, int64_t r, float* gw, double* sq_part);
+void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& g,
+                      float* gw, double* sq_part);
+// bias rule: gb[n,o] = sum over middle of hw; `hw_layout_conv` selects [b, o, P] vs [b, mid, o]
+void launch_gs_bias(dpg_ctx* ctx, const float* hw, int64_t b, int64_t mid, int64_t r,
+                    bool hw_layout_conv, float* gb, double* sq_part);
+// embedding: sort each sample's ids (validating them), then dense G and/or norms
+void launch_embed_sort(dpg_ctx* ctx, const float* idx, int64_t b, int64_t t, int64_t vocab,
+                       int32_t* sorted_v, int32_t* sorted_s);
+void launch_gs_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* sorted_s,
+                         const float* hw, int64_t b, int64_t t, int64_t vocab, int64_t dim,
+                         float* g, double* sq_part);
+// sum `rows` rows of a [rows, b] slab into out[b] (operator-ABI per-parameter norms)
+void launch_sq_reduce(dpg_ctx* ctx, const double* part, int rows, int64_t b, double* out);
+
+// clip.cu
+void launch_clip_factors(dpg_ctx* ctx, const double* slab, const int32_t* row_param, int rows,
+                         int64_t b, double c, double* norms, float* scale, int64_t* num_clipped);
+size_t clipped_sum_ws_linear(int64_t b, int64_t mid, int64_t d, int64_t r);
+size_t clipped_sum_ws_conv2d(const ConvGeom& g);
+void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw,
+                               const float* scale, int64_t b, int64_t mid, int64_t d, int64_t r,
+                               float* sw, float* sb, int accumulate, void* ws);
+void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
+                               const float* scale, const ConvGeom& g, float* sw, float* sb,
+                               int accumulate, void* ws);
+size_t clipped_sum_ws_embedding(int64_t b, int64_t vocab);
+void launch_clipped_sum_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* sorted_s,
+                                  const float* hw, const float* scale, int64_t b, int64_t t,
+                                  int64_t vocab, int64_t dim, float* summed, int accumulate,
+                                  void* ws);
+void launch_sq_materialised(dpg_ctx* ctx, const float* g, int64_t b, int64_t numel,
+                            double* sq_part);
+int sq_rows_materialised(int64_t numel);
+void launch_weighted_sum_materialised(dpg_ctx* ctx, const float* g, const float* scale, int64_t b,
+                                      int64_t numel, float* summed, int accumulate);
+
+// noise.cu
+void launch_noise_update(dpg_ctx* ctx, float* params, const float* summed, float* grad, int64_t n,
+                         double sigma, double c, double expected_batch, double lr, uint64_t seed,
+                         uint64_t step, const float* injected, const uint64_t* step_ptr);
+void launch_gaussian(dpg_ctx* ctx, float* out, int64_t n, double std_dev, uint64_t seed,
+                     uint64_t step);
+
+// layers.cu — supporting forward / backward
+void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
+                       const ConvGeom& g, float* y);
+void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
+                         const float* mask_src, float* dx);
+void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
+                       int64_t rows, int64_t d, int64_t r, float* y);
+void launch_linear_dgrad(dpg_ctx* ctx, const float* dy, const float* w, int64_t rows, int64_t d,
+                         int64_t r, const float* mask_src, float* dx);
+void launch_embedding_fwd(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* sorted_s,
+                          const float* table, int64_t b, int64_t t, int64_t dim, float* out);
+void launch_softmax_ce(dpg_ctx* ctx, const float* logits, int logits_relu, const float* targets,
+                       int64_t b, int64_t k, float* loss, float* grad);
+void launch_relu_mask(dpg_ctx* ctx, float* g, const float* mask_src, int64_t n);
+
+}  // namespace dpg

@@ -1,0 +1,336 @@
+// layers.cu — supporting forward / input-backward kernels for the full step on the device
+// (SURVEY.md §8a rows a12-a14): conv2d forward (implicit GEMM) and dgrad, linear forward and
+// dgrad, embedding gather, softmax cross-entropy. ReLU layers are folded into their consumers:
+// activations are stored pre-ReLU and the ReLU is applied on load (forward) or as a mask in
+// the producing dgrad epilogue (backward, layers.hpp:712-718).
+#include "conv_common.cuh"
+#include "igemm.cuh"
+
+namespace dpg {
+
+// ------------------------------------------------------------------------------------------
+// conv2d forward (layers.hpp:432-467): Y[n, oc, p] = bias[oc] + sum_k W[oc, k] X~[n, k, p];
+// GEMM M = oc, N = b*P, K = ic*kh*kw; the accumulator starts from the bias as the reference's
+// does (layers.hpp:458).
+// ------------------------------------------------------------------------------------------
+struct ConvFwdProb {
+  static constexpr bool kAMajorM = false;  // W[oc, k] contiguous in k
+  static constexpr bool kBMajorN = true;   // consecutive n -> consecutive output positions
+  static constexpr bool kExact = false;
+  Im2col xc;
+  const float* w;
+  const float* bias;
+  float* y;
+  int64_t M, N, K, P;
+  __device__ float init(int, int64_t m, int64_t) const { return (bias && m < M) ? __ldg(bias + m) : 0.f; }
+  __device__ float a(int, int64_t m, int64_t k) const { return __ldg(w + m * K + k); }
+  __device__ float b(int, int64_t k, int64_t nn) const {
+    const int64_t n = nn / P, p = nn - n * P;
+    return xc(n, (int)k, (int)p);
+  }
+  template <int TM, int TN>
+  __device__ void epilogue(int, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t m = m0 + ty + 16 * i, nn = n0 + tx + 16 * j;
+        if (m < M && nn < N) {
+          const int64_t n = nn / P, p = nn - n * P;
+          y[(n * M + m) * P + p] = acc[i][j];
+        }
+      }
+  }
+};
+
+void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
+                       const ConvGeom& g, float* y) {
+  if (g.b == 0) return;
+  ConvFwdProb p{make_im2col(x, x_relu, g), w, bias, y, g.oc, g.b * g.P(), g.K(), g.P()};
+  if (g.oc <= 32) launch_igemm<32, 128, 16>(ctx, p, 1);
+  else launch_igemm<64, 64, 16>(ctx, p, 1);
+}
+
+// ------------------------------------------------------------------------------------------
+// conv2d dgrad (layers.hpp:630-649 + col2im :326-358), implicit and gather-form: for stride s,
+// input pixels split into s*s parity classes (ry, rx) = ((iy+pad) % s, (ix+pad) % s); inside a
+// class the valid taps are ki = ry + s*a, kj = rx + s*c, so each class is a dense GEMM
+// M = ic, N = b * (class pixels), K = oc * taps with no wasted multiply-adds. The epilogue
+// applies the ReLU mask of the previous layer (the relu layer's backward, layers.hpp:712-718).
+// ------------------------------------------------------------------------------------------
+struct ConvDgradProb {
+  static constexpr bool kAMajorM = false;
+  static constexpr bool kBMajorN = true;
+  static constexpr bool kExact = false;
+  const float* dy;
+  const float* w;
+  const float* mask;
+  float* dx;
+  int64_t M, N, K;  // M = ic, N = b * hc * wc, K = oc * nki * nkj
+  int ic, h, wdt, oc, kh, kw, stride, pad, oh, ow;
+  int ry, rx, hc, wc, nki, nkj, iy0, ix0;
+  __device__ float init(int, int64_t, int64_t) const { return 0.f; }
+  // k = (o * nki + a) * nkj + c  ->  tap (ki, kj) = (ry + s*a, rx + s*c)
+  __device__ float a(int, int64_t m, int64_t k) const {
+    const int taps = nki * nkj;
+    const int o = (int)(k / taps), t = (int)(k - (int64_t)o * taps);
+    const int aa = t / nkj, cc = t - aa * nkj;
+    const int ki = ry + stride * aa, kj = rx + stride * cc;
+    return __ldg(w + (((int64_t)o * ic + m) * kh + ki) * kw + kj);
+  }
+  __device__ float b(int, int64_t k, int64_t nn) const {
+    const int taps = nki * nkj;
+    const int o = (int)(k / taps), t = (int)(k - (int64_t)o * taps);
+    const int aa = t / nkj, cc = t - aa * nkj;
+    const int64_t per = (int64_t)hc * wc;
+    const int64_t n = nn / per;
+    const int q = (int)(nn - n * per);
+    const int qy = q / wc, qx = q - qy * wc;
+    const int iy = iy0 + stride * qy, ix = ix0 + stride * qx;
+    // oy * s + ki - pad = iy  ->  oy = (iy + pad - ki) / s (exact by construction of the class)
+    const int oy = (iy + pad - (ry + stride * aa)) / stride;
+    const int ox = (ix + pad - (rx + stride * cc)) / stride;
+    if (oy < 0 || oy >= oh || ox < 0 || ox >= ow) return 0.f;
+    return __ldg(dy + (((int64_t)n * oc + o) * oh + oy) * ow + ox);
+  }
+  template <int TM, int TN>
+  __device__ void epilogue(int, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
+    const int64_t per = (int64_t)hc * wc;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t m = m0 + ty + 16 * i, nn = n0 + tx + 16 * j;
+        if (m < M && nn < N) {
+          const int64_t n = nn / per;
+          const int q = (int)(nn - n * per);
+          const int qy = q / wc, qx = q - qy * wc;
+          const int iy = iy0 + stride * qy, ix = ix0 + stride * qx;
+          const int64_t off = ((n * ic + m) * h + iy) * (int64_t)wdt + ix;
+          float v = acc[i][j];
+          if (mask && !(__ldg(mask + off) > 0.f)) v = 0.f;
+          dx[off] = v;
+        }
+      }
+  }
+};
+
+void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
+                         const float* mask_src, float* dx) {
+  if (g.b == 0) return;
+  const int s = (int)g.stride;
+  for (int ry = 0; ry < s; ++ry)
+    for (int rx = 0; rx < s; ++rx) {
+      ConvDgradProb p{};
+      p.dy = dy;
+      p.w = w;
+      p.mask = mask_src;
+      p.dx = dx;
+      p.ic = (int)g.ic; p.h = (int)g.h; p.wdt = (int)g.w; p.oc = (int)g.oc;
+      p.kh = (int)g.kh; p.kw = (int)g.kw; p.stride = s; p.pad = (int)g.pad;
+      p.oh = (int)g.oh; p.ow = (int)g.ow;
+      p.ry = ry; p.rx = rx;
+      // first input row iy >= 0 with (iy + pad) % s == ry
+      p.iy0 = ((ry - (int)g.pad) % s + s) % s;
+      p.ix0 = ((rx - (int)g.pad) % s + s) % s;
+      p.hc = p.iy0 < g.h ? (int)((g.h - p.iy0 + s - 1) / s) : 0;
+      p.wc = p.ix0 < g.w ? (int)((g.w - p.ix0 + s - 1) / s) : 0;
+      p.nki = ry < g.kh ? (int)((g.kh - ry + s - 1) / s) : 0;
+      p.nkj = rx < g.kw ? (int)((g.kw - rx + s - 1) / s) : 0;
+      if (p.hc == 0 || p.wc == 0) continue;
+      p.M = g.ic;
+      p.N = g.b * p.hc * p.wc;
+      p.K = g.oc * p.nki * p.nkj;
+      if (p.K == 0) {
+        // no tap reaches this class: the input gradient is exactly zero there
+        // (handled by a K = 0 GEMM: the epilogue stores the zero accumulators)
+      }
+      if (g.ic <= 32) launch_igemm<32, 128, 16>(ctx, p, 1);
+      else launch_igemm<64, 64, 16>(ctx, p, 1);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// linear forward (layers.hpp:389-413): y[r, o] = bias[o] + sum_j W[o, j] x[r, j].
+// Narrow outputs (o <= 32, every model on the hot path): one warp per row keeps all o partial
+// dot products in registers and reads the row once. Wide outputs: tiled GEMM.
+// ------------------------------------------------------------------------------------------
+template <int RMAX>
+__global__ void __launch_bounds__(256) linear_fwd_narrow_kernel(const float* __restrict__ x,
+                                                                int x_relu,
+                                                                const float* __restrict__ w,
+                                                                const float* __restrict__ bias,
+                                                                int64_t rows, int64_t d, int r,
+                                                                float* __restrict__ y) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float acc[RMAX];
+#pragma unroll
+  for (int o = 0; o < RMAX; ++o) acc[o] = 0.f;
+  const float* xr = x + row * d;
+  for (int64_t j = lane; j < d; j += 32) {
+    const float xv = relu_if(__ldg(xr + j), x_relu);
+#pragma unroll
+    for (int o = 0; o < RMAX; ++o)
+      if (o < r) acc[o] = fmaf(__ldg(w + (int64_t)o * d + j), xv, acc[o]);
+  }
+#pragma unroll
+  for (int o = 0; o < RMAX; ++o) {
+    if (o < r) {
+      const float s = warp_sum(acc[o]);
+      if (lane == 0) y[row * r + o] = (bias ? __ldg(bias + o) : 0.f) + s;
+    }
+  }
+}
+
+struct LinearFwdProb {
+  static constexpr bool kAMajorM = false;
+  static constexpr bool kBMajorN = false;
+  static constexpr bool kExact = false;
+  const float* x;
+  const float* w;
+  const float* bias;
+  float* y;
+  int x_relu;
+  int64_t M, N, K;  // rows, r, d
+  __device__ float init(int, int64_t, int64_t n) const { return (bias && n < N) ? __ldg(bias + n) : 0.f; }
+  __device__ float a(int, int64_t m, int64_t k) const { return relu_if(__ldg(x + m * K + k), x_relu); }
+  __device__ float b(int, int64_t k, int64_t n) const { return __ldg(w + n * K + k); }
+  template <int TM, int TN>
+  __device__ void epilogue(int, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+        if (m < M && n < N) y[m * N + n] = acc[i][j];
+      }
+  }
+};
+
+void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
+                       int64_t rows, int64_t d, int64_t r, float* y) {
+  if (rows == 0) return;
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  if (r <= 4) {
+    linear_fwd_narrow_kernel<4><<<grid, 256, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
+  } else if (r <= 16) {
+    linear_fwd_narrow_kernel<16><<<grid, 256, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
+  } else if (r <= 32) {
+    linear_fwd_narrow_kernel<32><<<grid, 256, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
+  } else {
+    LinearFwdProb p{x, w, bias, y, x_relu, rows, r, d};
+    launch_igemm<64, 64, 16>(ctx, p, 1);
+    return;
+  }
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// linear dgrad (layers.hpp:606-625): dx[row, j] = sum_o dy[row, o] W[o, j], o ascending, with
+// the ReLU mask of the producing layer.
+__global__ void __launch_bounds__(256) linear_dgrad_kernel(const float* __restrict__ dy,
+                                                           const float* __restrict__ w,
+                                                           int64_t rows, int64_t d, int64_t r,
+                                                           const float* __restrict__ mask,
+                                                           float* __restrict__ dx) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * d) return;
+  const int64_t row = e / d, j = e - row * d;
+  float acc = 0.f;
+  for (int64_t o = 0; o < r; ++o) acc = fmaf(__ldg(dy + row * r + o), __ldg(w + o * d + j), acc);
+  if (mask && !(__ldg(mask + e) > 0.f)) acc = 0.f;
+  dx[e] = acc;
+}
+
+void launch_linear_dgrad(dpg_ctx* ctx, const float* dy, const float* w, int64_t rows, int64_t d,
+                         int64_t r, const float* mask_src, float* dx) {
+  const int64_t n = rows * d;
+  if (n == 0) return;
+  linear_dgrad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(dy, w, rows, d, r, mask_src, dx);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// embedding forward (layers.hpp:414-431) from the sorted (id, position) lists: one warp per token.
+__global__ void __launch_bounds__(256) embedding_fwd_kernel(const int32_t* __restrict__ sorted_v,
+                                                            const int32_t* __restrict__ sorted_s,
+                                                            const float* __restrict__ table,
+                                                            int64_t total, int64_t t, int64_t dim,
+                                                            float* __restrict__ out) {
+  const int64_t tok = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (tok >= total) return;
+  const int64_t n = tok / t;
+  const int64_t v = sorted_v[tok], s = sorted_s[tok];
+  const float* src = table + v * dim;
+  float* dst = out + (n * t + s) * dim;
+  if ((dim & 3) == 0) {
+    for (int64_t d0 = 4 * lane; d0 < dim; d0 += 128)
+      *reinterpret_cast<float4*>(dst + d0) = __ldg(reinterpret_cast<const float4*>(src + d0));
+  } else {
+    for (int64_t d0 = lane; d0 < dim; d0 += 32) dst[d0] = __ldg(src + d0);
+  }
+}
+
+void launch_embedding_fwd(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* sorted_s,
+                          const float* table, int64_t b, int64_t t, int64_t dim, float* out) {
+  const int64_t total = b * t;
+  if (total == 0) return;
+  embedding_fwd_kernel<<<(unsigned)((total + 7) / 8), 256, 0, ctx->stream>>>(sorted_v, sorted_s, table, total, t, dim, out);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// softmax cross-entropy (layers.hpp:894-919), in double like the reference; per-sample loss
+// and d(loss_n)/d(logits_n) = p - onehot (not divided by b). Invalid targets report
+// (stage TARGET, sample n).
+__global__ void softmax_ce_kernel(const float* __restrict__ logits, int logits_relu,
+                                  const float* __restrict__ targets, int64_t b, int64_t k,
+                                  float* __restrict__ loss, float* __restrict__ grad,
+                                  DeviceErr* err) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= b) return;
+  const double tv = (double)targets[n];
+  int64_t cls = 0;
+  if (!(tv >= 0.0) || tv != floor(tv) || tv >= (double)k) {
+    report_error(err, err_key(ERR_STAGE_TARGET, 0, (uint64_t)n), (uint64_t)__float_as_uint(targets[n]));
+  } else {
+    cls = (int64_t)tv;
+  }
+  const float* row = logits + n * k;
+  double mx = (double)relu_if(row[0], logits_relu);
+  for (int64_t j = 1; j < k; ++j) {
+    const double v = (double)relu_if(row[j], logits_relu);
+    mx = mx < v ? v : mx;
+  }
+  double denom = 0.0;
+  for (int64_t j = 0; j < k; ++j) denom += exp((double)relu_if(row[j], logits_relu) - mx);
+  const double log_denom = log(denom);
+  if (loss) loss[n] = (float)(-((double)relu_if(row[cls], logits_relu) - mx - log_denom));
+  for (int64_t j = 0; j < k; ++j) {
+    const float lv = relu_if(row[j], logits_relu);
+    const double p = exp((double)lv - mx) / denom;
+    float gv = (float)(p - (j == cls ? 1.0 : 0.0));
+    if (logits_relu && !(row[j] > 0.f)) gv = 0.f;  // relu layer after the last linear
+    grad[n * k + j] = gv;
+  }
+}
+
+void launch_softmax_ce(dpg_ctx* ctx, const float* logits, int logits_relu, const float* targets,
+                       int64_t b, int64_t k, float* loss, float* grad) {
+  if (b == 0) return;
+  softmax_ce_kernel<<<(unsigned)((b + 127) / 128), 128, 0, ctx->stream>>>(logits, logits_relu, targets, b, k, loss, grad, ctx->dev_err);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+__global__ void relu_mask_kernel(float* __restrict__ g, const float* __restrict__ m, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && !(m[i] > 0.f)) g[i] = 0.f;
+}
+
+void launch_relu_mask(dpg_ctx* ctx, float* g, const float* mask_src, int64_t n) {
+  if (n == 0) return;
+  relu_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(g, mask_src, n);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace dpg

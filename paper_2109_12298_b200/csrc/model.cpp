@@ -1,0 +1,908 @@
+// model.cpp — the engine ABI (include/dpg.h, part 2): a device-resident ModelGraph
+// (layers.hpp:227-245) driven like GradSampleModule + DpOptimizer (optimizer.hpp:138-278,
+// 359-381), with the reference's lifecycle and error contract.
+//
+// Step structure (one CUDA stream, no host synchronisation, graph-capturable):
+//   forward_backward : forward (ReLU folded into consumers) -> softmax-CE -> reverse walk:
+//                      rule(l) with fused norm partials, then dgrad(l) with the ReLU mask
+//   step             : clip_factors -> clipped sums ((scale ⊙ B)^T A, or the record) ->
+//                      [NCCL all-reduce of the flat clipped sum] -> noise + update
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dpg_internal.h"
+
+using dpg::ConvGeom;
+using dpg::guard;
+using dpg::raise;
+
+namespace {
+
+struct ParamInfo {
+  int layer, slot;
+  int64_t numel, offset;
+  int sq_row0, sq_rows;
+  std::string name;
+  bool is_bias;
+};
+
+struct LayerPlan {
+  dpg_layer_desc d{};
+  int kind = 0;
+  // input activation: buffer index (-1 = model input), relu flag, per-sample numel
+  int in_buf = -1;
+  bool in_relu = false;
+  int64_t in_numel = 0;
+  int out_buf = -1;  // parametric layers own an output (pre-activation) buffer
+  int64_t out_numel = 0;
+  int param0 = -1, nparams = 0;
+  ConvGeom g{};            // conv2d (b filled per call)
+  int64_t mid = 1;         // linear: rows per sample
+  int64_t tokens = 0;      // embedding
+  int prev_param_layer = -1;  // previous parametric layer (whose output feeds this one)
+};
+
+int64_t conv_out_extent(int64_t in, int64_t kernel, int64_t stride, int64_t pad) {
+  const int64_t padded = in + 2 * pad;
+  if (padded < kernel) return 0;
+  return (padded - kernel) / stride + 1;
+}
+
+const char* kind_name(int k) {
+  static const char* names[] = {"linear", "embedding", "conv2d", "layer_norm", "group_norm",
+                                "relu", "flatten"};
+  return (k >= 0 && k < 7) ? names[k] : "custom";
+}
+
+std::string shape_str(const std::vector<int64_t>& s, int64_t b = -1) {
+  std::string out = "[";
+  bool first = true;
+  if (b >= 0) {
+    out += std::to_string(b);
+    first = false;
+  }
+  for (int64_t e : s) {
+    if (!first) out += ", ";
+    out += std::to_string(e);
+    first = false;
+  }
+  return out + "]";
+}
+
+}  // namespace
+
+struct dpg_model {
+  dpg_ctx* ctx = nullptr;
+  std::vector<LayerPlan> layers;
+  std::vector<ParamInfo> params;
+  std::vector<int64_t> in_shape;
+  int64_t in_numel = 0, max_b = 0, L = 0, out_width = 0;
+  int out_buf = -1;
+  bool out_relu = false;
+  int sq_rows = 0;
+  int embed_layer = -1;
+  int64_t embed_tokens = 0;
+  // arena
+  char* arena = nullptr;
+  float* p_params = nullptr;
+  std::vector<float*> bufs;      // per-parametric-layer outputs [max_b, out_numel]
+  std::vector<float*> highways;  // same shapes
+  int32_t* row_param = nullptr;
+  int32_t* sorted_v = nullptr;
+  int32_t* sorted_s = nullptr;
+  float* logits_grad = nullptr;
+  size_t ws_bytes = 0;
+  void* ws = nullptr;
+  float* x_stage = nullptr;  // host-path staging
+  float* y_stage = nullptr;
+  float* loss = nullptr;
+};
+
+struct dpg_optimizer {
+  dpg_model* m = nullptr;
+  dpg_optimizer_config cfg{};
+  // device state
+  char* arena = nullptr;
+  float* summed = nullptr;
+  float* grad = nullptr;
+  float* record = nullptr;  // [max_b * L] when materialised, else bias-only scratch
+  float* bias_scratch = nullptr;
+  double* slab = nullptr;
+  double* norms = nullptr;
+  float* scale = nullptr;
+  int64_t* num_clipped = nullptr;
+  uint64_t* step_dev = nullptr;
+  // GradientState (optimizer.hpp:47-57)
+  bool has_grad_sample = false, consumed = false, has_summed = false, has_grad = false;
+  int64_t accumulated = 0;
+  int64_t pending_b = 0, last_b = 0;
+  uint64_t steps = 0;
+  const float* injected = nullptr;
+  // the pending batch's input must stay valid until its fold: the first layer's clipped sum
+  // re-reads it, as the reference's forward cache keeps the input tensor (layers.hpp:249-256)
+  const float* pending_x = nullptr;
+  // CUDA graphs of the whole train step, per batch size
+  struct Graph {
+    int64_t b;
+    const float* x;
+    const float* y;
+    float* loss;
+    cudaGraphExec_t exec;
+    int64_t kernels;  // kernels per replay (gpu_launches evidence)
+  };
+  std::vector<Graph> graphs;
+};
+
+namespace {
+
+std::string err_namer(const void* user, uint64_t stage, uint64_t major) {
+  const dpg_model* m = static_cast<const dpg_model*>(user);
+  if (stage == dpg::ERR_STAGE_NONFINITE && major < m->params.size()) {
+    const ParamInfo& p = m->params[major];
+    return "layer " + std::to_string(p.layer) + " parameter '" + p.name + "'";
+  }
+  if (stage == dpg::ERR_STAGE_EMBED_INDEX && m->embed_layer >= 0)
+    return " [0, " + std::to_string(m->layers[m->embed_layer].d.vocab_size) + ")";
+  if (stage == dpg::ERR_STAGE_TARGET) return " [0, " + std::to_string(m->out_width) + ")";
+  return std::string();
+}
+
+void surface(dpg_model* m) { dpg::throw_device_error(m->ctx, err_namer, m); }
+
+// Parameter / record pointer of param p for batch b: the record packs [b, numel] blocks in
+// (layer, slot) order (GradSampleRecord, grad_sample.hpp:20-33).
+float* gs_ptr(dpg_optimizer* o, int p, int64_t b) {
+  const ParamInfo& pi = o->m->params[p];
+  if (o->cfg.materialise_grad_sample) return o->record + b * pi.offset;
+  if (pi.is_bias) return o->bias_scratch + b * pi.offset;  // bias_scratch indexed like record
+  return nullptr;
+}
+
+void forward_backward_impl(dpg_optimizer* o, const float* x, const float* targets, int64_t b,
+                           float* loss) {
+  dpg_model* m = o->m;
+  dpg_ctx* ctx = m->ctx;
+  float* P = m->p_params;
+  auto act = [&](int buf) -> const float* { return buf < 0 ? x : m->bufs[buf]; };
+  // ---- forward (layers.hpp:576-592) ----
+  for (size_t l = 0; l < m->layers.size(); ++l) {
+    LayerPlan& lp = m->layers[l];
+    if (lp.param0 < 0) continue;
+    const float* in = act(lp.in_buf);
+    const float* w = P + m->params[lp.param0].offset;
+    const float* bias = lp.nparams > 1 ? P + m->params[lp.param0 + 1].offset : nullptr;
+    float* out = m->bufs[lp.out_buf];
+    const double io = 4.0 * b * (lp.in_numel + lp.out_numel);
+    switch (lp.kind) {
+      case DPG_LAYER_LINEAR: {
+        dpg::ProfScope ps(ctx, "fwd.linear[" + std::to_string(l) + "]",
+                          io + 4.0 * m->params[lp.param0].numel,
+                          2.0 * b * lp.mid * lp.d.in_features * lp.d.out_features);
+        dpg::launch_linear_fwd(ctx, in, lp.in_relu, w, bias, b * lp.mid, lp.d.in_features,
+                               lp.d.out_features, out);
+        break;
+      }
+      case DPG_LAYER_CONV2D: {
+        ConvGeom g = lp.g;
+        g.b = b;
+        dpg::ProfScope ps(ctx, "fwd.conv2d[" + std::to_string(l) + "]",
+                          io + 4.0 * m->params[lp.param0].numel, 2.0 * b * g.oc * g.K() * g.P());
+        dpg::launch_conv2d_fwd(ctx, in, lp.in_relu, w, bias, g, out);
+        break;
+      }
+      case DPG_LAYER_EMBEDDING: {
+        dpg::ProfScope ps(ctx, "fwd.embedding[" + std::to_string(l) + "]",
+                          4.0 * b * lp.tokens * (1 + 2 * lp.d.embedding_dim), 0.0);
+        dpg::launch_embed_sort(ctx, in, b, lp.tokens, lp.d.vocab_size, m->sorted_v, m->sorted_s);
+        dpg::launch_embedding_fwd(ctx, m->sorted_v, m->sorted_s, w, b, lp.tokens,
+                                  lp.d.embedding_dim, out);
+        break;
+      }
+    }
+  }
+  // ---- loss (layers.hpp:894-919) ----
+  const float* logits = act(m->out_buf);
+  float* g_last = m->highways[m->out_buf];  // highway of the last parametric layer
+  {
+    dpg::ProfScope ps(ctx, "loss.softmax_ce", 4.0 * b * (2 * m->out_width + 2), 0.0);
+    dpg::launch_softmax_ce(ctx, logits, m->out_relu, targets, b, m->out_width, loss, g_last);
+  }
+  // ---- reverse walk (grad_sample.hpp:277-303) ----
+  double* slab = o->slab;
+  for (int l = (int)m->layers.size() - 1; l >= 0; --l) {
+    LayerPlan& lp = m->layers[l];
+    if (lp.param0 < 0) continue;
+    const float* in = act(lp.in_buf);
+    const float* hw = m->highways[lp.out_buf];
+    const ParamInfo& pw = m->params[lp.param0];
+    float* gw = gs_ptr(o, lp.param0, b);
+    double* sq_w = slab + (int64_t)pw.sq_row0 * b;
+    const std::string ls = "[" + std::to_string(l) + "]";
+    const double gwrite = gw ? 4.0 * b * pw.numel : 0.0;
+    auto bias_rule = [&](int64_t mid, int64_t r, bool conv_layout) {
+      const ParamInfo& pb = m->params[lp.param0 + 1];
+      dpg::ProfScope ps(ctx, "gs.bias" + ls, 4.0 * b * (lp.out_numel + r), 0.0);
+      dpg::launch_gs_bias(ctx, hw, b, mid, r, conv_layout, gs_ptr(o, lp.param0 + 1, b),
+                          slab + (int64_t)pb.sq_row0 * b);
+    };
+    switch (lp.kind) {
+      case DPG_LAYER_LINEAR: {
+        {
+          dpg::ProfScope ps(ctx, "gs.linear" + ls, 4.0 * b * (lp.in_numel + lp.out_numel) + gwrite,
+                            2.0 * b * lp.mid * lp.d.in_features * lp.d.out_features);
+          dpg::launch_gs_linear(ctx, in, lp.in_relu, hw, b, lp.mid, lp.d.in_features,
+                                lp.d.out_features, gw, sq_w);
+        }
+        if (lp.nparams > 1) bias_rule(lp.mid, lp.d.out_features, false);
+        break;
+      }
+      case DPG_LAYER_CONV2D: {
+        ConvGeom g = lp.g;
+        g.b = b;
+        {
+          dpg::ProfScope ps(ctx, "gs.conv2d" + ls, 4.0 * b * (lp.in_numel + lp.out_numel) + gwrite,
+                            2.0 * b * g.oc * g.K() * g.P());
+          dpg::launch_gs_conv2d(ctx, in, lp.in_relu, hw, g, gw, sq_w);
+        }
+        if (lp.nparams > 1) bias_rule(g.P(), g.oc, true);
+        break;
+      }
+      case DPG_LAYER_EMBEDDING: {
+        dpg::ProfScope ps(ctx, "gs.embedding" + ls, 4.0 * b * lp.out_numel + gwrite, 0.0);
+        dpg::launch_gs_embedding(ctx, m->sorted_v, m->sorted_s, hw, b, lp.tokens,
+                                 lp.d.vocab_size, lp.d.embedding_dim, gw, sq_w);
+        break;
+      }
+    }
+    // input gradient for the previous parametric layer, with the ReLU mask folded in
+    if (lp.prev_param_layer >= 0) {
+      const LayerPlan& prev = m->layers[lp.prev_param_layer];
+      float* dst = m->highways[prev.out_buf];
+      const float* mask = lp.in_relu ? m->bufs[prev.out_buf] : nullptr;
+      const float* w = P + pw.offset;
+      const double dio = 4.0 * (b * lp.out_numel + pw.numel + b * lp.in_numel * (mask ? 2 : 1));
+      switch (lp.kind) {
+        case DPG_LAYER_LINEAR: {
+          dpg::ProfScope ps(ctx, "dgrad.linear" + ls, dio,
+                            2.0 * b * lp.mid * lp.d.in_features * lp.d.out_features);
+          dpg::launch_linear_dgrad(ctx, hw, w, b * lp.mid, lp.d.in_features, lp.d.out_features,
+                                   mask, dst);
+          break;
+        }
+        case DPG_LAYER_CONV2D: {
+          ConvGeom g = lp.g;
+          g.b = b;
+          dpg::ProfScope ps(ctx, "dgrad.conv2d" + ls, dio, 2.0 * b * g.oc * g.K() * g.P());
+          dpg::launch_conv2d_dgrad(ctx, hw, w, g, mask, dst);
+          break;
+        }
+        default:
+          // embedding backward_input is zero (layers.hpp:626-629)
+          DPG_CUDA(cudaMemsetAsync(dst, 0, sizeof(float) * b * prev.out_numel, ctx->stream));
+      }
+    }
+  }
+}
+
+// clip_and_sum of the pending batch into summed (fold_pending, optimizer.hpp:240-254)
+void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
+  dpg_model* m = o->m;
+  dpg_ctx* ctx = m->ctx;
+  const int accumulate = o->has_summed ? 1 : 0;
+  {
+    dpg::ProfScope ps(ctx, "clip_factors", 8.0 * m->sq_rows * b + 12.0 * b, 0.0);
+    dpg::launch_clip_factors(ctx, o->slab, m->row_param, m->sq_rows, b, o->cfg.max_grad_norm,
+                             o->norms, o->scale, o->num_clipped);
+  }
+  auto act = [&](int buf) -> const float* { return buf < 0 ? x : m->bufs[buf]; };
+  for (size_t l = 0; l < m->layers.size(); ++l) {
+    LayerPlan& lp = m->layers[l];
+    if (lp.param0 < 0) continue;
+    for (int k = 0; k < lp.nparams; ++k) {
+      const int p = lp.param0 + k;
+      const ParamInfo& pi = m->params[p];
+      float* dst = o->summed + pi.offset;
+      float* rec = gs_ptr(o, p, b);
+      const std::string ls = "[" + std::to_string(l) + "]";
+      if (o->cfg.clipped_sum_from_record || pi.is_bias) {
+        // the reference's pass 2 over the stored per-sample gradients (exact order)
+        dpg::ProfScope ps(ctx, std::string(pi.is_bias ? "csum.bias" : "csum.record") + ls,
+                          4.0 * (b * pi.numel + 2 * pi.numel), 2.0 * b * pi.numel);
+        dpg::launch_weighted_sum_materialised(ctx, rec, o->scale, b, pi.numel, dst, accumulate);
+        continue;
+      }
+      const float* in = act(lp.in_buf);
+      const float* hw = m->highways[lp.out_buf];
+      const double cio = 4.0 * (b * (lp.in_numel + lp.out_numel) + 2 * pi.numel);
+      switch (lp.kind) {
+        case DPG_LAYER_LINEAR: {
+          dpg::ProfScope ps(ctx, "csum.linear" + ls, cio,
+                            2.0 * b * lp.mid * lp.d.in_features * lp.d.out_features);
+          dpg::launch_clipped_sum_linear(ctx, in, lp.in_relu, hw, o->scale, b, lp.mid,
+                                         lp.d.in_features, lp.d.out_features, dst, nullptr,
+                                         accumulate, m->ws);
+          break;
+        }
+        case DPG_LAYER_CONV2D: {
+          ConvGeom g = lp.g;
+          g.b = b;
+          dpg::ProfScope ps(ctx, "csum.conv2d" + ls, cio, 2.0 * b * g.oc * g.K() * g.P());
+          dpg::launch_clipped_sum_conv2d(ctx, in, lp.in_relu, hw, o->scale, g, dst, nullptr,
+                                         accumulate, m->ws);
+          break;
+        }
+        case DPG_LAYER_EMBEDDING: {
+          dpg::ProfScope ps(ctx, "csum.embedding" + ls, 4.0 * (b * lp.out_numel + 2 * pi.numel), 0.0);
+          dpg::launch_clipped_sum_embedding(ctx, m->sorted_v, m->sorted_s, hw, o->scale, b,
+                                            lp.tokens, lp.d.vocab_size, lp.d.embedding_dim, dst,
+                                            accumulate, m->ws);
+          break;
+        }
+      }
+    }
+  }
+  o->has_summed = true;
+  o->accumulated += b;
+  o->last_b = b;
+}
+
+// graph_mode: the Philox step is read from o->step_dev (graphs bake kernel arguments; the host
+// writes the step there before each replay) and the host counter is advanced by the caller.
+void finish_impl(dpg_optimizer* o, bool graph_mode) {
+  dpg_model* m = o->m;
+  dpg_ctx* ctx = m->ctx;
+  if (ctx->comm) {
+    dpg::ProfScope ps(ctx, "allreduce", 8.0 * m->L, 0.0);
+    DPG_NCCL(ncclAllReduce(o->summed, o->summed, (size_t)m->L, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
+  }
+  dpg::ProfScope ps(ctx, "noise_update", 16.0 * m->L, 0.0);
+  dpg::launch_noise_update(ctx, m->p_params, o->summed, o->grad, m->L, o->cfg.noise_multiplier,
+                           o->cfg.max_grad_norm, o->cfg.expected_batch_size,
+                           o->cfg.learning_rate, o->cfg.noise_seed, o->steps, o->injected,
+                           graph_mode ? o->step_dev : nullptr);
+  if (!graph_mode) ++o->steps;
+  o->has_grad = true;
+}
+
+// Lifecycle checks of set_grad_sample (optimizer.hpp:147-161)
+void check_set_grad_sample(dpg_optimizer* o) {
+  if (o->has_grad_sample && !o->consumed)
+    raise(DPG_ERR_LIFECYCLE, "previous grad_sample was never consumed; call virtual_step or step first");
+  if (o->has_grad) raise(DPG_ERR_LIFECYCLE, "grad from the last step is still present; call zero_grad first");
+}
+
+void step_impl(dpg_optimizer* o, const float* x, bool graph_mode) {
+  if (o->has_grad) raise(DPG_ERR_LIFECYCLE, "step called twice without zero_grad in between");
+  if (o->has_grad_sample && !o->consumed) {
+    fold_impl(o, o->pending_b, x);
+    o->consumed = true;
+  }
+  if (!o->has_summed)
+    raise(DPG_ERR_LIFECYCLE,
+          "step with no accumulated samples; run a backward or use step_empty_batch for a "
+          "noise-only update");
+  finish_impl(o, graph_mode);
+}
+
+void zero_grad_impl(dpg_optimizer* o) {
+  o->has_grad_sample = false;
+  o->consumed = false;
+  o->has_summed = false;
+  o->has_grad = false;
+  o->accumulated = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlayers,
+                            const int64_t* in_shape, int in_rank, int64_t max_batch,
+                            dpg_model** out) {
+  if (!out) return DPG_ERR_PARAMETER;
+  *out = nullptr;
+  dpg_model* m = new dpg_model();
+  const dpg_status st = guard(ctx, [&] {
+    if (!ctx) raise(DPG_ERR_PARAMETER, "null context");
+    DPG_CUDA(cudaSetDevice(ctx->device));
+    if (nlayers <= 0) raise(DPG_ERR_PARAMETER, "model needs at least one layer");
+    if (max_batch <= 0) raise(DPG_ERR_PARAMETER, "max_batch must be positive");
+    m->ctx = ctx;
+    m->max_b = max_batch;
+    m->in_shape.assign(in_shape, in_shape + in_rank);
+    m->in_numel = 1;
+    for (int64_t e : m->in_shape) m->in_numel *= e;
+    // ---- shape walk (layer_forward checks, layers.hpp:382-573) ----
+    std::vector<int64_t> shape = m->in_shape;
+    int cur_buf = -1;
+    bool cur_relu = false;
+    int last_param_layer = -1;
+    int64_t offset = 0;
+    std::vector<int64_t> buf_numel;
+    for (int l = 0; l < nlayers; ++l) {
+      LayerPlan lp;
+      lp.d = layers[l];
+      lp.kind = lp.d.kind;
+      int64_t numel = 1;
+      for (int64_t e : shape) numel *= e;
+      lp.in_buf = cur_buf;
+      lp.in_relu = cur_relu;
+      lp.in_numel = numel;
+      auto shape_err = [&](const std::string& what) {
+        raise(DPG_ERR_DIMENSION, "layer " + std::to_string(l) + " (" + kind_name(lp.kind) + "): " + what);
+      };
+      std::vector<std::pair<std::string, int64_t>> pshapes;
+      switch (lp.kind) {
+        case DPG_LAYER_LINEAR: {
+          if (lp.d.in_features <= 0 || lp.d.out_features <= 0)
+            raise(DPG_ERR_PARAMETER, "linear: feature counts must be positive");
+          if (shape.empty() || shape.back() != lp.d.in_features)
+            shape_err("expected trailing extent " + std::to_string(lp.d.in_features) + ", got input " +
+                      shape_str(shape, 1));
+          lp.mid = numel / lp.d.in_features;
+          shape.back() = lp.d.out_features;
+          pshapes.push_back({"weight", lp.d.out_features * lp.d.in_features});
+          if (lp.d.has_bias) pshapes.push_back({"bias", lp.d.out_features});
+          break;
+        }
+        case DPG_LAYER_EMBEDDING: {
+          if (lp.d.vocab_size <= 0 || lp.d.embedding_dim <= 0)
+            raise(DPG_ERR_PARAMETER, "embedding: extents must be positive");
+          if (shape.size() != 1) shape_err("expected [batch, tokens] indices, got " + shape_str(shape, 1));
+          if (l != 0 || cur_relu)
+            raise(DPG_ERR_REGISTRY, "device embedding rule needs the embedding to read the model input");
+          lp.tokens = shape[0];
+          if (lp.tokens > 4096) shape_err("at most 4096 tokens per sample on device");
+          shape = {lp.tokens, lp.d.embedding_dim};
+          pshapes.push_back({"table", lp.d.vocab_size * lp.d.embedding_dim});
+          m->embed_layer = l;
+          m->embed_tokens = lp.tokens;
+          break;
+        }
+        case DPG_LAYER_CONV2D: {
+          const dpg_layer_desc& d = lp.d;
+          if (d.in_channels <= 0 || d.out_channels <= 0 || d.kernel_h <= 0 || d.kernel_w <= 0 || d.stride <= 0)
+            raise(DPG_ERR_PARAMETER, "conv2d: channel, kernel, and stride extents must be positive");
+          if (shape.size() != 3 || shape[0] != d.in_channels)
+            shape_err("expected [batch, " + std::to_string(d.in_channels) + ", h, w], got " + shape_str(shape, 1));
+          const int64_t oh = conv_out_extent(shape[1], d.kernel_h, d.stride, d.padding);
+          const int64_t ow = conv_out_extent(shape[2], d.kernel_w, d.stride, d.padding);
+          if (oh == 0 || ow == 0) shape_err("kernel larger than padded input " + shape_str(shape, 1));
+          lp.g = ConvGeom{0, d.in_channels, shape[1], shape[2], d.out_channels, d.kernel_h, d.kernel_w,
+                          d.stride, d.padding, oh, ow};
+          shape = {d.out_channels, oh, ow};
+          pshapes.push_back({"weight", d.out_channels * d.in_channels * d.kernel_h * d.kernel_w});
+          if (d.has_bias) pshapes.push_back({"bias", d.out_channels});
+          break;
+        }
+        case DPG_LAYER_RELU:
+          cur_relu = true;
+          break;
+        case DPG_LAYER_FLATTEN:
+          shape = {numel};
+          break;
+        default:
+          raise(DPG_ERR_REGISTRY, std::string("no device grad-sample rule registered for kind '") +
+                                      kind_name(lp.kind) + "'");
+      }
+      if (!pshapes.empty()) {
+        lp.param0 = (int)m->params.size();
+        lp.nparams = (int)pshapes.size();
+        for (size_t k = 0; k < pshapes.size(); ++k) {
+          ParamInfo pi;
+          pi.layer = l;
+          pi.slot = (int)k;
+          pi.numel = pshapes[k].second;
+          pi.offset = offset;
+          pi.name = pshapes[k].first;
+          pi.is_bias = pi.name == "bias";
+          offset += pi.numel;
+          m->params.push_back(pi);
+        }
+        int64_t on = 1;
+        for (int64_t e : shape) on *= e;
+        lp.out_numel = on;
+        lp.out_buf = (int)buf_numel.size();
+        buf_numel.push_back(on);
+        lp.prev_param_layer = last_param_layer;
+        last_param_layer = l;
+        cur_buf = lp.out_buf;
+        cur_relu = false;
+      }
+      m->layers.push_back(lp);
+    }
+    if (last_param_layer < 0) raise(DPG_ERR_PARAMETER, "model has no trainable parameters");
+    if (shape.size() != 1)
+      raise(DPG_ERR_DIMENSION, "cross-entropy expects [batch, classes] logits, got " + shape_str(shape, 1));
+    m->out_width = shape[0];
+    m->out_buf = cur_buf;
+    m->out_relu = cur_relu;
+    m->L = offset;
+    // the first parametric layer gets no input gradient (grad_sample.hpp:300)
+    // ---- norm-partial rows (one row per producer output tile) ----
+    int rows = 0;
+    for (auto& lp : m->layers) {
+      if (lp.param0 < 0) continue;
+      for (int k = 0; k < lp.nparams; ++k) {
+        ParamInfo& pi = m->params[lp.param0 + k];
+        int r = 1;
+        if (!pi.is_bias) {
+          if (lp.kind == DPG_LAYER_LINEAR) r = dpg::sq_rows_linear(lp.mid, lp.d.in_features, lp.d.out_features);
+          else if (lp.kind == DPG_LAYER_CONV2D) r = dpg::sq_rows_conv2d(lp.g);
+          else r = dpg::sq_rows_embedding(lp.d.vocab_size, lp.d.embedding_dim);
+        }
+        pi.sq_row0 = rows;
+        pi.sq_rows = r;
+        rows += r;
+      }
+    }
+    m->sq_rows = rows;
+    // ---- workspace for the clipped sums (shared, stream-ordered) ----
+    size_t ws = 1 << 20;
+    for (auto& lp : m->layers) {
+      if (lp.kind == DPG_LAYER_LINEAR)
+        ws = std::max(ws, dpg::clipped_sum_ws_linear(max_batch, lp.mid, lp.d.in_features, lp.d.out_features));
+      if (lp.kind == DPG_LAYER_CONV2D) {
+        ConvGeom g = lp.g;
+        g.b = max_batch;
+        ws = std::max(ws, dpg::clipped_sum_ws_conv2d(g));
+        // smaller batches may pick more splits: bound by b = 1..max_b worst case
+        for (int64_t bb = 1; bb <= max_batch; bb = bb * 2) {
+          g.b = bb;
+          ws = std::max(ws, dpg::clipped_sum_ws_conv2d(g));
+        }
+      }
+      if (lp.kind == DPG_LAYER_EMBEDDING) ws = std::max(ws, dpg::clipped_sum_ws_embedding(max_batch, lp.d.vocab_size));
+    }
+    m->ws_bytes = ws;
+    // ---- arena ----
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    size_t total = al(sizeof(float) * m->L);
+    for (int64_t n : buf_numel) total += 2 * al(sizeof(float) * max_batch * n);
+    total += al(sizeof(int32_t) * rows);
+    total += 2 * al(sizeof(int32_t) * max_batch * std::max<int64_t>(1, m->embed_tokens));
+    total += al(ws);
+    total += al(sizeof(float) * max_batch * m->in_numel) + 2 * al(sizeof(float) * max_batch);
+    DPG_CUDA(cudaMalloc(&m->arena, total));
+    DPG_CUDA(cudaMemset(m->arena, 0, total));
+    char* p = m->arena;
+    auto take = [&](size_t bytes) {
+      char* r = p;
+      p += al(bytes);
+      return r;
+    };
+    m->p_params = reinterpret_cast<float*>(take(sizeof(float) * m->L));
+    for (int64_t n : buf_numel) {
+      m->bufs.push_back(reinterpret_cast<float*>(take(sizeof(float) * max_batch * n)));
+      m->highways.push_back(reinterpret_cast<float*>(take(sizeof(float) * max_batch * n)));
+    }
+    m->row_param = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * rows));
+    m->sorted_v = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * max_batch * std::max<int64_t>(1, m->embed_tokens)));
+    m->sorted_s = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * max_batch * std::max<int64_t>(1, m->embed_tokens)));
+    m->ws = take(ws);
+    m->x_stage = reinterpret_cast<float*>(take(sizeof(float) * max_batch * m->in_numel));
+    m->y_stage = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
+    m->loss = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
+    std::vector<int32_t> rp;
+    for (size_t q = 0; q < m->params.size(); ++q)
+      for (int r = 0; r < m->params[q].sq_rows; ++r) rp.push_back((int32_t)q);
+    DPG_CUDA(cudaMemcpy(m->row_param, rp.data(), sizeof(int32_t) * rp.size(), cudaMemcpyHostToDevice));
+  });
+  if (st != DPG_OK) {
+    if (m->arena) cudaFree(m->arena);
+    delete m;
+    return st;
+  }
+  *out = m;
+  return DPG_OK;
+}
+
+void dpg_model_destroy(dpg_model* m) {
+  if (!m) return;
+  cudaSetDevice(m->ctx->device);
+  cudaStreamSynchronize(m->ctx->stream);
+  if (m->arena) cudaFree(m->arena);
+  delete m;
+}
+
+int64_t dpg_model_parameter_count(const dpg_model* m) { return m ? m->L : 0; }
+int dpg_model_num_param_tensors(const dpg_model* m) { return m ? (int)m->params.size() : 0; }
+int64_t dpg_model_output_width(const dpg_model* m) { return m ? m->out_width : 0; }
+float* dpg_model_params(dpg_model* m) { return m ? m->p_params : nullptr; }
+
+dpg_status dpg_model_param_info(const dpg_model* m, int p, int* layer, int* slot, int64_t* numel,
+                                int64_t* offset) {
+  if (!m || p < 0 || p >= (int)m->params.size()) return DPG_ERR_PARAMETER;
+  const ParamInfo& pi = m->params[p];
+  if (layer) *layer = pi.layer;
+  if (slot) *slot = pi.slot;
+  if (numel) *numel = pi.numel;
+  if (offset) *offset = pi.offset;
+  return DPG_OK;
+}
+
+dpg_status dpg_model_load_params(dpg_model* m, const float* host) {
+  if (!m) return DPG_ERR_PARAMETER;
+  return guard(m->ctx, [&] {
+    DPG_CUDA(cudaSetDevice(m->ctx->device));
+    DPG_CUDA(cudaMemcpyAsync(m->p_params, host, sizeof(float) * m->L, cudaMemcpyHostToDevice, m->ctx->stream));
+    DPG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  });
+}
+
+dpg_status dpg_model_store_params(dpg_model* m, float* host) {
+  if (!m) return DPG_ERR_PARAMETER;
+  return guard(m->ctx, [&] {
+    DPG_CUDA(cudaSetDevice(m->ctx->device));
+    DPG_CUDA(cudaMemcpyAsync(host, m->p_params, sizeof(float) * m->L, cudaMemcpyDeviceToHost, m->ctx->stream));
+    DPG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  });
+}
+
+dpg_status dpg_optimizer_create(dpg_model* m, const dpg_optimizer_config* cfg, dpg_optimizer** out) {
+  if (!out || !m || !cfg) return DPG_ERR_PARAMETER;
+  *out = nullptr;
+  dpg_optimizer* o = new dpg_optimizer();
+  const dpg_status st = guard(m->ctx, [&] {
+    DPG_CUDA(cudaSetDevice(m->ctx->device));
+    // DpOptimizerConfig::check (optimizer.hpp:28-33)
+    if (cfg->noise_multiplier < 0.0) raise(DPG_ERR_PARAMETER, "noise multiplier must be >= 0");
+    if (!(cfg->max_grad_norm > 0.0)) raise(DPG_ERR_PARAMETER, "max grad norm must be > 0");
+    if (!(cfg->learning_rate > 0.0)) raise(DPG_ERR_PARAMETER, "learning rate must be > 0");
+    if (!(cfg->expected_batch_size > 0.0)) raise(DPG_ERR_PARAMETER, "expected batch size must be > 0");
+    if (cfg->clipped_sum_from_record && !cfg->materialise_grad_sample)
+      raise(DPG_ERR_PARAMETER, "clipped_sum_from_record needs materialise_grad_sample");
+    o->m = m;
+    o->cfg = *cfg;
+    const int64_t B = m->max_b, L = m->L;
+    int64_t bias_numel = 0;
+    for (auto& pi : m->params)
+      if (pi.is_bias) bias_numel = std::max(bias_numel, pi.offset + pi.numel);
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t rec = cfg->materialise_grad_sample ? sizeof(float) * (size_t)(B * L) : sizeof(float) * (size_t)(B * bias_numel);
+    size_t total = 2 * al(sizeof(float) * L) + al(rec) + al(sizeof(double) * m->sq_rows * B) +
+                   al(sizeof(double) * B) + al(sizeof(float) * B) + al(sizeof(int64_t)) + al(sizeof(uint64_t));
+    DPG_CUDA(cudaMalloc(&o->arena, total));
+    DPG_CUDA(cudaMemset(o->arena, 0, total));
+    char* p = o->arena;
+    auto take = [&](size_t bytes) {
+      char* r = p;
+      p += al(bytes);
+      return r;
+    };
+    o->summed = reinterpret_cast<float*>(take(sizeof(float) * L));
+    o->grad = reinterpret_cast<float*>(take(sizeof(float) * L));
+    float* r = reinterpret_cast<float*>(take(rec));
+    if (cfg->materialise_grad_sample) o->record = r; else o->bias_scratch = r;
+    o->slab = reinterpret_cast<double*>(take(sizeof(double) * m->sq_rows * B));
+    o->norms = reinterpret_cast<double*>(take(sizeof(double) * B));
+    o->scale = reinterpret_cast<float*>(take(sizeof(float) * B));
+    o->num_clipped = reinterpret_cast<int64_t*>(take(sizeof(int64_t)));
+    o->step_dev = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t)));
+  });
+  if (st != DPG_OK) {
+    if (o->arena) cudaFree(o->arena);
+    delete o;
+    return st;
+  }
+  *out = o;
+  return DPG_OK;
+}
+
+void dpg_optimizer_destroy(dpg_optimizer* o) {
+  if (!o) return;
+  cudaSetDevice(o->m->ctx->device);
+  cudaStreamSynchronize(o->m->ctx->stream);
+  for (auto& g : o->graphs) cudaGraphExecDestroy(g.exec);
+  if (o->arena) cudaFree(o->arena);
+  delete o;
+}
+
+dpg_status dpg_forward_backward(dpg_optimizer* o, const float* x, const float* targets, int64_t b,
+                                float* loss) {
+  if (!o) return DPG_ERR_PARAMETER;
+  return guard(o->m->ctx, [&] {
+    DPG_CUDA(cudaSetDevice(o->m->ctx->device));
+    if (b <= 0) raise(DPG_ERR_DIMENSION, "compute_grad_samples: batch must be non-empty");
+    if (b > o->m->max_b)
+      raise(DPG_ERR_DIMENSION, "batch " + std::to_string(b) + " exceeds the model's max_batch " +
+                                   std::to_string(o->m->max_b));
+    if (!x || !targets) raise(DPG_ERR_PARAMETER, "input and targets must not be NULL");
+    check_set_grad_sample(o);
+    forward_backward_impl(o, x, targets, b, loss);
+    o->has_grad_sample = true;
+    o->consumed = false;
+    o->pending_b = b;
+    o->pending_x = x;
+  });
+}
+
+dpg_status dpg_virtual_step(dpg_optimizer* o) {
+  if (!o) return DPG_ERR_PARAMETER;
+  return guard(o->m->ctx, [&] {
+    // optimizer.hpp:166-174
+    if (!o->has_grad_sample || o->consumed)
+      raise(DPG_ERR_LIFECYCLE, "virtual_step without a fresh grad_sample (run a backward first)");
+    fold_impl(o, o->pending_b, o->pending_x);
+    o->has_grad_sample = false;
+    o->consumed = false;
+  });
+}
+
+dpg_status dpg_step(dpg_optimizer* o) {
+  if (!o) return DPG_ERR_PARAMETER;
+  return guard(o->m->ctx, [&] { step_impl(o, o->pending_x, false); });
+}
+
+dpg_status dpg_step_empty_batch(dpg_optimizer* o) {
+  if (!o) return DPG_ERR_PARAMETER;
+  return guard(o->m->ctx, [&] {
+    // optimizer.hpp:197-213
+    if (o->has_grad) raise(DPG_ERR_LIFECYCLE, "step called twice without zero_grad in between");
+    if ((o->has_grad_sample && !o->consumed) || o->has_summed)
+      raise(DPG_ERR_LIFECYCLE, "step_empty_batch with gradients pending");
+    DPG_CUDA(cudaMemsetAsync(o->summed, 0, sizeof(float) * o->m->L, o->m->ctx->stream));
+    o->has_summed = true;
+    o->accumulated = 0;
+    finish_impl(o, false);
+  });
+}
+
+dpg_status dpg_zero_grad(dpg_optimizer* o) {
+  if (!o) return DPG_ERR_PARAMETER;
+  zero_grad_impl(o);
+  return DPG_OK;
+}
+
+dpg_status dpg_set_noise_multiplier(dpg_optimizer* o, double sigma) {
+  if (!o) return DPG_ERR_PARAMETER;
+  return guard(o->m->ctx, [&] {
+    if (sigma < 0.0) raise(DPG_ERR_PARAMETER, "noise multiplier must be >= 0");
+    o->cfg.noise_multiplier = sigma;
+    for (auto& g : o->graphs) cudaGraphExecDestroy(g.exec);
+    o->graphs.clear();
+  });
+}
+
+dpg_status dpg_set_expected_batch_size(dpg_optimizer* o, double e) {
+  if (!o) return DPG_ERR_PARAMETER;
+  return guard(o->m->ctx, [&] {
+    if (!(e > 0.0)) raise(DPG_ERR_PARAMETER, "expected batch size must be > 0");
+    o->cfg.expected_batch_size = e;
+    for (auto& g : o->graphs) cudaGraphExecDestroy(g.exec);
+    o->graphs.clear();
+  });
+}
+
+dpg_status dpg_set_injected_noise(dpg_optimizer* o, const float* noise) {
+  if (!o) return DPG_ERR_PARAMETER;
+  o->injected = noise;
+  for (auto& g : o->graphs) cudaGraphExecDestroy(g.exec);
+  o->graphs.clear();
+  return DPG_OK;
+}
+
+dpg_status dpg_last_clip_summary(dpg_optimizer* o, double* norms, double* scales,
+                                 int64_t* num_clipped) {
+  if (!o) return DPG_ERR_PARAMETER;
+  return guard(o->m->ctx, [&] {
+    dpg_ctx* ctx = o->m->ctx;
+    surface(o->m);
+    const int64_t b = o->last_b;
+    if (norms && b) DPG_CUDA(cudaMemcpy(norms, o->norms, sizeof(double) * b, cudaMemcpyDeviceToHost));
+    if (scales && b) {
+      // scale_factors are doubles in the reference (C / max(N, C)); recompute from the norms
+      std::vector<double> nrm(b);
+      DPG_CUDA(cudaMemcpy(nrm.data(), o->norms, sizeof(double) * b, cudaMemcpyDeviceToHost));
+      const double c = o->cfg.max_grad_norm;
+      for (int64_t i = 0; i < b; ++i) scales[i] = c / std::max(nrm[i], c);
+    }
+    if (num_clipped) DPG_CUDA(cudaMemcpy(num_clipped, o->num_clipped, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    (void)ctx;
+  });
+}
+
+const float* dpg_grad_sample(const dpg_optimizer* o) {
+  return (o && o->has_grad_sample && o->cfg.materialise_grad_sample) ? o->record : nullptr;
+}
+const float* dpg_summed_grad(const dpg_optimizer* o) { return (o && o->has_summed) ? o->summed : nullptr; }
+const float* dpg_grad(const dpg_optimizer* o) { return (o && o->has_grad) ? o->grad : nullptr; }
+int64_t dpg_accumulated_samples(const dpg_optimizer* o) { return o ? o->accumulated : 0; }
+
+dpg_status dpg_train_step(dpg_optimizer* o, const float* x, const float* targets, int64_t b,
+                          float* loss, int use_graph) {
+  if (!o) return DPG_ERR_PARAMETER;
+  dpg_model* m = o->m;
+  dpg_ctx* ctx = m->ctx;
+  return guard(ctx, [&] {
+    DPG_CUDA(cudaSetDevice(ctx->device));
+    if (b <= 0) raise(DPG_ERR_DIMENSION, "compute_grad_samples: batch must be non-empty");
+    if (b > m->max_b) raise(DPG_ERR_DIMENSION, "batch exceeds the model's max_batch");
+    if (!x || !targets) raise(DPG_ERR_PARAMETER, "input and targets must not be NULL");
+    // a train step opens a fresh logical batch: zero_grad, forward_backward, step
+    zero_grad_impl(o);
+    auto mark_done = [&] {
+      o->has_grad_sample = true;
+      o->consumed = true;
+      o->has_summed = true;
+      o->has_grad = true;
+      o->accumulated = b;
+      o->last_b = b;
+      o->pending_b = b;
+      o->pending_x = x;
+    };
+    if (!use_graph) {
+      forward_backward_impl(o, x, targets, b, loss);
+      o->has_grad_sample = true;
+      o->pending_b = b;
+      o->pending_x = x;
+      step_impl(o, x, false);
+      return;
+    }
+    dpg_optimizer::Graph* hit = nullptr;
+    for (auto& g : o->graphs)
+      if (g.b == b && g.x == x && g.y == targets && g.loss == loss) hit = &g;
+    if (!hit) {
+      cudaGraph_t graph;
+      const int64_t before = ctx->launches;
+      ctx->capturing = true;
+      DPG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        forward_backward_impl(o, x, targets, b, loss);
+        o->has_grad_sample = true;
+        o->pending_b = b;
+        o->pending_x = x;
+        step_impl(o, x, true);
+      } catch (...) {
+        cudaStreamEndCapture(ctx->stream, &graph);
+        ctx->capturing = false;
+        zero_grad_impl(o);
+        throw;
+      }
+      DPG_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+      ctx->capturing = false;
+      cudaGraphExec_t exec;
+      DPG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      DPG_CUDA(cudaGraphDestroy(graph));
+      o->graphs.push_back({b, x, targets, loss, exec, ctx->launches - before});
+      ctx->launches = before;
+      hit = &o->graphs.back();
+    }
+    DPG_CUDA(cudaMemcpyAsync(o->step_dev, &o->steps, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    DPG_CUDA(cudaGraphLaunch(hit->exec, ctx->stream));
+    ctx->launches += hit->kernels;
+    ++o->steps;
+    mark_done();
+  });
+}
+
+dpg_status dpg_train_step_host(dpg_optimizer* o, const float* x_host, const float* targets_host,
+                               int64_t b, float* loss_host) {
+  if (!o) return DPG_ERR_PARAMETER;
+  dpg_model* m = o->m;
+  dpg_ctx* ctx = m->ctx;
+  const dpg_status st = guard(ctx, [&] {
+    DPG_CUDA(cudaSetDevice(ctx->device));
+    if (b <= 0) raise(DPG_ERR_DIMENSION, "compute_grad_samples: batch must be non-empty");
+    if (b > m->max_b) raise(DPG_ERR_DIMENSION, "batch exceeds the model's max_batch");
+    DPG_CUDA(cudaMemcpyAsync(m->x_stage, x_host, sizeof(float) * b * m->in_numel, cudaMemcpyHostToDevice, ctx->stream));
+    DPG_CUDA(cudaMemcpyAsync(m->y_stage, targets_host, sizeof(float) * b, cudaMemcpyHostToDevice, ctx->stream));
+  });
+  if (st != DPG_OK) return st;
+  const dpg_status st2 = dpg_train_step(o, m->x_stage, m->y_stage, b, m->loss, 1);
+  if (st2 != DPG_OK) return st2;
+  return guard(ctx, [&] {
+    if (loss_host)
+      DPG_CUDA(cudaMemcpyAsync(loss_host, m->loss, sizeof(float) * b, cudaMemcpyDeviceToHost, ctx->stream));
+    try {
+      surface(m);
+    } catch (...) {
+      zero_grad_impl(o);
+      throw;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// noise.cu — Gaussian noise + averaged SGD update, fused (north-star subsystem 4).
+//
+// Reference: add_noise (optimizer.hpp:120-133) -> gaussian (tensor.hpp:343-354) ->
+// RngStream::normal (rng.cpp:40-53, Box-Muller in double), then finish_step
+// (optimizer.hpp:256-271): g = noised * (1/E), w = w - g * lr in fp32.
+//
+// The device stream is counter-based Philox4x32-10 (Salmon et al., Random123) keyed by the
+// 64-bit noise seed with counter (element pair, step): every rank and every replay draws the
+// same value for the same (seed, step, element) with no state to carry, which is what lets the
+// sample-sharded step add noise once after the all-reduce without a broadcast. Box-Muller uses
+// the reference's uniform construction: u1 = ((x >> 11) + 1) * 2^-53 in (0, 1],
+// u2 = (y >> 11) * 2^-53 in [0, 1); element 2q gets r cos(theta), 2q+1 gets r sin(theta).
+#include "dpg_device.cuh"
+
+namespace dpg {
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      key.x += W0;
+      key.y += W1;
+    }
+    const uint32_t hi0 = __umulhi(M0, ctr.x), lo0 = M0 * ctr.x;
+    const uint32_t hi1 = __umulhi(M1, ctr.z), lo1 = M1 * ctr.z;
+    ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+  }
+  return ctr;
+}
+
+__device__ __forceinline__ void normal_pair(uint64_t seed, uint64_t step, uint64_t q, double& z0,
+                                            double& z1) {
+  const uint4 r = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), (uint32_t)step,
+                                           (uint32_t)(step >> 32)),
+                                make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const uint64_t x = ((uint64_t)r.y << 32) | r.x;
+  const uint64_t y = ((uint64_t)r.w << 32) | r.z;
+  const double u1 = (double)((x >> 11) + 1) * 0x1.0p-53;
+  const double u2 = (double)(y >> 11) * 0x1.0p-53;
+  const double rad = sqrt(-2.0 * log(u1));
+  double s, c;
+  sincospi(2.0 * u2, &s, &c);
+  z0 = rad * c;
+  z1 = rad * s;
+}
+
+// One thread per element pair. If an earlier stage flagged an error (NumericError etc.) the
+// update is skipped: the reference throws before touching the parameters.
+__global__ void __launch_bounds__(256) noise_update_kernel(
+    float* __restrict__ params, const float* __restrict__ summed, float* __restrict__ grad,
+    int64_t n, double std_dev, float inv_e, float lr, uint64_t seed, uint64_t step,
+    const float* __restrict__ injected, const uint64_t* step_ptr, const DeviceErr* err) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = 2 * q;
+  if (i0 >= n) return;
+  if (error_pending(err)) return;
+  if (step_ptr) step = *step_ptr;
+  float nz[2] = {0.f, 0.f};
+  if (injected) {
+    nz[0] = injected[i0];
+    if (i0 + 1 < n) nz[1] = injected[i0 + 1];
+  } else if (std_dev != 0.0) {
+    double z0, z1;
+    normal_pair(seed, step, (uint64_t)q, z0, z1);
+    nz[0] = (float)(z0 * std_dev);
+    nz[1] = (float)(z1 * std_dev);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int64_t i = i0 + k;
+    if (i >= n) break;
+    const float noised = (injected || std_dev != 0.0) ? __fadd_rn(summed[i], nz[k]) : summed[i];
+    const float g = __fmul_rn(noised, inv_e);
+    params[i] = __fsub_rn(params[i], __fmul_rn(g, lr));
+    if (grad) grad[i] = g;
+  }
+}
+
+void launch_noise_update(dpg_ctx* ctx, float* params, const float* summed, float* grad, int64_t n,
+                         double sigma, double c, double expected_batch, double lr, uint64_t seed,
+                         uint64_t step, const float* injected, const uint64_t* step_ptr) {
+  if (n == 0) return;
+  const double std_dev = sigma * c;
+  const float denom = (float)expected_batch;
+  const float inv_e = 1.0f / denom;  // T(1) / denom (optimizer.hpp:259, 264)
+  const int64_t pairs = (n + 1) / 2;
+  noise_update_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, ctx->stream>>>(
+      params, summed, grad, n, std_dev, inv_e, (float)lr, seed, step, injected, step_ptr, ctx->dev_err);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+__global__ void gaussian_kernel(float* __restrict__ out, int64_t n, double std_dev, uint64_t seed,
+                                uint64_t step) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = 2 * q;
+  if (i0 >= n) return;
+  double z0, z1;
+  normal_pair(seed, step, (uint64_t)q, z0, z1);
+  out[i0] = (float)(z0 * std_dev);
+  if (i0 + 1 < n) out[i0 + 1] = (float)(z1 * std_dev);
+}
+
+void launch_gaussian(dpg_ctx* ctx, float* out, int64_t n, double std_dev, uint64_t seed,
+                     uint64_t step) {
+  if (n == 0) return;
+  if (std_dev == 0.0) {
+    DPG_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)n, ctx->stream));
+    return;
+  }
+  const int64_t pairs = (n + 1) / 2;
+  gaussian_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, ctx->stream>>>(out, n, std_dev, seed, step);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace dpg

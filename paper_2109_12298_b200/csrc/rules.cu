@@ -1,0 +1,390 @@
+// rules.cu — per-sample gradient kernels (north-star subsystem 1) with the per-sample squared
+// norm fused into their epilogues (subsystem 2).
+//
+//   linear  : per_sample_rule_linear   (grad_sample.hpp:53-59, tensor.hpp:303-338)
+//   conv2d  : per_sample_rule_conv2d   (grad_sample.hpp:135-150) with implicit im2col
+//   bias    : sum_middle               (tensor.hpp:188-207), double accumulator
+//   embedding: per_sample_rule_embedding (grad_sample.hpp:64-82), per-sample sorted token lists
+//
+// Norm partials go to a [rows, b] double slab (one row per output tile); clip_factors sums the
+// rows in parameter order (optimizer.hpp:67-89).
+#include "conv_common.cuh"
+#include "igemm.cuh"
+
+namespace dpg {
+
+// ------------------------------------------------------------------------------------------
+// Linear, mid == 1: G[n, o, i] = B[n, o] * A[n, i] — a single fp32 product per element, the
+// same value the reference stores (0 + b*a), so this path is bit-exact. Pure store-bound:
+// 128-bit streaming stores, norm accumulated in double from the stored values.
+// ------------------------------------------------------------------------------------------
+constexpr int kOuterChunk = 8192;  // elements of one sample's G per CTA
+
+__global__ void __launch_bounds__(256) gs_linear_outer_kernel(const float* __restrict__ acts,
+                                                              int acts_relu,
+                                                              const float* __restrict__ hw,
+                                                              int64_t d, int64_t r,
+                                                              float* __restrict__ gw,
+                                                              double* __restrict__ sq_part,
+                                                              int64_t b) {
+  const int n = blockIdx.y;
+  const int64_t total = r * d;
+  const int64_t c0 = (int64_t)blockIdx.x * kOuterChunk;
+  const int64_t c1 = c0 + kOuterChunk < total ? c0 + kOuterChunk : total;
+  const float* a = acts + (int64_t)n * d;
+  const float* bb = hw + (int64_t)n * r;
+  float* g = gw ? gw + (int64_t)n * total : nullptr;
+  double sq = 0.0;
+  if ((d & 3) == 0) {
+    for (int64_t e = c0 + 4 * threadIdx.x; e < c1; e += 4 * 256) {
+      const int64_t o = e / d, i = e - o * d;
+      const float bv = __ldg(bb + o);
+      float4 av = __ldg(reinterpret_cast<const float4*>(a + i));
+      av.x = relu_if(av.x, acts_relu); av.y = relu_if(av.y, acts_relu);
+      av.z = relu_if(av.z, acts_relu); av.w = relu_if(av.w, acts_relu);
+      const float4 v = make_float4(bv * av.x, bv * av.y, bv * av.z, bv * av.w);
+      if (g) st_stream4(g + e, v);
+      sq += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+    }
+  } else {
+    for (int64_t e = c0 + threadIdx.x; e < c1; e += 256) {
+      const int64_t o = e / d, i = e - o * d;
+      const float v = __ldg(bb + o) * relu_if(__ldg(a + i), acts_relu);
+      if (g) st_stream(g + e, v);
+      sq += (double)v * v;
+    }
+  }
+  __shared__ double red[8];
+  const double t = block_sum<256>(sq, red);
+  if (threadIdx.x == 0 && sq_part) sq_part[(int64_t)blockIdx.x * b + n] = t;
+}
+
+// Linear, mid > 1 (cfg2, T = 64): per-sample GEMM G[n] = B[n]^T A[n], M = r, N = d, K = mid.
+struct GsLinearProb {
+  static constexpr bool kAMajorM = true;   // hw[n, t, o]: contiguous along o (= m)
+  static constexpr bool kBMajorN = true;   // acts[n, t, i]: contiguous along i (= n)
+  static constexpr bool kExact = false;
+  const float* acts;
+  const float* hw;
+  float* gw;
+  double* sq_part;
+  int acts_relu;
+  int64_t M, N, K, bsz;
+  __device__ float init(int, int64_t, int64_t) const { return 0.f; }
+  __device__ float a(int z, int64_t m, int64_t k) const { return __ldg(hw + ((int64_t)z * K + k) * M + m); }
+  __device__ float b(int z, int64_t k, int64_t n) const {
+    return relu_if(__ldg(acts + ((int64_t)z * K + k) * N + n), acts_relu);
+  }
+  template <int TM, int TN>
+  __device__ void epilogue(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
+    double sq = 0.0;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+        if (m < M && n < N) {
+          if (gw) st_stream(gw + ((int64_t)z * M + m) * N + n, acc[i][j]);
+          sq += (double)acc[i][j] * acc[i][j];
+        }
+      }
+    tile_sq_store<TM, TN>(sq, sq_part, bsz, z);
+  }
+};
+
+constexpr int kLinBM = 64, kLinBN = 64, kLinBK = 16;
+
+int sq_rows_linear(int64_t mid, int64_t d, int64_t r) {
+  if (mid == 1) return (int)((r * d + kOuterChunk - 1) / kOuterChunk);
+  return (int)(((r + kLinBM - 1) / kLinBM) * ((d + kLinBN - 1) / kLinBN));
+}
+
+void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw, int64_t b,
+                      int64_t mid, int64_t d, int64_t r, float* gw, double* sq_part) {
+  if (b == 0) return;
+  if (mid == 1) {
+    dim3 grid((unsigned)((r * d + kOuterChunk - 1) / kOuterChunk), (unsigned)b);
+    gs_linear_outer_kernel<<<grid, 256, 0, ctx->stream>>>(acts, acts_relu, hw, d, r, gw, sq_part, b);
+    DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
+  GsLinearProb p{acts, hw, gw, sq_part, acts_relu, r, d, mid, b};
+  launch_igemm<kLinBM, kLinBN, kLinBK>(ctx, p, b);
+}
+
+// ------------------------------------------------------------------------------------------
+// Conv2d: G[n, oc, k] = sum_p B[n, oc, p] * X~[n, k, p], X~ = im2col(x) gathered on the fly
+// (layers.hpp:290-324 index map: k = (c*kh + ki)*kw + kj, p = oy*ow + ox).
+// ------------------------------------------------------------------------------------------
+struct GsConvProb {
+  static constexpr bool kAMajorM = false;  // hw[n, oc, p]: contiguous along p (= k)
+  static constexpr bool kBMajorN = false;  // X~[n, kcol, p]: walk p fastest
+  static constexpr bool kExact = false;
+  Im2col xc;
+  const float* hw;
+  float* gw;
+  double* sq_part;
+  int64_t M, N, K, bsz;  // M = oc, N = ic*kh*kw, K = P
+  __device__ float init(int, int64_t, int64_t) const { return 0.f; }
+  __device__ float a(int z, int64_t m, int64_t k) const { return __ldg(hw + ((int64_t)z * M + m) * K + k); }
+  __device__ float b(int z, int64_t k, int64_t n) const { return xc((int64_t)z, (int)n, (int)k); }
+  template <int TM, int TN>
+  __device__ void epilogue(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
+    double sq = 0.0;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+        if (m < M && n < N) {
+          if (gw) st_stream(gw + ((int64_t)z * M + m) * N + n, acc[i][j]);
+          sq += (double)acc[i][j] * acc[i][j];
+        }
+      }
+    tile_sq_store<TM, TN>(sq, sq_part, bsz, z);
+  }
+};
+
+static void conv_tiles(const ConvGeom& g, int& bm, int& bn) {
+  bm = g.oc <= 32 ? 32 : 64;
+  bn = g.K() <= 32 ? 32 : 64;
+}
+
+int sq_rows_conv2d(const ConvGeom& g) {
+  int bm, bn;
+  conv_tiles(g, bm, bn);
+  return (int)(((g.oc + bm - 1) / bm) * ((g.K() + bn - 1) / bn));
+}
+
+void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& g,
+                      float* gw, double* sq_part) {
+  if (g.b == 0) return;
+  GsConvProb p{make_im2col(x, x_relu, g), hw, gw, sq_part, g.oc, g.K(), g.P(), g.b};
+  int bm, bn;
+  conv_tiles(g, bm, bn);
+  if (bm == 32 && bn == 32) launch_igemm<32, 32, 16>(ctx, p, g.b);
+  else if (bm == 32) launch_igemm<32, 64, 16>(ctx, p, g.b);
+  else if (bn == 32) launch_igemm<64, 32, 16>(ctx, p, g.b);
+  else launch_igemm<64, 64, 16>(ctx, p, g.b);
+}
+
+// ------------------------------------------------------------------------------------------
+// Bias: gb[n, o] = (float) sum_mid (double) hw — sequential in the middle index, as
+// sum_middle does (tensor.hpp:197-205). One CTA per sample; norm partial = one row.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gs_bias_kernel(const float* __restrict__ hw, int64_t mid,
+                                                      int64_t r, int conv_layout,
+                                                      float* __restrict__ gb,
+                                                      double* __restrict__ sq_part, int64_t b) {
+  const int64_t n = blockIdx.x;
+  double sq = 0.0;
+  for (int64_t o = threadIdx.x; o < r; o += 256) {
+    double acc = 0.0;
+    if (conv_layout) {
+      const float* row = hw + (n * r + o) * mid;
+      for (int64_t m = 0; m < mid; ++m) acc += (double)__ldg(row + m);
+    } else {
+      const float* base = hw + n * mid * r + o;
+      for (int64_t m = 0; m < mid; ++m) acc += (double)__ldg(base + m * r);
+    }
+    const float v = (float)acc;
+    if (gb) gb[n * r + o] = v;
+    sq += (double)v * v;
+  }
+  __shared__ double red[8];
+  const double t = block_sum<256>(sq, red);
+  if (threadIdx.x == 0 && sq_part) sq_part[n] = t;
+}
+
+void launch_gs_bias(dpg_ctx* ctx, const float* hw, int64_t b, int64_t mid, int64_t r,
+                    bool hw_layout_conv, float* gb, double* sq_part) {
+  if (b == 0) return;
+  gs_bias_kernel<<<(unsigned)b, 256, 0, ctx->stream>>>(hw, mid, r, hw_layout_conv ? 1 : 0, gb, sq_part, b);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// ------------------------------------------------------------------------------------------
+// Embedding. Step 1: per-sample stable sort of the token ids (key = v * 2^32 + s), validating
+// each id as require_integral_index does (layers.hpp:368-376). Invalid ids report
+// (stage EMBED_INDEX, sample-major position n*t+s) and are clamped to 0.
+// ------------------------------------------------------------------------------------------
+constexpr int kSortThreads = 512;
+constexpr int kMaxTokens = 4096;
+
+__global__ void __launch_bounds__(kSortThreads) embed_sort_kernel(const float* __restrict__ idx,
+                                                                  int64_t t, int64_t vocab,
+                                                                  int32_t* __restrict__ sorted_v,
+                                                                  int32_t* __restrict__ sorted_s,
+                                                                  DeviceErr* err) {
+  __shared__ unsigned long long keys[kMaxTokens];
+  const int64_t n = blockIdx.x;
+  int p2 = 1;
+  while (p2 < t) p2 <<= 1;
+  for (int s = threadIdx.x; s < p2; s += kSortThreads) {
+    unsigned long long key = ~0ull;
+    if (s < t) {
+      const float raw = __ldg(idx + n * t + s);
+      const double v = (double)raw;
+      uint32_t vi = 0;
+      if (!(v >= 0.0) || v != floor(v) || v >= (double)vocab) {
+        report_error(err, err_key(ERR_STAGE_EMBED_INDEX, 0, (uint64_t)(n * t + s)),
+                     (uint64_t)__float_as_uint(raw));
+      } else {
+        vi = (uint32_t)v;
+      }
+      key = ((unsigned long long)vi << 32) | (unsigned long long)s;
+    }
+    keys[s] = key;
+  }
+  __syncthreads();
+  // bitonic sort, ascending
+  for (int k = 2; k <= p2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < p2; i += kSortThreads) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = keys[i], c = keys[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > c) == up) {
+            keys[i] = c;
+            keys[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int s = threadIdx.x; s < t; s += kSortThreads) {
+    sorted_v[n * t + s] = (int32_t)(keys[s] >> 32);
+    sorted_s[n * t + s] = (int32_t)(keys[s] & 0xFFFFFFFFull);
+  }
+}
+
+void launch_embed_sort(dpg_ctx* ctx, const float* idx, int64_t b, int64_t t, int64_t vocab,
+                       int32_t* sorted_v, int32_t* sorted_s) {
+  if (t > kMaxTokens) raise(DPG_ERR_DIMENSION, "embedding: at most 4096 tokens per sample on device");
+  if (b == 0 || t == 0) return;
+  embed_sort_kernel<<<(unsigned)b, kSortThreads, 0, ctx->stream>>>(idx, t, vocab, sorted_v, sorted_s, ctx->dev_err);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Step 2 (dense): each CTA writes kEmbRows full rows of one sample's [vocab, dim] gradient —
+// the row sum over its (ascending-s) duplicates, zeros elsewhere — in one streaming pass.
+constexpr int kEmbRows = 64;
+
+__global__ void __launch_bounds__(256) gs_embedding_dense_kernel(
+    const int32_t* __restrict__ sorted_v, const int32_t* __restrict__ sorted_s,
+    const float* __restrict__ hw, int64_t t, int64_t vocab, int64_t dim, float* __restrict__ g,
+    double* __restrict__ sq_part, int64_t b) {
+  extern __shared__ int32_t sv[];
+  const int64_t n = blockIdx.y;
+  const int64_t v0 = (int64_t)blockIdx.x * kEmbRows;
+  for (int s = threadIdx.x; s < t; s += 256) sv[s] = sorted_v[n * t + s];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t* ss = sorted_s + n * t;
+  const float* hwn = hw + n * t * dim;
+  double sq = 0.0;
+  for (int64_t v = v0 + warp; v < v0 + kEmbRows && v < vocab; v += 8) {
+    const int lo = lower_bound_i32(sv, (int)t, (int32_t)v);
+    int hi = lo;
+    while (hi < t && sv[hi] == v) ++hi;
+    float* row = g + (n * vocab + v) * dim;
+    if ((dim & 3) == 0) {
+      for (int64_t d0 = 4 * lane; d0 < dim; d0 += 128) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = lo; j < hi; ++j) {
+          const float4 h = __ldg(reinterpret_cast<const float4*>(hwn + (int64_t)ss[j] * dim + d0));
+          acc.x += h.x; acc.y += h.y; acc.z += h.z; acc.w += h.w;
+        }
+        st_stream4(row + d0, acc);
+        sq += (double)acc.x * acc.x + (double)acc.y * acc.y + (double)acc.z * acc.z + (double)acc.w * acc.w;
+      }
+    } else {
+      for (int64_t d0 = lane; d0 < dim; d0 += 32) {
+        float acc = 0.f;
+        for (int j = lo; j < hi; ++j) acc += __ldg(hwn + (int64_t)ss[j] * dim + d0);
+        st_stream(row + d0, acc);
+        sq += (double)acc * acc;
+      }
+    }
+  }
+  __shared__ double red[8];
+  const double tot = block_sum<256>(sq, red);
+  if (threadIdx.x == 0 && sq_part) sq_part[(int64_t)blockIdx.x * b + n] = tot;
+}
+
+// Step 2 (sparse): norms only — one CTA per sample walks its unique ids.
+__global__ void __launch_bounds__(256) gs_embedding_sq_kernel(
+    const int32_t* __restrict__ sorted_v, const int32_t* __restrict__ sorted_s,
+    const float* __restrict__ hw, int64_t t, int64_t dim, double* __restrict__ sq_part) {
+  const int64_t n = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t* sv = sorted_v + n * t;
+  const int32_t* ss = sorted_s + n * t;
+  const float* hwn = hw + n * t * dim;
+  double sq = 0.0;
+  for (int64_t j0 = warp; j0 < t; j0 += 8) {
+    if (j0 > 0 && sv[j0] == sv[j0 - 1]) continue;  // not a segment start
+    int64_t hi = j0;
+    while (hi < t && sv[hi] == sv[j0]) ++hi;
+    for (int64_t d0 = lane; d0 < dim; d0 += 32) {
+      float acc = 0.f;
+      for (int64_t j = j0; j < hi; ++j) acc += __ldg(hwn + (int64_t)ss[j] * dim + d0);
+      sq += (double)acc * acc;
+    }
+  }
+  __shared__ double red[8];
+  const double tot = block_sum<256>(sq, red);
+  if (threadIdx.x == 0) sq_part[n] = tot;
+}
+
+int sq_rows_embedding(int64_t vocab, int64_t dim) {
+  (void)dim;
+  return (int)((vocab + kEmbRows - 1) / kEmbRows);
+}
+
+void launch_gs_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* sorted_s,
+                         const float* hw, int64_t b, int64_t t, int64_t vocab, int64_t dim,
+                         float* g, double* sq_part) {
+  if (b == 0) return;
+  if (g) {
+    dim3 grid((unsigned)((vocab + kEmbRows - 1) / kEmbRows), (unsigned)b);
+    gs_embedding_dense_kernel<<<grid, 256, sizeof(int32_t) * t, ctx->stream>>>(
+        sorted_v, sorted_s, hw, t, vocab, dim, g, sq_part, b);
+  } else {
+    // sparse mode: the norm lands in the first row; the remaining rows are zero-filled so the
+    // slab layout does not depend on the mode
+    const int rows = sq_rows_embedding(vocab, dim);
+    if (rows > 1) DPG_CUDA(cudaMemsetAsync(sq_part + b, 0, sizeof(double) * (size_t)(rows - 1) * b, ctx->stream));
+    gs_embedding_sq_kernel<<<(unsigned)b, 256, 0, ctx->stream>>>(sorted_v, sorted_s, hw, t, dim, sq_part);
+  }
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// ------------------------------------------------------------------------------------------
+__global__ void sq_reduce_kernel(const double* __restrict__ part, int rows, int64_t b,
+                                 double* __restrict__ out) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= b) return;
+  double acc = 0.0;
+  for (int r = 0; r < rows; ++r) acc += part[(int64_t)r * b + n];
+  out[n] = acc;
+}
+
+void launch_sq_reduce(dpg_ctx* ctx, const double* part, int rows, int64_t b, double* out) {
+  if (b == 0) return;
+  sq_reduce_kernel<<<(unsigned)((b + 255) / 256), 256, 0, ctx->stream>>>(part, rows, b, out);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace dpg
