@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""bench.py — DP-SGD step throughput of the B200 path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+One "step" is one full DP-SGD step (forward, per-sample gradients with fused norms, clip factors,
+clipped sum, [NCCL all-reduce], noise + SGD update) over one synthetic batch, replayed from a
+CUDA graph. N=1 runs BASELINE configs[2] (CIFAR-10 4-layer CNN, batch 512); N>1 (torchrun, one
+rank per GPU) shards by sample with 512 samples per rank (weak scaling; N=8 is configs[4]'s
+global batch 4096) and one all-reduce of the clipped sum per step.
+
+Reported (rank 0 prints ONE JSON line):
+  value        samples/s over all ranks, inputs resident in HBM, device time (CUDA events on the
+               launching stream), L2 flushed (256 MiB write) before every timed step, max over ranks
+  e2e          the same metric through dpg_train_step_host with pinned HOST buffers: H2D of the
+               batch and D2H of the per-sample loss inside the timed region
+  roofline     dominant stage of an eager profiled pass: algorithmic bytes / its CUDA-event
+               duration vs the measured HBM peak; plus the whole-step fraction
+  cpu_baseline the reference compiled from its own sources (oracle/_ref, -O3), sample-sharded
+               over all host cores, timed on this box (rank 0, N=1 only)
+  --impl reference: the reference CPU path alone (rank 0), same metric / config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DP-SGD step samples/sec (CIFAR-10 CNN, B=512)"
+HBM_FALLBACK = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cifar_b512")
+    ap.add_argument("--sigma", type=float, default=1.0)
+    ap.add_argument("--max-grad-norm", type=float, default=1.0)
+    ap.add_argument("--no-materialise", action="store_true",
+                    help="norms without storing the GradSampleRecord (not the headline)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return HBM_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------------------ synthetic data
+def synth(workload, b, seed_params=1, seed_data=2):
+    """Random-init weights of the workload's architecture (U(+-1/sqrt(fan_in)), N(0,1) tables,
+    as build_model does) and a synthetic batch; numpy only, no oracle involved."""
+    import numpy as np
+    from paper_2109_12298_b200.configs import CONV2D, EMBEDDING, LINEAR, param_count
+    rng = np.random.default_rng(seed_params)
+    ps = []
+    for l in workload.layers:
+        if l.kind == LINEAR:
+            k = 1 / np.sqrt(l.in_features)
+            ps.append(rng.uniform(-k, k, l.out_features * l.in_features))
+            if l.has_bias:
+                ps.append(rng.uniform(-k, k, l.out_features))
+        elif l.kind == CONV2D:
+            k = 1 / np.sqrt(l.in_channels * l.kernel_h * l.kernel_w)
+            ps.append(rng.uniform(-k, k, l.out_channels * l.in_channels * l.kernel_h * l.kernel_w))
+            if l.has_bias:
+                ps.append(rng.uniform(-k, k, l.out_channels))
+        elif l.kind == EMBEDDING:
+            ps.append(rng.standard_normal(l.vocab_size * l.embedding_dim))
+    params = np.concatenate(ps).astype(np.float32)
+    assert params.size == param_count(workload.layers)
+    drng = np.random.default_rng(seed_data)
+    if workload.tokens:
+        x = drng.integers(0, workload.tokens, size=(b,) + workload.in_shape).astype(np.float32)
+    else:
+        x = drng.standard_normal((b,) + workload.in_shape).astype(np.float32)
+    y = drng.integers(0, workload.classes, size=b).astype(np.float32)
+    return params, x, y
+
+
+def step_bytes(workload, b, materialise=True):
+    """B_hot = 4[sum(|X_l| + |Y_l|) + b L + 4 L];
+    B_full = B_hot + forward sum 4(|X_l| + |Y_l|) + backward sum_{l>0} 4(|Y_l| + 2|X_l|)."""
+    from paper_2109_12298_b200.configs import CONV2D, EMBEDDING, FLATTEN, LINEAR, param_count
+    L = param_count(workload.layers)
+    shape = list(workload.in_shape)
+    xs, ys = [], []
+    for l in workload.layers:
+        n_in = 1
+        for e in shape:
+            n_in *= e
+        if l.kind == LINEAR:
+            shape[-1] = l.out_features
+        elif l.kind == CONV2D:
+            oh = (shape[1] + 2 * l.padding - l.kernel_h) // l.stride + 1
+            ow = (shape[2] + 2 * l.padding - l.kernel_w) // l.stride + 1
+            shape = [l.out_channels, oh, ow]
+        elif l.kind == EMBEDDING:
+            shape = [shape[0], l.embedding_dim]
+        elif l.kind == FLATTEN:
+            shape = [n_in]
+        else:
+            continue
+        if l.kind in (LINEAR, CONV2D, EMBEDDING):
+            n_out = 1
+            for e in shape:
+                n_out *= e
+            xs.append(b * n_in)
+            ys.append(b * n_out)
+    hot = 4 * (sum(xs) + sum(ys) + (b * L if materialise else 0) + 4 * L)
+    fwd = 4 * (sum(xs) + sum(ys))
+    bwd = 4 * sum(ys[i] + 2 * xs[i] for i in range(1, len(xs)))
+    return hot, hot + fwd + bwd
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ reference arm
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_sample_step(workload, b_sample, nthreads, fast=True):
+    """One DP-SGD step of the reference over b_sample samples of the workload; returns seconds
+    and the kind used. oracle/_ref (the reference built from its sources) when present."""
+    import numpy as np
+    import oracle
+    params, x, y = synth(workload, b_sample)
+    if oracle.reference_available(fast=fast):
+        ref = oracle.reference(fast=fast)
+        t0 = time.perf_counter()
+        ref.dpsgd_step_threads(workload.layers, workload.in_shape, params, x, y, 1.0, 1.0, 0.1,
+                               float(b_sample), 3, nthreads)
+        return time.perf_counter() - t0, "reference", nthreads
+    r = oracle.restatement()
+    t0 = time.perf_counter()
+    r.dpsgd_step(workload.layers, workload.in_shape, params, x, y, 1.0, 1.0, 0.1, float(b_sample),
+                 want_record=False)
+    return time.perf_counter() - t0, "port", 1
+
+
+def pick_sample(workload, nthreads, budget_s):
+    """Largest sample (multiple of nthreads, <= workload batch) whose step fits budget_s."""
+    b = max(nthreads, 8)
+    t, kind, cores = reference_sample_step(workload, b, nthreads)
+    per_sample = t / b
+    want = int(budget_s / max(per_sample, 1e-9))
+    want = max(b, min(workload.batch, want))
+    want -= want % max(1, min(nthreads, want))
+    return max(b, want), kind, cores
+
+
+def cpu_baseline(workload, budget_s=15.0):
+    nthreads = cpu_threads()
+    b, kind, cores = pick_sample(workload, nthreads, budget_s / 3)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while True:
+        t, kind, cores = reference_sample_step(workload, b, nthreads)
+        times.append(t)
+        if time.perf_counter() > t_end or len(times) >= 10:
+            break
+    med = statistics.median(times)
+    return {"value": b / med, "unit": "samples/s", "cores": cores, "kind": kind,
+            "sample": f"{workload.name}: full DP-SGD step of the reference over {b} samples, "
+                      f"median of {len(times)} steps, {'-O3 -march=x86-64-v3 ' if kind == 'reference' else ''}"
+                      f"{cores} host threads (sample-sharded, virtual-step semantics)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2109_12298_b200.configs import WORKLOADS
+    w = WORKLOADS[args.workload]
+    nthreads = cpu_threads()
+    # size each step so warmup + steps finish in about two minutes
+    b, kind, cores = pick_sample(w, nthreads, 120.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        reference_sample_step(w, b, nthreads)
+    total = 0.0
+    for _ in range(args.steps):
+        t, kind, cores = reference_sample_step(w, b, nthreads)
+        total += t
+    value = b * args.steps / total
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": w.name, "global_batch": w.batch * args.gpus, "per_step_sample": b},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
+                         "sample": f"{b} samples of {w.name} per step, {cores} host threads"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if world > 1 or args.gpus > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        return
+
+    import numpy as np
+    import torch
+    from paper_2109_12298_b200 import dpg
+    from paper_2109_12298_b200.configs import WORKLOADS
+
+    torch.cuda.set_device(local)
+    ctx = dpg.Context(local)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [dpg.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.init_comm(world, rank, obj[0])
+
+    w = WORKLOADS[args.workload]
+    b = w.batch
+    gb = b * world
+    params, _, _ = synth(w, b)
+    _, x, y = synth(w, b, seed_data=2 + rank)
+    model = dpg.Model(ctx, w.layers, w.in_shape, max_batch=b)
+    model.load_params(params)
+    materialise = not args.no_materialise
+    opt = dpg.DpOptimizer(model, noise_multiplier=args.sigma, max_grad_norm=args.max_grad_norm,
+                          learning_rate=0.1, expected_batch_size=float(gb), noise_seed=3,
+                          materialise_grad_sample=materialise)
+    xt = torch.from_numpy(x).cuda()
+    yt = torch.from_numpy(y).cuda()
+    loss = torch.zeros(b, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warmup (graph capture happens on the first step) ----
+    for _ in range(max(3, args.warmup)):
+        opt.train_step(xt, yt, loss)
+    ctx.sync()
+    t_soak = time.perf_counter() + 0.5  # bring SM clocks up before the timed region
+    while time.perf_counter() < t_soak:
+        opt.train_step(xt, yt, loss)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, per-step CUDA events, L2 flushed before each step ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.kernel_launches
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        opt.train_step(xt, yt, loss)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    gpu_launches = ctx.kernel_launches - launches0
+    ctx.sync()  # surfaces any device-side error
+    step_ms = [a.elapsed_time(c) for a, c in evs]
+    total_ms = max_over_ranks(sum(step_ms))
+    value = gb * args.steps / (total_ms / 1000.0)
+
+    # ---- end to end: pinned host buffers through dpg_train_step_host ----
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.from_numpy(y).pin_memory()
+    lh = torch.zeros(b).pin_memory()
+    for _ in range(3):
+        opt.train_step_host(xh, yh, lh)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        opt.train_step_host(xh, yh, lh)
+    t1 = time.perf_counter()
+    e2e_s = max_over_ranks(t1 - t0)
+    e2e = {"value": gb * args.steps / e2e_s, "unit": "samples/s",
+           "h2d_bytes_per_step": int(x.nbytes + y.nbytes) * world,
+           "d2h_bytes_per_step": int(lh.numel() * 4) * world}
+
+    # ---- roofline: eager profiled pass, per-stage CUDA events on the launching stream ----
+    ctx.set_profiling(True)
+    for _ in range(args.profile_steps):
+        flush.zero_()
+        opt.train_step(xt, yt, loss, use_graph=False)
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    hbm, peak_src = peaks()
+    stages = {k: {"ms": v["ms"] / v["count"], "gbs": (v["bytes"] / v["count"]) / (v["ms"] / v["count"] * 1e6),
+                  "tflops": (v["flops"] / v["count"]) / (v["ms"] / v["count"] * 1e9)}
+              for k, v in prof.items() if v["count"]}
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    d = prof[dom]
+    dom_ms = d["ms"] / d["count"]
+    achieved = (d["bytes"] / d["count"]) / (dom_ms * 1e6)  # GB/s
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(dom)
+    hot, full = step_bytes(w, b, materialise)
+    eager_step_ms = sum(v["ms"] for v in prof.values()) / args.profile_steps
+    ms_per_step = total_ms / args.steps
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic,
+                "algorithmic_bytes_per_launch": d["bytes"] / d["count"], "launch_ms": dom_ms,
+                "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured" else "fallback",
+                "step": {"bytes_full": full, "bytes_hot": hot,
+                         "frac_full": full / (ms_per_step * 1e6) / hbm,
+                         "floor_ms_full": full / (hbm * 1e6)},
+                "stages_ms": {k: round(v["ms"], 5) for k, v in sorted(stages.items(), key=lambda kv: -kv[1]["ms"])},
+                "eager_stage_sum_ms": eager_step_ms}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": w.name, "global_batch": gb, "per_rank_batch": b,
+                   "parallelism": f"dp{world} (sample shards, 1 NCCL all-reduce of the clipped sum)",
+                   "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
+                   "materialise_grad_sample": materialise, "graph": True,
+                   "l2": "256 MiB flush before every timed step (outside the step's events)"},
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": gpu_launches,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    barrier()
+
+
+if __name__ == "__main__":
+    main()
