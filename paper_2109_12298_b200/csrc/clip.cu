@@ -149,6 +149,7 @@ struct CsLinearProb : SplitKStore {
 
 size_t clipped_sum_ws_linear(int64_t b, int64_t mid, int64_t d, int64_t r) {
   if (mid == 1) return 0;
+  if (use_tc()) return sizeof(float) * (size_t)tc::csum_linear_splits(b, mid, d, r) * (size_t)(r * d);
   const int64_t tiles = ((r + 63) / 64) * ((d + 63) / 64);
   const int splits = pick_splits(b, tiles, mid);
   return sizeof(float) * (size_t)splits * (size_t)(r * d);
@@ -163,6 +164,12 @@ void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, c
     clipped_sum_linear_outer_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
         acts, acts_relu, hw, scale, b, d, r, sw, accumulate);
     DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
+  if (use_tc()) {
+    const int splits = tc::csum_linear_splits(b, mid, d, r);
+    tc::linear_csum(ctx, acts, acts_relu, hw, scale, b, mid, d, r, static_cast<float*>(ws), splits);
+    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, r * d, sw, accumulate);
     return;
   }
   const int64_t tiles = ((r + 63) / 64) * ((d + 63) / 64);
@@ -221,6 +228,7 @@ static void cs_conv_tiles(const ConvGeom& g, int& bm, int& bn) {
 }
 
 size_t clipped_sum_ws_conv2d(const ConvGeom& g) {
+  if (use_tc()) return sizeof(float) * (size_t)tc::csum_conv_splits(g) * (size_t)(g.oc * g.K());
   int bm, bn;
   cs_conv_tiles(g, bm, bn);
   const int64_t tiles = ((g.oc + bm - 1) / bm) * ((g.K() + bn - 1) / bn);
@@ -232,6 +240,12 @@ void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const f
                                const float* scale, const ConvGeom& g, float* sw, float* sb,
                                int accumulate, void* ws) {
   (void)sb;
+  if (use_tc()) {
+    const int splits = tc::csum_conv_splits(g);
+    tc::conv_csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
+    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, g.oc * g.K(), sw, accumulate);
+    return;
+  }
   int bm, bn;
   cs_conv_tiles(g, bm, bn);
   const int64_t tiles = ((g.oc + bm - 1) / bm) * ((g.K() + bn - 1) / bn);

@@ -1,11 +1,20 @@
 // ctx.cpp — dpg_ctx: stream, device error record, workspace, NCCL communicator.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
 #include "dpg_internal.h"
 
 namespace dpg {
+
+bool use_tc() {
+  static const bool on = [] {
+    const char* e = std::getenv("DPG_SIMT");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
 
 std::string& thread_err() {
   static thread_local std::string s;

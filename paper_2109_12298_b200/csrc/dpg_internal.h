@@ -155,6 +155,29 @@ struct ConvGeom {
   int64_t P() const { return oh * ow; }
 };
 
+// Kernel family selection: tcgen05 (default) or the SIMT implicit-GEMM path (DPG_SIMT=1,
+// kept for A/B measurements). Read once per process.
+bool use_tc();
+
+namespace tc {
+void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
+              const ConvGeom& cg, float* y);
+void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& cg,
+                const float* mask_src, float* dx);
+int gs_conv_rows(const ConvGeom& cg);
+void conv_gs(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& cg,
+             float* gw, double* sq_part);
+int csum_conv_splits(const ConvGeom& cg);
+void conv_csum(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const float* scale,
+               const ConvGeom& cg, float* part, int splits);
+int gs_linear_rows(int64_t d, int64_t r);
+void linear_gs(dpg_ctx* ctx, const float* acts, int relu, const float* hw, int64_t b, int64_t mid,
+               int64_t d, int64_t r, float* gw, double* sq_part);
+int csum_linear_splits(int64_t b, int64_t mid, int64_t d, int64_t r);
+void linear_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, const float* scale,
+                 int64_t b, int64_t mid, int64_t d, int64_t r, float* part, int splits);
+}  // namespace tc
+
 // rules.cu — per-sample gradients
 int sq_rows_linear(int64_t mid, int64_t d, int64_t r);
 int sq_rows_conv2d(const ConvGeom& g);

@@ -46,6 +46,10 @@ struct ConvFwdProb {
 void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
                        const ConvGeom& g, float* y) {
   if (g.b == 0) return;
+  if (use_tc()) {
+    tc::conv_fwd(ctx, x, x_relu, w, bias, g, y);
+    return;
+  }
   ConvFwdProb p{make_im2col(x, x_relu, g), w, bias, y, g.oc, g.b * g.P(), g.K(), g.P()};
   if (g.oc <= 32) launch_igemm<32, 128, 16>(ctx, p, 1);
   else launch_igemm<64, 64, 16>(ctx, p, 1);
@@ -118,6 +122,10 @@ struct ConvDgradProb {
 void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
                          const float* mask_src, float* dx) {
   if (g.b == 0) return;
+  if (use_tc()) {
+    tc::conv_dgrad(ctx, dy, w, g, mask_src, dx);
+    return;
+  }
   const int s = (int)g.stride;
   for (int ry = 0; ry < s; ++ry)
     for (int rx = 0; rx < s; ++rx) {

@@ -96,6 +96,7 @@ constexpr int kLinBM = 64, kLinBN = 64, kLinBK = 16;
 
 int sq_rows_linear(int64_t mid, int64_t d, int64_t r) {
   if (mid == 1) return (int)((r * d + kOuterChunk - 1) / kOuterChunk);
+  if (use_tc()) return tc::gs_linear_rows(d, r);
   return (int)(((r + kLinBM - 1) / kLinBM) * ((d + kLinBN - 1) / kLinBN));
 }
 
@@ -106,6 +107,10 @@ void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const floa
     dim3 grid((unsigned)((r * d + kOuterChunk - 1) / kOuterChunk), (unsigned)b);
     gs_linear_outer_kernel<<<grid, 256, 0, ctx->stream>>>(acts, acts_relu, hw, d, r, gw, sq_part, b);
     DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
+  if (use_tc()) {
+    tc::linear_gs(ctx, acts, acts_relu, hw, b, mid, d, r, gw, sq_part);
     return;
   }
   GsLinearProb p{acts, hw, gw, sq_part, acts_relu, r, d, mid, b};
@@ -151,6 +156,7 @@ static void conv_tiles(const ConvGeom& g, int& bm, int& bn) {
 }
 
 int sq_rows_conv2d(const ConvGeom& g) {
+  if (use_tc()) return tc::gs_conv_rows(g);
   int bm, bn;
   conv_tiles(g, bm, bn);
   return (int)(((g.oc + bm - 1) / bm) * ((g.K() + bn - 1) / bn));
@@ -159,6 +165,10 @@ int sq_rows_conv2d(const ConvGeom& g) {
 void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& g,
                       float* gw, double* sq_part) {
   if (g.b == 0) return;
+  if (use_tc()) {
+    tc::conv_gs(ctx, x, x_relu, hw, g, gw, sq_part);
+    return;
+  }
   GsConvProb p{make_im2col(x, x_relu, g), hw, gw, sq_part, g.oc, g.K(), g.P(), g.b};
   int bm, bn;
   conv_tiles(g, bm, bn);

@@ -1,0 +1,321 @@
+// tc_gemm.cuh — tcgen05 (5th-gen tensor core) implicit GEMM, 3xTF32 fp32-faithful.
+//
+//   C[z][m][n] = sum_k A(z, m, k) * B(z, n, k)         (both operands K-major)
+//
+// Operands are gathered by all threads of the CTA through a problem-specific index map (the
+// implicit im2col of the conv contractions lives in the Prob loaders), split into a TF32 "hi"
+// part (cvt.rna) and the TF32-rounded remainder "lo", and stored into shared memory in the
+// canonical 128B-swizzled K-major UMMA layout (8 rows x 128 B atoms, 1024 B aligned). One thread
+// issues tcgen05.mma.cta_group::1.kind::tf32 with the accumulator in tensor memory:
+// acc += A_lo B_hi + A_hi B_lo + A_hi B_hi per K=8 slice (the 3xTF32 scheme; relative error
+// ~2^-21, fp32-like). Stages are double buffered: the MMA of stage s runs asynchronously while
+// the threads gather stage s+1; tcgen05.commit arrives on the stage's mbarrier to release it.
+// The epilogue reads the accumulator back with tcgen05.ld (thread t of warp w owns row
+// 32w + t of the 128-row tile) and hands each row to Prob::epilogue_row.
+//
+// Tile: BM = 128 rows (UMMA M), BN in {16, 32, 64, 128, 256} columns (UMMA N), BK = 32 fp32
+// (one 128 B swizzle row) per stage; 128 threads.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dpg_device.cuh"
+
+namespace dpg {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 32;
+constexpr int kThreads = 128;
+constexpr int kStages = 2;
+
+// ---- integer division by a runtime constant (multiply-high), valid for n < 2^31 ----
+struct FastDiv {
+  uint32_t d = 1, m = 0, s = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    if (div <= 1) { m = 0; s = 0; return; }
+    uint32_t l = 0;
+    while ((1u << l) < div) ++l;  // ceil(log2 div)
+    s = 31 + l;
+    m = (uint32_t)(((1ull << s) + div - 1) / div);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return d == 1 ? n : (uint32_t)(((uint64_t)n * m) >> s);
+  }
+  __device__ __forceinline__ void divmod(uint32_t n, uint32_t& q, uint32_t& r) const {
+    q = div(n);
+    r = n - q * d;
+  }
+};
+
+// ---- PTX wrappers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// SW128 K-major shared memory descriptor (tcgen05 matrix descriptor, sm_100 version 1):
+// start >> 4 | LBO 16 B >> 4 | SBO 1024 B >> 4 | version 1 | layout SWIZZLE_128B (2)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// Instruction descriptor kind::tf32: D f32, A/B tf32, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// 16 consecutive fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// byte offset of (row, 16 B chunk q) in a 128B-swizzled K-major tile
+__device__ __forceinline__ uint32_t sw128_off(int row, int q) {
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((q ^ (row & 7)) << 4));
+}
+
+template <int BN>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int TOTAL = kStages * STAGE + 1024 /*align*/ + 64;
+};
+
+template <int BN>
+constexpr uint32_t tmem_cols() {
+  return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+}
+
+// Store 4 values (k .. k+3 of one row) as hi / lo TF32 into the swizzled stage buffers.
+__device__ __forceinline__ void put4(uint8_t* hi, uint8_t* lo, int row, int q, float a, float b,
+                                     float c, float d) {
+  const uint32_t off = sw128_off(row, q);
+  uint4 h, l;
+  h.x = to_tf32(a); l.x = to_tf32(a - __uint_as_float(h.x));
+  h.y = to_tf32(b); l.y = to_tf32(b - __uint_as_float(h.y));
+  h.z = to_tf32(c); l.z = to_tf32(c - __uint_as_float(h.z));
+  h.w = to_tf32(d); l.w = to_tf32(d - __uint_as_float(h.w));
+  *reinterpret_cast<uint4*>(hi + off) = h;
+  *reinterpret_cast<uint4*>(lo + off) = l;
+}
+
+// Prob interface:
+//   int64_t M, N, K;                            problem sizes (K may be 0)
+//   struct RowA; RowA row_a(int z, int64_t m) const;   per-row precompute for A (m < M)
+//   float a(const RowA&, int z, int64_t k) const;       A element (k < K)
+//   struct RowB; RowB row_b(int z, int64_t n) const;    per-row precompute for B
+//   float b(const RowB&, int z, int64_t k) const;
+//   void epilogue_row(int z, int64_t m, int64_t n0, const float* v, int nv, double& sq) const;
+//   void epilogue_cta(int z, double sq) const;          after all rows (block-reduced sq)
+template <int BN, class Prob>
+__global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using S = Smem<BN>;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * S::STAGE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kStages);
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int z = blockIdx.z;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  constexpr uint32_t kCols = tmem_cols<BN>();
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // this thread's A row (and B rows) for every stage
+  const int64_t am = m0 + tid;
+  const bool a_ok = am < p.M;
+  typename Prob::RowA ra{};
+  if (a_ok) ra = p.row_a(z, am);
+  constexpr int BROWS = (BN + kThreads - 1) / kThreads;
+  typename Prob::RowB rb[BROWS];
+  bool b_ok[BROWS];
+#pragma unroll
+  for (int i = 0; i < BROWS; ++i) {
+    const int r = tid + i * kThreads;
+    const int64_t bn = n0 + r;
+    b_ok[i] = r < BN && bn < p.N;
+    if (b_ok[i]) rb[i] = p.row_b(z, bn);
+  }
+
+  const int64_t K = p.K;
+  const int nk = (int)((K + BK - 1) / BK);
+  constexpr uint32_t idesc = idesc_tf32(BN);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % kStages;
+    uint8_t* st = smem + s * S::STAGE;
+    uint8_t* a_hi = st;
+    uint8_t* a_lo = st + S::A_BYTES;
+    uint8_t* b_hi = st + 2 * S::A_BYTES;
+    uint8_t* b_lo = b_hi + S::B_BYTES;
+    if (kt >= kStages) mbar_wait(&bars[s], ((kt / kStages) - 1) & 1);
+    const int64_t k0 = (int64_t)kt * BK;
+    // gather A row `tid`: 32 consecutive k
+#pragma unroll
+    for (int q = 0; q < BK / 4; ++q) {
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = (a_ok && k < K) ? p.a(ra, z, k) : 0.f;
+      }
+      put4(a_hi, a_lo, tid, q, v[0], v[1], v[2], v[3]);
+    }
+#pragma unroll
+    for (int i = 0; i < BROWS; ++i) {
+      const int r = tid + i * kThreads;
+      if (r < BN) {
+#pragma unroll
+        for (int q = 0; q < BK / 4; ++q) {
+          float v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int64_t k = k0 + 4 * q + e;
+            v[e] = (b_ok[i] && k < K) ? p.b(rb[i], z, k) : 0.f;
+          }
+          put4(b_hi, b_lo, r, q, v[0], v[1], v[2], v[3]);
+        }
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sa_hi = smem_u32(a_hi), sa_lo = smem_u32(a_lo);
+      const uint32_t sb_hi = smem_u32(b_hi), sb_lo = smem_u32(b_lo);
+#pragma unroll
+      for (int kk = 0; kk < BK / 8; ++kk) {
+        const uint32_t off = kk * 32;  // 8 tf32 = 32 B along the swizzled row
+        const uint32_t acc0 = (kt > 0 || kk > 0) ? 1u : 0u;
+        mma_tf32(tmem, sw128_desc(sa_lo + off), sw128_desc(sb_hi + off), idesc, acc0);
+        mma_tf32(tmem, sw128_desc(sa_hi + off), sw128_desc(sb_lo + off), idesc, 1u);
+        mma_tf32(tmem, sw128_desc(sa_hi + off), sw128_desc(sb_hi + off), idesc, 1u);
+      }
+      mma_commit(&bars[s]);
+    }
+  }
+  if (nk > 0) {
+    const int last = nk - 1;
+    mbar_wait(&bars[last % kStages], (last / kStages) & 1);
+  }
+  tc_fence_after();
+
+  // epilogue: warp w owns TMEM lanes [32w, 32w + 32) = tile rows
+  const int64_t m = m0 + 32 * warp + (tid & 31);
+  const bool row_ok = m < p.M;
+  double sq = 0.0;
+  float v[16];
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    if (nk > 0) {
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    }
+    const int64_t nrem = p.N - (n0 + c0);
+    const int nv = nrem >= 16 ? 16 : (nrem > 0 ? (int)nrem : 0);
+    if (row_ok && nv > 0) p.epilogue_row(z, m, n0 + c0, v, nv, sq);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+  }
+  if (Prob::kCtaReduce) {
+    __shared__ double red[kThreads / 32];
+    const double t = block_sum<kThreads>(sq, red);
+    if (tid == 0) p.epilogue_cta(z, t);
+  }
+}
+
+template <int BN, class Prob>
+void launch_tc(dpg_ctx* ctx, const Prob& p, int64_t batches) {
+  const int smem = Smem<BN>::TOTAL;
+  static bool attr = false;  // per template instance
+  if (!attr) {
+    DPG_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<BN, Prob>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)((p.M + BM - 1) / BM), (unsigned)((p.N + BN - 1) / BN), (unsigned)batches);
+  tc_gemm_kernel<BN, Prob><<<grid, kThreads, smem, ctx->stream>>>(p);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// pick the narrowest legal UMMA N that covers n (cta_group::1, M = 128: N % 16 == 0, <= 256)
+template <class Prob>
+void launch_tc_auto(dpg_ctx* ctx, const Prob& p, int64_t batches) {
+  if (p.N <= 16) launch_tc<16>(ctx, p, batches);
+  else if (p.N <= 32) launch_tc<32>(ctx, p, batches);
+  else if (p.N <= 64) launch_tc<64>(ctx, p, batches);
+  else launch_tc<128>(ctx, p, batches);
+}
+
+}  // namespace tc
+}  // namespace dpg
