@@ -101,22 +101,82 @@ static int pick_splits(int64_t b, int64_t tiles, int64_t per_sample_k) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Linear weight, mid == 1: S[o, i] = sum_n scale_n * (B[n,o] * A[n,i]) — the reference's
-// association (acc += w * g with g = b * a rounded, optimizer.hpp:107-110), so bit-exact.
+// Weighted sums over samples with few outputs: out[j] (+)= sum_n s_n v(n, j).
+// A CTA owns 32 consecutive outputs (lanes) and splits the samples into 8 contiguous ranges, one
+// per warp; loads are batched 8 deep for memory-level parallelism and the 8 partials are
+// combined in warp order (deterministic).
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) clipped_sum_linear_outer_kernel(
-    const float* __restrict__ acts, int acts_relu, const float* __restrict__ hw,
-    const float* __restrict__ scale, int64_t b, int64_t d, int64_t r, float* __restrict__ sw,
-    int accumulate) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= r * d) return;
-  const int64_t o = e / d, i = e - o * d;
-  float acc = 0.f;
-  for (int64_t n = 0; n < b; ++n) {
-    const float g = __fmul_rn(__ldg(hw + n * r + o), relu_if(__ldg(acts + n * d + i), acts_relu));
-    acc = __fadd_rn(acc, __fmul_rn(__ldg(scale + n), g));
+struct OuterV {  // linear, mid == 1: v(n, o*d + i) = B[n, o] * A[n, i]
+  const float* acts;
+  const float* hw;
+  int64_t d, r;
+  int relu;
+  __device__ __forceinline__ float operator()(int64_t n, int64_t j) const {
+    const int64_t o = j / d, i = j - o * d;
+    return __ldg(hw + n * r + o) * relu_if(__ldg(acts + n * d + i), relu);
   }
-  sw[e] = accumulate ? __fadd_rn(sw[e], acc) : acc;
+};
+struct RecordV {  // materialised per-sample values: v(n, j) = g[n, j]
+  const float* g;
+  int64_t numel;
+  __device__ __forceinline__ float operator()(int64_t n, int64_t j) const { return __ldg(g + n * numel + j); }
+};
+
+template <class V>
+__device__ __forceinline__ void wsum_body(const V& v, const float* __restrict__ scale, int64_t b,
+                                          int64_t numel, int64_t j0, float* __restrict__ out,
+                                          int accumulate) {
+  __shared__ float part[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = j0 + lane;
+  const int64_t n0 = b * warp / 8, n1 = b * (warp + 1) / 8;
+  float acc = 0.f;
+  if (j < numel) {
+    int64_t n = n0;
+    for (; n + 8 <= n1; n += 8) {
+      float vv[8], ss[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        vv[u] = v(n + u, j);
+        ss[u] = __ldg(scale + n + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fmaf(ss[u], vv[u], acc);
+    }
+    for (; n < n1; ++n) acc = fmaf(__ldg(scale + n), v(n, j), acc);
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && j < numel) {
+    float t = part[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) t += part[w][lane];
+    out[j] = accumulate ? out[j] + t : t;
+  }
+}
+
+__global__ void __launch_bounds__(256) wsum_outer_kernel(OuterV v, const float* scale, int64_t b,
+                                                         float* out, int accumulate) {
+  wsum_body(v, scale, b, v.d * v.r, (int64_t)blockIdx.x * 32, out, accumulate);
+}
+
+// all small per-sample records (the biases) of a model in one launch: blockIdx.y = item
+__global__ void __launch_bounds__(256) wsum_multi_kernel(WsumItems items, const float* scale,
+                                                         int64_t b, int accumulate) {
+  const WsumItem& it = items.item[blockIdx.y];
+  const int64_t j0 = (int64_t)blockIdx.x * 32;
+  if (j0 >= it.numel) return;
+  wsum_body(RecordV{it.g, it.numel}, scale, b, it.numel, j0, it.out, accumulate);
+}
+
+void launch_wsum_multi(dpg_ctx* ctx, const WsumItems& items, const float* scale, int64_t b,
+                       int accumulate) {
+  if (items.count == 0) return;
+  int64_t maxn = 0;
+  for (int i = 0; i < items.count; ++i) maxn = items.item[i].numel > maxn ? items.item[i].numel : maxn;
+  dim3 grid((unsigned)((maxn + 31) / 32), (unsigned)items.count);
+  wsum_multi_kernel<<<grid, 256, 0, ctx->stream>>>(items, scale, b, accumulate);
+  DPG_LAUNCH_CHECK(ctx);
 }
 
 // Linear weight, mid > 1: split-K GEMM over (n, t).
@@ -160,9 +220,8 @@ void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, c
                                float* sw, float* sb, int accumulate, void* ws) {
   (void)sb;  // the bias sum is formed from the per-sample bias record (launch_weighted_sum_...)
   if (mid == 1) {
-    const int64_t n = r * d;
-    clipped_sum_linear_outer_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
-        acts, acts_relu, hw, scale, b, d, r, sw, accumulate);
+    OuterV v{acts, hw, d, r, acts_relu};
+    wsum_outer_kernel<<<(unsigned)((r * d + 31) / 32), 256, 0, ctx->stream>>>(v, scale, b, sw, accumulate);
     DPG_LAUNCH_CHECK(ctx);
     return;
   }

@@ -160,10 +160,13 @@ struct ConvGeom {
 bool use_tc();
 
 namespace tc {
+size_t fwd_ws_bytes(const ConvGeom& cg);
 void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-              const ConvGeom& cg, float* y);
+              const ConvGeom& cg, float* y, void* ws);
+bool dgrad_supported(const ConvGeom& cg);
+size_t dgrad_ws_bytes(const ConvGeom& cg);
 void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& cg,
-                const float* mask_src, float* dx);
+                const float* mask_src, float* dx, void* ws);
 int gs_conv_rows(const ConvGeom& cg);
 void conv_gs(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& cg,
              float* gw, double* sq_part);
@@ -214,6 +217,18 @@ void launch_clipped_sum_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const i
                                   const float* hw, const float* scale, int64_t b, int64_t t,
                                   int64_t vocab, int64_t dim, float* summed, int accumulate,
                                   void* ws);
+// Several small weighted sums over samples in one launch (the bias parameters of a model)
+struct WsumItem {
+  const float* g;  // [b, numel] per-sample values
+  float* out;      // [numel]
+  int64_t numel;
+};
+struct WsumItems {
+  WsumItem item[16];
+  int count;
+};
+void launch_wsum_multi(dpg_ctx* ctx, const WsumItems& items, const float* scale, int64_t b,
+                       int accumulate);
 void launch_sq_materialised(dpg_ctx* ctx, const float* g, int64_t b, int64_t numel,
                             double* sq_part);
 int sq_rows_materialised(int64_t numel);
@@ -228,10 +243,13 @@ void launch_gaussian(dpg_ctx* ctx, float* out, int64_t n, double std_dev, uint64
                      uint64_t step);
 
 // layers.cu — supporting forward / backward
+// ws: split-K scratch of at least conv_fwd_ws_bytes / conv_dgrad_ws_bytes (nullable: no split)
+size_t conv_fwd_ws_bytes(const ConvGeom& g);
+size_t conv_dgrad_ws_bytes(const ConvGeom& g);
 void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-                       const ConvGeom& g, float* y);
+                       const ConvGeom& g, float* y, void* ws);
 void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
-                         const float* mask_src, float* dx);
+                         const float* mask_src, float* dx, void* ws);
 void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
                        int64_t rows, int64_t d, int64_t r, float* y);
 void launch_linear_dgrad(dpg_ctx* ctx, const float* dy, const float* w, int64_t rows, int64_t d,

@@ -43,11 +43,16 @@ struct ConvFwdProb {
   }
 };
 
+size_t conv_fwd_ws_bytes(const ConvGeom& g) { return use_tc() ? tc::fwd_ws_bytes(g) : 0; }
+size_t conv_dgrad_ws_bytes(const ConvGeom& g) {
+  return (use_tc() && tc::dgrad_supported(g)) ? tc::dgrad_ws_bytes(g) : 0;
+}
+
 void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-                       const ConvGeom& g, float* y) {
+                       const ConvGeom& g, float* y, void* ws) {
   if (g.b == 0) return;
   if (use_tc()) {
-    tc::conv_fwd(ctx, x, x_relu, w, bias, g, y);
+    tc::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws);
     return;
   }
   ConvFwdProb p{make_im2col(x, x_relu, g), w, bias, y, g.oc, g.b * g.P(), g.K(), g.P()};
@@ -120,10 +125,10 @@ struct ConvDgradProb {
 };
 
 void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
-                         const float* mask_src, float* dx) {
+                         const float* mask_src, float* dx, void* ws) {
   if (g.b == 0) return;
-  if (use_tc()) {
-    tc::conv_dgrad(ctx, dy, w, g, mask_src, dx);
+  if (use_tc() && tc::dgrad_supported(g)) {
+    tc::conv_dgrad(ctx, dy, w, g, mask_src, dx, ws);
     return;
   }
   const int s = (int)g.stride;

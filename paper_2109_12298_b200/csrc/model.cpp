@@ -189,7 +189,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
         g.b = b;
         dpg::ProfScope ps(ctx, "fwd.conv2d[" + std::to_string(l) + "]",
                           io + 4.0 * m->params[lp.param0].numel, 2.0 * b * g.oc * g.K() * g.P());
-        dpg::launch_conv2d_fwd(ctx, in, lp.in_relu, w, bias, g, out);
+        dpg::launch_conv2d_fwd(ctx, in, lp.in_relu, w, bias, g, out, m->ws);
         break;
       }
       case DPG_LAYER_EMBEDDING: {
@@ -275,7 +275,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
           ConvGeom g = lp.g;
           g.b = b;
           dpg::ProfScope ps(ctx, "dgrad.conv2d" + ls, dio, 2.0 * b * g.oc * g.K() * g.P());
-          dpg::launch_conv2d_dgrad(ctx, hw, w, g, mask, dst);
+          dpg::launch_conv2d_dgrad(ctx, hw, w, g, mask, dst, m->ws);
           break;
         }
         default:
@@ -297,6 +297,22 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
                              o->norms, o->scale, o->num_clipped);
   }
   auto act = [&](int buf) -> const float* { return buf < 0 ? x : m->bufs[buf]; };
+  // bias clipped sums: weighted sums of the per-sample bias records, all biases in one launch
+  if (!o->cfg.clipped_sum_from_record) {
+    dpg::WsumItems items{};
+    double bytes = 0;
+    for (auto& pi : m->params) {
+      if (!pi.is_bias) continue;
+      if (items.count == 16) {
+        dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+        items.count = 0;
+      }
+      items.item[items.count++] = {gs_ptr(o, (int)(&pi - &m->params[0]), b), o->summed + pi.offset, pi.numel};
+      bytes += 4.0 * (b * pi.numel + 2 * pi.numel);
+    }
+    dpg::ProfScope ps(ctx, "csum.bias[all]", bytes, 0.0);
+    dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+  }
   for (size_t l = 0; l < m->layers.size(); ++l) {
     LayerPlan& lp = m->layers[l];
     if (lp.param0 < 0) continue;
@@ -306,7 +322,8 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       float* dst = o->summed + pi.offset;
       float* rec = gs_ptr(o, p, b);
       const std::string ls = "[" + std::to_string(l) + "]";
-      if (o->cfg.clipped_sum_from_record || pi.is_bias) {
+      if (pi.is_bias && !o->cfg.clipped_sum_from_record) continue;  // done above
+      if (o->cfg.clipped_sum_from_record) {
         // the reference's pass 2 over the stored per-sample gradients (exact order)
         dpg::ProfScope ps(ctx, std::string(pi.is_bias ? "csum.bias" : "csum.record") + ls,
                           4.0 * (b * pi.numel + 2 * pi.numel), 2.0 * b * pi.numel);
@@ -548,10 +565,14 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
         ConvGeom g = lp.g;
         g.b = max_batch;
         ws = std::max(ws, dpg::clipped_sum_ws_conv2d(g));
+        ws = std::max(ws, dpg::conv_fwd_ws_bytes(g));
+        ws = std::max(ws, dpg::conv_dgrad_ws_bytes(g));
         // smaller batches may pick more splits: bound by b = 1..max_b worst case
         for (int64_t bb = 1; bb <= max_batch; bb = bb * 2) {
           g.b = bb;
           ws = std::max(ws, dpg::clipped_sum_ws_conv2d(g));
+          ws = std::max(ws, dpg::conv_fwd_ws_bytes(g));
+          ws = std::max(ws, dpg::conv_dgrad_ws_bytes(g));
         }
       }
       if (lp.kind == DPG_LAYER_EMBEDDING) ws = std::max(ws, dpg::clipped_sum_ws_embedding(max_batch, lp.d.vocab_size));

@@ -4,36 +4,25 @@
 //   conv dgrad        dX[(n,pix), c]  = sum_(oc,tap) dY[n, oc, o(pix,tap)] W[oc, c, tap]
 //                     per stride-parity class of input pixels (no wasted taps), ReLU mask fused
 //   per-sample conv   G[n][oc][kcol]  = sum_p X~[n, kcol, p] B[n, oc, p]   + fused ||G_n||^2
-//   clipped conv sum  S[oc][kcol]     = sum_(n,p) X~[n, kcol, p] (s_n B[n, oc, p])  (split-K)
+//   clipped conv sum  S[oc][kcol]     = sum_(n,p) X~[n, kcol, p] (s_n B[n, oc, p])  (split over n)
 //   per-sample linear G[n][o][i]      = sum_t A[n, t, i] B[n, t, o]           (mid > 1)
-//   clipped linear    S[o][i]         = sum_(n,t) A[n, t, i] (s_n B[n, t, o])  (split-K)
+//   clipped linear    S[o][i]         = sum_(n,t) A[n, t, i] (s_n B[n, t, o])  (split over n)
 //
-// The GEMM row dimension (UMMA M = 128 TMEM lanes = epilogue threads) is always the dimension
-// that is contiguous in the output, so the epilogue stores of a warp are coalesced.
+// The GEMM row dimension (UMMA M = 128 TMEM lanes) is always the dimension that is contiguous in
+// the output, so each warp's epilogue stores are coalesced. The implicit-im2col index maps are
+// precomputed once per CTA into shared-memory tables (k -> plane offset / tap, p -> (oy s, ox s),
+// row -> base offset), so each gathered element costs one broadcast table read, two bound checks
+// and one load.
 #include "conv_common.cuh"
 #include "tc_gemm.cuh"
 
 namespace dpg {
 namespace tc {
 
-// im2col column decoder kcol -> (c, ki, kj) with fast division
-struct KcolDec {
-  FastDiv khw, kw;
-  __device__ __forceinline__ void dec(uint32_t k, int& c, int& ki, int& kj) const {
-    uint32_t q, r, a, b;
-    khw.divmod(k, q, r);
-    kw.divmod(r, a, b);
-    c = (int)q;
-    ki = (int)a;
-    kj = (int)b;
-  }
-};
-
 struct Geo {
   int ic, h, w, oc, kh, kw, stride, pad, oh, ow;
   int64_t P, Kc;
-  KcolDec kd;
-  FastDiv fow, fP;
+  FastDiv fP, fow;
 };
 
 inline Geo make_geo(const ConvGeom& g) {
@@ -43,11 +32,34 @@ inline Geo make_geo(const ConvGeom& g) {
   r.oh = (int)g.oh; r.ow = (int)g.ow;
   r.P = g.P();
   r.Kc = g.K();
-  r.kd.khw = FastDiv((uint32_t)(g.kh * g.kw));
-  r.kd.kw = FastDiv((uint32_t)g.kw);
-  r.fow = FastDiv((uint32_t)g.ow);
   r.fP = FastDiv((uint32_t)g.P());
+  r.fow = FastDiv((uint32_t)g.ow);
   return r;
+}
+
+// kcol -> offset of (c, ki, kj) relative to a window origin, and the tap (ki, kj)
+struct KEnt {
+  int off;
+  short ki, kj;
+};
+// position p -> window origin (oy s - pad, ox s - pad)
+struct PEnt {
+  short y, x;
+};
+
+__device__ __forceinline__ void build_ktab(const Geo& g, KEnt* t, int tid) {
+  for (int k = tid; k < g.Kc; k += kThreads) {
+    const int khw = g.kh * g.kw;
+    const int c = k / khw, r = k - c * khw;
+    const int ki = r / g.kw, kj = r - ki * g.kw;
+    t[k] = KEnt{(c * g.h + ki) * g.w + kj, (short)ki, (short)kj};
+  }
+}
+__device__ __forceinline__ void build_ptab(const Geo& g, PEnt* t, int tid) {
+  for (int p = tid; p < g.P; p += kThreads) {
+    const int oy = p / g.ow, ox = p - oy * g.ow;
+    t[p] = PEnt{(short)(oy * g.stride - g.pad), (short)(ox * g.stride - g.pad)};
+  }
 }
 
 // ------------------------------------------------------------------------------ forward
@@ -59,48 +71,117 @@ struct ConvFwd {
   const float* wt;
   const float* bias;
   float* y;
+  float* part;  // split-K partials [ksplit][oc][M] (ksplit > 1)
   int64_t M, N, K;
-  struct RowA {
-    int64_t base;
+  int ksplit, scratch;
+  struct Row {
+    int64_t base;  // n*ic*h*w + iy0*w + ix0
     int iy0, ix0;
   };
-  struct RowB {
-    const float* w;
-  };
-  __device__ RowA row_a(int, int64_t m) const {
-    uint32_t n, p, oy, ox;
-    g.fP.divmod((uint32_t)m, n, p);
-    g.fow.divmod(p, oy, ox);
-    return RowA{(int64_t)n * g.ic * g.h * g.w, (int)oy * g.stride - g.pad, (int)ox * g.stride - g.pad};
+  __device__ int64_t mdim(int) const { return M; }
+  __device__ int64_t kdim(int) const { return K; }
+  __device__ void setup(int, int64_t m0, int64_t, uint8_t* s, int tid) const {
+    KEnt* kt = reinterpret_cast<KEnt*>(s);
+    Row* rows = reinterpret_cast<Row*>(s + ((8 * K + 15) & ~15));
+    build_ktab(g, kt, tid);
+    if (tid < BM && m0 + tid < M) {
+      uint32_t n, p, oy, ox;
+      g.fP.divmod((uint32_t)(m0 + tid), n, p);
+      g.fow.divmod(p, oy, ox);
+      const int iy0 = (int)oy * g.stride - g.pad, ix0 = (int)ox * g.stride - g.pad;
+      rows[tid] = Row{(int64_t)n * g.ic * g.h * g.w + (int64_t)iy0 * g.w + ix0, iy0, ix0};
+    }
   }
-  __device__ float a(const RowA& r, int, int64_t k) const {
-    int c, ki, kj;
-    g.kd.dec((uint32_t)k, c, ki, kj);
-    const int iy = r.iy0 + ki, ix = r.ix0 + kj;
-    if ((unsigned)iy >= (unsigned)g.h || (unsigned)ix >= (unsigned)g.w) return 0.f;
-    return relu_if(__ldg(x + r.base + ((int64_t)c * g.h + iy) * g.w + ix), relu);
+  template <int BN>
+  __device__ void load_stage(int, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
+                             const uint8_t* s, int tid) const {
+    const KEnt* kt = reinterpret_cast<const KEnt*>(s);
+    const Row* rows = reinterpret_cast<const Row*>(s + ((8 * K + 15) & ~15));
+    const bool rok = m0 + (tid & 127) < M;
+    const Row r = rows[tid & 127];
+    load_rows128(sb, tid, [&](int, int q) {
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = 0.f;
+        if (rok && k < K) {
+          const KEnt t = kt[k];
+          if ((unsigned)(r.iy0 + t.ki) < (unsigned)g.h && (unsigned)(r.ix0 + t.kj) < (unsigned)g.w)
+            v[e] = relu_if(__ldg(x + r.base + t.off), relu);
+        }
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
+    load_b_rows<BN>(sb, tid, [&](int row, int q) {
+      float v[4];
+      const int64_t n = n0 + row;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = (n < N && k < K) ? __ldg(wt + n * K + k) : 0.f;
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
   }
-  __device__ RowB row_b(int, int64_t n) const { return RowB{wt + n * g.Kc}; }
-  __device__ float b(const RowB& r, int, int64_t k) const { return __ldg(r.w + k); }
-  __device__ void epilogue_row(int, int64_t m, int64_t n0, const float* v, int nv, double&) const {
+  __device__ void epilogue_row(int, int split, int64_t m, int64_t n0, const float* v, int nv, double&) const {
+    if (ksplit > 1) {
+      float* out = part + ((int64_t)split * N + n0) * M + m;
+      for (int j = 0; j < nv; ++j) out[j * M] = v[j];
+      return;
+    }
     uint32_t n, p;
     g.fP.divmod((uint32_t)m, n, p);
     float* out = y + (int64_t)n * g.oc * g.P + p;
     for (int j = 0; j < nv; ++j) out[(n0 + j) * g.P] = v[j] + (bias ? __ldg(bias + n0 + j) : 0.f);
   }
-  __device__ void epilogue_cta(int, double) const {}
+  __device__ void epilogue_cta(int, int, double) const {}
 };
 
+// Y[n][oc][p] = bias[oc] + sum_s part[s][oc][n*P + p]
+__global__ void fwd_reduce_kernel(const float* __restrict__ part, int ksplit, int64_t M, int64_t oc,
+                                  int64_t P, const float* __restrict__ bias, float* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over oc * M, m fastest
+  if (i >= oc * M) return;
+  const int64_t c = i / M, m = i - c * M;
+  float acc = 0.f;
+  for (int s = 0; s < ksplit; ++s) acc += part[(int64_t)s * oc * M + i];
+  const int64_t n = m / P, p = m - n * P;
+  y[(n * oc + c) * P + p] = acc + (bias ? bias[c] : 0.f);
+}
+
+size_t fwd_ws_bytes(const ConvGeom& cg) {
+  const int ks = pick_ksplit(cg.b * cg.P(), cg.oc, cg.K(), 1);
+  return ks > 1 ? sizeof(float) * (size_t)ks * (size_t)(cg.oc * cg.b * cg.P()) : 0;
+}
+
 void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-              const ConvGeom& cg, float* y) {
+              const ConvGeom& cg, float* y, void* ws) {
   ConvFwd p;
   p.g = make_geo(cg);
   p.x = x; p.relu = x_relu; p.wt = w; p.bias = bias; p.y = y;
   p.M = cg.b * cg.P(); p.N = cg.oc; p.K = cg.K();
+  p.ksplit = ws ? pick_ksplit(p.M, p.N, p.K, 1) : 1;
+  p.part = static_cast<float*>(ws);
+  p.scratch = (int)(((8 * p.K + 15) & ~15) + sizeof(ConvFwd::Row) * BM);
   launch_tc_auto(ctx, p, 1);
+  if (p.ksplit > 1) {
+    const int64_t n = p.M * p.N;
+    fwd_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(p.part, p.ksplit, p.M, p.N, p.g.P, bias, y);
+    DPG_LAUNCH_CHECK(ctx);
+  }
 }
 
 // ------------------------------------------------------------------------------ dgrad
+// One launch covers every stride-parity class (blockIdx.z = class). Inside class (ry, rx) the
+// taps are ki = ry + s a, kj = rx + s c; for input pixel (iy, ix) of the class the output pixel of
+// tap (a, c) is (oy0 - a, ox0 - c), oy0 = (iy + pad - ry) / s. k = (o, a, c).
+constexpr int kMaxClasses = 16;
+struct DClass {
+  int ry, rx, iy0, ix0, hc, wc, nki, nkj;
+  int64_t M, K;
+};
+
 struct ConvDgrad {
   static constexpr bool kCtaReduce = false;
   Geo g;
@@ -108,52 +189,92 @@ struct ConvDgrad {
   const float* wt;
   const float* mask;
   float* dx;
-  int64_t M, N, K;
-  int ry, rx, hc, wc, nkj, iy0, ix0;
-  FastDiv fcls, fwc, ftaps, fnkj, fs;
-  struct RowA {
-    int64_t dybase;
-    int iy, ix;
+  float* part;  // split-K partials [ksplit][b*ic*h*w] (ksplit > 1)
+  int64_t M, N, K, dx_numel;
+  int ksplit, scratch, ncls;
+  DClass cls[kMaxClasses];
+  struct TEnt {
+    int delta;  // o*oh*ow - a*ow - c
+    unsigned char a, c;
+    short o;
   };
-  struct RowB {
-    int c;
+  struct Row {
+    int64_t base;  // dy offset of (n, 0, oy0, ox0)
+    int oy0, ox0;
   };
-  __device__ RowA row_a(int, int64_t m) const {
-    uint32_t n, q, qy, qx;
-    fcls.divmod((uint32_t)m, n, q);
-    fwc.divmod(q, qy, qx);
-    return RowA{(int64_t)n * g.oc * g.oh * g.ow, iy0 + g.stride * (int)qy, ix0 + g.stride * (int)qx};
+  __device__ int64_t mdim(int z) const { return cls[z].M; }
+  __device__ int64_t kdim(int z) const { return cls[z].K; }
+  __device__ void setup(int z, int64_t m0, int64_t, uint8_t* s, int tid) const {
+    const DClass& c = cls[z];
+    TEnt* tt = reinterpret_cast<TEnt*>(s);
+    Row* rows = reinterpret_cast<Row*>(s + ((8 * K + 15) & ~15));
+    const int taps = c.nki * c.nkj;
+    for (int k = tid; k < c.K; k += kThreads) {
+      const int o = k / taps, t = k - o * taps;
+      const int a = t / c.nkj, cc = t - a * c.nkj;
+      tt[k] = TEnt{(o * g.oh - a) * g.ow - cc, (unsigned char)a, (unsigned char)cc, (short)o};
+    }
+    if (tid < BM && m0 + tid < c.M) {
+      const int per = c.hc * c.wc;
+      const int64_t m = m0 + tid;
+      const int n = (int)(m / per), q = (int)(m - (int64_t)n * per);
+      const int qy = q / c.wc, qx = q - qy * c.wc;
+      const int iy = c.iy0 + g.stride * qy, ix = c.ix0 + g.stride * qx;
+      const int oy0 = (iy + g.pad - c.ry) / g.stride, ox0 = (ix + g.pad - c.rx) / g.stride;
+      rows[tid] = Row{(int64_t)n * g.oc * g.oh * g.ow + (int64_t)oy0 * g.ow + ox0, oy0, ox0};
+    }
   }
-  __device__ __forceinline__ void tap(int64_t k, int& o, int& ki, int& kj) const {
-    uint32_t oo, t, a, c;
-    ftaps.divmod((uint32_t)k, oo, t);
-    fnkj.divmod(t, a, c);
-    o = (int)oo;
-    ki = ry + g.stride * (int)a;
-    kj = rx + g.stride * (int)c;
+  template <int BN>
+  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
+                             const uint8_t* s, int tid) const {
+    const DClass& c = cls[z];
+    const TEnt* tt = reinterpret_cast<const TEnt*>(s);
+    const Row* rows = reinterpret_cast<const Row*>(s + ((8 * K + 15) & ~15));
+    const bool rok = m0 + (tid & 127) < c.M;
+    const Row r = rows[tid & 127];
+    load_rows128(sb, tid, [&](int, int q) {
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = 0.f;
+        if (rok && k < c.K) {
+          const TEnt t = tt[k];
+          if ((unsigned)(r.oy0 - t.a) < (unsigned)g.oh && (unsigned)(r.ox0 - t.c) < (unsigned)g.ow)
+            v[e] = __ldg(dy + r.base + t.delta);
+        }
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
+    load_b_rows<BN>(sb, tid, [&](int row, int q) {
+      float v[4];
+      const int64_t ch = n0 + row;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = 0.f;
+        if (ch < N && k < c.K) {
+          const TEnt t = tt[k];
+          v[e] = __ldg(wt + (((int64_t)t.o * g.ic + ch) * g.kh + c.ry + g.stride * t.a) * g.kw + c.rx +
+                       g.stride * t.c);
+        }
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
   }
-  __device__ float a(const RowA& r, int, int64_t k) const {
-    int o, ki, kj;
-    tap(k, o, ki, kj);
-    const int ty = r.iy + g.pad - ki, tx = r.ix + g.pad - kj;
-    if (ty < 0 || tx < 0) return 0.f;
-    const int oy = (int)fs.div((uint32_t)ty), ox = (int)fs.div((uint32_t)tx);
-    if (oy >= g.oh || ox >= g.ow) return 0.f;
-    return __ldg(dy + r.dybase + ((int64_t)o * g.oh + oy) * g.ow + ox);
-  }
-  __device__ RowB row_b(int, int64_t n) const { return RowB{(int)n}; }
-  __device__ float b(const RowB& r, int, int64_t k) const {
-    int o, ki, kj;
-    tap(k, o, ki, kj);
-    return __ldg(wt + (((int64_t)o * g.ic + r.c) * g.kh + ki) * g.kw + kj);
-  }
-  __device__ void epilogue_row(int, int64_t m, int64_t n0, const float* v, int nv, double&) const {
-    uint32_t n, q, qy, qx;
-    fcls.divmod((uint32_t)m, n, q);
-    fwc.divmod(q, qy, qx);
-    const int iy = iy0 + g.stride * (int)qy, ix = ix0 + g.stride * (int)qx;
+  __device__ void epilogue_row(int z, int split, int64_t m, int64_t n0, const float* v, int nv, double&) const {
+    const DClass& c = cls[z];
+    const int per = c.hc * c.wc;
+    const int n = (int)(m / per), q = (int)(m - (int64_t)n * per);
+    const int qy = q / c.wc, qx = q - qy * c.wc;
+    const int iy = c.iy0 + g.stride * qy, ix = c.ix0 + g.stride * qx;
     const int64_t hw = (int64_t)g.h * g.w;
     const int64_t base = (int64_t)n * g.ic * hw + (int64_t)iy * g.w + ix;
+    if (ksplit > 1) {
+      float* out = part + (int64_t)split * dx_numel;
+      for (int j = 0; j < nv; ++j) out[base + (n0 + j) * hw] = v[j];
+      return;
+    }
     for (int j = 0; j < nv; ++j) {
       const int64_t off = base + (n0 + j) * hw;
       float val = v[j];
@@ -161,35 +282,70 @@ struct ConvDgrad {
       dx[off] = val;
     }
   }
-  __device__ void epilogue_cta(int, double) const {}
+  __device__ void epilogue_cta(int, int, double) const {}
 };
 
-void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& cg,
-                const float* mask_src, float* dx) {
+// dx = mask ? (sum_s part[s]) : 0 (input-shaped partials; every class writes disjoint pixels)
+__global__ void dgrad_reduce_kernel(const float* __restrict__ part, int ksplit, int64_t n,
+                                    const float* __restrict__ mask, float* __restrict__ dx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float acc = 0.f;
+  for (int s = 0; s < ksplit; ++s) acc += part[(int64_t)s * n + i];
+  if (mask && !(mask[i] > 0.f)) acc = 0.f;
+  dx[i] = acc;
+}
+
+static void dgrad_classes(const ConvGeom& cg, ConvDgrad& p) {
   const int s = (int)cg.stride;
+  p.ncls = 0;
+  p.M = 0;
+  p.K = 0;
   for (int ry = 0; ry < s; ++ry)
     for (int rx = 0; rx < s; ++rx) {
-      ConvDgrad p;
-      p.g = make_geo(cg);
-      p.dy = dy; p.wt = w; p.mask = mask_src; p.dx = dx;
-      p.ry = ry; p.rx = rx;
-      p.iy0 = ((ry - (int)cg.pad) % s + s) % s;
-      p.ix0 = ((rx - (int)cg.pad) % s + s) % s;
-      p.hc = p.iy0 < cg.h ? (int)((cg.h - p.iy0 + s - 1) / s) : 0;
-      p.wc = p.ix0 < cg.w ? (int)((cg.w - p.ix0 + s - 1) / s) : 0;
-      const int nki = ry < cg.kh ? (int)((cg.kh - ry + s - 1) / s) : 0;
-      p.nkj = rx < cg.kw ? (int)((cg.kw - rx + s - 1) / s) : 0;
-      if (p.hc == 0 || p.wc == 0) continue;
-      p.M = cg.b * p.hc * p.wc;
-      p.N = cg.ic;
-      p.K = cg.oc * nki * p.nkj;
-      p.fcls = FastDiv((uint32_t)(p.hc * p.wc));
-      p.fwc = FastDiv((uint32_t)p.wc);
-      p.ftaps = FastDiv((uint32_t)std::max(1, nki * p.nkj));
-      p.fnkj = FastDiv((uint32_t)std::max(1, p.nkj));
-      p.fs = FastDiv((uint32_t)s);
-      launch_tc_auto(ctx, p, 1);
+      DClass c{};
+      c.ry = ry; c.rx = rx;
+      c.iy0 = ((ry - (int)cg.pad) % s + s) % s;
+      c.ix0 = ((rx - (int)cg.pad) % s + s) % s;
+      c.hc = c.iy0 < cg.h ? (int)((cg.h - c.iy0 + s - 1) / s) : 0;
+      c.wc = c.ix0 < cg.w ? (int)((cg.w - c.ix0 + s - 1) / s) : 0;
+      c.nki = ry < cg.kh ? (int)((cg.kh - ry + s - 1) / s) : 0;
+      c.nkj = rx < cg.kw ? (int)((cg.kw - rx + s - 1) / s) : 0;
+      c.M = cg.b * c.hc * c.wc;
+      c.K = cg.oc * c.nki * c.nkj;
+      p.cls[p.ncls++] = c;
+      p.M = std::max(p.M, c.M);
+      p.K = std::max(p.K, c.K);
     }
+}
+
+bool dgrad_supported(const ConvGeom& cg) { return cg.stride * cg.stride <= kMaxClasses; }
+
+size_t dgrad_ws_bytes(const ConvGeom& cg) {
+  ConvDgrad p;
+  dgrad_classes(cg, p);
+  const int ks = pick_ksplit(p.M, cg.ic, p.K, p.ncls);
+  return ks > 1 ? sizeof(float) * (size_t)ks * (size_t)(cg.b * cg.ic * cg.h * cg.w) : 0;
+}
+
+void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& cg,
+                const float* mask_src, float* dx, void* ws) {
+  ConvDgrad p;
+  p.g = make_geo(cg);
+  p.dy = dy; p.wt = w; p.mask = mask_src; p.dx = dx;
+  dgrad_classes(cg, p);
+  p.N = cg.ic;
+  p.dx_numel = cg.b * cg.ic * cg.h * cg.w;
+  p.ksplit = ws ? pick_ksplit(p.M, p.N, p.K, p.ncls) : 1;
+  p.part = static_cast<float*>(ws);
+  p.scratch = (int)(((8 * p.K + 15) & ~15) + sizeof(ConvDgrad::Row) * BM);
+  // every input pixel lies in exactly one parity class and every (class, row tile, split) CTA
+  // writes its rows (zeros when its K range is empty), so the partials need no clearing
+  launch_tc_auto(ctx, p, p.ncls);
+  if (p.ksplit > 1) {
+    dgrad_reduce_kernel<<<(unsigned)((p.dx_numel + 255) / 256), 256, 0, ctx->stream>>>(p.part, p.ksplit, p.dx_numel, mask_src, dx);
+    DPG_LAUNCH_CHECK(ctx);
+  }
 }
 
 // ------------------------------------------------------------------------------ per-sample conv
@@ -202,42 +358,74 @@ struct ConvGs {
   float* gw;
   double* sq_part;
   int64_t M, N, K, bsz;
-  struct RowA {
-    int64_t base;  // x offset of (n, c) plane
-    int ki, kj;
+  int ksplit, scratch;
+  struct Row {
+    int plane;  // c*h*w
+    short ki, kj;
   };
-  struct RowB {
-    const float* h;
-  };
-  __device__ RowA row_a(int z, int64_t m) const {
-    int c, ki, kj;
-    g.kd.dec((uint32_t)m, c, ki, kj);
-    return RowA{((int64_t)z * g.ic + c) * g.h * g.w, ki - g.pad, kj - g.pad};
+  __device__ int64_t mdim(int) const { return M; }
+  __device__ int64_t kdim(int) const { return K; }
+  __device__ void setup(int, int64_t m0, int64_t, uint8_t* s, int tid) const {
+    PEnt* pt = reinterpret_cast<PEnt*>(s);
+    Row* rows = reinterpret_cast<Row*>(s + ((4 * K + 15) & ~15));
+    build_ptab(g, pt, tid);
+    if (tid < BM && m0 + tid < M) {
+      const int k = (int)(m0 + tid);
+      const int khw = g.kh * g.kw;
+      const int c = k / khw, r = k - c * khw;
+      const int ki = r / g.kw, kj = r - ki * g.kw;
+      rows[tid] = Row{c * g.h * g.w, (short)ki, (short)kj};
+    }
   }
-  __device__ float a(const RowA& r, int, int64_t k) const {
-    uint32_t oy, ox;
-    g.fow.divmod((uint32_t)k, oy, ox);
-    const int iy = (int)oy * g.stride + r.ki, ix = (int)ox * g.stride + r.kj;
-    if ((unsigned)iy >= (unsigned)g.h || (unsigned)ix >= (unsigned)g.w) return 0.f;
-    return relu_if(__ldg(x + r.base + (int64_t)iy * g.w + ix), relu);
+  template <int BN>
+  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
+                             const uint8_t* s, int tid) const {
+    const PEnt* pt = reinterpret_cast<const PEnt*>(s);
+    const Row* rows = reinterpret_cast<const Row*>(s + ((4 * K + 15) & ~15));
+    const bool rok = m0 + (tid & 127) < M;
+    const Row r = rows[tid & 127];
+    const float* xs = x + (int64_t)z * g.ic * g.h * g.w + r.plane;
+    load_rows128(sb, tid, [&](int, int q) {
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = 0.f;
+        if (rok && k < K) {
+          const PEnt t = pt[k];
+          const int iy = t.y + r.ki, ix = t.x + r.kj;
+          if ((unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w)
+            v[e] = relu_if(__ldg(xs + iy * g.w + ix), relu);
+        }
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
+    const bool vec = (K & 3) == 0;
+    load_b_rows<BN>(sb, tid, [&](int row, int q) {
+      const int64_t oc = n0 + row;
+      const int64_t k = k0 + 4 * q;
+      const float* h = hw + ((int64_t)z * g.oc + oc) * K;
+      if (oc < N && vec && k < K) return __ldg(reinterpret_cast<const float4*>(h + k));
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = (oc < N && k + e < K) ? __ldg(h + k + e) : 0.f;
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
   }
-  __device__ RowB row_b(int z, int64_t n) const { return RowB{hw + ((int64_t)z * g.oc + n) * g.P}; }
-  __device__ float b(const RowB& r, int, int64_t k) const { return __ldg(r.h + k); }
-  __device__ void epilogue_row(int z, int64_t m, int64_t n0, const float* v, int nv, double& sq) const {
+  __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double& sq) const {
     float* out = gw ? gw + ((int64_t)z * g.oc + n0) * g.Kc + m : nullptr;
     for (int j = 0; j < nv; ++j) {
       if (out) st_stream(out + j * g.Kc, v[j]);
       sq += (double)v[j] * v[j];
     }
   }
-  __device__ void epilogue_cta(int z, double sq) const {
+  __device__ void epilogue_cta(int z, int, double sq) const {
     if (sq_part) sq_part[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * bsz + z] = sq;
   }
 };
 
 int gs_conv_rows(const ConvGeom& cg) {
-  const int64_t bn = cg.oc <= 16 ? 16 : cg.oc <= 32 ? 32 : cg.oc <= 64 ? 64 : 128;
-  return (int)(((cg.K() + BM - 1) / BM) * ((cg.oc + bn - 1) / bn));
+  return (int)(((cg.K() + BM - 1) / BM) * ((cg.oc + pick_bn(cg.oc) - 1) / pick_bn(cg.oc)));
 }
 
 void conv_gs(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& cg,
@@ -246,6 +434,8 @@ void conv_gs(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const Co
   p.g = make_geo(cg);
   p.x = x; p.relu = x_relu; p.hw = hw; p.gw = gw; p.sq_part = sq_part;
   p.M = cg.K(); p.N = cg.oc; p.K = cg.P(); p.bsz = cg.b;
+  p.ksplit = 1;
+  p.scratch = (int)(((4 * p.K + 15) & ~15) + sizeof(ConvGs::Row) * BM);
   launch_tc_auto(ctx, p, cg.b);
 }
 
@@ -259,46 +449,91 @@ struct ConvCsum {
   const float* scale;
   float* part;
   int64_t M, N, K, spl, bsz;
-  struct RowA {
-    int64_t cplane;  // c * h * w
-    int ki, kj;
+  int ksplit, scratch;
+  struct Row {
+    int plane;
+    short ki, kj;
   };
-  struct RowB {
-    int oc;
-  };
-  __device__ RowA row_a(int, int64_t m) const {
-    int c, ki, kj;
-    g.kd.dec((uint32_t)m, c, ki, kj);
-    return RowA{(int64_t)c * g.h * g.w, ki - g.pad, kj - g.pad};
+  __device__ int64_t mdim(int) const { return M; }
+  __device__ int64_t kdim(int) const { return K; }
+  __device__ void setup(int, int64_t m0, int64_t, uint8_t* s, int tid) const {
+    PEnt* pt = reinterpret_cast<PEnt*>(s);
+    Row* rows = reinterpret_cast<Row*>(s + ((4 * g.P + 15) & ~15));
+    build_ptab(g, pt, tid);
+    if (tid < BM && m0 + tid < M) {
+      const int k = (int)(m0 + tid);
+      const int khw = g.kh * g.kw;
+      const int c = k / khw, r = k - c * khw;
+      const int ki = r / g.kw, kj = r - ki * g.kw;
+      rows[tid] = Row{c * g.h * g.w, (short)ki, (short)kj};
+    }
   }
-  __device__ float a(const RowA& r, int z, int64_t k) const {
-    uint32_t q, p, oy, ox;
-    g.fP.divmod((uint32_t)k, q, p);
-    const int64_t n = (int64_t)z * spl + q;
-    if (n >= bsz) return 0.f;
-    g.fow.divmod(p, oy, ox);
-    const int iy = (int)oy * g.stride + r.ki, ix = (int)ox * g.stride + r.kj;
-    if ((unsigned)iy >= (unsigned)g.h || (unsigned)ix >= (unsigned)g.w) return 0.f;
-    return relu_if(__ldg(x + n * g.ic * g.h * g.w + r.cplane + (int64_t)iy * g.w + ix), relu);
+  template <int BN>
+  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
+                             const uint8_t* s, int tid) const {
+    const PEnt* pt = reinterpret_cast<const PEnt*>(s);
+    const Row* rows = reinterpret_cast<const Row*>(s + ((4 * g.P + 15) & ~15));
+    const bool rok = m0 + (tid & 127) < M;
+    const Row r = rows[tid & 127];
+    load_rows128(sb, tid, [&](int, int q) {
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = 0.f;
+        if (rok && k < K) {
+          uint32_t qq, p;
+          g.fP.divmod((uint32_t)k, qq, p);
+          const int64_t n = (int64_t)z * spl + qq;
+          if (n < bsz) {
+            const PEnt t = pt[p];
+            const int iy = t.y + r.ki, ix = t.x + r.kj;
+            if ((unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w)
+              v[e] = relu_if(__ldg(x + n * g.ic * g.h * g.w + r.plane + iy * g.w + ix), relu);
+          }
+        }
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
+    const bool vec = (g.P & 3) == 0;
+    load_b_rows<BN>(sb, tid, [&](int row, int q) {
+      const int64_t oc = n0 + row;
+      const int64_t k = k0 + 4 * q;
+      if (vec) {
+        uint32_t qq, p;
+        g.fP.divmod((uint32_t)k, qq, p);
+        const int64_t n = (int64_t)z * spl + qq;
+        if (oc < N && k < K && n < bsz) {
+          const float sc = __ldg(scale + n);
+          float4 h = __ldg(reinterpret_cast<const float4*>(hw + (n * g.oc + oc) * g.P + p));
+          h.x *= sc; h.y *= sc; h.z *= sc; h.w *= sc;
+          return h;
+        }
+        return make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[e] = 0.f;
+        if (oc < N && k + e < K) {
+          uint32_t qq, p;
+          g.fP.divmod((uint32_t)(k + e), qq, p);
+          const int64_t n = (int64_t)z * spl + qq;
+          if (n < bsz) v[e] = __ldg(scale + n) * __ldg(hw + (n * g.oc + oc) * g.P + p);
+        }
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
   }
-  __device__ RowB row_b(int, int64_t n) const { return RowB{(int)n}; }
-  __device__ float b(const RowB& r, int z, int64_t k) const {
-    uint32_t q, p;
-    g.fP.divmod((uint32_t)k, q, p);
-    const int64_t n = (int64_t)z * spl + q;
-    if (n >= bsz) return 0.f;
-    return __ldg(scale + n) * __ldg(hw + (n * g.oc + r.oc) * g.P + p);
-  }
-  __device__ void epilogue_row(int z, int64_t m, int64_t n0, const float* v, int nv, double&) const {
+  __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     float* out = part + ((int64_t)z * g.oc + n0) * g.Kc + m;
     for (int j = 0; j < nv; ++j) out[j * g.Kc] = v[j];
   }
-  __device__ void epilogue_cta(int, double) const {}
+  __device__ void epilogue_cta(int, int, double) const {}
 };
 
 int csum_conv_splits(const ConvGeom& cg) {
   const int64_t tiles = ((cg.K() + BM - 1) / BM) * ((cg.oc + 127) / 128);
-  // ~2 CTAs per SM, at least 2 k-stages of work per split
   int64_t splits = (2 * kNumSMs + tiles - 1) / tiles;
   const int64_t max_by_k = std::max<int64_t>(1, (cg.b * cg.P()) / (2 * BK));
   splits = std::min<int64_t>(std::min<int64_t>(splits, cg.b), max_by_k);
@@ -312,6 +547,8 @@ void conv_csum(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const 
   p.x = x; p.relu = x_relu; p.hw = hw; p.scale = scale; p.part = part;
   p.spl = (cg.b + splits - 1) / splits;
   p.M = cg.K(); p.N = cg.oc; p.K = p.spl * cg.P(); p.bsz = cg.b;
+  p.ksplit = 1;
+  p.scratch = (int)(((4 * cg.P() + 15) & ~15) + sizeof(ConvCsum::Row) * BM);
   launch_tc_auto(ctx, p, splits);
 }
 
@@ -324,38 +561,53 @@ struct LinGs {
   float* gw;
   double* sq_part;
   int64_t M, N, K, bsz;  // M = d (i), N = r (o), K = mid
-  struct RowA {
-    int64_t i;
-  };
-  struct RowB {
-    int64_t o;
-  };
-  __device__ RowA row_a(int, int64_t m) const { return RowA{m}; }
-  __device__ float a(const RowA& r, int z, int64_t k) const {
-    return relu_if(__ldg(acts + ((int64_t)z * K + k) * M + r.i), relu);
+  int ksplit, scratch;
+  __device__ int64_t mdim(int) const { return M; }
+  __device__ int64_t kdim(int) const { return K; }
+  __device__ void setup(int, int64_t, int64_t, uint8_t*, int) const {}
+  template <int BN>
+  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
+                             const uint8_t*, int tid) const {
+    const int64_t i = m0 + (tid & 127);
+    load_rows128(sb, tid, [&](int, int q) {
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = (i < M && k < K) ? relu_if(__ldg(acts + ((int64_t)z * K + k) * M + i), relu) : 0.f;
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
+    load_b_cols<BN>(sb, tid, [&](int row, int q) {
+      const int64_t o = n0 + row;
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = (o < N && k < K) ? __ldg(hw + ((int64_t)z * K + k) * N + o) : 0.f;
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
   }
-  __device__ RowB row_b(int, int64_t n) const { return RowB{n}; }
-  __device__ float b(const RowB& r, int z, int64_t k) const { return __ldg(hw + ((int64_t)z * K + k) * N + r.o); }
-  __device__ void epilogue_row(int z, int64_t m, int64_t n0, const float* v, int nv, double& sq) const {
+  __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double& sq) const {
     float* out = gw ? gw + ((int64_t)z * N + n0) * M + m : nullptr;
     for (int j = 0; j < nv; ++j) {
       if (out) st_stream(out + j * M, v[j]);
       sq += (double)v[j] * v[j];
     }
   }
-  __device__ void epilogue_cta(int z, double sq) const {
+  __device__ void epilogue_cta(int z, int, double sq) const {
     if (sq_part) sq_part[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * bsz + z] = sq;
   }
 };
 
 int gs_linear_rows(int64_t d, int64_t r) {
-  const int64_t bn = r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 128;
-  return (int)(((d + BM - 1) / BM) * ((r + bn - 1) / bn));
+  return (int)(((d + BM - 1) / BM) * ((r + pick_bn(r) - 1) / pick_bn(r)));
 }
 
 void linear_gs(dpg_ctx* ctx, const float* acts, int relu, const float* hw, int64_t b, int64_t mid,
                int64_t d, int64_t r, float* gw, double* sq_part) {
-  LinGs p{acts, relu, hw, gw, sq_part, d, r, mid, b};
+  LinGs p{acts, relu, hw, gw, sq_part, d, r, mid, b, 1, 0};
   launch_tc_auto(ctx, p, b);
 }
 
@@ -367,34 +619,52 @@ struct LinCsum {
   const float* scale;
   float* part;
   int64_t M, N, K, spl, mid, bsz;
+  int ksplit, scratch;
   FastDiv fmid;
-  struct RowA {
-    int64_t i;
-  };
-  struct RowB {
-    int64_t o;
-  };
-  __device__ RowA row_a(int, int64_t m) const { return RowA{m}; }
-  __device__ float a(const RowA& r, int z, int64_t k) const {
-    uint32_t q, t;
-    fmid.divmod((uint32_t)k, q, t);
-    const int64_t n = (int64_t)z * spl + q;
-    if (n >= bsz) return 0.f;
-    return relu_if(__ldg(acts + (n * mid + t) * M + r.i), relu);
+  __device__ int64_t mdim(int) const { return M; }
+  __device__ int64_t kdim(int) const { return K; }
+  __device__ void setup(int, int64_t, int64_t, uint8_t*, int) const {}
+  template <int BN>
+  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
+                             const uint8_t*, int tid) const {
+    const int64_t i = m0 + (tid & 127);
+    load_rows128(sb, tid, [&](int, int q) {
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = 0.f;
+        if (i < M && k < K) {
+          uint32_t qq, t;
+          fmid.divmod((uint32_t)k, qq, t);
+          const int64_t n = (int64_t)z * spl + qq;
+          if (n < bsz) v[e] = relu_if(__ldg(acts + (n * mid + t) * M + i), relu);
+        }
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
+    load_b_cols<BN>(sb, tid, [&](int row, int q) {
+      const int64_t o = n0 + row;
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = k0 + 4 * q + e;
+        v[e] = 0.f;
+        if (o < N && k < K) {
+          uint32_t qq, t;
+          fmid.divmod((uint32_t)k, qq, t);
+          const int64_t n = (int64_t)z * spl + qq;
+          if (n < bsz) v[e] = __ldg(scale + n) * __ldg(hw + (n * mid + t) * N + o);
+        }
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    });
   }
-  __device__ RowB row_b(int, int64_t n) const { return RowB{n}; }
-  __device__ float b(const RowB& r, int z, int64_t k) const {
-    uint32_t q, t;
-    fmid.divmod((uint32_t)k, q, t);
-    const int64_t n = (int64_t)z * spl + q;
-    if (n >= bsz) return 0.f;
-    return __ldg(scale + n) * __ldg(hw + (n * mid + t) * N + r.o);
-  }
-  __device__ void epilogue_row(int z, int64_t m, int64_t n0, const float* v, int nv, double&) const {
+  __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     float* out = part + ((int64_t)z * N + n0) * M + m;
     for (int j = 0; j < nv; ++j) out[j * M] = v[j];
   }
-  __device__ void epilogue_cta(int, double) const {}
+  __device__ void epilogue_cta(int, int, double) const {}
 };
 
 int csum_linear_splits(int64_t b, int64_t mid, int64_t d, int64_t r) {
@@ -411,6 +681,8 @@ void linear_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, con
   p.acts = acts; p.relu = relu; p.hw = hw; p.scale = scale; p.part = part;
   p.spl = (b + splits - 1) / splits;
   p.M = d; p.N = r; p.K = p.spl * mid; p.mid = mid; p.bsz = b;
+  p.ksplit = 1;
+  p.scratch = 0;
   p.fmid = FastDiv((uint32_t)mid);
   launch_tc_auto(ctx, p, splits);
 }

@@ -2,23 +2,28 @@
 //
 //   C[z][m][n] = sum_k A(z, m, k) * B(z, n, k)         (both operands K-major)
 //
-// Operands are gathered by all threads of the CTA through a problem-specific index map (the
-// implicit im2col of the conv contractions lives in the Prob loaders), split into a TF32 "hi"
-// part (cvt.rna) and the TF32-rounded remainder "lo", and stored into shared memory in the
-// canonical 128B-swizzled K-major UMMA layout (8 rows x 128 B atoms, 1024 B aligned). One thread
-// issues tcgen05.mma.cta_group::1.kind::tf32 with the accumulator in tensor memory:
-// acc += A_lo B_hi + A_hi B_lo + A_hi B_hi per K=8 slice (the 3xTF32 scheme; relative error
-// ~2^-21, fp32-like). Stages are double buffered: the MMA of stage s runs asynchronously while
-// the threads gather stage s+1; tcgen05.commit arrives on the stage's mbarrier to release it.
-// The epilogue reads the accumulator back with tcgen05.ld (thread t of warp w owns row
-// 32w + t of the 128-row tile) and hands each row to Prob::epilogue_row.
+// Operands are gathered by all threads of the CTA through a problem-specific stage loader (the
+// implicit im2col of the conv contractions lives there, driven by per-CTA index tables in shared
+// memory), split into a TF32 "hi" part (cvt.rna) and the TF32-rounded remainder "lo", and stored
+// into shared memory in the canonical 128B-swizzled K-major UMMA layout (8 rows x 128 B atoms,
+// 1024 B aligned). One thread issues tcgen05.mma.cta_group::1.kind::tf32 with the accumulator in
+// tensor memory: acc += A_lo B_hi + A_hi B_lo + A_hi B_hi per K=8 slice (3xTF32). Stages are
+// double buffered: the MMAs of stage s run asynchronously while the threads gather stage s+1;
+// tcgen05.commit arrives on the stage's mbarrier to release the buffer.
 //
-// Tile: BM = 128 rows (UMMA M), BN in {16, 32, 64, 128, 256} columns (UMMA N), BK = 32 fp32
-// (one 128 B swizzle row) per stage; 128 threads.
+// Epilogue: tcgen05.ld; warp w owns TMEM lanes [32 (w % 4), +32) (= tile rows) and the column
+// half w / 4; each thread hands its row's values to Prob::epilogue_row.
+//
+// Split-K: blockIdx.z = z * ksplit + split; split s covers K stages [s * nk / ksplit,
+// (s + 1) * nk / ksplit) and the Prob writes a partial that a fixed-order reduce combines.
+//
+// Tile: BM = 128 rows (UMMA M), BN in {16, 32, 64, 128} columns (UMMA N), BK = 32 fp32 (one
+// 128 B swizzle row) per stage; 256 threads.
 #pragma once
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "dpg_device.cuh"
@@ -28,7 +33,7 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 32;
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;
 constexpr int kStages = 2;
 
 // ---- integer division by a runtime constant (multiply-high), valid for n < 2^31 ----
@@ -36,7 +41,10 @@ struct FastDiv {
   uint32_t d = 1, m = 0, s = 0;
   FastDiv() = default;
   explicit FastDiv(uint32_t div) : d(div) {
-    if (div <= 1) { m = 0; s = 0; return; }
+    if (div <= 1) {
+      d = 1;
+      return;
+    }
     uint32_t l = 0;
     while ((1u << l) < div) ++l;  // ceil(log2 div)
     s = 31 + l;
@@ -127,19 +135,6 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int q) {
   return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((q ^ (row & 7)) << 4));
 }
 
-template <int BN>
-struct Smem {
-  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
-  static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int TOTAL = kStages * STAGE + 1024 /*align*/ + 64;
-};
-
-template <int BN>
-constexpr uint32_t tmem_cols() {
-  return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
-}
-
 // Store 4 values (k .. k+3 of one row) as hi / lo TF32 into the swizzled stage buffers.
 __device__ __forceinline__ void put4(uint8_t* hi, uint8_t* lo, int row, int q, float a, float b,
                                      float c, float d) {
@@ -152,15 +147,39 @@ __device__ __forceinline__ void put4(uint8_t* hi, uint8_t* lo, int row, int q, f
   *reinterpret_cast<uint4*>(hi + off) = h;
   *reinterpret_cast<uint4*>(lo + off) = l;
 }
+__device__ __forceinline__ void put4(uint8_t* hi, uint8_t* lo, int row, int q, float4 v) {
+  put4(hi, lo, row, q, v.x, v.y, v.z, v.w);
+}
+
+template <int BN>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int FIXED = kStages * STAGE + 64;
+};
+
+template <int BN>
+constexpr uint32_t tmem_cols() {
+  return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+}
+
+// Stage buffers handed to Prob::load_stage
+struct StageBufs {
+  uint8_t* a_hi;
+  uint8_t* a_lo;
+  uint8_t* b_hi;
+  uint8_t* b_lo;
+};
 
 // Prob interface:
-//   int64_t M, N, K;                            problem sizes (K may be 0)
-//   struct RowA; RowA row_a(int z, int64_t m) const;   per-row precompute for A (m < M)
-//   float a(const RowA&, int z, int64_t k) const;       A element (k < K)
-//   struct RowB; RowB row_b(int z, int64_t n) const;    per-row precompute for B
-//   float b(const RowB&, int z, int64_t k) const;
-//   void epilogue_row(int z, int64_t m, int64_t n0, const float* v, int nv, double& sq) const;
-//   void epilogue_cta(int z, double sq) const;          after all rows (block-reduced sq)
+//   int64_t M, N, K; int ksplit; int scratch;          max sizes, split-K factor, scratch bytes
+//   int64_t mdim(int z), kdim(int z) const;             per-batch M and K (<= M, K)
+//   void setup(int z, int64_t m0, int64_t n0, uint8_t* scratch, int tid) const;   once per CTA
+//   template <int BN> void load_stage(int z, int64_t m0, int64_t n0, int64_t k0,
+//                                     const StageBufs&, const uint8_t* scratch, int tid) const;
+//   void epilogue_row(int z, int split, int64_t m, int64_t n, const float* v, int nv, double& sq);
+//   static constexpr bool kCtaReduce; void epilogue_cta(int z, int split, double sq) const;
 template <int BN, class Prob>
 __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
   extern __shared__ uint8_t smem_raw[];
@@ -168,11 +187,14 @@ __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
   using S = Smem<BN>;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * S::STAGE);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kStages);
+  uint8_t* scratch = smem + S::FIXED;
 
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int z = blockIdx.z;
+  const int z = blockIdx.z / p.ksplit, split = blockIdx.z % p.ksplit;
   const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
   constexpr uint32_t kCols = tmem_cols<BN>();
+  const int64_t Mz = p.mdim(z), Kz = p.kdim(z);
+  if (m0 >= Mz) return;  // ragged batches (e.g. dgrad parity classes): whole CTA idle
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -183,76 +205,33 @@ __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  p.setup(z, m0, n0, scratch, tid);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // this thread's A row (and B rows) for every stage
-  const int64_t am = m0 + tid;
-  const bool a_ok = am < p.M;
-  typename Prob::RowA ra{};
-  if (a_ok) ra = p.row_a(z, am);
-  constexpr int BROWS = (BN + kThreads - 1) / kThreads;
-  typename Prob::RowB rb[BROWS];
-  bool b_ok[BROWS];
-#pragma unroll
-  for (int i = 0; i < BROWS; ++i) {
-    const int r = tid + i * kThreads;
-    const int64_t bn = n0 + r;
-    b_ok[i] = r < BN && bn < p.N;
-    if (b_ok[i]) rb[i] = p.row_b(z, bn);
-  }
-
-  const int64_t K = p.K;
-  const int nk = (int)((K + BK - 1) / BK);
+  const int nk_all = (int)((Kz + BK - 1) / BK);
+  const int ks0 = (int)((int64_t)split * nk_all / p.ksplit);
+  const int ks1 = (int)((int64_t)(split + 1) * nk_all / p.ksplit);
+  const int nk = ks1 - ks0;
   constexpr uint32_t idesc = idesc_tf32(BN);
-  for (int kt = 0; kt < nk; ++kt) {
-    const int s = kt % kStages;
+  for (int i = 0; i < nk; ++i) {
+    const int s = i % kStages;
     uint8_t* st = smem + s * S::STAGE;
-    uint8_t* a_hi = st;
-    uint8_t* a_lo = st + S::A_BYTES;
-    uint8_t* b_hi = st + 2 * S::A_BYTES;
-    uint8_t* b_lo = b_hi + S::B_BYTES;
-    if (kt >= kStages) mbar_wait(&bars[s], ((kt / kStages) - 1) & 1);
-    const int64_t k0 = (int64_t)kt * BK;
-    // gather A row `tid`: 32 consecutive k
-#pragma unroll
-    for (int q = 0; q < BK / 4; ++q) {
-      float v[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = (a_ok && k < K) ? p.a(ra, z, k) : 0.f;
-      }
-      put4(a_hi, a_lo, tid, q, v[0], v[1], v[2], v[3]);
-    }
-#pragma unroll
-    for (int i = 0; i < BROWS; ++i) {
-      const int r = tid + i * kThreads;
-      if (r < BN) {
-#pragma unroll
-        for (int q = 0; q < BK / 4; ++q) {
-          float v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int64_t k = k0 + 4 * q + e;
-            v[e] = (b_ok[i] && k < K) ? p.b(rb[i], z, k) : 0.f;
-          }
-          put4(b_hi, b_lo, r, q, v[0], v[1], v[2], v[3]);
-        }
-      }
-    }
+    StageBufs sb{st, st + S::A_BYTES, st + 2 * S::A_BYTES, st + 2 * S::A_BYTES + S::B_BYTES};
+    if (i >= kStages) mbar_wait(&bars[s], ((i / kStages) - 1) & 1);
+    p.template load_stage<BN>(z, m0, n0, (int64_t)(ks0 + i) * BK, sb, scratch, tid);
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      const uint32_t sa_hi = smem_u32(a_hi), sa_lo = smem_u32(a_lo);
-      const uint32_t sb_hi = smem_u32(b_hi), sb_lo = smem_u32(b_lo);
+      const uint32_t sa_hi = smem_u32(sb.a_hi), sa_lo = smem_u32(sb.a_lo);
+      const uint32_t sb_hi = smem_u32(sb.b_hi), sb_lo = smem_u32(sb.b_lo);
 #pragma unroll
       for (int kk = 0; kk < BK / 8; ++kk) {
         const uint32_t off = kk * 32;  // 8 tf32 = 32 B along the swizzled row
-        const uint32_t acc0 = (kt > 0 || kk > 0) ? 1u : 0u;
+        const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
         mma_tf32(tmem, sw128_desc(sa_lo + off), sw128_desc(sb_hi + off), idesc, acc0);
         mma_tf32(tmem, sw128_desc(sa_hi + off), sw128_desc(sb_lo + off), idesc, 1u);
         mma_tf32(tmem, sw128_desc(sa_hi + off), sw128_desc(sb_hi + off), idesc, 1u);
@@ -260,28 +239,30 @@ __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
       mma_commit(&bars[s]);
     }
   }
-  if (nk > 0) {
-    const int last = nk - 1;
-    mbar_wait(&bars[last % kStages], (last / kStages) & 1);
-  }
+  if (nk > 0) mbar_wait(&bars[(nk - 1) % kStages], ((nk - 1) / kStages) & 1);
   tc_fence_after();
 
-  // epilogue: warp w owns TMEM lanes [32w, 32w + 32) = tile rows
-  const int64_t m = m0 + 32 * warp + (tid & 31);
-  const bool row_ok = m < p.M;
+  // epilogue: warp w -> TMEM lanes [32 (w % 4), +32), columns [(w / 4) BN / 2, +BN / 2)
+  const int lane_base = 32 * (warp & 3);
+  const int64_t m = m0 + lane_base + (tid & 31);
+  const bool row_ok = m < Mz;
+  constexpr int HALF = BN / 2 >= 16 ? BN / 2 : 16;
+  const int c_begin = (warp >> 2) * HALF;
   double sq = 0.0;
   float v[16];
+  if (c_begin < BN) {
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    if (nk > 0) {
-      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
-    } else {
+    for (int c0 = c_begin; c0 < c_begin + HALF && c0 < BN; c0 += 16) {
+      if (nk > 0) {
+        tmem_ld16(tmem + ((uint32_t)lane_base << 16) + (uint32_t)c0, v);
+      } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        for (int q = 0; q < 16; ++q) v[q] = 0.f;
+      }
+      const int64_t nrem = p.N - (n0 + c0);
+      const int nv = nrem >= 16 ? 16 : (nrem > 0 ? (int)nrem : 0);
+      if (row_ok && nv > 0) p.epilogue_row(z, split, m, n0 + c0, v, nv, sq);
     }
-    const int64_t nrem = p.N - (n0 + c0);
-    const int nv = nrem >= 16 ? 16 : (nrem > 0 ? (int)nrem : 0);
-    if (row_ok && nv > 0) p.epilogue_row(z, m, n0 + c0, v, nv, sq);
   }
   tc_fence_before();
   __syncthreads();
@@ -291,30 +272,74 @@ __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
   if (Prob::kCtaReduce) {
     __shared__ double red[kThreads / 32];
     const double t = block_sum<kThreads>(sq, red);
-    if (tid == 0) p.epilogue_cta(z, t);
+    if (tid == 0) p.epilogue_cta(z, split, t);
   }
 }
 
 template <int BN, class Prob>
 void launch_tc(dpg_ctx* ctx, const Prob& p, int64_t batches) {
-  const int smem = Smem<BN>::TOTAL;
-  static bool attr = false;  // per template instance
-  if (!attr) {
+  const int smem = Smem<BN>::FIXED + 1024 + p.scratch;
+  static int attr = 0;  // per template instance: largest dynamic smem configured so far
+  if (smem > attr) {
     DPG_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<BN, Prob>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+    attr = smem;
   }
-  dim3 grid((unsigned)((p.M + BM - 1) / BM), (unsigned)((p.N + BN - 1) / BN), (unsigned)batches);
+  dim3 grid((unsigned)((p.M + BM - 1) / BM), (unsigned)((p.N + BN - 1) / BN), (unsigned)(batches * p.ksplit));
   tc_gemm_kernel<BN, Prob><<<grid, kThreads, smem, ctx->stream>>>(p);
   DPG_LAUNCH_CHECK(ctx);
 }
 
-// pick the narrowest legal UMMA N that covers n (cta_group::1, M = 128: N % 16 == 0, <= 256)
+inline int pick_bn(int64_t n) { return n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : 128; }
+
+// the narrowest legal UMMA N covering n (cta_group::1, M = 128: N % 16 == 0)
 template <class Prob>
 void launch_tc_auto(dpg_ctx* ctx, const Prob& p, int64_t batches) {
-  if (p.N <= 16) launch_tc<16>(ctx, p, batches);
-  else if (p.N <= 32) launch_tc<32>(ctx, p, batches);
-  else if (p.N <= 64) launch_tc<64>(ctx, p, batches);
-  else launch_tc<128>(ctx, p, batches);
+  switch (pick_bn(p.N)) {
+    case 16: launch_tc<16>(ctx, p, batches); break;
+    case 32: launch_tc<32>(ctx, p, batches); break;
+    case 64: launch_tc<64>(ctx, p, batches); break;
+    default: launch_tc<128>(ctx, p, batches); break;
+  }
+}
+
+// split-K factor so that tiles * batches * ksplit ~ 2 CTAs per SM, >= 2 K stages per split
+inline int pick_ksplit(int64_t M, int64_t N, int64_t K, int64_t batches) {
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + 127) / 128) * batches;
+  const int64_t nk = (K + BK - 1) / BK;
+  int64_t ks = (2 * kNumSMs + tiles - 1) / tiles;
+  ks = std::min<int64_t>(ks, std::max<int64_t>(1, nk / 2));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ks, 16));
+}
+
+// ---- common loader patterns (256 threads) ----
+// A tile: 128 rows x 8 quads; thread t owns row t & 127, quads (t >> 7) + 2 i, i = 0..3
+template <class F>
+__device__ __forceinline__ void load_rows128(const StageBufs& sb, int tid, F&& quad /* float4(row, q) */) {
+  const int row = tid & 127;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = (tid >> 7) + 2 * i;
+    put4(sb.a_hi, sb.a_lo, row, q, quad(row, q));
+  }
+}
+// B tile, row-major spread: consecutive threads take consecutive rows (coalesced when the
+// operand's rows are contiguous in memory and its K is strided)
+template <int BN, class F>
+__device__ __forceinline__ void load_b_cols(const StageBufs& sb, int tid, F&& quad) {
+#pragma unroll
+  for (int idx = tid; idx < BN * 8; idx += kThreads) {
+    const int row = idx % BN, q = idx / BN;
+    put4(sb.b_hi, sb.b_lo, row, q, quad(row, q));
+  }
+}
+// B tile: BN rows x 8 quads spread over the 256 threads, quads of a row on consecutive threads
+template <int BN, class F>
+__device__ __forceinline__ void load_b_rows(const StageBufs& sb, int tid, F&& quad) {
+#pragma unroll
+  for (int idx = tid; idx < BN * 8; idx += kThreads) {
+    const int row = idx >> 3, q = idx & 7;
+    put4(sb.b_hi, sb.b_lo, row, q, quad(row, q));
+  }
 }
 
 }  // namespace tc
