@@ -287,6 +287,8 @@ static void cs_conv_tiles(const ConvGeom& g, int& bm, int& bn) {
 }
 
 size_t clipped_sum_ws_conv2d(const ConvGeom& g) {
+  if (ds::enabled()) return sizeof(float) * (size_t)ds::csum_splits(g) * (size_t)(g.oc * g.K());
+  if (ps::supported_csum(g)) return sizeof(float) * (size_t)ps::csum_splits(g) * (size_t)(g.oc * g.K());
   if (use_tc()) return sizeof(float) * (size_t)tc::csum_conv_splits(g) * (size_t)(g.oc * g.K());
   int bm, bn;
   cs_conv_tiles(g, bm, bn);
@@ -299,6 +301,18 @@ void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const f
                                const float* scale, const ConvGeom& g, float* sw, float* sb,
                                int accumulate, void* ws) {
   (void)sb;
+  if (ds::enabled()) {
+    const int splits = ds::csum_splits(g);
+    ds::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
+    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, g.oc * g.K(), sw, accumulate);
+    return;
+  }
+  if (ps::supported_csum(g)) {
+    const int splits = ps::csum_splits(g);
+    ps::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
+    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, g.oc * g.K(), sw, accumulate);
+    return;
+  }
   if (use_tc()) {
     const int splits = tc::csum_conv_splits(g);
     tc::conv_csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);

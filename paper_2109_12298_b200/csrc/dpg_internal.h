@@ -181,6 +181,27 @@ void linear_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, con
                  int64_t b, int64_t mid, int64_t d, int64_t r, float* part, int splits);
 }  // namespace tc
 
+namespace ds {
+bool enabled();
+int gs_rows(const ConvGeom& g);
+void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
+        double* sq_part);
+int csum_splits(const ConvGeom& g);
+void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* scale,
+          const ConvGeom& g, float* part, int splits);
+}  // namespace ds
+
+namespace ps {
+bool supported(const ConvGeom& g);       // per-sample gradient path
+bool supported_csum(const ConvGeom& g);  // clipped-sum path (A/B only)
+int gs_rows(const ConvGeom& g);
+void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
+        double* sq_part);
+int csum_splits(const ConvGeom& g);
+void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* scale,
+          const ConvGeom& g, float* part, int splits);
+}  // namespace ps
+
 // rules.cu — per-sample gradients
 int sq_rows_linear(int64_t mid, int64_t d, int64_t r);
 int sq_rows_conv2d(const ConvGeom& g);

@@ -156,6 +156,8 @@ static void conv_tiles(const ConvGeom& g, int& bm, int& bn) {
 }
 
 int sq_rows_conv2d(const ConvGeom& g) {
+  if (ds::enabled()) return ds::gs_rows(g);
+  if (ps::supported(g)) return ps::gs_rows(g);
   if (use_tc()) return tc::gs_conv_rows(g);
   int bm, bn;
   conv_tiles(g, bm, bn);
@@ -165,6 +167,14 @@ int sq_rows_conv2d(const ConvGeom& g) {
 void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& g,
                       float* gw, double* sq_part) {
   if (g.b == 0) return;
+  if (ds::enabled()) {
+    ds::gs(ctx, x, x_relu, hw, g, gw, sq_part);
+    return;
+  }
+  if (ps::supported(g)) {
+    ps::gs(ctx, x, x_relu, hw, g, gw, sq_part);
+    return;
+  }
   if (use_tc()) {
     tc::conv_gs(ctx, x, x_relu, hw, g, gw, sq_part);
     return;

@@ -47,12 +47,19 @@ struct PEnt {
   short y, x;
 };
 
-__device__ __forceinline__ void build_ktab(const Geo& g, KEnt* t, int tid) {
-  for (int k = tid; k < g.Kc; k += kThreads) {
-    const int khw = g.kh * g.kw;
-    const int c = k / khw, r = k - c * khw;
-    const int ki = r / g.kw, kj = r - ki * g.kw;
-    t[k] = KEnt{(c * g.h + ki) * g.w + kj, (short)ki, (short)kj};
+constexpr int kBad = -(1 << 14);  // sentinel coordinate: (unsigned)(kBad + small) >= h, w
+
+// k-table for kcol 0 .. kpad (entries >= K are sentinels that fail every bound check)
+__device__ __forceinline__ void build_ktab(const Geo& g, KEnt* t, int tid, int K, int kpad) {
+  for (int k = tid; k < kpad; k += kThreads) {
+    if (k < K) {
+      const int khw = g.kh * g.kw;
+      const int c = k / khw, r = k - c * khw;
+      const int ki = r / g.kw, kj = r - ki * g.kw;
+      t[k] = KEnt{(c * g.h + ki) * g.w + kj, (short)ki, (short)kj};
+    } else {
+      t[k] = KEnt{0, (short)kBad, (short)kBad};
+    }
   }
 }
 __device__ __forceinline__ void build_ptab(const Geo& g, PEnt* t, int tid) {
@@ -75,54 +82,48 @@ struct ConvFwd {
   int64_t M, N, K;
   int ksplit, scratch;
   struct Row {
-    int64_t base;  // n*ic*h*w + iy0*w + ix0
-    int iy0, ix0;
+    const float* xr;  // x + n*ic*h*w + iy0*w + ix0
+    int iy0, ix0;     // window origin; kBad for rows beyond M (every bound check fails)
   };
   __device__ int64_t mdim(int) const { return M; }
   __device__ int64_t kdim(int) const { return K; }
+  __device__ int ktab_bytes() const { return (int)(8 * ((K + BK - 1) / BK) * BK); }
   __device__ void setup(int, int64_t m0, int64_t, uint8_t* s, int tid) const {
     KEnt* kt = reinterpret_cast<KEnt*>(s);
-    Row* rows = reinterpret_cast<Row*>(s + ((8 * K + 15) & ~15));
-    build_ktab(g, kt, tid);
-    if (tid < BM && m0 + tid < M) {
-      uint32_t n, p, oy, ox;
-      g.fP.divmod((uint32_t)(m0 + tid), n, p);
-      g.fow.divmod(p, oy, ox);
-      const int iy0 = (int)oy * g.stride - g.pad, ix0 = (int)ox * g.stride - g.pad;
-      rows[tid] = Row{(int64_t)n * g.ic * g.h * g.w + (int64_t)iy0 * g.w + ix0, iy0, ix0};
+    Row* rows = reinterpret_cast<Row*>(s + ktab_bytes());
+    build_ktab(g, kt, tid, (int)K, (int)((K + BK - 1) / BK) * BK);
+    if (tid < BM) {
+      Row r{x, kBad, kBad};
+      if (m0 + tid < M) {
+        uint32_t n, p, oy, ox;
+        g.fP.divmod((uint32_t)(m0 + tid), n, p);
+        g.fow.divmod(p, oy, ox);
+        const int iy0 = (int)oy * g.stride - g.pad, ix0 = (int)ox * g.stride - g.pad;
+        r = Row{x + (int64_t)n * g.ic * g.h * g.w + (int64_t)iy0 * g.w + ix0, iy0, ix0};
+      }
+      rows[tid] = r;
     }
   }
-  template <int BN>
-  __device__ void load_stage(int, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
-                             const uint8_t* s, int tid) const {
-    const KEnt* kt = reinterpret_cast<const KEnt*>(s);
-    const Row* rows = reinterpret_cast<const Row*>(s + ((8 * K + 15) & ~15));
-    const bool rok = m0 + (tid & 127) < M;
-    const Row r = rows[tid & 127];
-    load_rows128(sb, tid, [&](int, int q) {
-      float v[4];
+  static constexpr bool kAQuadMajor = false;  // rows = output positions: lanes walk ox
+  static constexpr bool kBQuadMajor = true;   // W rows contiguous in kcol
+  __device__ float4 a_quad(int, int64_t, int row, int64_t k, const uint8_t* s) const {
+    const KEnt* kt = reinterpret_cast<const KEnt*>(s) + (int)k;
+    const Row r = reinterpret_cast<const Row*>(s + ktab_bytes())[row];
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = 0.f;
-        if (rok && k < K) {
-          const KEnt t = kt[k];
-          if ((unsigned)(r.iy0 + t.ki) < (unsigned)g.h && (unsigned)(r.ix0 + t.kj) < (unsigned)g.w)
-            v[e] = relu_if(__ldg(x + r.base + t.off), relu);
-        }
-      }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
-    load_b_rows<BN>(sb, tid, [&](int row, int q) {
-      float v[4];
-      const int64_t n = n0 + row;
+    for (int e = 0; e < 4; ++e) {
+      const KEnt t = kt[e];
+      const bool ok = (unsigned)(r.iy0 + t.ki) < (unsigned)g.h && (unsigned)(r.ix0 + t.kj) < (unsigned)g.w;
+      v[e] = ok ? relu_if(__ldg(r.xr + t.off), relu) : 0.f;
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ float4 b_quad(int, int64_t n0, int row, int64_t k, const uint8_t*) const {
+    const int64_t n = n0 + row;
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = (n < N && k < K) ? __ldg(wt + n * K + k) : 0.f;
-      }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
+    for (int e = 0; e < 4; ++e) v[e] = (n < N && k + e < K) ? __ldg(wt + n * K + k + e) : 0.f;
+    return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ void epilogue_row(int, int split, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     if (ksplit > 1) {
@@ -163,7 +164,7 @@ void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const fl
   p.M = cg.b * cg.P(); p.N = cg.oc; p.K = cg.K();
   p.ksplit = ws ? pick_ksplit(p.M, p.N, p.K, 1) : 1;
   p.part = static_cast<float*>(ws);
-  p.scratch = (int)(((8 * p.K + 15) & ~15) + sizeof(ConvFwd::Row) * BM);
+  p.scratch = (int)(8 * ((p.K + BK - 1) / BK) * BK + sizeof(ConvFwd::Row) * BM);
   launch_tc_auto(ctx, p, 1);
   if (p.ksplit > 1) {
     const int64_t n = p.M * p.N;
@@ -199,68 +200,70 @@ struct ConvDgrad {
     short o;
   };
   struct Row {
-    int64_t base;  // dy offset of (n, 0, oy0, ox0)
-    int oy0, ox0;
+    const float* dr;  // dy + (n, 0, oy0, ox0)
+    int oy0, ox0;     // kBad-based for rows beyond the class (every bound check fails)
   };
   __device__ int64_t mdim(int z) const { return cls[z].M; }
   __device__ int64_t kdim(int z) const { return cls[z].K; }
+  __device__ int ttab_bytes() const { return (int)(8 * ((K + BK - 1) / BK) * BK); }
   __device__ void setup(int z, int64_t m0, int64_t, uint8_t* s, int tid) const {
     const DClass& c = cls[z];
     TEnt* tt = reinterpret_cast<TEnt*>(s);
-    Row* rows = reinterpret_cast<Row*>(s + ((8 * K + 15) & ~15));
+    Row* rows = reinterpret_cast<Row*>(s + ttab_bytes());
     const int taps = c.nki * c.nkj;
-    for (int k = tid; k < c.K; k += kThreads) {
-      const int o = k / taps, t = k - o * taps;
-      const int a = t / c.nkj, cc = t - a * c.nkj;
-      tt[k] = TEnt{(o * g.oh - a) * g.ow - cc, (unsigned char)a, (unsigned char)cc, (short)o};
+    const int kpad = (int)((c.K + BK - 1) / BK) * BK;
+    for (int k = tid; k < kpad; k += kThreads) {
+      if (k < c.K) {
+        const int o = k / taps, t = k - o * taps;
+        const int a = t / c.nkj, cc = t - a * c.nkj;
+        tt[k] = TEnt{(o * g.oh - a) * g.ow - cc, (unsigned char)a, (unsigned char)cc, (short)o};
+      } else {
+        tt[k] = TEnt{0, (unsigned char)255, (unsigned char)255, (short)0};  // oy0 - 255 < 0: fails
+      }
     }
-    if (tid < BM && m0 + tid < c.M) {
-      const int per = c.hc * c.wc;
-      const int64_t m = m0 + tid;
-      const int n = (int)(m / per), q = (int)(m - (int64_t)n * per);
-      const int qy = q / c.wc, qx = q - qy * c.wc;
-      const int iy = c.iy0 + g.stride * qy, ix = c.ix0 + g.stride * qx;
-      const int oy0 = (iy + g.pad - c.ry) / g.stride, ox0 = (ix + g.pad - c.rx) / g.stride;
-      rows[tid] = Row{(int64_t)n * g.oc * g.oh * g.ow + (int64_t)oy0 * g.ow + ox0, oy0, ox0};
+    if (tid < BM) {
+      Row r{dy, kBad, kBad};
+      if (m0 + tid < c.M) {
+        const int per = c.hc * c.wc;
+        const int64_t m = m0 + tid;
+        const int n = (int)(m / per), q = (int)(m - (int64_t)n * per);
+        const int qy = q / c.wc, qx = q - qy * c.wc;
+        const int iy = c.iy0 + g.stride * qy, ix = c.ix0 + g.stride * qx;
+        const int oy0 = (iy + g.pad - c.ry) / g.stride, ox0 = (ix + g.pad - c.rx) / g.stride;
+        r = Row{dy + (int64_t)n * g.oc * g.oh * g.ow + (int64_t)oy0 * g.ow + ox0, oy0, ox0};
+      }
+      rows[tid] = r;
     }
   }
-  template <int BN>
-  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
-                             const uint8_t* s, int tid) const {
+  static constexpr bool kAQuadMajor = false;  // rows = input pixels of the class
+  static constexpr bool kBQuadMajor = true;
+  __device__ float4 a_quad(int, int64_t, int row, int64_t k, const uint8_t* s) const {
+    const TEnt* tt = reinterpret_cast<const TEnt*>(s) + (int)k;
+    const Row r = reinterpret_cast<const Row*>(s + ttab_bytes())[row];
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const TEnt t = tt[e];
+      const bool ok = (unsigned)(r.oy0 - t.a) < (unsigned)g.oh && (unsigned)(r.ox0 - t.c) < (unsigned)g.ow;
+      v[e] = ok ? __ldg(r.dr + t.delta) : 0.f;
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t* s) const {
     const DClass& c = cls[z];
     const TEnt* tt = reinterpret_cast<const TEnt*>(s);
-    const Row* rows = reinterpret_cast<const Row*>(s + ((8 * K + 15) & ~15));
-    const bool rok = m0 + (tid & 127) < c.M;
-    const Row r = rows[tid & 127];
-    load_rows128(sb, tid, [&](int, int q) {
-      float v[4];
+    const int64_t ch = n0 + row;
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = 0.f;
-        if (rok && k < c.K) {
-          const TEnt t = tt[k];
-          if ((unsigned)(r.oy0 - t.a) < (unsigned)g.oh && (unsigned)(r.ox0 - t.c) < (unsigned)g.ow)
-            v[e] = __ldg(dy + r.base + t.delta);
-        }
+    for (int e = 0; e < 4; ++e) {
+      v[e] = 0.f;
+      if (ch < N && k + e < c.K) {
+        const TEnt t = tt[k + e];
+        v[e] = __ldg(wt + (((int64_t)t.o * g.ic + ch) * g.kh + c.ry + g.stride * t.a) * g.kw + c.rx +
+                     g.stride * t.c);
       }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
-    load_b_rows<BN>(sb, tid, [&](int row, int q) {
-      float v[4];
-      const int64_t ch = n0 + row;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = 0.f;
-        if (ch < N && k < c.K) {
-          const TEnt t = tt[k];
-          v[e] = __ldg(wt + (((int64_t)t.o * g.ic + ch) * g.kh + c.ry + g.stride * t.a) * g.kw + c.rx +
-                       g.stride * t.c);
-        }
-      }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ void epilogue_row(int z, int split, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     const DClass& c = cls[z];
@@ -319,7 +322,10 @@ static void dgrad_classes(const ConvGeom& cg, ConvDgrad& p) {
     }
 }
 
-bool dgrad_supported(const ConvGeom& cg) { return cg.stride * cg.stride <= kMaxClasses; }
+// (tap tables use a one-byte tap index with 255 as the out-of-range sentinel)
+bool dgrad_supported(const ConvGeom& cg) {
+  return cg.stride * cg.stride <= kMaxClasses && cg.oh < 255 && cg.ow < 255 && cg.kh < 255 && cg.kw < 255;
+}
 
 size_t dgrad_ws_bytes(const ConvGeom& cg) {
   ConvDgrad p;
@@ -338,7 +344,7 @@ void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& c
   p.dx_numel = cg.b * cg.ic * cg.h * cg.w;
   p.ksplit = ws ? pick_ksplit(p.M, p.N, p.K, p.ncls) : 1;
   p.part = static_cast<float*>(ws);
-  p.scratch = (int)(((8 * p.K + 15) & ~15) + sizeof(ConvDgrad::Row) * BM);
+  p.scratch = (int)(8 * ((p.K + BK - 1) / BK) * BK + sizeof(ConvDgrad::Row) * BM);
   // every input pixel lies in exactly one parity class and every (class, row tile, split) CTA
   // writes its rows (zeros when its K range is empty), so the partials need no clearing
   launch_tc_auto(ctx, p, p.ncls);
@@ -377,40 +383,33 @@ struct ConvGs {
       rows[tid] = Row{c * g.h * g.w, (short)ki, (short)kj};
     }
   }
-  template <int BN>
-  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
-                             const uint8_t* s, int tid) const {
+  static constexpr bool kAQuadMajor = true;  // rows = kcol; lanes walk positions
+  static constexpr bool kBQuadMajor = true;  // highway rows contiguous in p
+  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t* s) const {
     const PEnt* pt = reinterpret_cast<const PEnt*>(s);
-    const Row* rows = reinterpret_cast<const Row*>(s + ((4 * K + 15) & ~15));
-    const bool rok = m0 + (tid & 127) < M;
-    const Row r = rows[tid & 127];
+    const Row r = reinterpret_cast<const Row*>(s + ((4 * K + 15) & ~15))[row];
     const float* xs = x + (int64_t)z * g.ic * g.h * g.w + r.plane;
-    load_rows128(sb, tid, [&](int, int q) {
-      float v[4];
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = 0.f;
-        if (rok && k < K) {
-          const PEnt t = pt[k];
-          const int iy = t.y + r.ki, ix = t.x + r.kj;
-          if ((unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w)
-            v[e] = relu_if(__ldg(xs + iy * g.w + ix), relu);
-        }
+    for (int e = 0; e < 4; ++e) {
+      v[e] = 0.f;
+      if (m0 + row < M && k + e < K) {
+        const PEnt t = pt[k + e];
+        const int iy = t.y + r.ki, ix = t.x + r.kj;
+        if ((unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w)
+          v[e] = relu_if(__ldg(xs + iy * g.w + ix), relu);
       }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
-    const bool vec = (K & 3) == 0;
-    load_b_rows<BN>(sb, tid, [&](int row, int q) {
-      const int64_t oc = n0 + row;
-      const int64_t k = k0 + 4 * q;
-      const float* h = hw + ((int64_t)z * g.oc + oc) * K;
-      if (oc < N && vec && k < K) return __ldg(reinterpret_cast<const float4*>(h + k));
-      float v[4];
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
+    const int64_t oc = n0 + row;
+    const float* h = hw + ((int64_t)z * g.oc + oc) * K;
+    if (oc < N && (K & 3) == 0 && k < K) return __ldg(reinterpret_cast<const float4*>(h + k));
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = (oc < N && k + e < K) ? __ldg(h + k + e) : 0.f;
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
+    for (int e = 0; e < 4; ++e) v[e] = (oc < N && k + e < K) ? __ldg(h + k + e) : 0.f;
+    return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double& sq) const {
     float* out = gw ? gw + ((int64_t)z * g.oc + n0) * g.Kc + m : nullptr;
@@ -468,62 +467,55 @@ struct ConvCsum {
       rows[tid] = Row{c * g.h * g.w, (short)ki, (short)kj};
     }
   }
-  template <int BN>
-  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
-                             const uint8_t* s, int tid) const {
+  static constexpr bool kAQuadMajor = true;
+  static constexpr bool kBQuadMajor = true;
+  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t* s) const {
     const PEnt* pt = reinterpret_cast<const PEnt*>(s);
-    const Row* rows = reinterpret_cast<const Row*>(s + ((4 * g.P + 15) & ~15));
-    const bool rok = m0 + (tid & 127) < M;
-    const Row r = rows[tid & 127];
-    load_rows128(sb, tid, [&](int, int q) {
-      float v[4];
+    const Row r = reinterpret_cast<const Row*>(s + ((4 * g.P + 15) & ~15))[row];
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = 0.f;
-        if (rok && k < K) {
-          uint32_t qq, p;
-          g.fP.divmod((uint32_t)k, qq, p);
-          const int64_t n = (int64_t)z * spl + qq;
-          if (n < bsz) {
-            const PEnt t = pt[p];
-            const int iy = t.y + r.ki, ix = t.x + r.kj;
-            if ((unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w)
-              v[e] = relu_if(__ldg(x + n * g.ic * g.h * g.w + r.plane + iy * g.w + ix), relu);
-          }
-        }
-      }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
-    const bool vec = (g.P & 3) == 0;
-    load_b_rows<BN>(sb, tid, [&](int row, int q) {
-      const int64_t oc = n0 + row;
-      const int64_t k = k0 + 4 * q;
-      if (vec) {
-        uint32_t qq, p;
-        g.fP.divmod((uint32_t)k, qq, p);
+    for (int e = 0; e < 4; ++e) {
+      v[e] = 0.f;
+      if (m0 + row < M && k + e < K) {
+        uint32_t qq, pp;
+        g.fP.divmod((uint32_t)(k + e), qq, pp);
         const int64_t n = (int64_t)z * spl + qq;
-        if (oc < N && k < K && n < bsz) {
-          const float sc = __ldg(scale + n);
-          float4 h = __ldg(reinterpret_cast<const float4*>(hw + (n * g.oc + oc) * g.P + p));
-          h.x *= sc; h.y *= sc; h.z *= sc; h.w *= sc;
-          return h;
+        if (n < bsz) {
+          const PEnt t = pt[pp];
+          const int iy = t.y + r.ki, ix = t.x + r.kj;
+          if ((unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w)
+            v[e] = relu_if(__ldg(x + n * g.ic * g.h * g.w + r.plane + iy * g.w + ix), relu);
         }
-        return make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      float v[4];
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
+    const int64_t oc = n0 + row;
+    if ((g.P & 3) == 0) {
+      uint32_t qq, pp;
+      g.fP.divmod((uint32_t)k, qq, pp);
+      const int64_t n = (int64_t)z * spl + qq;
+      if (oc < N && k < K && n < bsz) {
+        const float sc = __ldg(scale + n);
+        float4 h = __ldg(reinterpret_cast<const float4*>(hw + (n * g.oc + oc) * g.P + pp));
+        h.x *= sc; h.y *= sc; h.z *= sc; h.w *= sc;
+        return h;
+      }
+      return make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        v[e] = 0.f;
-        if (oc < N && k + e < K) {
-          uint32_t qq, p;
-          g.fP.divmod((uint32_t)(k + e), qq, p);
-          const int64_t n = (int64_t)z * spl + qq;
-          if (n < bsz) v[e] = __ldg(scale + n) * __ldg(hw + (n * g.oc + oc) * g.P + p);
-        }
+    for (int e = 0; e < 4; ++e) {
+      v[e] = 0.f;
+      if (oc < N && k + e < K) {
+        uint32_t qq, pp;
+        g.fP.divmod((uint32_t)(k + e), qq, pp);
+        const int64_t n = (int64_t)z * spl + qq;
+        if (n < bsz) v[e] = __ldg(scale + n) * __ldg(hw + (n * g.oc + oc) * g.P + pp);
       }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     float* out = part + ((int64_t)z * g.oc + n0) * g.Kc + m;
@@ -565,29 +557,22 @@ struct LinGs {
   __device__ int64_t mdim(int) const { return M; }
   __device__ int64_t kdim(int) const { return K; }
   __device__ void setup(int, int64_t, int64_t, uint8_t*, int) const {}
-  template <int BN>
-  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
-                             const uint8_t*, int tid) const {
-    const int64_t i = m0 + (tid & 127);
-    load_rows128(sb, tid, [&](int, int q) {
-      float v[4];
+  static constexpr bool kAQuadMajor = false;  // rows = i contiguous
+  static constexpr bool kBQuadMajor = false;  // rows = o contiguous
+  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t*) const {
+    const int64_t i = m0 + row;
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = (i < M && k < K) ? relu_if(__ldg(acts + ((int64_t)z * K + k) * M + i), relu) : 0.f;
-      }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
-    load_b_cols<BN>(sb, tid, [&](int row, int q) {
-      const int64_t o = n0 + row;
-      float v[4];
+    for (int e = 0; e < 4; ++e)
+      v[e] = (i < M && k + e < K) ? relu_if(__ldg(acts + ((int64_t)z * K + k + e) * M + i), relu) : 0.f;
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
+    const int64_t o = n0 + row;
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = (o < N && k < K) ? __ldg(hw + ((int64_t)z * K + k) * N + o) : 0.f;
-      }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
+    for (int e = 0; e < 4; ++e) v[e] = (o < N && k + e < K) ? __ldg(hw + ((int64_t)z * K + k + e) * N + o) : 0.f;
+    return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double& sq) const {
     float* out = gw ? gw + ((int64_t)z * N + n0) * M + m : nullptr;
@@ -624,41 +609,37 @@ struct LinCsum {
   __device__ int64_t mdim(int) const { return M; }
   __device__ int64_t kdim(int) const { return K; }
   __device__ void setup(int, int64_t, int64_t, uint8_t*, int) const {}
-  template <int BN>
-  __device__ void load_stage(int z, int64_t m0, int64_t n0, int64_t k0, const StageBufs& sb,
-                             const uint8_t*, int tid) const {
-    const int64_t i = m0 + (tid & 127);
-    load_rows128(sb, tid, [&](int, int q) {
-      float v[4];
+  static constexpr bool kAQuadMajor = false;
+  static constexpr bool kBQuadMajor = false;
+  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t*) const {
+    const int64_t i = m0 + row;
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = 0.f;
-        if (i < M && k < K) {
-          uint32_t qq, t;
-          fmid.divmod((uint32_t)k, qq, t);
-          const int64_t n = (int64_t)z * spl + qq;
-          if (n < bsz) v[e] = relu_if(__ldg(acts + (n * mid + t) * M + i), relu);
-        }
+    for (int e = 0; e < 4; ++e) {
+      v[e] = 0.f;
+      if (i < M && k + e < K) {
+        uint32_t qq, t;
+        fmid.divmod((uint32_t)(k + e), qq, t);
+        const int64_t n = (int64_t)z * spl + qq;
+        if (n < bsz) v[e] = relu_if(__ldg(acts + (n * mid + t) * M + i), relu);
       }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
-    load_b_cols<BN>(sb, tid, [&](int row, int q) {
-      const int64_t o = n0 + row;
-      float v[4];
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
+    const int64_t o = n0 + row;
+    float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t k = k0 + 4 * q + e;
-        v[e] = 0.f;
-        if (o < N && k < K) {
-          uint32_t qq, t;
-          fmid.divmod((uint32_t)k, qq, t);
-          const int64_t n = (int64_t)z * spl + qq;
-          if (n < bsz) v[e] = __ldg(scale + n) * __ldg(hw + (n * mid + t) * N + o);
-        }
+    for (int e = 0; e < 4; ++e) {
+      v[e] = 0.f;
+      if (o < N && k + e < K) {
+        uint32_t qq, t;
+        fmid.divmod((uint32_t)(k + e), qq, t);
+        const int64_t n = (int64_t)z * spl + qq;
+        if (n < bsz) v[e] = __ldg(scale + n) * __ldg(hw + (n * mid + t) * N + o);
       }
-      return make_float4(v[0], v[1], v[2], v[3]);
-    });
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     float* out = part + ((int64_t)z * N + n0) * M + m;

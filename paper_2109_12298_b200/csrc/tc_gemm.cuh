@@ -11,6 +11,8 @@
 // double buffered: the MMAs of stage s run asynchronously while the threads gather stage s+1;
 // tcgen05.commit arrives on the stage's mbarrier to release the buffer.
 //
+// Operands for stage s+1 are fetched into registers while stage s is stored and its MMAs run.
+//
 // Epilogue: tcgen05.ld; warp w owns TMEM lanes [32 (w % 4), +32) (= tile rows) and the column
 // half w / 4; each thread hands its row's values to Prob::epilogue_row.
 //
@@ -164,22 +166,96 @@ constexpr uint32_t tmem_cols() {
   return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
 }
 
-// Stage buffers handed to Prob::load_stage
-struct StageBufs {
+// Stage buffers
+struct StageBufsT {
   uint8_t* a_hi;
   uint8_t* a_lo;
   uint8_t* b_hi;
   uint8_t* b_lo;
 };
 
+// Operand registers of one stage: each thread fetches 4 quads of A (16 floats) and BQ quads of B
+// for the NEXT stage while the current one is converted, stored and consumed by the MMA, so
+// ~16 + 4 BQ independent loads per thread stay in flight.
+//
+// Thread -> (row, quad) maps (i = 0..3 for A, i = 0..BQ-1 for B):
+//   A row-major  (kAQuadMajor = false): row = tid & 127, quad = (tid >> 7) + 2 i
+//                 — a warp covers 32 rows at one k (coalesced when rows are contiguous)
+//   A quad-major (kAQuadMajor = true):  idx = tid + 256 i, row = idx >> 3, quad = idx & 7
+//                 — a warp covers 4 rows x 8 quads (coalesced when K is contiguous)
+//   B: idx = tid + 256 i, row = idx >> 3, quad = idx & 7 (kBQuadMajor) or row = idx % BN,
+//      quad = idx / BN
+template <int BN>
+struct Frag {
+  static constexpr int BQ = (BN * 8 + kThreads - 1) / kThreads;
+};
+
+__device__ __forceinline__ void a_map(bool quad_major, int tid, int i, int& row, int& q) {
+  if (quad_major) {
+    const int idx = tid + kThreads * i;
+    row = idx >> 3;
+    q = idx & 7;
+  } else {
+    row = tid & 127;
+    q = (tid >> 7) + 2 * i;
+  }
+}
+template <int BN>
+__device__ __forceinline__ bool b_map(bool quad_major, int tid, int i, int& row, int& q) {
+  const int idx = tid + kThreads * i;
+  if (quad_major) {
+    row = idx >> 3;
+    q = idx & 7;
+  } else {
+    row = idx % BN;
+    q = idx / BN;
+  }
+  return idx < BN * 8;
+}
+
 // Prob interface:
 //   int64_t M, N, K; int ksplit; int scratch;          max sizes, split-K factor, scratch bytes
 //   int64_t mdim(int z), kdim(int z) const;             per-batch M and K (<= M, K)
+//   static constexpr bool kAQuadMajor, kBQuadMajor, kCtaReduce;
 //   void setup(int z, int64_t m0, int64_t n0, uint8_t* scratch, int tid) const;   once per CTA
-//   template <int BN> void load_stage(int z, int64_t m0, int64_t n0, int64_t k0,
-//                                     const StageBufs&, const uint8_t* scratch, int tid) const;
+//   float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t* scratch) const;
+//   float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t* scratch) const;
+//        (4 consecutive k starting at k; zero outside the problem)
 //   void epilogue_row(int z, int split, int64_t m, int64_t n, const float* v, int nv, double& sq);
-//   static constexpr bool kCtaReduce; void epilogue_cta(int z, int split, double sq) const;
+//   void epilogue_cta(int z, int split, double sq) const;
+template <int BN, class Prob>
+__device__ __forceinline__ void fetch(const Prob& p, int z, int64_t m0, int64_t n0, int64_t k0,
+                                      const uint8_t* scratch, int tid, float4 (&ra)[4],
+                                      float4 (&rb)[Frag<BN>::BQ]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int row, q;
+    a_map(Prob::kAQuadMajor, tid, i, row, q);
+    ra[i] = p.a_quad(z, m0, row, k0 + 4 * q, scratch);
+  }
+#pragma unroll
+  for (int i = 0; i < Frag<BN>::BQ; ++i) {
+    int row, q;
+    if (b_map<BN>(Prob::kBQuadMajor, tid, i, row, q)) rb[i] = p.b_quad(z, n0, row, k0 + 4 * q, scratch);
+  }
+}
+
+template <int BN, class Prob>
+__device__ __forceinline__ void stash(int tid, const StageBufsT& sb, const float4 (&ra)[4],
+                                      const float4 (&rb)[Frag<BN>::BQ]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int row, q;
+    a_map(Prob::kAQuadMajor, tid, i, row, q);
+    put4(sb.a_hi, sb.a_lo, row, q, ra[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < Frag<BN>::BQ; ++i) {
+    int row, q;
+    if (b_map<BN>(Prob::kBQuadMajor, tid, i, row, q)) put4(sb.b_hi, sb.b_lo, row, q, rb[i]);
+  }
+}
+
 template <int BN, class Prob>
 __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
   extern __shared__ uint8_t smem_raw[];
@@ -216,12 +292,15 @@ __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
   const int ks1 = (int)((int64_t)(split + 1) * nk_all / p.ksplit);
   const int nk = ks1 - ks0;
   constexpr uint32_t idesc = idesc_tf32(BN);
+  float4 ra[4], rb[Frag<BN>::BQ];
+  if (nk > 0) fetch<BN>(p, z, m0, n0, (int64_t)ks0 * BK, scratch, tid, ra, rb);
   for (int i = 0; i < nk; ++i) {
     const int s = i % kStages;
     uint8_t* st = smem + s * S::STAGE;
-    StageBufs sb{st, st + S::A_BYTES, st + 2 * S::A_BYTES, st + 2 * S::A_BYTES + S::B_BYTES};
+    const StageBufsT sb{st, st + S::A_BYTES, st + 2 * S::A_BYTES, st + 2 * S::A_BYTES + S::B_BYTES};
     if (i >= kStages) mbar_wait(&bars[s], ((i / kStages) - 1) & 1);
-    p.template load_stage<BN>(z, m0, n0, (int64_t)(ks0 + i) * BK, sb, scratch, tid);
+    stash<BN, Prob>(tid, sb, ra, rb);
+    if (i + 1 < nk) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + i + 1) * BK, scratch, tid, ra, rb);
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
@@ -302,44 +381,15 @@ void launch_tc_auto(dpg_ctx* ctx, const Prob& p, int64_t batches) {
   }
 }
 
-// split-K factor so that tiles * batches * ksplit ~ 2 CTAs per SM, >= 2 K stages per split
+// split-K factor: only when the output tiles alone leave SMs idle; then ~2 CTAs per SM with
+// >= 2 K stages per split
 inline int pick_ksplit(int64_t M, int64_t N, int64_t K, int64_t batches) {
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + 127) / 128) * batches;
+  if (tiles >= kNumSMs) return 1;
   const int64_t nk = (K + BK - 1) / BK;
   int64_t ks = (2 * kNumSMs + tiles - 1) / tiles;
   ks = std::min<int64_t>(ks, std::max<int64_t>(1, nk / 2));
   return (int)std::max<int64_t>(1, std::min<int64_t>(ks, 16));
-}
-
-// ---- common loader patterns (256 threads) ----
-// A tile: 128 rows x 8 quads; thread t owns row t & 127, quads (t >> 7) + 2 i, i = 0..3
-template <class F>
-__device__ __forceinline__ void load_rows128(const StageBufs& sb, int tid, F&& quad /* float4(row, q) */) {
-  const int row = tid & 127;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int q = (tid >> 7) + 2 * i;
-    put4(sb.a_hi, sb.a_lo, row, q, quad(row, q));
-  }
-}
-// B tile, row-major spread: consecutive threads take consecutive rows (coalesced when the
-// operand's rows are contiguous in memory and its K is strided)
-template <int BN, class F>
-__device__ __forceinline__ void load_b_cols(const StageBufs& sb, int tid, F&& quad) {
-#pragma unroll
-  for (int idx = tid; idx < BN * 8; idx += kThreads) {
-    const int row = idx % BN, q = idx / BN;
-    put4(sb.b_hi, sb.b_lo, row, q, quad(row, q));
-  }
-}
-// B tile: BN rows x 8 quads spread over the 256 threads, quads of a row on consecutive threads
-template <int BN, class F>
-__device__ __forceinline__ void load_b_rows(const StageBufs& sb, int tid, F&& quad) {
-#pragma unroll
-  for (int idx = tid; idx < BN * 8; idx += kThreads) {
-    const int row = idx >> 3, q = idx & 7;
-    put4(sb.b_hi, sb.b_lo, row, q, quad(row, q));
-  }
 }
 
 }  // namespace tc
