@@ -60,17 +60,18 @@ void launch_clip_factors(dpg_ctx* ctx, const double* slab, const int32_t* row_pa
 // optimizer.hpp:245-250 when accumulating over virtual steps.
 // ------------------------------------------------------------------------------------------
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int64_t n,
-                                     float* __restrict__ out, int accumulate) {
+                                     int64_t zstride, float* __restrict__ out, int accumulate) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float acc = 0.f;
-  for (int z = 0; z < splits; ++z) acc = __fadd_rn(acc, part[(int64_t)z * n + i]);
+  for (int z = 0; z < splits; ++z) acc = __fadd_rn(acc, part[(int64_t)z * zstride + i]);
   out[i] = accumulate ? __fadd_rn(out[i], acc) : acc;
 }
 
 static void launch_splitk_reduce(dpg_ctx* ctx, const float* part, int splits, int64_t n, float* out,
-                                 int accumulate) {
-  splitk_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(part, splits, n, out, accumulate);
+                                 int accumulate, int64_t zstride = -1) {
+  splitk_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+      part, splits, n, zstride < 0 ? n : zstride, out, accumulate);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -300,23 +301,24 @@ size_t clipped_sum_ws_conv2d(const ConvGeom& g) {
 void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
                                const float* scale, const ConvGeom& g, float* sw, float* sb,
                                int accumulate, void* ws) {
-  (void)sb;
+  (void)sb;  // the bias clipped sum is a weighted sum of the bias records (launch_wsum_multi)
+  const int64_t nw = g.oc * g.K();
   if (ds::enabled()) {
     const int splits = ds::csum_splits(g);
     ds::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
-    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, g.oc * g.K(), sw, accumulate);
+    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
     return;
   }
   if (ps::supported_csum(g)) {
     const int splits = ps::csum_splits(g);
     ps::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
-    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, g.oc * g.K(), sw, accumulate);
+    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
     return;
   }
   if (use_tc()) {
     const int splits = tc::csum_conv_splits(g);
     tc::conv_csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
-    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, g.oc * g.K(), sw, accumulate);
+    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
     return;
   }
   int bm, bn;

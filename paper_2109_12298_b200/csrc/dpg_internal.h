@@ -181,6 +181,18 @@ void linear_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, con
                  int64_t b, int64_t mid, int64_t d, int64_t r, float* part, int splits);
 }  // namespace tc
 
+namespace cv {
+bool enabled();
+bool fwd_supported(const ConvGeom& g);
+size_t fwd_ws_bytes(const ConvGeom& g);
+void conv_fwd(dpg_ctx* ctx, const float* x, int relu, const float* w, const float* bias, const ConvGeom& g,
+              float* y, void* ws);
+bool dgrad_supported(const ConvGeom& g);
+size_t dgrad_ws_bytes(const ConvGeom& g);
+void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g, const float* mask,
+                float* dx, void* ws);
+}  // namespace cv
+
 namespace ds {
 bool enabled();
 int gs_rows(const ConvGeom& g);
@@ -196,7 +208,7 @@ bool supported(const ConvGeom& g);       // per-sample gradient path
 bool supported_csum(const ConvGeom& g);  // clipped-sum path (A/B only)
 int gs_rows(const ConvGeom& g);
 void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
-        double* sq_part);
+        double* sq_part, float* gb = nullptr, double* sq_b = nullptr);
 int csum_splits(const ConvGeom& g);
 void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* scale,
           const ConvGeom& g, float* part, int splits);
@@ -208,8 +220,12 @@ int sq_rows_conv2d(const ConvGeom& g);
 int sq_rows_embedding(int64_t vocab, int64_t dim);
 void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw, int64_t b,
                       int64_t mid, int64_t d, int64_t r, float* gw, double* sq_part);
+// gb / sq_b (optional): the bias rule fused into the same launch when gs_conv2d_fuses_bias(g)
+// (sq_b then has sq_rows_conv2d_bias(g) rows), else a separate bias launch (one row)
 void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& g,
-                      float* gw, double* sq_part);
+                      float* gw, double* sq_part, float* gb = nullptr, double* sq_b = nullptr);
+bool gs_conv2d_fuses_bias(const ConvGeom& g);
+int sq_rows_conv2d_bias(const ConvGeom& g);
 // bias rule: gb[n,o] = sum over middle of hw; `hw_layout_conv` selects [b, o, P] vs [b, mid, o]
 void launch_gs_bias(dpg_ctx* ctx, const float* hw, int64_t b, int64_t mid, int64_t r,
                     bool hw_layout_conv, float* gb, double* sq_part);

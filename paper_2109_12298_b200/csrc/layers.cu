@@ -43,14 +43,22 @@ struct ConvFwdProb {
   }
 };
 
-size_t conv_fwd_ws_bytes(const ConvGeom& g) { return use_tc() ? tc::fwd_ws_bytes(g) : 0; }
+size_t conv_fwd_ws_bytes(const ConvGeom& g) {
+  if (cv::fwd_supported(g)) return cv::fwd_ws_bytes(g);
+  return use_tc() ? tc::fwd_ws_bytes(g) : 0;
+}
 size_t conv_dgrad_ws_bytes(const ConvGeom& g) {
+  if (cv::dgrad_supported(g)) return cv::dgrad_ws_bytes(g);
   return (use_tc() && tc::dgrad_supported(g)) ? tc::dgrad_ws_bytes(g) : 0;
 }
 
 void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
                        const ConvGeom& g, float* y, void* ws) {
   if (g.b == 0) return;
+  if (ws && cv::fwd_supported(g)) {
+    cv::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws);
+    return;
+  }
   if (use_tc()) {
     tc::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws);
     return;
@@ -127,6 +135,10 @@ struct ConvDgradProb {
 void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
                          const float* mask_src, float* dx, void* ws) {
   if (g.b == 0) return;
+  if (ws && cv::dgrad_supported(g)) {
+    cv::conv_dgrad(ctx, dy, w, g, mask_src, dx, ws);
+    return;
+  }
   if (use_tc() && tc::dgrad_supported(g)) {
     tc::conv_dgrad(ctx, dy, w, g, mask_src, dx, ws);
     return;

@@ -244,6 +244,12 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
         {
           dpg::ProfScope ps(ctx, "gs.conv2d" + ls, 4.0 * b * (lp.in_numel + lp.out_numel) + gwrite,
                             2.0 * b * g.oc * g.K() * g.P());
+          if (lp.nparams > 1 && dpg::gs_conv2d_fuses_bias(g)) {
+            // bias rule in the same launch (its norm rows: one per oc tile)
+            dpg::launch_gs_conv2d(ctx, in, lp.in_relu, hw, g, gw, sq_w, gs_ptr(o, lp.param0 + 1, b),
+                                  slab + (int64_t)m->params[lp.param0 + 1].sq_row0 * b);
+            break;
+          }
           dpg::launch_gs_conv2d(ctx, in, lp.in_relu, hw, g, gw, sq_w);
         }
         if (lp.nparams > 1) bias_rule(g.P(), g.oc, true);
@@ -545,6 +551,7 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
       for (int k = 0; k < lp.nparams; ++k) {
         ParamInfo& pi = m->params[lp.param0 + k];
         int r = 1;
+        if (pi.is_bias && lp.kind == DPG_LAYER_CONV2D) r = dpg::sq_rows_conv2d_bias(lp.g);
         if (!pi.is_bias) {
           if (lp.kind == DPG_LAYER_LINEAR) r = dpg::sq_rows_linear(lp.mid, lp.d.in_features, lp.d.out_features);
           else if (lp.kind == DPG_LAYER_CONV2D) r = dpg::sq_rows_conv2d(lp.g);

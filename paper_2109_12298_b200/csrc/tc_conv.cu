@@ -47,7 +47,13 @@ struct PEnt {
   short y, x;
 };
 
-constexpr int kBad = -(1 << 14);  // sentinel coordinate: (unsigned)(kBad + small) >= h, w
+constexpr int kBad = -(1 << 14);
+
+__device__ __forceinline__ float4 relu4(float4 v, int relu) {
+  return make_float4(relu_if(v.x, relu), relu_if(v.y, relu), relu_if(v.z, relu), relu_if(v.w, relu));
+}
+#define DPG_NO_FIX(NAME) \
+  __device__ float4 NAME(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return v; }  // sentinel coordinate: (unsigned)(kBad + small) >= h, w
 
 // k-table for kcol 0 .. kpad (entries >= K are sentinels that fail every bound check)
 __device__ __forceinline__ void build_ktab(const Geo& g, KEnt* t, int tid, int K, int kpad) {
@@ -114,17 +120,20 @@ struct ConvFwd {
     for (int e = 0; e < 4; ++e) {
       const KEnt t = kt[e];
       const bool ok = (unsigned)(r.iy0 + t.ki) < (unsigned)g.h && (unsigned)(r.ix0 + t.kj) < (unsigned)g.w;
-      v[e] = ok ? relu_if(__ldg(r.xr + t.off), relu) : 0.f;
+      v[e] = __ldg(ok ? r.xr + t.off : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
   __device__ float4 b_quad(int, int64_t n0, int row, int64_t k, const uint8_t*) const {
     const int64_t n = n0 + row;
+    if ((K & 3) == 0) return __ldg(reinterpret_cast<const float4*>(n < N && k < K ? wt + n * K + k : g_zero4));
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = (n < N && k + e < K) ? __ldg(wt + n * K + k + e) : 0.f;
+    for (int e = 0; e < 4; ++e) v[e] = __ldg(n < N && k + e < K ? wt + n * K + k + e : g_zero4);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  DPG_NO_FIX(b_fix)
   __device__ void epilogue_row(int, int split, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     if (ksplit > 1) {
       float* out = part + ((int64_t)split * N + n0) * M + m;
@@ -245,10 +254,11 @@ struct ConvDgrad {
     for (int e = 0; e < 4; ++e) {
       const TEnt t = tt[e];
       const bool ok = (unsigned)(r.oy0 - t.a) < (unsigned)g.oh && (unsigned)(r.ox0 - t.c) < (unsigned)g.ow;
-      v[e] = ok ? __ldg(r.dr + t.delta) : 0.f;
+      v[e] = __ldg(ok ? r.dr + t.delta : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  DPG_NO_FIX(a_fix)
   __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t* s) const {
     const DClass& c = cls[z];
     const TEnt* tt = reinterpret_cast<const TEnt*>(s);
@@ -256,15 +266,15 @@ struct ConvDgrad {
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      v[e] = 0.f;
-      if (ch < N && k + e < c.K) {
-        const TEnt t = tt[k + e];
-        v[e] = __ldg(wt + (((int64_t)t.o * g.ic + ch) * g.kh + c.ry + g.stride * t.a) * g.kw + c.rx +
-                     g.stride * t.c);
-      }
+      const TEnt t = tt[k + e];  // (table padded to whole stages)
+      const bool ok = ch < N && k + e < c.K;
+      v[e] = __ldg(ok ? wt + (((int64_t)t.o * g.ic + ch) * g.kh + c.ry + g.stride * t.a) * g.kw + c.rx +
+                            g.stride * t.c
+                      : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  DPG_NO_FIX(b_fix)
   __device__ void epilogue_row(int z, int split, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     const DClass& c = cls[z];
     const int per = c.hc * c.wc;
@@ -389,28 +399,28 @@ struct ConvGs {
     const PEnt* pt = reinterpret_cast<const PEnt*>(s);
     const Row r = reinterpret_cast<const Row*>(s + ((4 * K + 15) & ~15))[row];
     const float* xs = x + (int64_t)z * g.ic * g.h * g.w + r.plane;
+    const bool row_ok = m0 + row < M;
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      v[e] = 0.f;
-      if (m0 + row < M && k + e < K) {
-        const PEnt t = pt[k + e];
-        const int iy = t.y + r.ki, ix = t.x + r.kj;
-        if ((unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w)
-          v[e] = relu_if(__ldg(xs + iy * g.w + ix), relu);
-      }
+      const PEnt t = pt[min((int)(k + e), (int)K - 1)];
+      const int iy = t.y + r.ki, ix = t.x + r.kj;
+      const bool ok = row_ok && k + e < K && (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
+      v[e] = __ldg(ok ? xs + iy * g.w + ix : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
   __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
     const int64_t oc = n0 + row;
     const float* h = hw + ((int64_t)z * g.oc + oc) * K;
-    if (oc < N && (K & 3) == 0 && k < K) return __ldg(reinterpret_cast<const float4*>(h + k));
+    if ((K & 3) == 0) return __ldg(reinterpret_cast<const float4*>(oc < N && k < K ? h + k : g_zero4));
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = (oc < N && k + e < K) ? __ldg(h + k + e) : 0.f;
+    for (int e = 0; e < 4; ++e) v[e] = __ldg(oc < N && k + e < K ? h + k + e : g_zero4);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  DPG_NO_FIX(b_fix)
   __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double& sq) const {
     float* out = gw ? gw + ((int64_t)z * g.oc + n0) * g.Kc + m : nullptr;
     for (int j = 0; j < nv; ++j) {
@@ -472,50 +482,51 @@ struct ConvCsum {
   __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t* s) const {
     const PEnt* pt = reinterpret_cast<const PEnt*>(s);
     const Row r = reinterpret_cast<const Row*>(s + ((4 * g.P + 15) & ~15))[row];
+    const bool row_ok = m0 + row < M;
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      v[e] = 0.f;
-      if (m0 + row < M && k + e < K) {
-        uint32_t qq, pp;
-        g.fP.divmod((uint32_t)(k + e), qq, pp);
-        const int64_t n = (int64_t)z * spl + qq;
-        if (n < bsz) {
-          const PEnt t = pt[pp];
-          const int iy = t.y + r.ki, ix = t.x + r.kj;
-          if ((unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w)
-            v[e] = relu_if(__ldg(x + n * g.ic * g.h * g.w + r.plane + iy * g.w + ix), relu);
-        }
-      }
+      uint32_t qq, pp;
+      g.fP.divmod((uint32_t)(k + e), qq, pp);
+      const int64_t n = (int64_t)z * spl + qq;
+      const PEnt t = pt[pp];
+      const int iy = t.y + r.ki, ix = t.x + r.kj;
+      const bool ok = row_ok && k + e < K && n < bsz && (unsigned)iy < (unsigned)g.h &&
+                      (unsigned)ix < (unsigned)g.w;
+      v[e] = __ldg(ok ? x + n * g.ic * g.h * g.w + r.plane + iy * g.w + ix : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
+  // raw highway values; the clip scale s_n is applied when the stage is stored (b_fix)
   __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
     const int64_t oc = n0 + row;
     if ((g.P & 3) == 0) {
       uint32_t qq, pp;
       g.fP.divmod((uint32_t)k, qq, pp);
       const int64_t n = (int64_t)z * spl + qq;
-      if (oc < N && k < K && n < bsz) {
-        const float sc = __ldg(scale + n);
-        float4 h = __ldg(reinterpret_cast<const float4*>(hw + (n * g.oc + oc) * g.P + pp));
-        h.x *= sc; h.y *= sc; h.z *= sc; h.w *= sc;
-        return h;
-      }
-      return make_float4(0.f, 0.f, 0.f, 0.f);
+      const bool ok = oc < N && k < K && n < bsz;
+      return __ldg(reinterpret_cast<const float4*>(ok ? hw + (n * g.oc + oc) * g.P + pp : g_zero4));
     }
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      v[e] = 0.f;
-      if (oc < N && k + e < K) {
-        uint32_t qq, pp;
-        g.fP.divmod((uint32_t)(k + e), qq, pp);
-        const int64_t n = (int64_t)z * spl + qq;
-        if (n < bsz) v[e] = __ldg(scale + n) * __ldg(hw + (n * g.oc + oc) * g.P + pp);
-      }
+      uint32_t qq, pp;
+      g.fP.divmod((uint32_t)(k + e), qq, pp);
+      const int64_t n = (int64_t)z * spl + qq;
+      const bool ok = oc < N && k + e < K && n < bsz;
+      v[e] = __ldg(ok ? hw + (n * g.oc + oc) * g.P + pp : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ float4 b_fix(int z, int64_t, int, int64_t k, const uint8_t*, float4 v) const {
+    float sc[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t n = (int64_t)z * spl + g.fP.div((uint32_t)(k + e));
+      sc[e] = __ldg(n < bsz ? scale + n : g_zero4);
+    }
+    return make_float4(sc[0] * v.x, sc[1] * v.y, sc[2] * v.z, sc[3] * v.w);
   }
   __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     float* out = part + ((int64_t)z * g.oc + n0) * g.Kc + m;
@@ -564,16 +575,18 @@ struct LinGs {
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      v[e] = (i < M && k + e < K) ? relu_if(__ldg(acts + ((int64_t)z * K + k + e) * M + i), relu) : 0.f;
+      v[e] = __ldg(i < M && k + e < K ? acts + ((int64_t)z * K + k + e) * M + i : g_zero4);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
   __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
     const int64_t o = n0 + row;
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = (o < N && k + e < K) ? __ldg(hw + ((int64_t)z * K + k + e) * N + o) : 0.f;
+    for (int e = 0; e < 4; ++e) v[e] = __ldg(o < N && k + e < K ? hw + ((int64_t)z * K + k + e) * N + o : g_zero4);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  DPG_NO_FIX(b_fix)
   __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double& sq) const {
     float* out = gw ? gw + ((int64_t)z * N + n0) * M + m : nullptr;
     for (int j = 0; j < nv; ++j) {
@@ -616,30 +629,35 @@ struct LinCsum {
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      v[e] = 0.f;
-      if (i < M && k + e < K) {
-        uint32_t qq, t;
-        fmid.divmod((uint32_t)(k + e), qq, t);
-        const int64_t n = (int64_t)z * spl + qq;
-        if (n < bsz) v[e] = relu_if(__ldg(acts + (n * mid + t) * M + i), relu);
-      }
+      uint32_t qq, t;
+      fmid.divmod((uint32_t)(k + e), qq, t);
+      const int64_t n = (int64_t)z * spl + qq;
+      v[e] = __ldg(i < M && k + e < K && n < bsz ? acts + (n * mid + t) * M + i : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
+  __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
+  // raw highway values; the clip scale s_n is applied when the stage is stored (b_fix)
   __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
     const int64_t o = n0 + row;
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      v[e] = 0.f;
-      if (o < N && k + e < K) {
-        uint32_t qq, t;
-        fmid.divmod((uint32_t)(k + e), qq, t);
-        const int64_t n = (int64_t)z * spl + qq;
-        if (n < bsz) v[e] = __ldg(scale + n) * __ldg(hw + (n * mid + t) * N + o);
-      }
+      uint32_t qq, t;
+      fmid.divmod((uint32_t)(k + e), qq, t);
+      const int64_t n = (int64_t)z * spl + qq;
+      v[e] = __ldg(o < N && k + e < K && n < bsz ? hw + (n * mid + t) * N + o : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ float4 b_fix(int z, int64_t, int, int64_t k, const uint8_t*, float4 v) const {
+    float sc[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t n = (int64_t)z * spl + fmid.div((uint32_t)(k + e));
+      sc[e] = __ldg(n < bsz ? scale + n : g_zero4);
+    }
+    return make_float4(sc[0] * v.x, sc[1] * v.y, sc[2] * v.z, sc[3] * v.w);
   }
   __device__ void epilogue_row(int z, int, int64_t m, int64_t n0, const float* v, int nv, double&) const {
     float* out = part + ((int64_t)z * N + n0) * M + m;

@@ -11,7 +11,7 @@
 // double buffered: the MMAs of stage s run asynchronously while the threads gather stage s+1;
 // tcgen05.commit arrives on the stage's mbarrier to release the buffer.
 //
-// Operands for stage s+1 are fetched into registers while stage s is stored and its MMAs run.
+// Operands for stage s+2 are fetched into registers while stage s is stored and its MMAs run.
 //
 // Epilogue: tcgen05.ld; warp w owns TMEM lanes [32 (w % 4), +32) (= tile rows) and the column
 // half w / 4; each thread hands its row's values to Prob::epilogue_row.
@@ -213,6 +213,11 @@ __device__ __forceinline__ bool b_map(bool quad_major, int tid, int i, int& row,
   return idx < BN * 8;
 }
 
+// Zero word that out-of-range gathers load from: operand loads are unconditional (the address is
+// selected, not the load), so a thread's gathers for a stage are all in flight at once and nothing
+// consumes a loaded value before the stage is stored.
+static __device__ __align__(16) const float g_zero4[4] = {0.f, 0.f, 0.f, 0.f};
+
 // Prob interface:
 //   int64_t M, N, K; int ksplit; int scratch;          max sizes, split-K factor, scratch bytes
 //   int64_t mdim(int z), kdim(int z) const;             per-batch M and K (<= M, K)
@@ -220,7 +225,9 @@ __device__ __forceinline__ bool b_map(bool quad_major, int tid, int i, int& row,
 //   void setup(int z, int64_t m0, int64_t n0, uint8_t* scratch, int tid) const;   once per CTA
 //   float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t* scratch) const;
 //   float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t* scratch) const;
-//        (4 consecutive k starting at k; zero outside the problem)
+//        (4 consecutive k starting at k, raw loads; zero outside the problem)
+//   float4 a_fix(...same..., float4 v) const; float4 b_fix(...same..., float4 v) const;
+//        (applied when the stage is stored: ReLU of a folded activation, clip scale, ...)
 //   void epilogue_row(int z, int split, int64_t m, int64_t n, const float* v, int nv, double& sq);
 //   void epilogue_cta(int z, int split, double sq) const;
 template <int BN, class Prob>
@@ -241,25 +248,29 @@ __device__ __forceinline__ void fetch(const Prob& p, int z, int64_t m0, int64_t 
 }
 
 template <int BN, class Prob>
-__device__ __forceinline__ void stash(int tid, const StageBufsT& sb, const float4 (&ra)[4],
-                                      const float4 (&rb)[Frag<BN>::BQ]) {
+__device__ __forceinline__ void stash(const Prob& p, int z, int64_t m0, int64_t n0, int64_t k0,
+                                      const uint8_t* scratch, int tid, const StageBufsT& sb,
+                                      const float4 (&ra)[4], const float4 (&rb)[Frag<BN>::BQ]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int row, q;
     a_map(Prob::kAQuadMajor, tid, i, row, q);
-    put4(sb.a_hi, sb.a_lo, row, q, ra[i]);
+    put4(sb.a_hi, sb.a_lo, row, q, p.a_fix(z, m0, row, k0 + 4 * q, scratch, ra[i]));
   }
 #pragma unroll
   for (int i = 0; i < Frag<BN>::BQ; ++i) {
     int row, q;
-    if (b_map<BN>(Prob::kBQuadMajor, tid, i, row, q)) put4(sb.b_hi, sb.b_lo, row, q, rb[i]);
+    if (b_map<BN>(Prob::kBQuadMajor, tid, i, row, q))
+      put4(sb.b_hi, sb.b_lo, row, q, p.b_fix(z, n0, row, k0 + 4 * q, scratch, rb[i]));
   }
 }
 
 template <int BN, class Prob>
-__global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
+__global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const Prob p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024 B alignment by pointer arithmetic on the __shared__ array, so the compiler keeps the
+  // shared address space (LDS / STS, not generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   using S = Smem<BN>;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * S::STAGE);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kStages);
@@ -292,15 +303,18 @@ __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
   const int ks1 = (int)((int64_t)(split + 1) * nk_all / p.ksplit);
   const int nk = ks1 - ks0;
   constexpr uint32_t idesc = idesc_tf32(BN);
-  float4 ra[4], rb[Frag<BN>::BQ];
-  if (nk > 0) fetch<BN>(p, z, m0, n0, (int64_t)ks0 * BK, scratch, tid, ra, rb);
-  for (int i = 0; i < nk; ++i) {
+  // Two register sets: the operands of stage i + 2 are requested while stage i is stored, so each
+  // gather has a full stage period (store + barrier + MMA issue of the previous stage) to land.
+  float4 ra0[4], rb0[Frag<BN>::BQ], ra1[4], rb1[Frag<BN>::BQ];
+  if (nk > 0) fetch<BN>(p, z, m0, n0, (int64_t)ks0 * BK, scratch, tid, ra0, rb0);
+  if (nk > 1) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + 1) * BK, scratch, tid, ra1, rb1);
+  auto stage = [&](int i, float4 (&ra)[4], float4 (&rb)[Frag<BN>::BQ]) {
     const int s = i % kStages;
     uint8_t* st = smem + s * S::STAGE;
     const StageBufsT sb{st, st + S::A_BYTES, st + 2 * S::A_BYTES, st + 2 * S::A_BYTES + S::B_BYTES};
     if (i >= kStages) mbar_wait(&bars[s], ((i / kStages) - 1) & 1);
-    stash<BN, Prob>(tid, sb, ra, rb);
-    if (i + 1 < nk) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + i + 1) * BK, scratch, tid, ra, rb);
+    stash<BN, Prob>(p, z, m0, n0, (int64_t)(ks0 + i) * BK, scratch, tid, sb, ra, rb);
+    if (i + 2 < nk) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + i + 2) * BK, scratch, tid, ra, rb);
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
@@ -317,6 +331,11 @@ __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const Prob p) {
       }
       mma_commit(&bars[s]);
     }
+  };
+#pragma unroll 1
+  for (int i = 0; i < nk; i += 2) {
+    stage(i, ra0, rb0);
+    if (i + 1 < nk) stage(i + 1, ra1, rb1);
   }
   if (nk > 0) mbar_wait(&bars[(nk - 1) % kStages], ((nk - 1) / kStages) & 1);
   tc_fence_after();
