@@ -203,6 +203,13 @@ void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* 
           const ConvGeom& g, float* part, int splits);
 }  // namespace ds
 
+namespace rs {
+bool supported(const ConvGeom& g);  // per-sample gradients, P <= 16
+int gs_rows(const ConvGeom& g);
+void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
+        double* sq_part, float* gb = nullptr, double* sq_b = nullptr);
+}  // namespace rs
+
 namespace ps {
 bool supported(const ConvGeom& g);       // per-sample gradient path
 bool supported_csum(const ConvGeom& g);  // clipped-sum path (A/B only)

@@ -309,12 +309,8 @@ static int force_mode() {
   return force;
 }
 
-// Per-sample gradients with few positions per sample (P <= 16: 4-16 MACs per stored float) are
-// store-bound and go to this kernel; larger P to tcgen05 (measured).
-bool supported(const ConvGeom& g) {
-  if (!fits(g) || force_mode() == 0) return false;
-  return force_mode() == 1 || g.P() <= 16;
-}
+// A/B alternative to rows_conv (P <= 16) and tcgen05 (larger P): forced with DPG_PS=1.
+bool supported(const ConvGeom& g) { return force_mode() == 1 && fits(g); }
 // the clipped sums stay on tcgen05 unless forced (measured faster there)
 bool supported_csum(const ConvGeom& g) { return force_mode() == 1 && fits(g); }
 

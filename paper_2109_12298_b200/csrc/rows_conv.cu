@@ -1,0 +1,227 @@
+// rows_conv.cu — per-sample conv gradients for layers with few positions per sample (P <= 16).
+//
+//   G[n][oc][kcol] = sum_p B[n, oc, p] X~[n, kcol, p]     (per_sample_rule_conv2d,
+//                    grad_sample.hpp:135-150) + the fused ||G_n||^2 partial
+//   gb[n][oc]      = (float) sum_p (double) B[n, oc, p]   (bias rule, sum_middle order,
+//                    tensor.hpp:197-205) + its squared norm
+//
+// With P <= 16 every output costs at most 16 MACs, so the layer is bound by the HBM write of G
+// (the largest stream of the whole step: CIFAR conv4 alone is 151 MB at b = 512). The kernel is
+// built around that store stream: one CTA owns one sample and a contiguous half (or all) of its
+// output channels; im2col of the sample (P x Kc, ReLU applied) and the highway rows of its channels
+// are staged once in shared memory; then each warp produces two output rows at a time — the P
+// highway values of each row are warp-uniform registers, lanes walk the row in 16-byte chunks,
+// every chunk is P shared-memory reads shared by both rows, 8 P FMAs and two 128-bit streaming
+// stores, so consecutive lanes write consecutive 16 B of G (512 B per warp store).
+#include <cstdlib>
+
+#include "conv_common.cuh"
+
+namespace dpg {
+namespace rs {
+
+constexpr int kThreads = 256;
+constexpr int kMaxP = 16;
+
+struct Params {
+  const float* x;
+  int relu;
+  const float* hw;
+  float* gw;         // [b, oc, Kc] (nullptr: norms only)
+  double* sq_part;   // [osplit, b]
+  float* gb;         // [b, oc] (nullptr: no bias record)
+  double* sq_b;      // [osplit, b] (nullptr: no bias rule)
+  int64_t b;
+  int ic, h, w, oc, kh, kw, stride, pad, ow, P, Kc, Kc4, osplit, opart;
+};
+
+template <int PT>
+__global__ void __launch_bounds__(kThreads, 2) gs_rows_kernel(const Params p) {
+  extern __shared__ __align__(16) float sm[];
+  float* xt = sm;                                          // [PT][Kc4], rows >= P are zero
+  float* hs = xt + PT * p.Kc4;                             // [opart][PT], cols >= P are zero
+  int* kt = reinterpret_cast<int*>(hs + p.opart * PT);     // [Kc4] packed (c, ki, kj) or -1
+  __shared__ double red[2][kThreads / 32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = blockIdx.y;
+  const int part = blockIdx.x;
+  const int o_begin = part * p.opart;
+  const int o_end = min(p.oc, o_begin + p.opart);
+  const int nrow = o_end - o_begin;
+  const int hwsz = p.h * p.w;
+
+  for (int k = tid; k < p.Kc4; k += kThreads) {
+    int e = -1;
+    if (k < p.Kc) {
+      const int khw = p.kh * p.kw;
+      const int c = k / khw, r = k - c * khw;
+      const int ki = r / p.kw, kj = r - ki * p.kw;
+      e = (c << 10) | (ki << 5) | kj;  // ic < 2^21, kh, kw < 32
+    }
+    kt[k] = e;
+  }
+  // highway rows of this part: contiguous [nrow][P] in B[n]
+  const float* hrow = p.hw + ((int64_t)n * p.oc + o_begin) * p.P;
+  for (int i = tid; i < nrow * PT; i += kThreads) {
+    const int o = i / PT, q = i - o * PT;
+    hs[i] = q < p.P ? __ldg(hrow + o * p.P + q) : 0.f;
+  }
+  __syncthreads();
+  // im2col of sample n: xt[q][k] = relu(x[n, c, oy s + ki - pad, ox s + kj - pad])
+  const float* xn = p.x + n * p.ic * hwsz;
+  int by[PT], bx[PT];  // window origin of each position
+#pragma unroll
+  for (int q = 0; q < PT; ++q) {
+    const int oy = q / p.ow, ox = q - oy * p.ow;
+    by[q] = oy * p.stride - p.pad;
+    bx[q] = ox * p.stride - p.pad;
+  }
+  for (int k = tid; k < p.Kc4; k += kThreads) {
+    const int e = kt[k];
+    const int coff = (e >> 10) * hwsz, ki = (e >> 5) & 31, kj = e & 31;
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+      const int iy = by[q] + ki, ix = bx[q] + kj;
+      const bool ok = e >= 0 && q < p.P && (unsigned)iy < (unsigned)p.h && (unsigned)ix < (unsigned)p.w;
+      const float v = __ldg(ok ? xn + coff + iy * p.w + ix : xn);
+      xt[q * p.Kc4 + k] = ok ? relu_if(v, p.relu) : 0.f;
+    }
+  }
+  __syncthreads();
+
+  double sq = 0.0, sqb = 0.0;
+  const int nq = p.Kc4 >> 2;
+  const bool vec = (p.Kc & 3) == 0;
+  for (int r0 = 2 * warp; r0 < nrow; r0 += 2 * (kThreads / 32)) {
+    const bool two = r0 + 1 < nrow;
+    float b0[PT], b1[PT];
+#pragma unroll
+    for (int q = 0; q < PT; q += 4) {
+      const float4 u = *reinterpret_cast<const float4*>(hs + r0 * PT + q);
+      const float4 v = two ? *reinterpret_cast<const float4*>(hs + (r0 + 1) * PT + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      b0[q] = u.x; b0[q + 1] = u.y; b0[q + 2] = u.z; b0[q + 3] = u.w;
+      b1[q] = v.x; b1[q + 1] = v.y; b1[q + 2] = v.z; b1[q + 3] = v.w;
+    }
+    if (p.sq_b && lane < 2 && (lane == 0 || two)) {
+      // bias rule for row r0 + lane: sequential fp64 sum over the P positions
+      const float* hb = hs + (r0 + lane) * PT;
+      double a = 0.0;
+      for (int q = 0; q < p.P; ++q) a += (double)hb[q];
+      const float v = (float)a;
+      if (p.gb) p.gb[n * p.oc + o_begin + r0 + lane] = v;
+      sqb += (double)v * v;
+    }
+    float* g0 = p.gw ? p.gw + (n * p.oc + o_begin + r0) * (int64_t)p.Kc : nullptr;
+    for (int j = lane; j < nq; j += 32) {
+      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+#pragma unroll
+      for (int q = 0; q < PT; ++q) {
+        const float4 xv = *reinterpret_cast<const float4*>(xt + q * p.Kc4 + 4 * j);
+        a0.x = fmaf(b0[q], xv.x, a0.x); a0.y = fmaf(b0[q], xv.y, a0.y);
+        a0.z = fmaf(b0[q], xv.z, a0.z); a0.w = fmaf(b0[q], xv.w, a0.w);
+        a1.x = fmaf(b1[q], xv.x, a1.x); a1.y = fmaf(b1[q], xv.y, a1.y);
+        a1.z = fmaf(b1[q], xv.z, a1.z); a1.w = fmaf(b1[q], xv.w, a1.w);
+      }
+      const int k0 = 4 * j;
+      if (vec) {
+        if (g0) {
+          st_stream4(g0 + k0, a0);
+          if (two) st_stream4(g0 + p.Kc + k0, a1);
+        }
+        sq += (double)a0.x * a0.x + (double)a0.y * a0.y + (double)a0.z * a0.z + (double)a0.w * a0.w;
+        if (two) sq += (double)a1.x * a1.x + (double)a1.y * a1.y + (double)a1.z * a1.z + (double)a1.w * a1.w;
+      } else {
+        const float v0[4] = {a0.x, a0.y, a0.z, a0.w}, v1[4] = {a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (k0 + e >= p.Kc) continue;
+          if (g0) st_stream(g0 + k0 + e, v0[e]);
+          sq += (double)v0[e] * v0[e];
+          if (two) {
+            if (g0) st_stream(g0 + p.Kc + k0 + e, v1[e]);
+            sq += (double)v1[e] * v1[e];
+          }
+        }
+      }
+    }
+  }
+  // deterministic block sums (fixed tree)
+  sq = warp_sum(sq);
+  sqb = warp_sum(sqb);
+  if (lane == 0) {
+    red[0][warp] = sq;
+    red[1][warp] = sqb;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0, tb = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) {
+      t += red[0][i];
+      tb += red[1][i];
+    }
+    if (p.sq_part) p.sq_part[(int64_t)part * p.b + n] = t;
+    if (p.sq_b) p.sq_b[(int64_t)part * p.b + n] = tb;
+  }
+}
+
+static int pick_pt(int P) { return P <= 4 ? 4 : (P <= 8 ? 8 : 16); }
+
+static Params make_params(const float* x, int relu, const float* hw, const ConvGeom& g) {
+  Params p{};
+  p.x = x; p.relu = relu; p.hw = hw;
+  p.b = g.b;
+  p.ic = (int)g.ic; p.h = (int)g.h; p.w = (int)g.w; p.oc = (int)g.oc;
+  p.kh = (int)g.kh; p.kw = (int)g.kw; p.stride = (int)g.stride; p.pad = (int)g.pad;
+  p.ow = (int)g.ow; p.P = (int)g.P(); p.Kc = (int)g.K();
+  p.Kc4 = (p.Kc + 3) & ~3;
+  // two channel halves per sample for wide layers: twice the CTAs (shorter tail), im2col built twice
+  p.osplit = g.oc >= 64 ? 2 : 1;
+  p.opart = (int)((g.oc + p.osplit - 1) / p.osplit);
+  return p;
+}
+
+static size_t smem_bytes(const Params& p) {
+  const int PT = pick_pt(p.P);
+  return sizeof(float) * ((size_t)PT * p.Kc4 + (size_t)p.opart * PT) + sizeof(int) * (size_t)p.Kc4;
+}
+
+bool supported(const ConvGeom& g) {
+  static const bool off = [] {
+    const char* e = std::getenv("DPG_RS");
+    return e && e[0] == '0';
+  }();
+  if (off || g.P() > kMaxP || g.kh >= 32 || g.kw >= 32 || g.ic >= (1 << 21)) return false;
+  return smem_bytes(make_params(nullptr, 0, nullptr, g)) <= 160 * 1024;
+}
+
+int gs_rows(const ConvGeom& g) { return make_params(nullptr, 0, nullptr, g).osplit; }
+
+void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
+        double* sq_part, float* gb, double* sq_b) {
+  Params p = make_params(x, relu, hw, g);
+  p.gw = gw;
+  p.sq_part = sq_part;
+  p.gb = gb;
+  p.sq_b = (gb || sq_b) ? sq_b : nullptr;
+  if (gb && !sq_b) raise(DPG_ERR_INTERNAL, "rs::gs: bias record without its norm rows");
+  const size_t smem = smem_bytes(p);
+  dim3 grid((unsigned)p.osplit, (unsigned)g.b);
+  auto go = [&](auto kern) {
+    static int attr = 0;
+    if ((int)smem > attr) {
+      DPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      attr = 160 * 1024;
+    }
+    kern<<<grid, kThreads, smem, ctx->stream>>>(p);
+  };
+  switch (pick_pt(p.P)) {
+    case 4: go(gs_rows_kernel<4>); break;
+    case 8: go(gs_rows_kernel<8>); break;
+    default: go(gs_rows_kernel<16>); break;
+  }
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace rs
+}  // namespace dpg
