@@ -29,7 +29,18 @@ __global__ void __launch_bounds__(256) clip_factors_kernel(const double* __restr
   if (n < b) {
     double sq = 0.0;
     int bad = -1;
-    for (int r = 0; r < rows; ++r) {
+    int r = 0;
+    for (; r + 8 <= rows; r += 8) {  // 8 independent loads in flight, summed in row order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = slab[(int64_t)(r + u) * b + n];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (bad < 0 && !isfinite(v[u])) bad = row_param ? row_param[r + u] : 0;
+        sq += v[u];
+      }
+    }
+    for (; r < rows; ++r) {
       const double v = slab[(int64_t)r * b + n];
       if (bad < 0 && !isfinite(v)) bad = row_param ? row_param[r] : 0;
       sq += v;
@@ -49,29 +60,76 @@ void launch_clip_factors(dpg_ctx* ctx, const double* slab, const int32_t* row_pa
                          int64_t b, double c, double* norms, float* scale, int64_t* num_clipped) {
   if (num_clipped) DPG_CUDA(cudaMemsetAsync(num_clipped, 0, sizeof(int64_t), ctx->stream));
   if (b == 0) return;
-  clip_factors_kernel<<<(unsigned)((b + 255) / 256), 256, 0, ctx->stream>>>(
+  clip_factors_kernel<<<(unsigned)((b + 127) / 128), 128, 0, ctx->stream>>>(
       slab, row_param, rows, b, c, norms, scale, reinterpret_cast<unsigned long long*>(num_clipped),
       ctx->dev_err);
   DPG_LAUNCH_CHECK(ctx);
 }
 
 // ------------------------------------------------------------------------------------------
-// Split-K reduction: out = [out +] sum_z part[z] (z ascending) — the fold of
-// optimizer.hpp:245-250 when accumulating over virtual steps.
+// Column sums over a leading index z (samples or split-K partials):
+//   out[j] = [out[j] +] sum_z c(z) v(z, j)
+// A CTA owns 32 consecutive columns (lanes) and splits z into kColWarps contiguous ranges, one per
+// warp; each warp keeps kColBatch loads in flight and the warp partials are combined in warp order,
+// so the result is deterministic (identical on every run and replay).
 // ------------------------------------------------------------------------------------------
-__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int64_t n,
-                                     int64_t zstride, float* __restrict__ out, int accumulate) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+constexpr int kColWarps = 16;
+constexpr int kColBatch = 16;
+
+template <class V, class C>
+__device__ __forceinline__ void colsum_body(const V& v, const C& c, int64_t nz, int64_t ncol,
+                                            int64_t j0, float* __restrict__ out, int accumulate) {
+  __shared__ float part[kColWarps][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = j0 + lane;
+  const int64_t z0 = nz * warp / kColWarps, z1 = nz * (warp + 1) / kColWarps;
   float acc = 0.f;
-  for (int z = 0; z < splits; ++z) acc = __fadd_rn(acc, part[(int64_t)z * zstride + i]);
-  out[i] = accumulate ? __fadd_rn(out[i], acc) : acc;
+  if (j < ncol) {
+    int64_t z = z0;
+    for (; z + kColBatch <= z1; z += kColBatch) {
+      float vv[kColBatch], cc[kColBatch];
+#pragma unroll
+      for (int u = 0; u < kColBatch; ++u) {
+        vv[u] = v(z + u, j);
+        cc[u] = c(z + u);
+      }
+#pragma unroll
+      for (int u = 0; u < kColBatch; ++u) acc = fmaf(cc[u], vv[u], acc);
+    }
+    for (; z < z1; ++z) acc = fmaf(c(z), v(z, j), acc);
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && j < ncol) {
+    float t = part[0][lane];
+#pragma unroll
+    for (int w = 1; w < kColWarps; ++w) t += part[w][lane];
+    out[j] = accumulate ? out[j] + t : t;
+  }
+}
+
+struct PartV {  // split-K partials: v(z, j) = part[z * zstride + j]
+  const float* part;
+  int64_t zstride;
+  __device__ __forceinline__ float operator()(int64_t z, int64_t j) const { return __ldg(part + z * zstride + j); }
+};
+struct OneC {
+  __device__ __forceinline__ float operator()(int64_t) const { return 1.f; }
+};
+struct ScaleC {
+  const float* scale;
+  __device__ __forceinline__ float operator()(int64_t n) const { return __ldg(scale + n); }
+};
+
+__global__ void __launch_bounds__(32 * kColWarps) splitk_reduce_kernel(PartV v, int splits, int64_t n,
+                                                                       float* out, int accumulate) {
+  colsum_body(v, OneC{}, splits, n, (int64_t)blockIdx.x * 32, out, accumulate);
 }
 
 static void launch_splitk_reduce(dpg_ctx* ctx, const float* part, int splits, int64_t n, float* out,
-                                 int accumulate, int64_t zstride = -1) {
-  splitk_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
-      part, splits, n, zstride < 0 ? n : zstride, out, accumulate);
+                                 int accumulate) {
+  splitk_reduce_kernel<<<(unsigned)((n + 31) / 32), 32 * kColWarps, 0, ctx->stream>>>(
+      PartV{part, n}, splits, n, out, accumulate);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -102,10 +160,7 @@ static int pick_splits(int64_t b, int64_t tiles, int64_t per_sample_k) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Weighted sums over samples with few outputs: out[j] (+)= sum_n s_n v(n, j).
-// A CTA owns 32 consecutive outputs (lanes) and splits the samples into 8 contiguous ranges, one
-// per warp; loads are batched 8 deep for memory-level parallelism and the 8 partials are
-// combined in warp order (deterministic).
+// Weighted sums over samples with few outputs: out[j] (+)= sum_n s_n v(n, j) (colsum_body).
 // ------------------------------------------------------------------------------------------
 struct OuterV {  // linear, mid == 1: v(n, o*d + i) = B[n, o] * A[n, i]
   const float* acts;
@@ -113,7 +168,7 @@ struct OuterV {  // linear, mid == 1: v(n, o*d + i) = B[n, o] * A[n, i]
   int64_t d, r;
   int relu;
   __device__ __forceinline__ float operator()(int64_t n, int64_t j) const {
-    const int64_t o = j / d, i = j - o * d;
+    const int64_t o = (uint32_t)j / (uint32_t)d, i = j - o * d;  // d * r < 2^31 (launch check)
     return __ldg(hw + n * r + o) * relu_if(__ldg(acts + n * d + i), relu);
   }
 };
@@ -123,51 +178,18 @@ struct RecordV {  // materialised per-sample values: v(n, j) = g[n, j]
   __device__ __forceinline__ float operator()(int64_t n, int64_t j) const { return __ldg(g + n * numel + j); }
 };
 
-template <class V>
-__device__ __forceinline__ void wsum_body(const V& v, const float* __restrict__ scale, int64_t b,
-                                          int64_t numel, int64_t j0, float* __restrict__ out,
-                                          int accumulate) {
-  __shared__ float part[8][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t j = j0 + lane;
-  const int64_t n0 = b * warp / 8, n1 = b * (warp + 1) / 8;
-  float acc = 0.f;
-  if (j < numel) {
-    int64_t n = n0;
-    for (; n + 8 <= n1; n += 8) {
-      float vv[8], ss[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        vv[u] = v(n + u, j);
-        ss[u] = __ldg(scale + n + u);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc = fmaf(ss[u], vv[u], acc);
-    }
-    for (; n < n1; ++n) acc = fmaf(__ldg(scale + n), v(n, j), acc);
-  }
-  part[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && j < numel) {
-    float t = part[0][lane];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) t += part[w][lane];
-    out[j] = accumulate ? out[j] + t : t;
-  }
-}
-
-__global__ void __launch_bounds__(256) wsum_outer_kernel(OuterV v, const float* scale, int64_t b,
-                                                         float* out, int accumulate) {
-  wsum_body(v, scale, b, v.d * v.r, (int64_t)blockIdx.x * 32, out, accumulate);
+__global__ void __launch_bounds__(32 * kColWarps) wsum_outer_kernel(OuterV v, const float* scale, int64_t b,
+                                                                    float* out, int accumulate) {
+  colsum_body(v, ScaleC{scale}, b, v.d * v.r, (int64_t)blockIdx.x * 32, out, accumulate);
 }
 
 // all small per-sample records (the biases) of a model in one launch: blockIdx.y = item
-__global__ void __launch_bounds__(256) wsum_multi_kernel(WsumItems items, const float* scale,
-                                                         int64_t b, int accumulate) {
+__global__ void __launch_bounds__(32 * kColWarps) wsum_multi_kernel(WsumItems items, const float* scale,
+                                                                    int64_t b, int accumulate) {
   const WsumItem& it = items.item[blockIdx.y];
   const int64_t j0 = (int64_t)blockIdx.x * 32;
   if (j0 >= it.numel) return;
-  wsum_body(RecordV{it.g, it.numel}, scale, b, it.numel, j0, it.out, accumulate);
+  colsum_body(RecordV{it.g, it.numel}, ScaleC{scale}, b, it.numel, j0, it.out, accumulate);
 }
 
 void launch_wsum_multi(dpg_ctx* ctx, const WsumItems& items, const float* scale, int64_t b,
@@ -176,7 +198,7 @@ void launch_wsum_multi(dpg_ctx* ctx, const WsumItems& items, const float* scale,
   int64_t maxn = 0;
   for (int i = 0; i < items.count; ++i) maxn = items.item[i].numel > maxn ? items.item[i].numel : maxn;
   dim3 grid((unsigned)((maxn + 31) / 32), (unsigned)items.count);
-  wsum_multi_kernel<<<grid, 256, 0, ctx->stream>>>(items, scale, b, accumulate);
+  wsum_multi_kernel<<<grid, 32 * kColWarps, 0, ctx->stream>>>(items, scale, b, accumulate);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -221,8 +243,9 @@ void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, c
                                float* sw, float* sb, int accumulate, void* ws) {
   (void)sb;  // the bias sum is formed from the per-sample bias record (launch_weighted_sum_...)
   if (mid == 1) {
+    if (d * r >= (int64_t(1) << 31)) raise(DPG_ERR_DIMENSION, "linear clipped sum: d * r too large");
     OuterV v{acts, hw, d, r, acts_relu};
-    wsum_outer_kernel<<<(unsigned)((r * d + 31) / 32), 256, 0, ctx->stream>>>(v, scale, b, sw, accumulate);
+    wsum_outer_kernel<<<(unsigned)((r * d + 31) / 32), 32 * kColWarps, 0, ctx->stream>>>(v, scale, b, sw, accumulate);
     DPG_LAUNCH_CHECK(ctx);
     return;
   }

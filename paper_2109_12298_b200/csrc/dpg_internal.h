@@ -181,18 +181,6 @@ void linear_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, con
                  int64_t b, int64_t mid, int64_t d, int64_t r, float* part, int splits);
 }  // namespace tc
 
-namespace cv {
-bool enabled();
-bool fwd_supported(const ConvGeom& g);
-size_t fwd_ws_bytes(const ConvGeom& g);
-void conv_fwd(dpg_ctx* ctx, const float* x, int relu, const float* w, const float* bias, const ConvGeom& g,
-              float* y, void* ws);
-bool dgrad_supported(const ConvGeom& g);
-size_t dgrad_ws_bytes(const ConvGeom& g);
-void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g, const float* mask,
-                float* dx, void* ws);
-}  // namespace cv
-
 namespace ds {
 bool enabled();
 int gs_rows(const ConvGeom& g);

@@ -44,21 +44,15 @@ struct ConvFwdProb {
 };
 
 size_t conv_fwd_ws_bytes(const ConvGeom& g) {
-  if (cv::fwd_supported(g)) return cv::fwd_ws_bytes(g);
   return use_tc() ? tc::fwd_ws_bytes(g) : 0;
 }
 size_t conv_dgrad_ws_bytes(const ConvGeom& g) {
-  if (cv::dgrad_supported(g)) return cv::dgrad_ws_bytes(g);
   return (use_tc() && tc::dgrad_supported(g)) ? tc::dgrad_ws_bytes(g) : 0;
 }
 
 void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
                        const ConvGeom& g, float* y, void* ws) {
   if (g.b == 0) return;
-  if (ws && cv::fwd_supported(g)) {
-    cv::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws);
-    return;
-  }
   if (use_tc()) {
     tc::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws);
     return;
@@ -135,10 +129,6 @@ struct ConvDgradProb {
 void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
                          const float* mask_src, float* dx, void* ws) {
   if (g.b == 0) return;
-  if (ws && cv::dgrad_supported(g)) {
-    cv::conv_dgrad(ctx, dy, w, g, mask_src, dx, ws);
-    return;
-  }
   if (use_tc() && tc::dgrad_supported(g)) {
     tc::conv_dgrad(ctx, dy, w, g, mask_src, dx, ws);
     return;
@@ -209,6 +199,69 @@ __global__ void __launch_bounds__(256) linear_fwd_narrow_kernel(const float* __r
   }
 }
 
+// Narrow outputs with d % 4 == 0: a CTA owns kFwdRows rows; thread t walks the 16-byte column
+// chunks t, t + 128, ... of those rows, reading each weight chunk once for all of them, so every
+// load is a coalesced 128-bit load and each thread keeps ~kFwdRows + 1 of them in flight.
+// Per-row dot products are reduced warp then CTA in a fixed order.
+constexpr int kFwdRows = 4;
+constexpr int kFwdThreads = 128;
+template <int RMAX>
+__global__ void __launch_bounds__(kFwdThreads) linear_fwd_rows_kernel(const float* __restrict__ x,
+                                                                     int x_relu,
+                                                                     const float* __restrict__ w,
+                                                                     const float* __restrict__ bias,
+                                                                     int64_t rows, int64_t d, int r,
+                                                                     float* __restrict__ y) {
+  __shared__ float red[kFwdThreads / 32][kFwdRows * RMAX];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t row0 = (int64_t)blockIdx.x * kFwdRows;
+  float acc[kFwdRows][RMAX];
+#pragma unroll
+  for (int i = 0; i < kFwdRows; ++i)
+#pragma unroll
+    for (int o = 0; o < RMAX; ++o) acc[i][o] = 0.f;
+  const int64_t d4 = d >> 2;
+  for (int64_t j = tid; j < d4; j += kFwdThreads) {
+    float4 xv[kFwdRows];
+#pragma unroll
+    for (int i = 0; i < kFwdRows; ++i) {
+      xv[i] = row0 + i < rows ? __ldg(reinterpret_cast<const float4*>(x + (row0 + i) * d) + j)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+      xv[i] = make_float4(relu_if(xv[i].x, x_relu), relu_if(xv[i].y, x_relu), relu_if(xv[i].z, x_relu),
+                          relu_if(xv[i].w, x_relu));
+    }
+#pragma unroll
+    for (int o = 0; o < RMAX; ++o) {
+      if (o >= r) break;
+      const float4 wv = __ldg(reinterpret_cast<const float4*>(w + (int64_t)o * d) + j);
+#pragma unroll
+      for (int i = 0; i < kFwdRows; ++i) {
+        acc[i][o] = fmaf(wv.x, xv[i].x, acc[i][o]);
+        acc[i][o] = fmaf(wv.y, xv[i].y, acc[i][o]);
+        acc[i][o] = fmaf(wv.z, xv[i].z, acc[i][o]);
+        acc[i][o] = fmaf(wv.w, xv[i].w, acc[i][o]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kFwdRows; ++i)
+#pragma unroll
+    for (int o = 0; o < RMAX; ++o) {
+      if (o >= r) break;
+      const float v = warp_sum(acc[i][o]);
+      if (lane == 0) red[warp][i * RMAX + o] = v;
+    }
+  __syncthreads();
+  for (int e = tid; e < kFwdRows * RMAX; e += kFwdThreads) {
+    const int i = e / RMAX, o = e - i * RMAX;
+    if (o >= r || row0 + i >= rows) continue;
+    float t = red[0][e];
+#pragma unroll
+    for (int q = 1; q < kFwdThreads / 32; ++q) t += red[q][e];
+    y[(row0 + i) * r + o] = (bias ? __ldg(bias + o) : 0.f) + t;
+  }
+}
+
 struct LinearFwdProb {
   static constexpr bool kAMajorM = false;
   static constexpr bool kBMajorN = false;
@@ -237,6 +290,15 @@ struct LinearFwdProb {
 void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
                        int64_t rows, int64_t d, int64_t r, float* y) {
   if (rows == 0) return;
+  const bool aligned = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(w) & 15) == 0;
+  if (aligned && r <= 16) {
+    const unsigned g4 = (unsigned)((rows + kFwdRows - 1) / kFwdRows);
+    if (r <= 4) linear_fwd_rows_kernel<4><<<g4, kFwdThreads, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
+    else linear_fwd_rows_kernel<16><<<g4, kFwdThreads, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
+    DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
   const unsigned grid = (unsigned)((rows + 7) / 8);
   if (r <= 4) {
     linear_fwd_narrow_kernel<4><<<grid, 256, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
@@ -261,7 +323,9 @@ __global__ void __launch_bounds__(256) linear_dgrad_kernel(const float* __restri
                                                            float* __restrict__ dx) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * d) return;
-  const int64_t row = e / d, j = e - row * d;
+  // 32-bit division when the index fits (the common case; int64 division is a long sequence)
+  const int64_t row = (rows * d < (int64_t(1) << 31)) ? (int64_t)((uint32_t)e / (uint32_t)d) : e / d;
+  const int64_t j = e - row * d;
   float acc = 0.f;
   for (int64_t o = 0; o < r; ++o) acc = fmaf(__ldg(dy + row * r + o), __ldg(w + o * d + j), acc);
   if (mask && !(__ldg(mask + e) > 0.f)) acc = 0.f;
@@ -307,31 +371,42 @@ void launch_embedding_fwd(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* 
 
 // softmax cross-entropy (layers.hpp:894-919), in double like the reference; per-sample loss
 // and d(loss_n)/d(logits_n) = p - onehot (not divided by b). Invalid targets report
-// (stage TARGET, sample n).
-__global__ void softmax_ce_kernel(const float* __restrict__ logits, int logits_relu,
-                                  const float* __restrict__ targets, int64_t b, int64_t k,
-                                  float* __restrict__ loss, float* __restrict__ grad,
-                                  DeviceErr* err) {
-  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// (stage TARGET, sample n). One warp per sample: lanes own classes, max and sum by a fixed
+// shuffle tree (the fp64 sum is associated differently from the reference's loop; the float
+// outputs agree to rounding).
+__global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict__ logits, int logits_relu,
+                                                         const float* __restrict__ targets, int64_t b,
+                                                         int64_t k, float* __restrict__ loss,
+                                                         float* __restrict__ grad, DeviceErr* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (n >= b) return;
   const double tv = (double)targets[n];
   int64_t cls = 0;
   if (!(tv >= 0.0) || tv != floor(tv) || tv >= (double)k) {
-    report_error(err, err_key(ERR_STAGE_TARGET, 0, (uint64_t)n), (uint64_t)__float_as_uint(targets[n]));
+    if (lane == 0)
+      report_error(err, err_key(ERR_STAGE_TARGET, 0, (uint64_t)n), (uint64_t)__float_as_uint(targets[n]));
   } else {
     cls = (int64_t)tv;
   }
   const float* row = logits + n * k;
-  double mx = (double)relu_if(row[0], logits_relu);
-  for (int64_t j = 1; j < k; ++j) {
+  double mx = -INFINITY;
+  for (int64_t j = lane; j < k; j += 32) {
     const double v = (double)relu_if(row[j], logits_relu);
     mx = mx < v ? v : mx;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = mx < t ? t : mx;
+  }
   double denom = 0.0;
-  for (int64_t j = 0; j < k; ++j) denom += exp((double)relu_if(row[j], logits_relu) - mx);
+  for (int64_t j = lane; j < k; j += 32) denom += exp((double)relu_if(row[j], logits_relu) - mx);
+  denom = warp_sum(denom);
   const double log_denom = log(denom);
-  if (loss) loss[n] = (float)(-((double)relu_if(row[cls], logits_relu) - mx - log_denom));
-  for (int64_t j = 0; j < k; ++j) {
+  if (loss && lane == 0)
+    loss[n] = (float)(-((double)relu_if(row[cls], logits_relu) - mx - log_denom));
+  for (int64_t j = lane; j < k; j += 32) {
     const float lv = relu_if(row[j], logits_relu);
     const double p = exp((double)lv - mx) / denom;
     float gv = (float)(p - (j == cls ? 1.0 : 0.0));
@@ -343,7 +418,7 @@ __global__ void softmax_ce_kernel(const float* __restrict__ logits, int logits_r
 void launch_softmax_ce(dpg_ctx* ctx, const float* logits, int logits_relu, const float* targets,
                        int64_t b, int64_t k, float* loss, float* grad) {
   if (b == 0) return;
-  softmax_ce_kernel<<<(unsigned)((b + 127) / 128), 128, 0, ctx->stream>>>(logits, logits_relu, targets, b, k, loss, grad, ctx->dev_err);
+  softmax_ce_kernel<<<(unsigned)((b + 7) / 8), 256, 0, ctx->stream>>>(logits, logits_relu, targets, b, k, loss, grad, ctx->dev_err);
   DPG_LAUNCH_CHECK(ctx);
 }
 

@@ -347,9 +347,9 @@ void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom&
 int csum_splits(const ConvGeom& g) {
   const Params p = make_params(nullptr, 0, nullptr, g);
   const int64_t tiles = (g.oc + p.oct - 1) / p.oct;
-  // ~3 resident CTAs per SM, at least ~8 samples per split so the partials stay small
-  int64_t splits = (3 * kNumSMs + tiles - 1) / tiles;
-  splits = std::max<int64_t>(1, std::min<int64_t>(splits, (g.b + 7) / 8));
+  // ~4 CTAs per SM (the fixed-order split reduce is cheap next to an idle SM)
+  int64_t splits = (4 * kNumSMs + tiles - 1) / tiles;
+  splits = std::max<int64_t>(1, std::min<int64_t>(splits, g.b));
   const int64_t spl = (g.b + splits - 1) / splits;
   return (int)std::max<int64_t>(1, (g.b + spl - 1) / spl);  // every split non-empty
 }

@@ -9,9 +9,9 @@
 // (the largest stream of the whole step: CIFAR conv4 alone is 151 MB at b = 512). The kernel is
 // built around that store stream: one CTA owns one sample and a contiguous half (or all) of its
 // output channels; im2col of the sample (P x Kc, ReLU applied) and the highway rows of its channels
-// are staged once in shared memory; then each warp produces two output rows at a time — the P
-// highway values of each row are warp-uniform registers, lanes walk the row in 16-byte chunks,
-// every chunk is P shared-memory reads shared by both rows, 8 P FMAs and two 128-bit streaming
+// are staged once in shared memory; then each warp produces R (2 or 4) output rows at a time — the
+// P highway values of each row are warp-uniform registers, lanes walk the rows in 16-byte chunks,
+// every chunk is P shared-memory reads shared by the R rows, 4 R P FMAs and R 128-bit streaming
 // stores, so consecutive lanes write consecutive 16 B of G (512 B per warp store).
 #include <cstdlib>
 
@@ -93,17 +93,21 @@ __global__ void __launch_bounds__(kThreads, 2) gs_rows_kernel(const Params p) {
   double sq = 0.0, sqb = 0.0;
   const int nq = p.Kc4 >> 2;
   const bool vec = (p.Kc & 3) == 0;
-  for (int r0 = 2 * warp; r0 < nrow; r0 += 2 * (kThreads / 32)) {
-    const bool two = r0 + 1 < nrow;
-    float b0[PT], b1[PT];
+  // R rows per warp pass: every 128-bit im2col read feeds 4 R FMAs (R = 4 for P > 8 keeps the
+  // shared-memory traffic under the FMA time)
+  constexpr int R = PT > 8 ? 4 : 2;
+  for (int r0 = R * warp; r0 < nrow; r0 += R * (kThreads / 32)) {
+    float bv[R][PT];
 #pragma unroll
-    for (int q = 0; q < PT; q += 4) {
-      const float4 u = *reinterpret_cast<const float4*>(hs + r0 * PT + q);
-      const float4 v = two ? *reinterpret_cast<const float4*>(hs + (r0 + 1) * PT + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-      b0[q] = u.x; b0[q + 1] = u.y; b0[q + 2] = u.z; b0[q + 3] = u.w;
-      b1[q] = v.x; b1[q + 1] = v.y; b1[q + 2] = v.z; b1[q + 3] = v.w;
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int q = 0; q < PT; q += 4) {
+        const float4 u = r0 + r < nrow ? *reinterpret_cast<const float4*>(hs + (r0 + r) * PT + q)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        bv[r][q] = u.x; bv[r][q + 1] = u.y; bv[r][q + 2] = u.z; bv[r][q + 3] = u.w;
+      }
     }
-    if (p.sq_b && lane < 2 && (lane == 0 || two)) {
+    if (p.sq_b && lane < R && r0 + lane < nrow) {
       // bias rule for row r0 + lane: sequential fp64 sum over the P positions
       const float* hb = hs + (r0 + lane) * PT;
       double a = 0.0;
@@ -114,33 +118,35 @@ __global__ void __launch_bounds__(kThreads, 2) gs_rows_kernel(const Params p) {
     }
     float* g0 = p.gw ? p.gw + (n * p.oc + o_begin + r0) * (int64_t)p.Kc : nullptr;
     for (int j = lane; j < nq; j += 32) {
-      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+      float4 acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < PT; ++q) {
         const float4 xv = *reinterpret_cast<const float4*>(xt + q * p.Kc4 + 4 * j);
-        a0.x = fmaf(b0[q], xv.x, a0.x); a0.y = fmaf(b0[q], xv.y, a0.y);
-        a0.z = fmaf(b0[q], xv.z, a0.z); a0.w = fmaf(b0[q], xv.w, a0.w);
-        a1.x = fmaf(b1[q], xv.x, a1.x); a1.y = fmaf(b1[q], xv.y, a1.y);
-        a1.z = fmaf(b1[q], xv.z, a1.z); a1.w = fmaf(b1[q], xv.w, a1.w);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc[r].x = fmaf(bv[r][q], xv.x, acc[r].x); acc[r].y = fmaf(bv[r][q], xv.y, acc[r].y);
+          acc[r].z = fmaf(bv[r][q], xv.z, acc[r].z); acc[r].w = fmaf(bv[r][q], xv.w, acc[r].w);
+        }
       }
       const int k0 = 4 * j;
-      if (vec) {
-        if (g0) {
-          st_stream4(g0 + k0, a0);
-          if (two) st_stream4(g0 + p.Kc + k0, a1);
-        }
-        sq += (double)a0.x * a0.x + (double)a0.y * a0.y + (double)a0.z * a0.z + (double)a0.w * a0.w;
-        if (two) sq += (double)a1.x * a1.x + (double)a1.y * a1.y + (double)a1.z * a1.z + (double)a1.w * a1.w;
-      } else {
-        const float v0[4] = {a0.x, a0.y, a0.z, a0.w}, v1[4] = {a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (k0 + e >= p.Kc) continue;
-          if (g0) st_stream(g0 + k0 + e, v0[e]);
-          sq += (double)v0[e] * v0[e];
-          if (two) {
-            if (g0) st_stream(g0 + p.Kc + k0 + e, v1[e]);
-            sq += (double)v1[e] * v1[e];
+      for (int r = 0; r < R; ++r) {
+        if (r0 + r >= nrow) break;
+        const float4 a = acc[r];
+        if (vec) {
+          if (g0) st_stream4(g0 + (int64_t)r * p.Kc + k0, a);
+#ifndef DPG_EXPERIMENT_NOSQ
+          sq += (double)a.x * a.x + (double)a.y * a.y + (double)a.z * a.z + (double)a.w * a.w;
+#endif
+        } else {
+          const float v[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (k0 + e >= p.Kc) break;
+            if (g0) st_stream(g0 + (int64_t)r * p.Kc + k0 + e, v[e]);
+            sq += (double)v[e] * v[e];
           }
         }
       }

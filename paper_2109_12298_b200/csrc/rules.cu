@@ -206,8 +206,9 @@ void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
 }
 
 // ------------------------------------------------------------------------------------------
-// Bias: gb[n, o] = (float) sum_mid (double) hw — sequential in the middle index, as
-// sum_middle does (tensor.hpp:197-205). One CTA per sample; norm partial = one row.
+// Bias: gb[n, o] = (float) sum_mid (double) hw (sum_middle, tensor.hpp:197-205). Conv layout:
+// one warp per row with a fixed fp64 tree; linear layout [mid][r]: sequential in mid, coalesced
+// over o. One CTA per sample; norm partial = one row.
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) gs_bias_kernel(const float* __restrict__ hw, int64_t mid,
                                                       int64_t r, int conv_layout,
@@ -215,18 +216,33 @@ __global__ void __launch_bounds__(256) gs_bias_kernel(const float* __restrict__ 
                                                       double* __restrict__ sq_part, int64_t b) {
   const int64_t n = blockIdx.x;
   double sq = 0.0;
-  for (int64_t o = threadIdx.x; o < r; o += 256) {
-    double acc = 0.0;
-    if (conv_layout) {
+  if (conv_layout) {
+    // rows [r][mid] of sample n are contiguous: one warp per row, lanes take strided elements,
+    // fp64 partials combined by a fixed shuffle tree (a different association of the same fp64
+    // sum than the reference's sequential loop: the float result agrees to the last bit except
+    // in rare rounding-boundary cases, within the 1e-7 bias tolerance)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t o = warp; o < r; o += 8) {
       const float* row = hw + (n * r + o) * mid;
-      for (int64_t m = 0; m < mid; ++m) acc += (double)__ldg(row + m);
-    } else {
-      const float* base = hw + n * mid * r + o;
-      for (int64_t m = 0; m < mid; ++m) acc += (double)__ldg(base + m * r);
+      double acc = 0.0;
+#pragma unroll 8
+      for (int64_t m = lane; m < mid; m += 32) acc += (double)__ldg(row + m);
+      acc = warp_sum(acc);
+      const float v = (float)acc;
+      if (lane == 0) {
+        if (gb) gb[n * r + o] = v;
+        sq += (double)v * v;
+      }
     }
-    const float v = (float)acc;
-    if (gb) gb[n * r + o] = v;
-    sq += (double)v * v;
+  } else {
+    for (int64_t o = threadIdx.x; o < r; o += 256) {
+      double acc = 0.0;
+      const float* col = hw + n * mid * r + o;
+      for (int64_t m = 0; m < mid; ++m) acc += (double)__ldg(col + m * r);
+      const float v = (float)acc;
+      if (gb) gb[n * r + o] = v;
+      sq += (double)v * v;
+    }
   }
   __shared__ double red[8];
   const double t = block_sum<256>(sq, red);
