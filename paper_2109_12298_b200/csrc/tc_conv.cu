@@ -520,6 +520,11 @@ struct ConvCsum {
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ float4 b_fix(int z, int64_t, int, int64_t k, const uint8_t*, float4 v) const {
+    if ((g.P & 3) == 0) {
+      const int64_t n = (int64_t)z * spl + g.fP.div((uint32_t)k);
+      const float sc = __ldg(n < bsz ? scale + n : g_zero4);
+      return make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
+    }
     float sc[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {

@@ -4,7 +4,7 @@
 //
 // Operands are gathered by all threads of the CTA through a problem-specific stage loader (the
 // implicit im2col of the conv contractions lives there, driven by per-CTA index tables in shared
-// memory), split into a TF32 "hi" part (cvt.rna) and the TF32-rounded remainder "lo", and stored
+// memory), split into a TF32 "hi" part and the TF32-rounded remainder "lo" (split_tf32), and stored
 // into shared memory in the canonical 128B-swizzled K-major UMMA layout (8 rows x 128 B atoms,
 // 1024 B aligned). One thread issues tcgen05.mma.cta_group::1.kind::tf32 with the accumulator in
 // tensor memory: acc += A_lo B_hi + A_hi B_lo + A_hi B_hi per K=8 slice (3xTF32). Stages are
@@ -86,11 +86,6 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
 
 // SW128 K-major shared memory descriptor (tcgen05 matrix descriptor, sm_100 version 1):
 // start >> 4 | LBO 16 B >> 4 | SBO 1024 B >> 4 | version 1 | layout SWIZZLE_128B (2)
@@ -137,15 +132,25 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int q) {
   return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((q ^ (row & 7)) << 4));
 }
 
+// 3xTF32 split of a finite fp32 value, both parts rounded to nearest TF32 (ties away from zero,
+// as cvt.rna) by integer add + mask on the bit pattern: hi = rna(x), lo = rna(x - hi) with x - hi
+// exact in fp32 and |x - hi| <= 2^-11 |x|. Five ops and no special-case branches (cvt.rna.tf32
+// is emulated with an Inf/NaN guard); a non-finite x still gives a non-finite product, which the
+// clip-factor check reports.
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+  lo = (__float_as_uint(x - __uint_as_float(hi)) + 0x1000u) & 0xffffe000u;
+}
+
 // Store 4 values (k .. k+3 of one row) as hi / lo TF32 into the swizzled stage buffers.
 __device__ __forceinline__ void put4(uint8_t* hi, uint8_t* lo, int row, int q, float a, float b,
                                      float c, float d) {
   const uint32_t off = sw128_off(row, q);
   uint4 h, l;
-  h.x = to_tf32(a); l.x = to_tf32(a - __uint_as_float(h.x));
-  h.y = to_tf32(b); l.y = to_tf32(b - __uint_as_float(h.y));
-  h.z = to_tf32(c); l.z = to_tf32(c - __uint_as_float(h.z));
-  h.w = to_tf32(d); l.w = to_tf32(d - __uint_as_float(h.w));
+  split_tf32(a, h.x, l.x);
+  split_tf32(b, h.y, l.y);
+  split_tf32(c, h.z, l.z);
+  split_tf32(d, h.w, l.w);
   *reinterpret_cast<uint4*>(hi + off) = h;
   *reinterpret_cast<uint4*>(lo + off) = l;
 }
