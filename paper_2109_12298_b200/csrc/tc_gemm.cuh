@@ -235,37 +235,42 @@ static __device__ __align__(16) const float g_zero4[4] = {0.f, 0.f, 0.f, 0.f};
 //        (applied when the stage is stored: ReLU of a folded activation, clip scale, ...)
 //   void epilogue_row(int z, int split, int64_t m, int64_t n, const float* v, int nv, double& sq);
 //   void epilogue_cta(int z, int split, double sq) const;
+// Rows of the tile beyond the problem (row >= mrows / nrows: padding of a small M or N up to the
+// UMMA shape) are neither gathered nor stored: their shared-memory rows keep stale values, which
+// only reach accumulator rows / columns that the epilogue never writes.
 template <int BN, class Prob>
 __device__ __forceinline__ void fetch(const Prob& p, int z, int64_t m0, int64_t n0, int64_t k0,
-                                      const uint8_t* scratch, int tid, float4 (&ra)[4],
-                                      float4 (&rb)[Frag<BN>::BQ]) {
+                                      const uint8_t* scratch, int tid, int mrows, int nrows,
+                                      float4 (&ra)[4], float4 (&rb)[Frag<BN>::BQ]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int row, q;
     a_map(Prob::kAQuadMajor, tid, i, row, q);
-    ra[i] = p.a_quad(z, m0, row, k0 + 4 * q, scratch);
+    if (row < mrows) ra[i] = p.a_quad(z, m0, row, k0 + 4 * q, scratch);
   }
 #pragma unroll
   for (int i = 0; i < Frag<BN>::BQ; ++i) {
     int row, q;
-    if (b_map<BN>(Prob::kBQuadMajor, tid, i, row, q)) rb[i] = p.b_quad(z, n0, row, k0 + 4 * q, scratch);
+    if (b_map<BN>(Prob::kBQuadMajor, tid, i, row, q) && row < nrows)
+      rb[i] = p.b_quad(z, n0, row, k0 + 4 * q, scratch);
   }
 }
 
 template <int BN, class Prob>
 __device__ __forceinline__ void stash(const Prob& p, int z, int64_t m0, int64_t n0, int64_t k0,
-                                      const uint8_t* scratch, int tid, const StageBufsT& sb,
-                                      const float4 (&ra)[4], const float4 (&rb)[Frag<BN>::BQ]) {
+                                      const uint8_t* scratch, int tid, int mrows, int nrows,
+                                      const StageBufsT& sb, const float4 (&ra)[4],
+                                      const float4 (&rb)[Frag<BN>::BQ]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int row, q;
     a_map(Prob::kAQuadMajor, tid, i, row, q);
-    put4(sb.a_hi, sb.a_lo, row, q, p.a_fix(z, m0, row, k0 + 4 * q, scratch, ra[i]));
+    if (row < mrows) put4(sb.a_hi, sb.a_lo, row, q, p.a_fix(z, m0, row, k0 + 4 * q, scratch, ra[i]));
   }
 #pragma unroll
   for (int i = 0; i < Frag<BN>::BQ; ++i) {
     int row, q;
-    if (b_map<BN>(Prob::kBQuadMajor, tid, i, row, q))
+    if (b_map<BN>(Prob::kBQuadMajor, tid, i, row, q) && row < nrows)
       put4(sb.b_hi, sb.b_lo, row, q, p.b_fix(z, n0, row, k0 + 4 * q, scratch, rb[i]));
   }
 }
@@ -311,15 +316,17 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const Prob p) {
   // Two register sets: the operands of stage i + 2 are requested while stage i is stored, so each
   // gather has a full stage period (store + barrier + MMA issue of the previous stage) to land.
   float4 ra0[4], rb0[Frag<BN>::BQ], ra1[4], rb1[Frag<BN>::BQ];
-  if (nk > 0) fetch<BN>(p, z, m0, n0, (int64_t)ks0 * BK, scratch, tid, ra0, rb0);
-  if (nk > 1) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + 1) * BK, scratch, tid, ra1, rb1);
+  const int mrows = (int)std::min<int64_t>(BM, Mz - m0);
+  const int nrows = (int)std::min<int64_t>(BN, p.N - n0);
+  if (nk > 0) fetch<BN>(p, z, m0, n0, (int64_t)ks0 * BK, scratch, tid, mrows, nrows, ra0, rb0);
+  if (nk > 1) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + 1) * BK, scratch, tid, mrows, nrows, ra1, rb1);
   auto stage = [&](int i, float4 (&ra)[4], float4 (&rb)[Frag<BN>::BQ]) {
     const int s = i % kStages;
     uint8_t* st = smem + s * S::STAGE;
     const StageBufsT sb{st, st + S::A_BYTES, st + 2 * S::A_BYTES, st + 2 * S::A_BYTES + S::B_BYTES};
     if (i >= kStages) mbar_wait(&bars[s], ((i / kStages) - 1) & 1);
-    stash<BN, Prob>(p, z, m0, n0, (int64_t)(ks0 + i) * BK, scratch, tid, sb, ra, rb);
-    if (i + 2 < nk) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + i + 2) * BK, scratch, tid, ra, rb);
+    stash<BN, Prob>(p, z, m0, n0, (int64_t)(ks0 + i) * BK, scratch, tid, mrows, nrows, sb, ra, rb);
+    if (i + 2 < nk) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + i + 2) * BK, scratch, tid, mrows, nrows, ra, rb);
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
