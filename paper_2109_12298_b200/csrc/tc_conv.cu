@@ -75,6 +75,19 @@ __device__ __forceinline__ void build_ptab(const Geo& g, PEnt* t, int tid) {
   }
 }
 
+// The gathers use 32-bit element offsets: every tensor a contraction reads must have < 2^31
+// elements (2^31 floats = 8 GiB; the per-sample gradient record is written with 64-bit offsets).
+static void check_i32(const ConvGeom& cg) {
+  const int64_t lim = int64_t(1) << 31;
+  if (cg.b * cg.ic * cg.h * cg.w >= lim || cg.b * cg.oc * cg.P() >= lim || cg.oc * cg.K() >= lim)
+    raise(DPG_ERR_DIMENSION, "conv2d: a tensor of this batch exceeds 2^31 elements");
+}
+static void check_i32_linear(int64_t b, int64_t mid, int64_t d, int64_t r) {
+  const int64_t lim = int64_t(1) << 31;
+  if (b * mid * d >= lim || b * mid * r >= lim || d * r >= lim)
+    raise(DPG_ERR_DIMENSION, "linear: a tensor of this batch exceeds 2^31 elements");
+}
+
 // ------------------------------------------------------------------------------ forward
 struct ConvFwd {
   static constexpr bool kCtaReduce = false;
@@ -125,12 +138,13 @@ struct ConvFwd {
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
-  __device__ float4 b_quad(int, int64_t n0, int row, int64_t k, const uint8_t*) const {
-    const int64_t n = n0 + row;
-    if ((K & 3) == 0) return __ldg(reinterpret_cast<const float4*>(n < N && k < K ? wt + n * K + k : g_zero4));
+  __device__ float4 b_quad(int, int64_t n0, int row, int64_t k64, const uint8_t*) const {
+    // (32-bit index math: every operand has < 2^31 elements, checked at launch)
+    const int n = (int)n0 + row, k = (int)k64, Ni = (int)N, Ki = (int)K;
+    if ((Ki & 3) == 0) return __ldg(reinterpret_cast<const float4*>(n < Ni && k < Ki ? wt + (n * Ki + k) : g_zero4));
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = __ldg(n < N && k + e < K ? wt + n * K + k + e : g_zero4);
+    for (int e = 0; e < 4; ++e) v[e] = __ldg(n < Ni && k + e < Ki ? wt + (n * Ki + k + e) : g_zero4);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   DPG_NO_FIX(b_fix)
@@ -167,6 +181,7 @@ size_t fwd_ws_bytes(const ConvGeom& cg) {
 
 void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
               const ConvGeom& cg, float* y, void* ws) {
+  check_i32(cg);
   ConvFwd p;
   p.g = make_geo(cg);
   p.x = x; p.relu = x_relu; p.wt = w; p.bias = bias; p.y = y;
@@ -259,17 +274,17 @@ struct ConvDgrad {
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   DPG_NO_FIX(a_fix)
-  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t* s) const {
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k64, const uint8_t* s) const {
     const DClass& c = cls[z];
     const TEnt* tt = reinterpret_cast<const TEnt*>(s);
-    const int64_t ch = n0 + row;
+    const int ch = (int)n0 + row, k = (int)k64, Kc = (int)c.K;
+    const bool ch_ok = ch < (int)N;
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const TEnt t = tt[k + e];  // (table padded to whole stages)
-      const bool ok = ch < N && k + e < c.K;
-      v[e] = __ldg(ok ? wt + (((int64_t)t.o * g.ic + ch) * g.kh + c.ry + g.stride * t.a) * g.kw + c.rx +
-                            g.stride * t.c
+      const bool ok = ch_ok && k + e < Kc;
+      v[e] = __ldg(ok ? wt + (((t.o * g.ic + ch) * g.kh + c.ry + g.stride * t.a) * g.kw + c.rx + g.stride * t.c)
                       : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
@@ -346,6 +361,7 @@ size_t dgrad_ws_bytes(const ConvGeom& cg) {
 
 void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& cg,
                 const float* mask_src, float* dx, void* ws) {
+  check_i32(cg);
   ConvDgrad p;
   p.g = make_geo(cg);
   p.dy = dy; p.wt = w; p.mask = mask_src; p.dx = dx;
@@ -395,29 +411,29 @@ struct ConvGs {
   }
   static constexpr bool kAQuadMajor = true;  // rows = kcol; lanes walk positions
   static constexpr bool kBQuadMajor = true;  // highway rows contiguous in p
-  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t* s) const {
+  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k64, const uint8_t* s) const {
     const PEnt* pt = reinterpret_cast<const PEnt*>(s);
-    const Row r = reinterpret_cast<const Row*>(s + ((4 * K + 15) & ~15))[row];
-    const float* xs = x + (int64_t)z * g.ic * g.h * g.w + r.plane;
-    const bool row_ok = m0 + row < M;
+    const int Ki = (int)K, k = (int)k64;
+    const Row r = reinterpret_cast<const Row*>(s + ((4 * Ki + 15) & ~15))[row];
+    const int base = z * (g.ic * g.h * g.w) + r.plane;  // < 2^31 (launch check)
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const PEnt t = pt[min((int)(k + e), (int)K - 1)];
+      const PEnt t = pt[min(k + e, Ki - 1)];
       const int iy = t.y + r.ki, ix = t.x + r.kj;
-      const bool ok = row_ok && k + e < K && (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
-      v[e] = __ldg(ok ? xs + iy * g.w + ix : g_zero4);
+      const bool ok = k + e < Ki && (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
+      v[e] = __ldg(ok ? x + (base + iy * g.w + ix) : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
-  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
-    const int64_t oc = n0 + row;
-    const float* h = hw + ((int64_t)z * g.oc + oc) * K;
-    if ((K & 3) == 0) return __ldg(reinterpret_cast<const float4*>(oc < N && k < K ? h + k : g_zero4));
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k64, const uint8_t*) const {
+    const int oc = (int)n0 + row, Ki = (int)K, k = (int)k64;
+    const int h = (z * g.oc + oc) * Ki;
+    if ((Ki & 3) == 0) return __ldg(reinterpret_cast<const float4*>(k < Ki ? hw + (h + k) : g_zero4));
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = __ldg(oc < N && k + e < K ? h + k + e : g_zero4);
+    for (int e = 0; e < 4; ++e) v[e] = __ldg(k + e < Ki ? hw + (h + k + e) : g_zero4);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   DPG_NO_FIX(b_fix)
@@ -439,6 +455,7 @@ int gs_conv_rows(const ConvGeom& cg) {
 
 void conv_gs(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& cg,
              float* gw, double* sq_part) {
+  check_i32(cg);
   ConvGs p;
   p.g = make_geo(cg);
   p.x = x; p.relu = x_relu; p.hw = hw; p.gw = gw; p.sq_part = sq_part;
@@ -479,57 +496,57 @@ struct ConvCsum {
   }
   static constexpr bool kAQuadMajor = true;
   static constexpr bool kBQuadMajor = true;
-  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t* s) const {
+  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k64, const uint8_t* s) const {
     const PEnt* pt = reinterpret_cast<const PEnt*>(s);
     const Row r = reinterpret_cast<const Row*>(s + ((4 * g.P + 15) & ~15))[row];
-    const bool row_ok = m0 + row < M;
+    const int k = (int)k64, Ki = (int)K, n_end = (int)bsz, chw = g.ic * g.h * g.w;
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t qq, pp;
       g.fP.divmod((uint32_t)(k + e), qq, pp);
-      const int64_t n = (int64_t)z * spl + qq;
+      const int n = z * (int)spl + (int)qq;
       const PEnt t = pt[pp];
       const int iy = t.y + r.ki, ix = t.x + r.kj;
-      const bool ok = row_ok && k + e < K && n < bsz && (unsigned)iy < (unsigned)g.h &&
-                      (unsigned)ix < (unsigned)g.w;
-      v[e] = __ldg(ok ? x + n * g.ic * g.h * g.w + r.plane + iy * g.w + ix : g_zero4);
+      const bool ok = k + e < Ki && n < n_end && (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
+      v[e] = __ldg(ok ? x + (n * chw + r.plane + iy * g.w + ix) : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
   // raw highway values; the clip scale s_n is applied when the stage is stored (b_fix)
-  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
-    const int64_t oc = n0 + row;
-    if ((g.P & 3) == 0) {
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k64, const uint8_t*) const {
+    const int oc = (int)n0 + row, k = (int)k64, Ki = (int)K, n_end = (int)bsz, P = (int)g.P;
+    if ((P & 3) == 0) {
       uint32_t qq, pp;
       g.fP.divmod((uint32_t)k, qq, pp);
-      const int64_t n = (int64_t)z * spl + qq;
-      const bool ok = oc < N && k < K && n < bsz;
-      return __ldg(reinterpret_cast<const float4*>(ok ? hw + (n * g.oc + oc) * g.P + pp : g_zero4));
+      const int n = z * (int)spl + (int)qq;
+      const bool ok = k < Ki && n < n_end;
+      return __ldg(reinterpret_cast<const float4*>(ok ? hw + ((n * g.oc + oc) * P + (int)pp) : g_zero4));
     }
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t qq, pp;
       g.fP.divmod((uint32_t)(k + e), qq, pp);
-      const int64_t n = (int64_t)z * spl + qq;
-      const bool ok = oc < N && k + e < K && n < bsz;
-      v[e] = __ldg(ok ? hw + (n * g.oc + oc) * g.P + pp : g_zero4);
+      const int n = z * (int)spl + (int)qq;
+      const bool ok = k + e < Ki && n < n_end;
+      v[e] = __ldg(ok ? hw + ((n * g.oc + oc) * P + (int)pp) : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
-  __device__ float4 b_fix(int z, int64_t, int, int64_t k, const uint8_t*, float4 v) const {
+  __device__ float4 b_fix(int z, int64_t, int, int64_t k64, const uint8_t*, float4 v) const {
+    const int k = (int)k64, n_end = (int)bsz;
     if ((g.P & 3) == 0) {
-      const int64_t n = (int64_t)z * spl + g.fP.div((uint32_t)k);
-      const float sc = __ldg(n < bsz ? scale + n : g_zero4);
+      const int n = z * (int)spl + (int)g.fP.div((uint32_t)k);
+      const float sc = __ldg(n < n_end ? scale + n : g_zero4);
       return make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
     }
     float sc[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int64_t n = (int64_t)z * spl + g.fP.div((uint32_t)(k + e));
-      sc[e] = __ldg(n < bsz ? scale + n : g_zero4);
+      const int n = z * (int)spl + (int)g.fP.div((uint32_t)(k + e));
+      sc[e] = __ldg(n < n_end ? scale + n : g_zero4);
     }
     return make_float4(sc[0] * v.x, sc[1] * v.y, sc[2] * v.z, sc[3] * v.w);
   }
@@ -550,6 +567,7 @@ int csum_conv_splits(const ConvGeom& cg) {
 
 void conv_csum(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const float* scale,
                const ConvGeom& cg, float* part, int splits) {
+  check_i32(cg);
   ConvCsum p;
   p.g = make_geo(cg);
   p.x = x; p.relu = x_relu; p.hw = hw; p.scale = scale; p.part = part;
@@ -575,20 +593,19 @@ struct LinGs {
   __device__ void setup(int, int64_t, int64_t, uint8_t*, int) const {}
   static constexpr bool kAQuadMajor = false;  // rows = i contiguous
   static constexpr bool kBQuadMajor = false;  // rows = o contiguous
-  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t*) const {
-    const int64_t i = m0 + row;
+  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k64, const uint8_t*) const {
+    const int i = (int)m0 + row, k = (int)k64, Ki = (int)K, Mi = (int)M;
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      v[e] = __ldg(i < M && k + e < K ? acts + ((int64_t)z * K + k + e) * M + i : g_zero4);
+    for (int e = 0; e < 4; ++e) v[e] = __ldg(k + e < Ki ? acts + ((z * Ki + k + e) * Mi + i) : g_zero4);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
-  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
-    const int64_t o = n0 + row;
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k64, const uint8_t*) const {
+    const int o = (int)n0 + row, k = (int)k64, Ki = (int)K, Ni = (int)N;
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = __ldg(o < N && k + e < K ? hw + ((int64_t)z * K + k + e) * N + o : g_zero4);
+    for (int e = 0; e < 4; ++e) v[e] = __ldg(k + e < Ki ? hw + ((z * Ki + k + e) * Ni + o) : g_zero4);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   DPG_NO_FIX(b_fix)
@@ -610,6 +627,7 @@ int gs_linear_rows(int64_t d, int64_t r) {
 
 void linear_gs(dpg_ctx* ctx, const float* acts, int relu, const float* hw, int64_t b, int64_t mid,
                int64_t d, int64_t r, float* gw, double* sq_part) {
+  check_i32_linear(b, mid, d, r);
   LinGs p{acts, relu, hw, gw, sq_part, d, r, mid, b, 1, 0};
   launch_tc_auto(ctx, p, b);
 }
@@ -629,29 +647,29 @@ struct LinCsum {
   __device__ void setup(int, int64_t, int64_t, uint8_t*, int) const {}
   static constexpr bool kAQuadMajor = false;
   static constexpr bool kBQuadMajor = false;
-  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k, const uint8_t*) const {
-    const int64_t i = m0 + row;
+  __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k64, const uint8_t*) const {
+    const int i = (int)m0 + row, k = (int)k64, Ki = (int)K, Mi = (int)M, midi = (int)mid;
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t qq, t;
       fmid.divmod((uint32_t)(k + e), qq, t);
-      const int64_t n = (int64_t)z * spl + qq;
-      v[e] = __ldg(i < M && k + e < K && n < bsz ? acts + (n * mid + t) * M + i : g_zero4);
+      const int n = z * (int)spl + (int)qq;
+      v[e] = __ldg(k + e < Ki && n < (int)bsz ? acts + ((n * midi + (int)t) * Mi + i) : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
   // raw highway values; the clip scale s_n is applied when the stage is stored (b_fix)
-  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k, const uint8_t*) const {
-    const int64_t o = n0 + row;
+  __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k64, const uint8_t*) const {
+    const int o = (int)n0 + row, k = (int)k64, Ki = (int)K, Ni = (int)N, midi = (int)mid;
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t qq, t;
       fmid.divmod((uint32_t)(k + e), qq, t);
-      const int64_t n = (int64_t)z * spl + qq;
-      v[e] = __ldg(o < N && k + e < K && n < bsz ? hw + (n * mid + t) * N + o : g_zero4);
+      const int n = z * (int)spl + (int)qq;
+      v[e] = __ldg(k + e < Ki && n < (int)bsz ? hw + ((n * midi + (int)t) * Ni + o) : g_zero4);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -681,6 +699,7 @@ int csum_linear_splits(int64_t b, int64_t mid, int64_t d, int64_t r) {
 
 void linear_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, const float* scale,
                  int64_t b, int64_t mid, int64_t d, int64_t r, float* part, int splits) {
+  check_i32_linear(b, mid, d, r);
   LinCsum p;
   p.acts = acts; p.relu = relu; p.hw = hw; p.scale = scale; p.part = part;
   p.spl = (b + splits - 1) / splits;
