@@ -38,7 +38,7 @@ inline Geo make_geo(const ConvGeom& g) {
 }
 
 // kcol -> offset of (c, ki, kj) relative to a window origin, and the tap (ki, kj)
-struct KEnt {
+struct KEnt {  // (read back as one int2: {off, ki | kj << 16})
   int off;
   short ki, kj;
 };
@@ -131,9 +131,10 @@ struct ConvFwd {
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const KEnt t = kt[e];
-      const bool ok = (unsigned)(r.iy0 + t.ki) < (unsigned)g.h && (unsigned)(r.ix0 + t.kj) < (unsigned)g.w;
-      v[e] = __ldg(ok ? r.xr + t.off : g_zero4);
+      const int2 t = *reinterpret_cast<const int2*>(kt + e);  // one 64-bit read: {off, ki | kj << 16}
+      const int ki = (int)(short)(t.y & 0xffff), kj = t.y >> 16;
+      const bool ok = (unsigned)(r.iy0 + ki) < (unsigned)g.h && (unsigned)(r.ix0 + kj) < (unsigned)g.w;
+      v[e] = ldg_or_zero(r.xr + t.x, ok);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -141,10 +142,10 @@ struct ConvFwd {
   __device__ float4 b_quad(int, int64_t n0, int row, int64_t k64, const uint8_t*) const {
     // (32-bit index math: every operand has < 2^31 elements, checked at launch)
     const int n = (int)n0 + row, k = (int)k64, Ni = (int)N, Ki = (int)K;
-    if ((Ki & 3) == 0) return __ldg(reinterpret_cast<const float4*>(n < Ni && k < Ki ? wt + (n * Ki + k) : g_zero4));
+    if ((Ki & 3) == 0) return ldg4_or_zero(wt + (n * Ki + k), n < Ni && k < Ki);
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = __ldg(n < Ni && k + e < Ki ? wt + (n * Ki + k + e) : g_zero4);
+    for (int e = 0; e < 4; ++e) v[e] = ldg_or_zero(wt + (n * Ki + k + e), n < Ni && k + e < Ki);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   DPG_NO_FIX(b_fix)
@@ -218,7 +219,7 @@ struct ConvDgrad {
   int64_t M, N, K, dx_numel;
   int ksplit, scratch, ncls;
   DClass cls[kMaxClasses];
-  struct TEnt {
+  struct TEnt {  // (read back as one int2: {delta, a | c << 8 | o << 16})
     int delta;  // o*oh*ow - a*ow - c
     unsigned char a, c;
     short o;
@@ -267,9 +268,10 @@ struct ConvDgrad {
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const TEnt t = tt[e];
-      const bool ok = (unsigned)(r.oy0 - t.a) < (unsigned)g.oh && (unsigned)(r.ox0 - t.c) < (unsigned)g.ow;
-      v[e] = __ldg(ok ? r.dr + t.delta : g_zero4);
+      const int2 t = *reinterpret_cast<const int2*>(tt + e);  // {delta, a | c << 8 | o << 16}
+      const int ta = t.y & 0xff, tc = (t.y >> 8) & 0xff;
+      const bool ok = (unsigned)(r.oy0 - ta) < (unsigned)g.oh && (unsigned)(r.ox0 - tc) < (unsigned)g.ow;
+      v[e] = ldg_or_zero(r.dr + t.x, ok);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -282,10 +284,10 @@ struct ConvDgrad {
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const TEnt t = tt[k + e];  // (table padded to whole stages)
+      const int2 t = *reinterpret_cast<const int2*>(tt + k + e);  // (table padded to whole stages)
+      const int ta = t.y & 0xff, tc = (t.y >> 8) & 0xff, to = t.y >> 16;
       const bool ok = ch_ok && k + e < Kc;
-      v[e] = __ldg(ok ? wt + (((t.o * g.ic + ch) * g.kh + c.ry + g.stride * t.a) * g.kw + c.rx + g.stride * t.c)
-                      : g_zero4);
+      v[e] = ldg_or_zero(wt + (((to * g.ic + ch) * g.kh + c.ry + g.stride * ta) * g.kw + c.rx + g.stride * tc), ok);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -422,7 +424,7 @@ struct ConvGs {
       const PEnt t = pt[min(k + e, Ki - 1)];
       const int iy = t.y + r.ki, ix = t.x + r.kj;
       const bool ok = k + e < Ki && (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
-      v[e] = __ldg(ok ? x + (base + iy * g.w + ix) : g_zero4);
+      v[e] = ldg_or_zero(x + (base + iy * g.w + ix), ok);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -430,10 +432,10 @@ struct ConvGs {
   __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k64, const uint8_t*) const {
     const int oc = (int)n0 + row, Ki = (int)K, k = (int)k64;
     const int h = (z * g.oc + oc) * Ki;
-    if ((Ki & 3) == 0) return __ldg(reinterpret_cast<const float4*>(k < Ki ? hw + (h + k) : g_zero4));
+    if ((Ki & 3) == 0) return ldg4_or_zero(hw + (h + k), k < Ki);
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = __ldg(k + e < Ki ? hw + (h + k + e) : g_zero4);
+    for (int e = 0; e < 4; ++e) v[e] = ldg_or_zero(hw + (h + k + e), k + e < Ki);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   DPG_NO_FIX(b_fix)
@@ -509,7 +511,7 @@ struct ConvCsum {
       const PEnt t = pt[pp];
       const int iy = t.y + r.ki, ix = t.x + r.kj;
       const bool ok = k + e < Ki && n < n_end && (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
-      v[e] = __ldg(ok ? x + (n * chw + r.plane + iy * g.w + ix) : g_zero4);
+      v[e] = ldg_or_zero(x + (n * chw + r.plane + iy * g.w + ix), ok);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -522,7 +524,7 @@ struct ConvCsum {
       g.fP.divmod((uint32_t)k, qq, pp);
       const int n = z * (int)spl + (int)qq;
       const bool ok = k < Ki && n < n_end;
-      return __ldg(reinterpret_cast<const float4*>(ok ? hw + ((n * g.oc + oc) * P + (int)pp) : g_zero4));
+      return ldg4_or_zero(hw + ((n * g.oc + oc) * P + (int)pp), ok);
     }
     float v[4];
 #pragma unroll
@@ -531,7 +533,7 @@ struct ConvCsum {
       g.fP.divmod((uint32_t)(k + e), qq, pp);
       const int n = z * (int)spl + (int)qq;
       const bool ok = k + e < Ki && n < n_end;
-      v[e] = __ldg(ok ? hw + ((n * g.oc + oc) * P + (int)pp) : g_zero4);
+      v[e] = ldg_or_zero(hw + ((n * g.oc + oc) * P + (int)pp), ok);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -539,14 +541,14 @@ struct ConvCsum {
     const int k = (int)k64, n_end = (int)bsz;
     if ((g.P & 3) == 0) {
       const int n = z * (int)spl + (int)g.fP.div((uint32_t)k);
-      const float sc = __ldg(n < n_end ? scale + n : g_zero4);
+      const float sc = ldg_or_zero(scale + n, n < n_end);
       return make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
     }
     float sc[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int n = z * (int)spl + (int)g.fP.div((uint32_t)(k + e));
-      sc[e] = __ldg(n < n_end ? scale + n : g_zero4);
+      sc[e] = ldg_or_zero(scale + n, n < n_end);
     }
     return make_float4(sc[0] * v.x, sc[1] * v.y, sc[2] * v.z, sc[3] * v.w);
   }
@@ -597,7 +599,7 @@ struct LinGs {
     const int i = (int)m0 + row, k = (int)k64, Ki = (int)K, Mi = (int)M;
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = __ldg(k + e < Ki ? acts + ((z * Ki + k + e) * Mi + i) : g_zero4);
+    for (int e = 0; e < 4; ++e) v[e] = ldg_or_zero(acts + ((z * Ki + k + e) * Mi + i), k + e < Ki);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ float4 a_fix(int, int64_t, int, int64_t, const uint8_t*, float4 v) const { return relu4(v, relu); }
@@ -605,7 +607,7 @@ struct LinGs {
     const int o = (int)n0 + row, k = (int)k64, Ki = (int)K, Ni = (int)N;
     float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = __ldg(k + e < Ki ? hw + ((z * Ki + k + e) * Ni + o) : g_zero4);
+    for (int e = 0; e < 4; ++e) v[e] = ldg_or_zero(hw + ((z * Ki + k + e) * Ni + o), k + e < Ki);
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   DPG_NO_FIX(b_fix)
@@ -655,7 +657,7 @@ struct LinCsum {
       uint32_t qq, t;
       fmid.divmod((uint32_t)(k + e), qq, t);
       const int n = z * (int)spl + (int)qq;
-      v[e] = __ldg(k + e < Ki && n < (int)bsz ? acts + ((n * midi + (int)t) * Mi + i) : g_zero4);
+      v[e] = ldg_or_zero(acts + ((n * midi + (int)t) * Mi + i), k + e < Ki && n < (int)bsz);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -669,7 +671,7 @@ struct LinCsum {
       uint32_t qq, t;
       fmid.divmod((uint32_t)(k + e), qq, t);
       const int n = z * (int)spl + (int)qq;
-      v[e] = __ldg(k + e < Ki && n < (int)bsz ? hw + ((n * midi + (int)t) * Ni + o) : g_zero4);
+      v[e] = ldg_or_zero(hw + ((n * midi + (int)t) * Ni + o), k + e < Ki && n < (int)bsz);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -678,7 +680,7 @@ struct LinCsum {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int64_t n = (int64_t)z * spl + fmid.div((uint32_t)(k + e));
-      sc[e] = __ldg(n < bsz ? scale + n : g_zero4);
+      sc[e] = ldg_or_zero(scale + n, n < bsz);
     }
     return make_float4(sc[0] * v.x, sc[1] * v.y, sc[2] * v.z, sc[3] * v.w);
   }
