@@ -40,6 +40,28 @@ __device__ __forceinline__ double block_sum(double v, double* smem /* >= NT/32 *
   return t;
 }
 
+// Zero word that out-of-range gathers load from: operand loads are unconditional (the address is
+// selected, not the load), so a thread's gathers are all in flight at once and nothing consumes
+// a loaded value before it is needed.
+static __device__ __align__(16) const float g_zero4[4] = {0.f, 0.f, 0.f, 0.f};
+
+// Load *p when ok, else the zero word. The address is selected with selp (both candidates are
+// computed unconditionally), so the compiler cannot turn the gather into a branch per element.
+__device__ __forceinline__ float ldg_or_zero(const float* p, bool ok) {
+  const float* q;
+  asm("{\n\t.reg .pred sel;\n\tsetp.ne.b32 sel, %3, 0;\n\tselp.b64 %0, %1, %2, sel;\n\t}"
+      : "=l"(q)
+      : "l"(p), "l"(g_zero4), "r"((int)ok));
+  return __ldg(q);
+}
+__device__ __forceinline__ float4 ldg4_or_zero(const float* p, bool ok) {
+  const float* q;
+  asm("{\n\t.reg .pred sel;\n\tsetp.ne.b32 sel, %3, 0;\n\tselp.b64 %0, %1, %2, sel;\n\t}"
+      : "=l"(q)
+      : "l"(p), "l"(g_zero4), "r"((int)ok));
+  return __ldg(reinterpret_cast<const float4*>(q));
+}
+
 __device__ __forceinline__ void report_error(DeviceErr* err, uint64_t key, uint64_t aux) {
   const unsigned long long old = atomicMin(&err->key, (unsigned long long)key);
   if (key < old) atomicExch(&err->aux, (unsigned long long)aux);

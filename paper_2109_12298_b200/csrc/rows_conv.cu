@@ -80,13 +80,15 @@ __global__ void __launch_bounds__(kThreads, 2) gs_rows_kernel(const Params p) {
   for (int k = tid; k < p.Kc4; k += kThreads) {
     const int e = kt[k];
     const int coff = (e >> 10) * hwsz, ki = (e >> 5) & 31, kj = e & 31;
+    float v[PT];
 #pragma unroll
-    for (int q = 0; q < PT; ++q) {
+    for (int q = 0; q < PT; ++q) {  // all PT loads in flight, then ReLU and store
       const int iy = by[q] + ki, ix = bx[q] + kj;
       const bool ok = e >= 0 && q < p.P && (unsigned)iy < (unsigned)p.h && (unsigned)ix < (unsigned)p.w;
-      const float v = __ldg(ok ? xn + coff + iy * p.w + ix : xn);
-      xt[q * p.Kc4 + k] = ok ? relu_if(v, p.relu) : 0.f;
+      v[q] = ldg_or_zero(xn + (coff + iy * p.w + ix), ok);
     }
+#pragma unroll
+    for (int q = 0; q < PT; ++q) xt[q * p.Kc4 + k] = relu_if(v[q], p.relu);
   }
   __syncthreads();
 

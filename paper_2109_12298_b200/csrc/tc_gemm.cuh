@@ -218,28 +218,6 @@ __device__ __forceinline__ bool b_map(bool quad_major, int tid, int i, int& row,
   return idx < BN * 8;
 }
 
-// Zero word that out-of-range gathers load from: operand loads are unconditional (the address is
-// selected, not the load), so a thread's gathers for a stage are all in flight at once and nothing
-// consumes a loaded value before the stage is stored.
-static __device__ __align__(16) const float g_zero4[4] = {0.f, 0.f, 0.f, 0.f};
-
-// Load *p when ok, else the zero word. The address is selected with selp (both candidates are
-// computed unconditionally), so the compiler cannot turn the gather into a branch per element.
-__device__ __forceinline__ float ldg_or_zero(const float* p, bool ok) {
-  const float* q;
-  asm("{\n\t.reg .pred sel;\n\tsetp.ne.b32 sel, %3, 0;\n\tselp.b64 %0, %1, %2, sel;\n\t}"
-      : "=l"(q)
-      : "l"(p), "l"(g_zero4), "r"((int)ok));
-  return __ldg(q);
-}
-__device__ __forceinline__ float4 ldg4_or_zero(const float* p, bool ok) {
-  const float* q;
-  asm("{\n\t.reg .pred sel;\n\tsetp.ne.b32 sel, %3, 0;\n\tselp.b64 %0, %1, %2, sel;\n\t}"
-      : "=l"(q)
-      : "l"(p), "l"(g_zero4), "r"((int)ok));
-  return __ldg(reinterpret_cast<const float4*>(q));
-}
-
 // Prob interface:
 //   int64_t M, N, K; int ksplit; int scratch;          max sizes, split-K factor, scratch bytes
 //   int64_t mdim(int z), kdim(int z) const;             per-batch M and K (<= M, K)
