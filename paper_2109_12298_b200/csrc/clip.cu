@@ -156,7 +156,8 @@ static int pick_splits(int64_t b, int64_t tiles, int64_t per_sample_k) {
   const int64_t max_by_k = (b * per_sample_k) / 64;
   if (want > max_by_k) want = max_by_k;
   if (want < 1) want = 1;
-  return (int)want;
+  const int64_t spl = (b + want - 1) / want;
+  return (int)((b + spl - 1) / spl);  // every split non-empty
 }
 
 // ------------------------------------------------------------------------------------------

@@ -561,10 +561,11 @@ struct ConvCsum {
 
 int csum_conv_splits(const ConvGeom& cg) {
   const int64_t tiles = ((cg.K() + BM - 1) / BM) * ((cg.oc + 127) / 128);
-  int64_t splits = (2 * kNumSMs + tiles - 1) / tiles;
+  int64_t splits = (kMinBlocks * kNumSMs + tiles - 1) / tiles;
   const int64_t max_by_k = std::max<int64_t>(1, (cg.b * cg.P()) / (2 * BK));
-  splits = std::min<int64_t>(std::min<int64_t>(splits, cg.b), max_by_k);
-  return (int)std::max<int64_t>(1, splits);
+  splits = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(splits, cg.b), max_by_k));
+  const int64_t spl = (cg.b + splits - 1) / splits;
+  return (int)((cg.b + spl - 1) / spl);  // every split non-empty
 }
 
 void conv_csum(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const float* scale,
@@ -693,10 +694,11 @@ struct LinCsum {
 
 int csum_linear_splits(int64_t b, int64_t mid, int64_t d, int64_t r) {
   const int64_t tiles = ((d + BM - 1) / BM) * ((r + 127) / 128);
-  int64_t splits = (2 * kNumSMs + tiles - 1) / tiles;
+  int64_t splits = (kMinBlocks * kNumSMs + tiles - 1) / tiles;
   const int64_t max_by_k = std::max<int64_t>(1, (b * mid) / (2 * BK));
-  splits = std::min<int64_t>(std::min<int64_t>(splits, b), max_by_k);
-  return (int)std::max<int64_t>(1, splits);
+  splits = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(splits, b), max_by_k));
+  const int64_t spl = (b + splits - 1) / splits;
+  return (int)((b + spl - 1) / spl);  // every split non-empty
 }
 
 void linear_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, const float* scale,

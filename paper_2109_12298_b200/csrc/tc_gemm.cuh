@@ -5,8 +5,8 @@
 // Operands are gathered by all threads of the CTA through a problem-specific stage loader (the
 // implicit im2col of the conv contractions lives there, driven by per-CTA index tables in shared
 // memory), split into a TF32 "hi" part and the TF32-rounded remainder "lo" (split_tf32), and stored
-// into shared memory in the canonical 128B-swizzled K-major UMMA layout (8 rows x 128 B atoms,
-// 1024 B aligned). One thread issues tcgen05.mma.cta_group::1.kind::tf32 with the accumulator in
+// into shared memory in the canonical swizzled K-major UMMA layout (8-row atoms of 64 B or 128 B
+// rows, 1024 B aligned). One thread issues tcgen05.mma.cta_group::1.kind::tf32 with the accumulator in
 // tensor memory: acc += A_lo B_hi + A_hi B_lo + A_hi B_hi per K=8 slice (3xTF32). Stages are
 // double buffered: the MMAs of stage s run asynchronously while the threads gather stage s+1;
 // tcgen05.commit arrives on the stage's mbarrier to release the buffer.
@@ -19,8 +19,8 @@
 // Split-K: blockIdx.z = z * ksplit + split; split s covers K stages [s * nk / ksplit,
 // (s + 1) * nk / ksplit) and the Prob writes a partial that a fixed-order reduce combines.
 //
-// Tile: BM = 128 rows (UMMA M), BN in {16, 32, 64, 128} columns (UMMA N), BK = 32 fp32 (one
-// 128 B swizzle row) per stage; 256 threads.
+// Tile: BM = 128 rows (UMMA M), BN in {16, 32, 64, 128} columns (UMMA N), BK = 16 fp32 (one
+// 64 B swizzle row; 32 with DPG_TC_BK=32) per stage; 256 threads.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -34,7 +34,19 @@ namespace dpg {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 32;
+// K per stage: 16 fp32 = one 64 B swizzle row (SWIZZLE_64B) keeps a stage at 24 KB for BN = 64, so
+// three CTAs fit an SM (shared memory and registers); DPG_TC_BK=32 selects 128 B rows (SWIZZLE_128B).
+#ifndef DPG_TC_BK
+#define DPG_TC_BK 16
+#endif
+constexpr int BK = DPG_TC_BK;
+static_assert(BK == 16 || BK == 32, "BK: one 64 B or 128 B swizzle row");
+constexpr int kQuadsPerRow = BK / 4;                 // 16 B chunks per K-major row
+constexpr int kRowBytes = BK * 4;                    // 64 or 128
+constexpr int kAtomBytes = 8 * kRowBytes;            // 8-row swizzle atom: 512 or 1024
+constexpr int kAQ = BM * kQuadsPerRow / 256;         // A quads per thread per stage: 2 or 4
+constexpr uint64_t kLayoutType = BK == 32 ? 2 : 4;   // UMMA layout: SWIZZLE_128B / SWIZZLE_64B
+constexpr int kMinBlocks = BK == 32 ? 2 : 3;         // resident CTAs per SM the kernel is built for
 constexpr int kThreads = 256;
 constexpr int kStages = 2;
 
@@ -87,11 +99,11 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// SW128 K-major shared memory descriptor (tcgen05 matrix descriptor, sm_100 version 1):
-// start >> 4 | LBO 16 B >> 4 | SBO 1024 B >> 4 | version 1 | layout SWIZZLE_128B (2)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+// Swizzled K-major shared memory descriptor (tcgen05 matrix descriptor, sm_100 version 1):
+// start >> 4 | LBO 16 B >> 4 | SBO = one 8-row atom >> 4 | version 1 | layout (SWIZZLE_64B/128B)
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(kAtomBytes >> 4) << 32) |
+         ((uint64_t)1 << 46) | (kLayoutType << 61);
 }
 
 // Instruction descriptor kind::tf32: D f32, A/B tf32, both K-major, M = 128, N = n.
@@ -127,9 +139,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// byte offset of (row, 16 B chunk q) in a 128B-swizzled K-major tile
-__device__ __forceinline__ uint32_t sw128_off(int row, int q) {
-  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((q ^ (row & 7)) << 4));
+// byte offset of (row, 16 B chunk q) in a swizzled K-major tile: the 16 B chunk index is XORed
+// with address bits [7, 7 + log2(chunks per row)) — (row & 7) for 128 B rows, (row >> 1) & 3 for
+// 64 B rows (CuTe Swizzle<3,4,3> / Swizzle<2,4,3>)
+__device__ __forceinline__ uint32_t sw_off(int row, int q) {
+  const int x = BK == 32 ? (row & 7) : ((row >> 1) & 3);
+  return (uint32_t)((row >> 3) * kAtomBytes + (row & 7) * kRowBytes + ((q ^ x) << 4));
 }
 
 // 3xTF32 split of a finite fp32 value, both parts rounded to nearest TF32 (ties away from zero,
@@ -145,7 +160,7 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
 // Store 4 values (k .. k+3 of one row) as hi / lo TF32 into the swizzled stage buffers.
 __device__ __forceinline__ void put4(uint8_t* hi, uint8_t* lo, int row, int q, float a, float b,
                                      float c, float d) {
-  const uint32_t off = sw128_off(row, q);
+  const uint32_t off = sw_off(row, q);
   uint4 h, l;
   split_tf32(a, h.x, l.x);
   split_tf32(b, h.y, l.y);
@@ -160,7 +175,7 @@ __device__ __forceinline__ void put4(uint8_t* hi, uint8_t* lo, int row, int q, f
 
 template <int BN>
 struct Smem {
-  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
+  static constexpr int A_BYTES = BM * BK * 4;  // 8 or 16 KB
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int FIXED = kStages * STAGE + 64;
@@ -183,23 +198,23 @@ struct StageBufsT {
 // for the NEXT stage while the current one is converted, stored and consumed by the MMA, so
 // ~16 + 4 BQ independent loads per thread stay in flight.
 //
-// Thread -> (row, quad) maps (i = 0..3 for A, i = 0..BQ-1 for B):
+// Thread -> (row, quad) maps (i = 0..kAQ-1 for A, i = 0..BQ-1 for B; Q = quads per row):
 //   A row-major  (kAQuadMajor = false): row = tid & 127, quad = (tid >> 7) + 2 i
 //                 — a warp covers 32 rows at one k (coalesced when rows are contiguous)
-//   A quad-major (kAQuadMajor = true):  idx = tid + 256 i, row = idx >> 3, quad = idx & 7
-//                 — a warp covers 4 rows x 8 quads (coalesced when K is contiguous)
-//   B: idx = tid + 256 i, row = idx >> 3, quad = idx & 7 (kBQuadMajor) or row = idx % BN,
+//   A quad-major (kAQuadMajor = true):  idx = tid + 256 i, row = idx / Q, quad = idx % Q
+//                 — a warp covers 32 / Q rows x Q quads (coalesced when K is contiguous)
+//   B: idx = tid + 256 i, row = idx / Q, quad = idx % Q (kBQuadMajor) or row = idx % BN,
 //      quad = idx / BN
 template <int BN>
 struct Frag {
-  static constexpr int BQ = (BN * 8 + kThreads - 1) / kThreads;
+  static constexpr int BQ = (BN * kQuadsPerRow + kThreads - 1) / kThreads;
 };
 
 __device__ __forceinline__ void a_map(bool quad_major, int tid, int i, int& row, int& q) {
   if (quad_major) {
     const int idx = tid + kThreads * i;
-    row = idx >> 3;
-    q = idx & 7;
+    row = idx / kQuadsPerRow;
+    q = idx % kQuadsPerRow;
   } else {
     row = tid & 127;
     q = (tid >> 7) + 2 * i;
@@ -209,13 +224,13 @@ template <int BN>
 __device__ __forceinline__ bool b_map(bool quad_major, int tid, int i, int& row, int& q) {
   const int idx = tid + kThreads * i;
   if (quad_major) {
-    row = idx >> 3;
-    q = idx & 7;
+    row = idx / kQuadsPerRow;
+    q = idx % kQuadsPerRow;
   } else {
     row = idx % BN;
     q = idx / BN;
   }
-  return idx < BN * 8;
+  return idx < BN * kQuadsPerRow;
 }
 
 // Prob interface:
@@ -236,9 +251,9 @@ __device__ __forceinline__ bool b_map(bool quad_major, int tid, int i, int& row,
 template <int BN, class Prob>
 __device__ __forceinline__ void fetch(const Prob& p, int z, int64_t m0, int64_t n0, int64_t k0,
                                       const uint8_t* scratch, int tid, int mrows, int nrows,
-                                      float4 (&ra)[4], float4 (&rb)[Frag<BN>::BQ]) {
+                                      float4 (&ra)[kAQ], float4 (&rb)[Frag<BN>::BQ]) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < kAQ; ++i) {
     int row, q;
     a_map(Prob::kAQuadMajor, tid, i, row, q);
     if (row < mrows) ra[i] = p.a_quad(z, m0, row, k0 + 4 * q, scratch);
@@ -254,10 +269,10 @@ __device__ __forceinline__ void fetch(const Prob& p, int z, int64_t m0, int64_t 
 template <int BN, class Prob>
 __device__ __forceinline__ void stash(const Prob& p, int z, int64_t m0, int64_t n0, int64_t k0,
                                       const uint8_t* scratch, int tid, int mrows, int nrows,
-                                      const StageBufsT& sb, const float4 (&ra)[4],
+                                      const StageBufsT& sb, const float4 (&ra)[kAQ],
                                       const float4 (&rb)[Frag<BN>::BQ]) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < kAQ; ++i) {
     int row, q;
     a_map(Prob::kAQuadMajor, tid, i, row, q);
     if (row < mrows) put4(sb.a_hi, sb.a_lo, row, q, p.a_fix(z, m0, row, k0 + 4 * q, scratch, ra[i]));
@@ -271,7 +286,7 @@ __device__ __forceinline__ void stash(const Prob& p, int z, int64_t m0, int64_t 
 }
 
 template <int BN, class Prob>
-__global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const Prob p) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Prob p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024 B alignment by pointer arithmetic on the __shared__ array, so the compiler keeps the
   // shared address space (LDS / STS, not generic LD / ST)
@@ -310,12 +325,12 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const Prob p) {
   constexpr uint32_t idesc = idesc_tf32(BN);
   // Two register sets: the operands of stage i + 2 are requested while stage i is stored, so each
   // gather has a full stage period (store + barrier + MMA issue of the previous stage) to land.
-  float4 ra0[4], rb0[Frag<BN>::BQ], ra1[4], rb1[Frag<BN>::BQ];
+  float4 ra0[kAQ], rb0[Frag<BN>::BQ], ra1[kAQ], rb1[Frag<BN>::BQ];
   const int mrows = (int)std::min<int64_t>(BM, Mz - m0);
   const int nrows = (int)std::min<int64_t>(BN, p.N - n0);
   if (nk > 0) fetch<BN>(p, z, m0, n0, (int64_t)ks0 * BK, scratch, tid, mrows, nrows, ra0, rb0);
   if (nk > 1) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + 1) * BK, scratch, tid, mrows, nrows, ra1, rb1);
-  auto stage = [&](int i, float4 (&ra)[4], float4 (&rb)[Frag<BN>::BQ]) {
+  auto stage = [&](int i, float4 (&ra)[kAQ], float4 (&rb)[Frag<BN>::BQ]) {
     const int s = i % kStages;
     uint8_t* st = smem + s * S::STAGE;
     const StageBufsT sb{st, st + S::A_BYTES, st + 2 * S::A_BYTES, st + 2 * S::A_BYTES + S::B_BYTES};
@@ -332,9 +347,9 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const Prob p) {
       for (int kk = 0; kk < BK / 8; ++kk) {
         const uint32_t off = kk * 32;  // 8 tf32 = 32 B along the swizzled row
         const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
-        mma_tf32(tmem, sw128_desc(sa_lo + off), sw128_desc(sb_hi + off), idesc, acc0);
-        mma_tf32(tmem, sw128_desc(sa_hi + off), sw128_desc(sb_lo + off), idesc, 1u);
-        mma_tf32(tmem, sw128_desc(sa_hi + off), sw128_desc(sb_hi + off), idesc, 1u);
+        mma_tf32(tmem, sw_desc(sa_lo + off), sw_desc(sb_hi + off), idesc, acc0);
+        mma_tf32(tmem, sw_desc(sa_hi + off), sw_desc(sb_lo + off), idesc, 1u);
+        mma_tf32(tmem, sw_desc(sa_hi + off), sw_desc(sb_hi + off), idesc, 1u);
       }
       mma_commit(&bars[s]);
     }
@@ -413,7 +428,7 @@ inline int pick_ksplit(int64_t M, int64_t N, int64_t K, int64_t batches) {
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + 127) / 128) * batches;
   if (tiles >= kNumSMs) return 1;
   const int64_t nk = (K + BK - 1) / BK;
-  int64_t ks = (2 * kNumSMs + tiles - 1) / tiles;
+  int64_t ks = (kMinBlocks * kNumSMs + tiles - 1) / tiles;
   ks = std::min<int64_t>(ks, std::max<int64_t>(1, nk / 2));
   return (int)std::max<int64_t>(1, std::min<int64_t>(ks, 16));
 }
