@@ -12,8 +12,9 @@ global batch 4096) and one all-reduce of the clipped sum per step.
 Reported (rank 0 prints ONE JSON line):
   value        samples/s over all ranks, inputs resident in HBM, device time (CUDA events on the
                launching stream), L2 flushed (256 MiB write) before every timed step, max over ranks
-  e2e          the same metric through dpg_train_step_host with pinned HOST buffers: H2D of the
-               batch and D2H of the per-sample loss inside the timed region
+  e2e          the same metric through dpg_train_step_host_async with pinned HOST buffers: H2D of
+               the batch and D2H of the per-sample loss inside the timed region every step (the
+               copies of step k + 1 overlap the kernels of step k)
   roofline     dominant stage of an eager profiled pass: algorithmic bytes / its CUDA-event
                duration vs the measured HBM peak; plus the whole-step fraction
   cpu_baseline the reference compiled from its own sources (oracle/_ref, -O3), sample-sharded
@@ -361,16 +362,19 @@ def main():
     total_ms = max_over_ranks(sum(step_ms))
     value = gb * args.steps / (total_ms / 1000.0)
 
-    # ---- end to end: pinned host buffers through dpg_train_step_host ----
+    # ---- end to end: pinned host buffers through dpg_train_step_host_async (per step: H2D of the
+    # batch, the step, D2H of the per-sample loss; copies pipelined against the previous step) ----
     xh = torch.from_numpy(x).pin_memory()
     yh = torch.from_numpy(y).pin_memory()
     lh = torch.zeros(b).pin_memory()
     for _ in range(3):
-        opt.train_step_host(xh, yh, lh)
+        opt.train_step_host_async(xh, yh, lh)
+    ctx.sync()
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        opt.train_step_host(xh, yh, lh)
+    for _ in range(args.steps):  # H2D of step k+1 overlaps the kernels of step k
+        opt.train_step_host_async(xh, yh, lh)
+    ctx.sync()
     t1 = time.perf_counter()
     e2e_s = max_over_ranks(t1 - t0)
     e2e = {"value": gb * args.steps / e2e_s, "unit": "samples/s",

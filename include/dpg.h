@@ -280,6 +280,13 @@ DPG_API int64_t dpg_accumulated_samples(const dpg_optimizer* opt);
  * returns any device-detected error. */
 DPG_API dpg_status dpg_train_step_host(dpg_optimizer* opt, const float* x_host,
                                        const float* targets_host, int64_t b, float* loss_host);
+/* Pipelined variant of dpg_train_step_host for training loops: enqueues the H2D of x and
+ * targets (into one of two device staging slots, on a copy stream), the step and the D2H of the
+ * per-sample loss, and returns without waiting, so the copies of the next call overlap this
+ * step's kernels. Host buffers must stay valid (pinned for overlap) until dpg_ctx_sync, which
+ * also surfaces device-detected errors. Same semantics per step as dpg_train_step_host. */
+DPG_API dpg_status dpg_train_step_host_async(dpg_optimizer* opt, const float* x_host,
+                                             const float* targets_host, int64_t b, float* loss_host);
 /* The same step on device buffers, asynchronous; replayed from a CUDA graph captured on the
  * first call for each batch size (set use_graph = 0 to launch eagerly). */
 DPG_API dpg_status dpg_train_step(dpg_optimizer* opt, const float* x, const float* targets,

@@ -98,6 +98,13 @@ struct dpg_model {
   float* x_stage = nullptr;  // host-path staging
   float* y_stage = nullptr;
   float* loss = nullptr;
+  // pipelined host path (dpg_train_step_host_async): two staging slots filled on a copy stream
+  float* xs[2] = {nullptr, nullptr};
+  float* ys[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr};   // slot's H2D done
+  cudaEvent_t consumed[2] = {nullptr, nullptr}; // step that read the slot done
+  int64_t async_calls = 0;
 };
 
 struct dpg_optimizer {
@@ -133,6 +140,12 @@ struct dpg_optimizer {
     int64_t kernels;  // kernels per replay (gpu_launches evidence)
   };
   std::vector<Graph> graphs;
+  // pinned ring the graph replays read their Philox step from (a pageable source could make the
+  // H2D wait for the stream); a slot is reused only after the copy that read it has executed
+  static constexpr int kStepRing = 16;
+  uint64_t* step_ring = nullptr;  // pinned host [kStepRing]
+  cudaEvent_t ring_ev[kStepRing] = {};
+  bool ring_used[kStepRing] = {};
 };
 
 namespace {
@@ -592,7 +605,8 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     total += al(sizeof(int32_t) * rows);
     total += 2 * al(sizeof(int32_t) * max_batch * std::max<int64_t>(1, m->embed_tokens));
     total += al(ws);
-    total += al(sizeof(float) * max_batch * m->in_numel) + 2 * al(sizeof(float) * max_batch);
+    total += 3 * (al(sizeof(float) * max_batch * m->in_numel) + al(sizeof(float) * max_batch));
+    total += al(sizeof(float) * max_batch);
     DPG_CUDA(cudaMalloc(&m->arena, total));
     DPG_CUDA(cudaMemset(m->arena, 0, total));
     char* p = m->arena;
@@ -612,6 +626,10 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     m->ws = take(ws);
     m->x_stage = reinterpret_cast<float*>(take(sizeof(float) * max_batch * m->in_numel));
     m->y_stage = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
+    for (int q = 0; q < 2; ++q) {
+      m->xs[q] = reinterpret_cast<float*>(take(sizeof(float) * max_batch * m->in_numel));
+      m->ys[q] = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
+    }
     m->loss = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
     std::vector<int32_t> rp;
     for (size_t q = 0; q < m->params.size(); ++q)
@@ -631,6 +649,14 @@ void dpg_model_destroy(dpg_model* m) {
   if (!m) return;
   cudaSetDevice(m->ctx->device);
   cudaStreamSynchronize(m->ctx->stream);
+  if (m->copy_stream) {
+    cudaStreamSynchronize(m->copy_stream);
+    cudaStreamDestroy(m->copy_stream);
+  }
+  for (int q = 0; q < 2; ++q) {
+    if (m->copied[q]) cudaEventDestroy(m->copied[q]);
+    if (m->consumed[q]) cudaEventDestroy(m->consumed[q]);
+  }
   if (m->arena) cudaFree(m->arena);
   delete m;
 }
@@ -724,6 +750,9 @@ void dpg_optimizer_destroy(dpg_optimizer* o) {
   cudaSetDevice(o->m->ctx->device);
   cudaStreamSynchronize(o->m->ctx->stream);
   for (auto& g : o->graphs) cudaGraphExecDestroy(g.exec);
+  for (auto e : o->ring_ev)
+    if (e) cudaEventDestroy(e);
+  if (o->step_ring) cudaFreeHost(o->step_ring);
   if (o->arena) cudaFree(o->arena);
   delete o;
 }
@@ -898,7 +927,16 @@ dpg_status dpg_train_step(dpg_optimizer* o, const float* x, const float* targets
       ctx->launches = before;
       hit = &o->graphs.back();
     }
-    DPG_CUDA(cudaMemcpyAsync(o->step_dev, &o->steps, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    if (!o->step_ring) {
+      DPG_CUDA(cudaHostAlloc(&o->step_ring, sizeof(uint64_t) * dpg_optimizer::kStepRing, cudaHostAllocDefault));
+      for (auto& e : o->ring_ev) DPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int slot = (int)(o->steps % dpg_optimizer::kStepRing);
+    if (o->ring_used[slot]) DPG_CUDA(cudaEventSynchronize(o->ring_ev[slot]));
+    o->step_ring[slot] = o->steps;
+    DPG_CUDA(cudaMemcpyAsync(o->step_dev, &o->step_ring[slot], sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    DPG_CUDA(cudaEventRecord(o->ring_ev[slot], ctx->stream));
+    o->ring_used[slot] = true;
     DPG_CUDA(cudaGraphLaunch(hit->exec, ctx->stream));
     ctx->launches += hit->kernels;
     ++o->steps;
@@ -930,6 +968,46 @@ dpg_status dpg_train_step_host(dpg_optimizer* o, const float* x_host, const floa
       zero_grad_impl(o);
       throw;
     }
+  });
+}
+
+// Pipelined host path: the H2D of call k goes to staging slot k % 2 on the model's copy stream
+// (after the step that last read that slot), the step waits for it on the compute stream, and
+// the loss D2H follows the step. Nothing blocks the host, so the copies of step k + 1 overlap
+// the kernels of step k.
+dpg_status dpg_train_step_host_async(dpg_optimizer* o, const float* x_host, const float* targets_host,
+                                     int64_t b, float* loss_host) {
+  if (!o) return DPG_ERR_PARAMETER;
+  dpg_model* m = o->m;
+  dpg_ctx* ctx = m->ctx;
+  int slot = 0;
+  const dpg_status st = guard(ctx, [&] {
+    DPG_CUDA(cudaSetDevice(ctx->device));
+    if (b <= 0) raise(DPG_ERR_DIMENSION, "compute_grad_samples: batch must be non-empty");
+    if (b > m->max_b) raise(DPG_ERR_DIMENSION, "batch exceeds the model's max_batch");
+    if (!x_host || !targets_host) raise(DPG_ERR_PARAMETER, "input and targets must not be NULL");
+    if (!m->copy_stream) {
+      DPG_CUDA(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+      for (int q = 0; q < 2; ++q) {
+        DPG_CUDA(cudaEventCreateWithFlags(&m->copied[q], cudaEventDisableTiming));
+        DPG_CUDA(cudaEventCreateWithFlags(&m->consumed[q], cudaEventDisableTiming));
+      }
+    }
+    slot = (int)(m->async_calls & 1);
+    if (m->async_calls >= 2) DPG_CUDA(cudaStreamWaitEvent(m->copy_stream, m->consumed[slot], 0));
+    DPG_CUDA(cudaMemcpyAsync(m->xs[slot], x_host, sizeof(float) * b * m->in_numel, cudaMemcpyHostToDevice, m->copy_stream));
+    DPG_CUDA(cudaMemcpyAsync(m->ys[slot], targets_host, sizeof(float) * b, cudaMemcpyHostToDevice, m->copy_stream));
+    DPG_CUDA(cudaEventRecord(m->copied[slot], m->copy_stream));
+    DPG_CUDA(cudaStreamWaitEvent(ctx->stream, m->copied[slot], 0));
+    ++m->async_calls;
+  });
+  if (st != DPG_OK) return st;
+  const dpg_status st2 = dpg_train_step(o, m->xs[slot], m->ys[slot], b, m->loss, 1);
+  if (st2 != DPG_OK) return st2;
+  return guard(ctx, [&] {
+    DPG_CUDA(cudaEventRecord(m->consumed[slot], ctx->stream));
+    if (loss_host)
+      DPG_CUDA(cudaMemcpyAsync(loss_host, m->loss, sizeof(float) * b, cudaMemcpyDeviceToHost, ctx->stream));
   });
 }
 

@@ -130,6 +130,7 @@ _SIGS = {
     "dpg_grad": (_P, [_P]),
     "dpg_accumulated_samples": (_I64, [_P]),
     "dpg_train_step_host": (_I32, [_P, _P, _P, _I64, _P]),
+    "dpg_train_step_host_async": (_I32, [_P, _P, _P, _I64, _P]),
     "dpg_train_step": (_I32, [_P, _P, _P, _I64, _P, _I32]),
 }
 
@@ -492,6 +493,20 @@ class DpOptimizer:
         self._b = x.shape[0]
         self._x, self._y = x, targets
         _check(lib().dpg_train_step(self.h, _p(x), _p(targets), x.shape[0], _p(loss), int(use_graph)),
+               self.ctx.h)
+
+    def train_step_host_async(self, x_host, targets_host, loss_host=None):
+        """Pipelined host step (dpg_train_step_host_async): returns before the step finishes;
+        the host buffers must stay alive until ctx.sync()."""
+        def hp(a):
+            if a is None:
+                return None
+            if isinstance(a, torch.Tensor):
+                return ctypes.c_void_p(a.data_ptr())
+            return a.ctypes.data_as(_P)
+        b = x_host.shape[0]
+        self._b = b
+        _check(lib().dpg_train_step_host_async(self.h, hp(x_host), hp(targets_host), b, hp(loss_host)),
                self.ctx.h)
 
     def train_step_host(self, x_host, targets_host, loss_host=None):

@@ -239,6 +239,26 @@ def test_graph_replay_equals_eager(ctx):
         o3.train_step_host(np.ascontiguousarray(x, dtype=np.float32), np.ascontiguousarray(y, dtype=np.float32), lh)
     assert np.array_equal(m.store_params(), eager)
     assert np.all(np.isfinite(lh))
+    # pipelined host path (two staging slots, copies on a second stream) == device path,
+    # with a different input per step so a slot mix-up would show
+    xs = [np.ascontiguousarray(x + np.float32(0.01 * k), dtype=np.float32) for k in range(4)]
+    yc = np.ascontiguousarray(y, dtype=np.float32)
+    m.load_params(params)
+    o4 = dpg.DpOptimizer(m, **cfg)
+    for k in range(4):
+        o4.train_step(_t(xs[k]), yt, loss, use_graph=True)
+    ctx.sync()
+    ref = m.store_params()
+    m.load_params(params)
+    o5 = dpg.DpOptimizer(m, **cfg)
+    xh = [torch.from_numpy(a).pin_memory() for a in xs]
+    yh = torch.from_numpy(yc).pin_memory()  # host buffers stay alive until ctx.sync()
+    lhs = [torch.zeros(b).pin_memory() for _ in range(4)]
+    for k in range(4):
+        o5.train_step_host_async(xh[k], yh, lhs[k])
+    ctx.sync()
+    assert np.array_equal(m.store_params(), ref), "pipelined host steps must equal device steps"
+    assert all(np.all(np.isfinite(t.numpy())) for t in lhs)
 
 
 def test_degenerate_dp_equals_sgd(ctx):

@@ -1,7 +1,7 @@
 cd $GRAFT_REPO_ROOT
 timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
 python bench.py --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/bench10.json 2> gpurun_out/bench10.err; tail -2 gpurun_out/bench10.err
-DPG_CV=1 python bench.py --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/bench10_tc.json 2>&1
+DPG_RS=0 python bench.py --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/bench10_tc.json 2>&1
 python - <<'PY'
 import json
 a=json.load(open('gpurun_out/bench10.json')); b=json.load(open('gpurun_out/bench10_tc.json'))
