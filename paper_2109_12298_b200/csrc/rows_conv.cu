@@ -183,8 +183,9 @@ static Params make_params(const float* x, int relu, const float* hw, const ConvG
   p.kh = (int)g.kh; p.kw = (int)g.kw; p.stride = (int)g.stride; p.pad = (int)g.pad;
   p.ow = (int)g.ow; p.P = (int)g.P(); p.Kc = (int)g.K();
   p.Kc4 = (p.Kc + 3) & ~3;
-  // two channel halves per sample for wide layers: twice the CTAs (shorter tail), im2col built twice
-  p.osplit = g.oc >= 64 ? 2 : 1;
+  // two channel halves per sample for wide layers with few positions (cheap im2col): twice the
+  // CTAs (shorter tail), im2col built twice
+  p.osplit = (g.oc >= 64 && g.P() <= 8) ? 2 : 1;
   p.opart = (int)((g.oc + p.osplit - 1) / p.osplit);
   return p;
 }
