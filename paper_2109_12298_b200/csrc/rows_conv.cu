@@ -9,10 +9,10 @@
 // (the largest stream of the whole step: CIFAR conv4 alone is 151 MB at b = 512). The kernel is
 // built around that store stream: one CTA owns one sample and a contiguous half (or all) of its
 // output channels; im2col of the sample (P x Kc, ReLU applied) and the highway rows of its channels
-// are staged once in shared memory; then each warp produces R (2 or 4) output rows at a time — the
-// P highway values of each row are warp-uniform registers, lanes walk the rows in 16-byte chunks,
-// every chunk is P shared-memory reads shared by the R rows, 4 R P FMAs and R 128-bit streaming
-// stores, so consecutive lanes write consecutive 16 B of G (512 B per warp store).
+// are staged once in shared memory (the highway tile transposed, [p][oc]); then each warp produces
+// 4 output rows at a time — lanes walk the rows in 16-byte chunks, every chunk is P pairs of
+// 128-bit shared reads (im2col, and the 4 rows' highway values as a broadcast), 16 P FMAs and four
+// 128-bit streaming stores, so consecutive lanes write consecutive 16 B of G (512 B per store).
 #include <cstdlib>
 
 #include "conv_common.cuh"
@@ -36,11 +36,12 @@ struct Params {
 };
 
 template <int PT>
-__global__ void __launch_bounds__(kThreads, 2) gs_rows_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, 4) gs_rows_kernel(const Params p) {
   extern __shared__ __align__(16) float sm[];
   float* xt = sm;                                          // [PT][Kc4], rows >= P are zero
-  float* hs = xt + PT * p.Kc4;                             // [opart][PT], cols >= P are zero
-  int* kt = reinterpret_cast<int*>(hs + p.opart * PT);     // [Kc4] packed (c, ki, kj) or -1
+  const int ostr = (p.opart + 3) & ~3;                     // row stride of the transposed tile
+  float* hs = xt + PT * p.Kc4;                             // [PT][ostr] = B[n, o, q] transposed
+  int* kt = reinterpret_cast<int*>(hs + PT * ostr);        // [Kc4] packed (c, ki, kj) or -1
   __shared__ double red[2][kThreads / 32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -63,9 +64,9 @@ __global__ void __launch_bounds__(kThreads, 2) gs_rows_kernel(const Params p) {
   }
   // highway rows of this part: contiguous [nrow][P] in B[n]
   const float* hrow = p.hw + ((int64_t)n * p.oc + o_begin) * p.P;
-  for (int i = tid; i < nrow * PT; i += kThreads) {
-    const int o = i / PT, q = i - o * PT;
-    hs[i] = q < p.P ? __ldg(hrow + o * p.P + q) : 0.f;
+  for (int i = tid; i < ostr * PT; i += kThreads) {
+    const int o = i / PT, q = i - o * PT;  // coalesced global reads, transposed shared stores
+    hs[q * ostr + o] = (q < p.P && o < nrow) ? __ldg(hrow + o * p.P + q) : 0.f;
   }
   __syncthreads();
   // im2col of sample n: xt[q][k] = relu(x[n, c, oy s + ki - pad, ox s + kj - pad])
@@ -95,25 +96,16 @@ __global__ void __launch_bounds__(kThreads, 2) gs_rows_kernel(const Params p) {
   double sq = 0.0, sqb = 0.0;
   const int nq = p.Kc4 >> 2;
   const bool vec = (p.Kc & 3) == 0;
-  // R rows per warp pass: every 128-bit im2col read feeds 4 R FMAs (R = 4 for P > 8 keeps the
-  // shared-memory traffic under the FMA time)
-  constexpr int R = PT > 8 ? 4 : 2;
+  // 4 rows per warp pass: per position, one 128-bit im2col read and one 128-bit (broadcast) read
+  // of the 4 rows' highway values feed 16 FMAs; few registers, so several CTAs share an SM and
+  // one's staging overlaps another's stores
+  constexpr int R = 4;
   for (int r0 = R * warp; r0 < nrow; r0 += R * (kThreads / 32)) {
-    float bv[R][PT];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-#pragma unroll
-      for (int q = 0; q < PT; q += 4) {
-        const float4 u = r0 + r < nrow ? *reinterpret_cast<const float4*>(hs + (r0 + r) * PT + q)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-        bv[r][q] = u.x; bv[r][q + 1] = u.y; bv[r][q + 2] = u.z; bv[r][q + 3] = u.w;
-      }
-    }
     if (p.sq_b && lane < R && r0 + lane < nrow) {
       // bias rule for row r0 + lane: sequential fp64 sum over the P positions
-      const float* hb = hs + (r0 + lane) * PT;
+      const float* hb = hs + r0 + lane;
       double a = 0.0;
-      for (int q = 0; q < p.P; ++q) a += (double)hb[q];
+      for (int q = 0; q < p.P; ++q) a += (double)hb[q * ostr];
       const float v = (float)a;
       if (p.gb) p.gb[n * p.oc + o_begin + r0 + lane] = v;
       sqb += (double)v * v;
@@ -126,10 +118,12 @@ __global__ void __launch_bounds__(kThreads, 2) gs_rows_kernel(const Params p) {
 #pragma unroll
       for (int q = 0; q < PT; ++q) {
         const float4 xv = *reinterpret_cast<const float4*>(xt + q * p.Kc4 + 4 * j);
+        const float4 b4 = *reinterpret_cast<const float4*>(hs + q * ostr + r0);
+        const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          acc[r].x = fmaf(bv[r][q], xv.x, acc[r].x); acc[r].y = fmaf(bv[r][q], xv.y, acc[r].y);
-          acc[r].z = fmaf(bv[r][q], xv.z, acc[r].z); acc[r].w = fmaf(bv[r][q], xv.w, acc[r].w);
+          acc[r].x = fmaf(bv[r], xv.x, acc[r].x); acc[r].y = fmaf(bv[r], xv.y, acc[r].y);
+          acc[r].z = fmaf(bv[r], xv.z, acc[r].z); acc[r].w = fmaf(bv[r], xv.w, acc[r].w);
         }
       }
       const int k0 = 4 * j;
@@ -139,9 +133,7 @@ __global__ void __launch_bounds__(kThreads, 2) gs_rows_kernel(const Params p) {
         const float4 a = acc[r];
         if (vec) {
           if (g0) st_stream4(g0 + (int64_t)r * p.Kc + k0, a);
-#ifndef DPG_EXPERIMENT_NOSQ
           sq += (double)a.x * a.x + (double)a.y * a.y + (double)a.z * a.z + (double)a.w * a.w;
-#endif
         } else {
           const float v[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
@@ -192,7 +184,7 @@ static Params make_params(const float* x, int relu, const float* hw, const ConvG
 
 static size_t smem_bytes(const Params& p) {
   const int PT = pick_pt(p.P);
-  return sizeof(float) * ((size_t)PT * p.Kc4 + (size_t)p.opart * PT) + sizeof(int) * (size_t)p.Kc4;
+  return sizeof(float) * ((size_t)PT * p.Kc4 + (size_t)PT * ((p.opart + 3) & ~3)) + sizeof(int) * (size_t)p.Kc4;
 }
 
 bool supported(const ConvGeom& g) {
