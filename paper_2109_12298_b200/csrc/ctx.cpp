@@ -78,11 +78,14 @@ ProfScope::ProfScope(dpg_ctx* c, std::string name, double bytes, double flops)
   rec.flops = flops;
   rec.a = pooled_event(ctx);
   rec.b = pooled_event(ctx);
+  rec.kernels = ctx->launches;
+  rec.seq = ctx->prof_seq++;
   DPG_CUDA(cudaEventRecord(rec.a, ctx->stream));
 }
 
 ProfScope::~ProfScope() {
   if (!on) return;
+  rec.kernels = ctx->launches - rec.kernels;
   cudaEventRecord(rec.b, ctx->stream);
   ctx->prof_pending.push_back(rec);
 }
@@ -179,7 +182,10 @@ dpg_status dpg_ctx_set_profiling(dpg_ctx* ctx, int on) {
   if (!ctx) return DPG_ERR_PARAMETER;
   return guard(ctx, [&] {
     ctx->profiling = on != 0;
-    if (on) ctx->prof_agg.clear();
+    if (on) {
+      ctx->prof_agg.clear();
+      ctx->prof_seq = 0;
+    }
   });
 }
 
@@ -195,6 +201,8 @@ const char* dpg_ctx_profile_read(dpg_ctx* ctx) {
       a.bytes += r.bytes;
       a.flops += r.flops;
       a.count += 1;
+      a.kernels += r.kernels;
+      if (a.first_seq < 0) a.first_seq = r.seq;
       ctx->event_pool.push_back(r.a);
       ctx->event_pool.push_back(r.b);
     }
@@ -202,8 +210,8 @@ const char* dpg_ctx_profile_read(dpg_ctx* ctx) {
     std::string out;
     char line[512];
     for (auto& [name, a] : ctx->prof_agg) {
-      std::snprintf(line, sizeof line, "%s %.6f %lld %.1f %.1f\n", name.c_str(), a.ms,
-                    (long long)a.count, a.bytes, a.flops);
+      std::snprintf(line, sizeof line, "%s %.6f %lld %.1f %.1f %lld %lld\n", name.c_str(), a.ms,
+                    (long long)a.count, a.bytes, a.flops, (long long)a.kernels, (long long)a.first_seq);
       out += line;
     }
     ctx->prof_text = out;

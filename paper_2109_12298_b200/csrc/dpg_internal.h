@@ -82,11 +82,14 @@ struct dpg_ctx {
     std::string name;
     double bytes, flops;
     cudaEvent_t a, b;
+    int64_t kernels = 0;  // launches inside the scope
+    int64_t seq = 0;      // enqueue order of the scope
   };
   struct ProfAgg {
     double ms = 0, bytes = 0, flops = 0;
-    int64_t count = 0;
+    int64_t count = 0, kernels = 0, first_seq = -1;
   };
+  int64_t prof_seq = 0;
   bool profiling = false;
   std::vector<ProfRec> prof_pending;
   std::map<std::string, ProfAgg> prof_agg;

@@ -2,11 +2,16 @@
 // (layers.hpp:227-245) driven like GradSampleModule + DpOptimizer (optimizer.hpp:138-278,
 // 359-381), with the reference's lifecycle and error contract.
 //
-// Step structure (one CUDA stream, no host synchronisation, graph-capturable):
+// Step structure (no host synchronisation, graph-capturable):
 //   forward_backward : forward (ReLU folded into consumers) -> softmax-CE -> reverse walk:
 //                      rule(l) with fused norm partials, then dgrad(l) with the ReLU mask
 //   step             : clip_factors -> clipped sums ((scale ⊙ B)^T A, or the record) ->
 //                      [NCCL all-reduce of the flat clipped sum] -> noise + update
+// Independent launches run on branches (aux streams forked from and joined back into the
+// caller's stream, so a captured graph holds them as parallel nodes): rule(l) only needs
+// highway(l), so the rules run beside the dgrad chain; the per-layer clipped sums are mutually
+// independent (disjoint slices of `summed`, private split-K workspaces). Stage profiling keeps
+// everything on one stream.
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -94,7 +99,15 @@ struct dpg_model {
   int32_t* sorted_s = nullptr;
   float* logits_grad = nullptr;
   size_t ws_bytes = 0;
-  void* ws = nullptr;
+  void* ws = nullptr;            // fwd / dgrad split-K partials (main stream only)
+  std::vector<void*> csum_ws;    // per layer: clipped-sum split-K partials (any branch)
+  // branches: aux streams + a ring of fork/join events
+  static constexpr int kAux = 2;
+  cudaStream_t aux[kAux] = {nullptr, nullptr};
+  bool aux_dirty[kAux] = {false, false};
+  static constexpr int kEvents = 64;
+  cudaEvent_t evs[kEvents] = {};
+  int ev_next = 0;
   float* x_stage = nullptr;  // host-path staging
   float* y_stage = nullptr;
   float* loss = nullptr;
@@ -163,6 +176,48 @@ std::string err_namer(const void* user, uint64_t stage, uint64_t major) {
 }
 
 void surface(dpg_model* m) { dpg::throw_device_error(m->ctx, err_namer, m); }
+
+bool branches_on(const dpg_model* m) { return m->aux[0] && !m->ctx->profiling; }
+
+cudaEvent_t next_event(dpg_model* m) {
+  cudaEvent_t e = m->evs[m->ev_next];
+  m->ev_next = (m->ev_next + 1) % dpg_model::kEvents;
+  return e;
+}
+
+// Enqueue f's launches on aux stream i, ordered after everything already on the caller's stream.
+template <class F>
+void on_branch(dpg_model* m, int i, F&& f) {
+  dpg_ctx* ctx = m->ctx;
+  if (i < 0 || !branches_on(m)) {
+    f();
+    return;
+  }
+  const cudaEvent_t e = next_event(m);
+  DPG_CUDA(cudaEventRecord(e, ctx->stream));
+  DPG_CUDA(cudaStreamWaitEvent(m->aux[i], e, 0));
+  const cudaStream_t main = ctx->stream;
+  ctx->stream = m->aux[i];
+  m->aux_dirty[i] = true;
+  try {
+    f();
+  } catch (...) {
+    ctx->stream = main;
+    throw;
+  }
+  ctx->stream = main;
+}
+
+// The caller's stream waits for every branch forked since the last join.
+void join_branches(dpg_model* m) {
+  for (int i = 0; i < dpg_model::kAux; ++i) {
+    if (!m->aux_dirty[i]) continue;
+    const cudaEvent_t e = next_event(m);
+    DPG_CUDA(cudaEventRecord(e, m->aux[i]));
+    DPG_CUDA(cudaStreamWaitEvent(m->ctx->stream, e, 0));
+    m->aux_dirty[i] = false;
+  }
+}
 
 // Parameter / record pointer of param p for batch b: the record packs [b, numel] blocks in
 // (layer, slot) order (GradSampleRecord, grad_sample.hpp:20-33).
@@ -240,6 +295,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
       dpg::launch_gs_bias(ctx, hw, b, mid, r, conv_layout, gs_ptr(o, lp.param0 + 1, b),
                           slab + (int64_t)pb.sq_row0 * b);
     };
+    on_branch(m, 0, [&] {
     switch (lp.kind) {
       case DPG_LAYER_LINEAR: {
         {
@@ -275,6 +331,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
         break;
       }
     }
+    });
     // input gradient for the previous parametric layer, with the ReLU mask folded in
     if (lp.prev_param_layer >= 0) {
       const LayerPlan& prev = m->layers[lp.prev_param_layer];
@@ -303,6 +360,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
       }
     }
   }
+  join_branches(m);
 }
 
 // clip_and_sum of the pending batch into summed (fold_pending, optimizer.hpp:240-254)
@@ -332,6 +390,7 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
     dpg::ProfScope ps(ctx, "csum.bias[all]", bytes, 0.0);
     dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
   }
+  int branch = 0;  // weight clipped sums round-robin over aux 0, aux 1, the caller's stream
   for (size_t l = 0; l < m->layers.size(); ++l) {
     LayerPlan& lp = m->layers[l];
     if (lp.param0 < 0) continue;
@@ -352,13 +411,16 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       const float* in = act(lp.in_buf);
       const float* hw = m->highways[lp.out_buf];
       const double cio = 4.0 * (b * (lp.in_numel + lp.out_numel) + 2 * pi.numel);
+      void* ws = m->csum_ws[l];
+      const int br = branch++ % (dpg_model::kAux + 1);
+      on_branch(m, br < dpg_model::kAux ? br : -1, [&] {
       switch (lp.kind) {
         case DPG_LAYER_LINEAR: {
           dpg::ProfScope ps(ctx, "csum.linear" + ls, cio,
                             2.0 * b * lp.mid * lp.d.in_features * lp.d.out_features);
           dpg::launch_clipped_sum_linear(ctx, in, lp.in_relu, hw, o->scale, b, lp.mid,
                                          lp.d.in_features, lp.d.out_features, dst, nullptr,
-                                         accumulate, m->ws);
+                                         accumulate, ws);
           break;
         }
         case DPG_LAYER_CONV2D: {
@@ -366,19 +428,21 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
           g.b = b;
           dpg::ProfScope ps(ctx, "csum.conv2d" + ls, cio, 2.0 * b * g.oc * g.K() * g.P());
           dpg::launch_clipped_sum_conv2d(ctx, in, lp.in_relu, hw, o->scale, g, dst, nullptr,
-                                         accumulate, m->ws);
+                                         accumulate, ws);
           break;
         }
         case DPG_LAYER_EMBEDDING: {
           dpg::ProfScope ps(ctx, "csum.embedding" + ls, 4.0 * (b * lp.out_numel + 2 * pi.numel), 0.0);
           dpg::launch_clipped_sum_embedding(ctx, m->sorted_v, m->sorted_s, hw, o->scale, b,
                                             lp.tokens, lp.d.vocab_size, lp.d.embedding_dim, dst,
-                                            accumulate, m->ws);
+                                            accumulate, ws);
           break;
         }
       }
+      });
     }
   }
+  join_branches(m);
   o->has_summed = true;
   o->accumulated += b;
   o->last_b = b;
@@ -576,26 +640,30 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
       }
     }
     m->sq_rows = rows;
-    // ---- workspace for the clipped sums (shared, stream-ordered) ----
+    // ---- split-K workspaces: one for fwd / dgrad (main stream), one per layer for the clipped
+    // sums (they run on concurrent branches); smaller batches may pick more splits, so each is
+    // bounded over b = 1, 2, 4, ..., max_b and max_b ----
     size_t ws = 1 << 20;
-    for (auto& lp : m->layers) {
+    std::vector<size_t> csum_bytes(m->layers.size(), 0);
+    for (size_t li = 0; li < m->layers.size(); ++li) {
+      const LayerPlan& lp = m->layers[li];
+      size_t& cs = csum_bytes[li];
       if (lp.kind == DPG_LAYER_LINEAR)
-        ws = std::max(ws, dpg::clipped_sum_ws_linear(max_batch, lp.mid, lp.d.in_features, lp.d.out_features));
+        for (int64_t bb = 1;; bb = std::min(bb * 2, max_batch)) {
+          cs = std::max(cs, dpg::clipped_sum_ws_linear(bb, lp.mid, lp.d.in_features, lp.d.out_features));
+          if (bb == max_batch) break;
+        }
       if (lp.kind == DPG_LAYER_CONV2D) {
         ConvGeom g = lp.g;
-        g.b = max_batch;
-        ws = std::max(ws, dpg::clipped_sum_ws_conv2d(g));
-        ws = std::max(ws, dpg::conv_fwd_ws_bytes(g));
-        ws = std::max(ws, dpg::conv_dgrad_ws_bytes(g));
-        // smaller batches may pick more splits: bound by b = 1..max_b worst case
-        for (int64_t bb = 1; bb <= max_batch; bb = bb * 2) {
+        for (int64_t bb = 1;; bb = std::min(bb * 2, max_batch)) {
           g.b = bb;
-          ws = std::max(ws, dpg::clipped_sum_ws_conv2d(g));
+          cs = std::max(cs, dpg::clipped_sum_ws_conv2d(g));
           ws = std::max(ws, dpg::conv_fwd_ws_bytes(g));
           ws = std::max(ws, dpg::conv_dgrad_ws_bytes(g));
+          if (bb == max_batch) break;
         }
       }
-      if (lp.kind == DPG_LAYER_EMBEDDING) ws = std::max(ws, dpg::clipped_sum_ws_embedding(max_batch, lp.d.vocab_size));
+      if (lp.kind == DPG_LAYER_EMBEDDING) cs = std::max(cs, dpg::clipped_sum_ws_embedding(max_batch, lp.d.vocab_size));
     }
     m->ws_bytes = ws;
     // ---- arena ----
@@ -605,6 +673,7 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     total += al(sizeof(int32_t) * rows);
     total += 2 * al(sizeof(int32_t) * max_batch * std::max<int64_t>(1, m->embed_tokens));
     total += al(ws);
+    for (size_t cs : csum_bytes) total += al(cs);
     total += 3 * (al(sizeof(float) * max_batch * m->in_numel) + al(sizeof(float) * max_batch));
     total += al(sizeof(float) * max_batch);
     DPG_CUDA(cudaMalloc(&m->arena, total));
@@ -624,6 +693,9 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     m->sorted_v = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * max_batch * std::max<int64_t>(1, m->embed_tokens)));
     m->sorted_s = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * max_batch * std::max<int64_t>(1, m->embed_tokens)));
     m->ws = take(ws);
+    for (size_t cs : csum_bytes) m->csum_ws.push_back(cs ? take(cs) : nullptr);
+    for (auto& st : m->aux) DPG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : m->evs) DPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     m->x_stage = reinterpret_cast<float*>(take(sizeof(float) * max_batch * m->in_numel));
     m->y_stage = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
     for (int q = 0; q < 2; ++q) {
@@ -653,6 +725,13 @@ void dpg_model_destroy(dpg_model* m) {
     cudaStreamSynchronize(m->copy_stream);
     cudaStreamDestroy(m->copy_stream);
   }
+  for (auto& st : m->aux)
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  for (auto& e : m->evs)
+    if (e) cudaEventDestroy(e);
   for (int q = 0; q < 2; ++q) {
     if (m->copied[q]) cudaEventDestroy(m->copied[q]);
     if (m->consumed[q]) cudaEventDestroy(m->consumed[q]);

@@ -202,12 +202,14 @@ class Context:
         _check(lib().dpg_ctx_set_profiling(self.h, int(on)), self.h)
 
     def profile(self):
-        """{stage: {"ms": total, "count": n, "bytes": algorithmic bytes total, "flops": ...}}"""
+        """{stage: {"ms": total, "count": n, "bytes": algorithmic bytes total, "flops": ...,
+        "kernels": launches total, "seq": enqueue order of the first occurrence}}"""
         txt = lib().dpg_ctx_profile_read(self.h).decode()
         out = {}
         for line in txt.strip().splitlines():
-            name, ms, cnt, by, fl = line.split()
-            out[name] = {"ms": float(ms), "count": int(cnt), "bytes": float(by), "flops": float(fl)}
+            name, ms, cnt, by, fl, kern, seq = line.split()
+            out[name] = {"ms": float(ms), "count": int(cnt), "bytes": float(by), "flops": float(fl),
+                         "kernels": int(kern), "seq": int(seq)}
         return out
 
     def init_comm(self, nranks: int, rank: int, uid: bytes):

@@ -1,5 +1,6 @@
 """One eager (non-graph) CIFAR b=512 DP-SGD step for ncu: every kernel of the step launched once
 after a warm-up step. Usage: ncu ... python tools/prof_step.py [workload] [batch]"""
+import json
 import os
 import sys
 
@@ -23,8 +24,18 @@ xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
 for _ in range(2):
     o.train_step(xt, yt, use_graph=False)
 ctx.sync()
+# the profiled step runs with stage profiling on: one stream, and the stage sequence (name, kernels)
+# is written next to the ncu output so tools/ncu_stages.py can attribute each launch to its stage
+ctx.set_profiling(True)
 torch.cuda.profiler.start()
 o.train_step(xt, yt, use_graph=False)
 ctx.sync()
 torch.cuda.profiler.stop()
+prof = ctx.profile()
+ctx.set_profiling(False)
+seq = sorted(((v["seq"], k, v["kernels"]) for k, v in prof.items()))
+os.makedirs("gpurun_out", exist_ok=True)
+with open(os.path.join("gpurun_out", f"stages_{name}.json"), "w") as f:
+    json.dump([{"stage": k, "kernels": n, "bytes": prof[k]["bytes"], "flops": prof[k]["flops"]}
+               for _, k, n in seq], f, indent=1)
 print("launches", ctx.kernel_launches)
