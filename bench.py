@@ -250,6 +250,16 @@ def cpu_baseline(workload, budget_s=15.0):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if args.workload == "linear_t64":
+        cb = cpu_baseline_linear_t64(budget_s=60.0)
+        line = {"metric": LINEAR_T64_METRIC, "value": cb["value"], "unit": "samples/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+                "config": {"workload": "linear_t64"}, "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     from paper_2109_12298_b200.configs import WORKLOADS
     w = WORKLOADS[args.workload]
     nthreads = cpu_threads()
@@ -275,6 +285,197 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------ cfg2 harness
+LINEAR_T64_METRIC = "DP-SGD per-layer step samples/sec (Linear 512->512, T=64, B=256)"
+
+
+def tf32_peak_tflops():
+    """Dense TF32 tensor throughput measured here (torch.matmul 8192^3, allow_tf32, best of 5)."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, device="cuda")
+    b = torch.randn(n, n, device="cuda")
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    best = 1e9
+    try:
+        for _ in range(2):
+            a @ b
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def run_linear_t64(args, rank, world):
+    """BASELINE configs[1]: per_sample_rule_linear on A, B [256, 64, 512] (tcgen05 3xTF32, fused
+    norms) + bias rule -> clip factors -> clipped sum (s . B)^T A -> noise + SGD update, through
+    the operator ABI (dpg_grad_sample_linear, dpg_clip_factors, dpg_clipped_sum_linear,
+    dpg_noise_update) on device-resident buffers."""
+    import ctypes
+    import torch
+    from paper_2109_12298_b200 import dpg
+    from paper_2109_12298_b200.configs import LINEAR_T64 as C
+    torch.cuda.set_device(0)
+    ctx = dpg.Context(0)
+    lib = dpg.lib()
+    b, t, d, r = C["b"], C["t"], C["d"], C["r"]
+    L = r * d + r
+    g = torch.Generator(device="cpu").manual_seed(2)
+    A = torch.randn(b, t, d, generator=g).cuda()
+    B = torch.randn(b, t, r, generator=g).cuda()
+    gw = torch.empty(b, r, d, device="cuda")
+    gb = torch.empty(b, r, device="cuda")
+    sq = torch.empty(2, b, dtype=torch.float64, device="cuda")
+    norms = torch.empty(b, dtype=torch.float64, device="cuda")
+    scale = torch.empty(b, device="cuda")
+    nclip = torch.zeros(1, dtype=torch.int64, device="cuda")
+    summed = torch.empty(L, device="cuda")
+    params = (torch.rand(L, generator=g) - 0.5).cuda() / d ** 0.5
+    grad = torch.empty(L, device="cuda")
+    P = dpg._p
+    step_no = [0]
+
+    def stages():
+        return [
+            ("gs.linear+bias", lambda: dpg._check(lib.dpg_grad_sample_linear(
+                ctx.h, P(A), P(B), b, t, d, r, P(gw), P(gb), P(sq[0]), P(sq[1])), ctx.h),
+             4.0 * (b * t * (d + r) + b * r * d + b * r), 2.0 * b * t * d * r),
+            ("clip_factors", lambda: dpg._check(lib.dpg_clip_factors(
+                ctx.h, P(sq), 2, b, args.max_grad_norm, P(norms), P(scale), P(nclip)), ctx.h),
+             8.0 * 2 * b + 12.0 * b, 0.0),
+            ("csum.linear+bias", lambda: dpg._check(lib.dpg_clipped_sum_linear(
+                ctx.h, P(A), P(B), P(scale), b, t, d, r, P(summed), P(summed[r * d:]), 0), ctx.h),
+             4.0 * (b * t * (d + r) + 2 * L), 2.0 * b * t * d * r),
+            ("noise_update", lambda: dpg._check(lib.dpg_noise_update(
+                ctx.h, P(params), P(summed), P(grad), L, args.sigma, args.max_grad_norm, float(b), 0.1,
+                3, step_no[0], None), ctx.h), 16.0 * L, 0.0),
+        ]
+
+    st = stages()
+
+    def step():
+        for _, f, _, _ in st:
+            f()
+        step_no[0] += 1
+
+    stream = ctx.stream
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    launches0 = ctx.kernel_launches
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    gpu_launches = ctx.kernel_launches - launches0
+    ctx.sync()
+    total_ms = sum(a.elapsed_time(c) for a, c in evs)
+    value = b * args.steps / (total_ms / 1000.0)
+    # per-stage device time (events around each stage; G = 268 MB > L2, so no flush is needed)
+    per = {name: 0.0 for name, _, _, _ in st}
+    reps = 10
+    for _ in range(reps):
+        for name, f, _, _ in st:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            f()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            per[name] += e0.elapsed_time(e1) / reps
+    hbm, peak_src = peaks()
+    tf32 = tf32_peak_tflops()
+    name, _, by, fl = st[0]
+    ms = per[name]
+    achieved_gbs = by / (ms * 1e6)
+    achieved_tf = fl / (ms * 1e9)
+    # end to end: pinned host A, B -> device, step, norms back
+    Ah, Bh = A.cpu().pin_memory(), B.cpu().pin_memory()
+    nh = torch.empty(b, dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        A.copy_(Ah, non_blocking=True)
+        B.copy_(Bh, non_blocking=True)
+        step()
+        nh.copy_(norms, non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    line = {
+        "metric": LINEAR_T64_METRIC, "value": value, "unit": "samples/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "linear_t64", "batch": b, "seq_len": t, "in": d, "out": r,
+                   "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
+                   "l2": "no flush: the 268 MB per-sample gradient exceeds L2 every step"},
+        "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved_gbs / hbm, "traffic": None,
+                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
+                     "algorithmic_bytes_per_launch": by, "launch_ms": ms,
+                     "tensor": {"achieved_tflops": achieved_tf, "tf32_peak_tflops_measured": tf32,
+                                "peak_3xtf32_tflops": tf32 / 3.0, "frac_3xtf32": achieved_tf / (tf32 / 3.0)},
+                     "stages_ms": per},
+        "e2e": {"value": b * args.steps / e2e_s, "unit": "samples/s",
+                "h2d_bytes_per_step": int(A.numel() + B.numel()) * 4, "d2h_bytes_per_step": b * 8},
+        "gpu_launches": gpu_launches, "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_linear_t64()
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_linear_t64(budget_s=15.0):
+    """The reference's per_sample_rule_linear + clip_and_sum on sample shards (one host thread per
+    shard, as the virtual-step thread pool does), then the shard sums added and add_noise, on a
+    bounded sample of the cfg2 batch (oracle/_ref built -O3 from the reference's sources)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import numpy as np
+    import oracle
+    from paper_2109_12298_b200.configs import LINEAR_T64 as C
+    if not oracle.reference_available(fast=True):
+        return None
+    ref = oracle.reference(fast=True)
+    nthreads = cpu_threads()
+    b = 2 * nthreads
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((b, C["t"], C["d"])).astype(np.float32)
+    B = rng.standard_normal((b, C["t"], C["r"])).astype(np.float32)
+    shards = np.array_split(np.arange(b), nthreads)
+
+    def shard(ix):
+        gw, gb = ref.rule_linear(np.ascontiguousarray(A[ix]), np.ascontiguousarray(B[ix]))
+        return ref.clip_and_sum([gw, gb], 1.0)[0]
+
+    times = []
+    t_end = time.perf_counter() + budget_s
+    with ThreadPoolExecutor(nthreads) as ex:
+        while True:
+            t0 = time.perf_counter()
+            parts = list(ex.map(shard, shards))
+            summed = np.concatenate([sum(p[k] for p in parts) for k in range(2)])
+            ref.add_noise(summed, 1.0, 1.0, 3)
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() > t_end or len(times) >= 5:
+                break
+    med = statistics.median(times)
+    return {"value": b / med, "unit": "samples/s", "cores": nthreads, "kind": "reference",
+            "sample": f"linear_t64: {b} samples per step (rule + clip_and_sum per {len(shards)} "
+                      f"thread shards, add_noise), median of {len(times)}, -O3 -march=x86-64-v3"}
+
+
 # ------------------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -283,6 +484,10 @@ def main():
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("gloo")
+    if args.workload == "linear_t64" and args.impl == "ours":
+        if rank == 0:
+            run_linear_t64(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         if world > 1:

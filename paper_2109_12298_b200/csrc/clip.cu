@@ -313,6 +313,7 @@ static void cs_conv_tiles(const ConvGeom& g, int& bm, int& bn) {
 
 size_t clipped_sum_ws_conv2d(const ConvGeom& g) {
   if (ds::enabled()) return sizeof(float) * (size_t)ds::csum_splits(g) * (size_t)(g.oc * g.K());
+  if (tk::supported(g)) return sizeof(float) * (size_t)tk::csum_splits(g) * (size_t)(g.oc * g.K());
   if (ps::supported_csum(g)) return sizeof(float) * (size_t)ps::csum_splits(g) * (size_t)(g.oc * g.K());
   if (use_tc()) return sizeof(float) * (size_t)tc::csum_conv_splits(g) * (size_t)(g.oc * g.K());
   int bm, bn;
@@ -330,6 +331,12 @@ void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const f
   if (ds::enabled()) {
     const int splits = ds::csum_splits(g);
     ds::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
+    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
+    return;
+  }
+  if (tk::supported(g)) {
+    const int splits = tk::csum_splits(g);
+    tk::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
     launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
     return;
   }

@@ -194,6 +194,15 @@ void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* 
           const ConvGeom& g, float* part, int splits);
 }  // namespace ds
 
+namespace tk {  // thin-K conv layers (ic*kh*kw <= 32) on CUDA cores: rule (+ bias rule), clipped sum
+bool supported(const ConvGeom& g);
+void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
+        double* sq_part, float* gb, double* sq_b);
+int csum_splits(const ConvGeom& g);
+void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* scale,
+          const ConvGeom& g, float* part, int splits);
+}  // namespace tk
+
 namespace rs {
 bool supported(const ConvGeom& g);  // per-sample gradients, P <= 16
 int gs_rows(const ConvGeom& g);

@@ -157,6 +157,7 @@ static void conv_tiles(const ConvGeom& g, int& bm, int& bn) {
 
 int sq_rows_conv2d(const ConvGeom& g) {
   if (ds::enabled()) return ds::gs_rows(g);
+  if (tk::supported(g)) return 1;
   if (rs::supported(g)) return rs::gs_rows(g);  // (ds is opt-in and overrides both)
   if (ps::supported(g)) return ps::gs_rows(g);
   if (use_tc()) return tc::gs_conv_rows(g);
@@ -166,10 +167,11 @@ int sq_rows_conv2d(const ConvGeom& g) {
 }
 
 bool gs_conv2d_fuses_bias(const ConvGeom& g) {
-  return !ds::enabled() && (rs::supported(g) || ps::supported(g));
+  return !ds::enabled() && (tk::supported(g) || rs::supported(g) || ps::supported(g));
 }
 int sq_rows_conv2d_bias(const ConvGeom& g) {
   if (ds::enabled()) return 1;
+  if (tk::supported(g)) return 1;
   if (rs::supported(g)) return rs::gs_rows(g);
   if (ps::supported(g)) return ps::gs_rows(g);
   return 1;
@@ -179,6 +181,10 @@ void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
                       float* gw, double* sq_part, float* gb, double* sq_b) {
   if (g.b == 0) return;
   const bool bias = gb || sq_b;
+  if (!ds::enabled() && tk::supported(g)) {
+    tk::gs(ctx, x, x_relu, hw, g, gw, sq_part, gb, sq_b);
+    return;
+  }
   if (!ds::enabled() && rs::supported(g)) {
     rs::gs(ctx, x, x_relu, hw, g, gw, sq_part, gb, sq_b);
     return;

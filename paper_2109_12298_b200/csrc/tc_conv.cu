@@ -160,7 +160,7 @@ struct ConvFwd {
     float* out = y + (int64_t)n * g.oc * g.P + p;
     for (int j = 0; j < nv; ++j) out[(n0 + j) * g.P] = v[j] + (bias ? __ldg(bias + n0 + j) : 0.f);
   }
-  __device__ void epilogue_cta(int, int, double) const {}
+  __device__ void epilogue_cta(int, int, int, double) const {}
 };
 
 // Y[n][oc][p] = bias[oc] + sum_s part[s][oc][n*P + p]
@@ -312,7 +312,7 @@ struct ConvDgrad {
       dx[off] = val;
     }
   }
-  __device__ void epilogue_cta(int, int, double) const {}
+  __device__ void epilogue_cta(int, int, int, double) const {}
 };
 
 // dx = mask ? (sum_s part[s]) : 0 (input-shaped partials; every class writes disjoint pixels)
@@ -446,8 +446,8 @@ struct ConvGs {
       sq += (double)v[j] * v[j];
     }
   }
-  __device__ void epilogue_cta(int z, int, double sq) const {
-    if (sq_part) sq_part[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * bsz + z] = sq;
+  __device__ void epilogue_cta(int z, int, int tile_mn, double sq) const {
+    if (sq_part) sq_part[(int64_t)tile_mn * bsz + z] = sq;
   }
 };
 
@@ -556,12 +556,12 @@ struct ConvCsum {
     float* out = part + ((int64_t)z * g.oc + n0) * g.Kc + m;
     for (int j = 0; j < nv; ++j) out[j * g.Kc] = v[j];
   }
-  __device__ void epilogue_cta(int, int, double) const {}
+  __device__ void epilogue_cta(int, int, int, double) const {}
 };
 
 int csum_conv_splits(const ConvGeom& cg) {
   const int64_t tiles = ((cg.K() + BM - 1) / BM) * ((cg.oc + 127) / 128);
-  int64_t splits = (kMinBlocks * kNumSMs + tiles - 1) / tiles;
+  int64_t splits = (ctas_target() + tiles - 1) / tiles;
   const int64_t max_by_k = std::max<int64_t>(1, (cg.b * cg.P()) / (2 * BK));
   splits = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(splits, cg.b), max_by_k));
   const int64_t spl = (cg.b + splits - 1) / splits;
@@ -619,8 +619,8 @@ struct LinGs {
       sq += (double)v[j] * v[j];
     }
   }
-  __device__ void epilogue_cta(int z, int, double sq) const {
-    if (sq_part) sq_part[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * bsz + z] = sq;
+  __device__ void epilogue_cta(int z, int, int tile_mn, double sq) const {
+    if (sq_part) sq_part[(int64_t)tile_mn * bsz + z] = sq;
   }
 };
 
@@ -689,12 +689,12 @@ struct LinCsum {
     float* out = part + ((int64_t)z * N + n0) * M + m;
     for (int j = 0; j < nv; ++j) out[j * M] = v[j];
   }
-  __device__ void epilogue_cta(int, int, double) const {}
+  __device__ void epilogue_cta(int, int, int, double) const {}
 };
 
 int csum_linear_splits(int64_t b, int64_t mid, int64_t d, int64_t r) {
   const int64_t tiles = ((d + BM - 1) / BM) * ((r + 127) / 128);
-  int64_t splits = (kMinBlocks * kNumSMs + tiles - 1) / tiles;
+  int64_t splits = (ctas_target() + tiles - 1) / tiles;
   const int64_t max_by_k = std::max<int64_t>(1, (b * mid) / (2 * BK));
   splits = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(splits, b), max_by_k));
   const int64_t spl = (b + splits - 1) / splits;

@@ -20,7 +20,8 @@ import torch
 from .configs import LayerDesc, c_layers, params_meta
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdpg.so")
+# DPG_LIB: an alternative in-tree build of the same sources (A/B experiments only)
+LIB_PATH = os.path.join(HERE, os.environ.get("DPG_LIB", "libdpg.so"))
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
