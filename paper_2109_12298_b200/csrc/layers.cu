@@ -199,6 +199,55 @@ __global__ void __launch_bounds__(256) linear_fwd_narrow_kernel(const float* __r
   }
 }
 
+// Narrow outputs (r <= 64) with d % 4 == 0: one CTA per row, its 4 warps split the row's 16-byte
+// chunks; every lane keeps the r weight chunks of its column in flight (coalesced 128-bit loads),
+// per-row dot products are reduced warp (fixed shuffle tree) then across the 4 warps in order.
+constexpr int kRowWarps = 4;
+template <int RMAX>
+__global__ void __launch_bounds__(32 * kRowWarps) linear_fwd_row_kernel(const float* __restrict__ x,
+                                                                       int x_relu,
+                                                                       const float* __restrict__ w,
+                                                                       const float* __restrict__ bias,
+                                                                       int64_t d, int r,
+                                                                       float* __restrict__ y) {
+  __shared__ float part[kRowWarps][RMAX];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = blockIdx.x;
+  float acc[RMAX];
+#pragma unroll
+  for (int o = 0; o < RMAX; ++o) acc[o] = 0.f;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * d);
+  const int64_t d4 = d >> 2;
+  for (int64_t c = (int64_t)warp * 32 + lane; c < d4; c += 32 * kRowWarps) {
+    float4 xv = __ldg(xr + c);
+    xv = make_float4(relu_if(xv.x, x_relu), relu_if(xv.y, x_relu), relu_if(xv.z, x_relu), relu_if(xv.w, x_relu));
+#pragma unroll
+    for (int o = 0; o < RMAX; ++o) {
+      if (o < r) {
+        const float4 wv = __ldg(reinterpret_cast<const float4*>(w + (int64_t)o * d) + c);
+        acc[o] = fmaf(wv.x, xv.x, acc[o]);
+        acc[o] = fmaf(wv.y, xv.y, acc[o]);
+        acc[o] = fmaf(wv.z, xv.z, acc[o]);
+        acc[o] = fmaf(wv.w, xv.w, acc[o]);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < RMAX; ++o) {
+    if (o < r) {
+      const float v = warp_sum(acc[o]);
+      if (lane == 0) part[warp][o] = v;
+    }
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < r; o += 32 * kRowWarps) {
+    float t = part[0][o];
+#pragma unroll
+    for (int q = 1; q < kRowWarps; ++q) t += part[q][o];
+    y[row * r + o] = (bias ? __ldg(bias + o) : 0.f) + t;
+  }
+}
+
 // Narrow outputs with d % 4 == 0: a CTA owns kFwdRows rows; thread t walks the 16-byte column
 // chunks t, t + 128, ... of those rows, reading each weight chunk once for all of them, so every
 // load is a coalesced 128-bit load and each thread keeps ~kFwdRows + 1 of them in flight.
@@ -292,6 +341,13 @@ void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w,
   if (rows == 0) return;
   const bool aligned = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(w) & 15) == 0;
+  if (aligned && r <= 64) {
+    if (r <= 16) linear_fwd_row_kernel<16><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y);
+    else if (r <= 32) linear_fwd_row_kernel<32><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y);
+    else linear_fwd_row_kernel<64><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y);
+    DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
   if (aligned && r <= 16) {
     const unsigned g4 = (unsigned)((rows + kFwdRows - 1) / kFwdRows);
     if (r <= 4) linear_fwd_rows_kernel<4><<<g4, kFwdThreads, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);

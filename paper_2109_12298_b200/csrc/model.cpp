@@ -387,8 +387,10 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       items.item[items.count++] = {gs_ptr(o, (int)(&pi - &m->params[0]), b), o->summed + pi.offset, pi.numel};
       bytes += 4.0 * (b * pi.numel + 2 * pi.numel);
     }
-    dpg::ProfScope ps(ctx, "csum.bias[all]", bytes, 0.0);
-    dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+    on_branch(m, 1, [&] {
+      dpg::ProfScope ps(ctx, "csum.bias[all]", bytes, 0.0);
+      dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+    });
   }
   int branch = 0;  // weight clipped sums round-robin over aux 0, aux 1, the caller's stream
   for (size_t l = 0; l < m->layers.size(); ++l) {
