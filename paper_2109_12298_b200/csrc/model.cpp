@@ -13,6 +13,7 @@
 // independent (disjoint slices of `summed`, private split-K workspaces). Stage profiling keeps
 // everything on one stream.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>

@@ -13,6 +13,8 @@
 // precomputed once per CTA into shared-memory tables (k -> plane offset / tap, p -> (oy s, ox s),
 // row -> base offset), so each gathered element costs one broadcast table read, two bound checks
 // and one load.
+#include <cstdlib>
+
 #include "conv_common.cuh"
 #include "tc_gemm.cuh"
 
@@ -163,14 +165,28 @@ struct ConvFwd {
   __device__ void epilogue_cta(int, int, int, double) const {}
 };
 
+// sum_s part[s * stride + i] in split order, 8 independent loads in flight per round
+__device__ __forceinline__ float sum_splits(const float* __restrict__ part, int ksplit, int64_t stride, int64_t i) {
+  float acc = 0.f;
+  int s = 0;
+  for (; s + 8 <= ksplit; s += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(part + (int64_t)(s + u) * stride + i);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
+  }
+  for (; s < ksplit; ++s) acc += __ldg(part + (int64_t)s * stride + i);
+  return acc;
+}
+
 // Y[n][oc][p] = bias[oc] + sum_s part[s][oc][n*P + p]
 __global__ void fwd_reduce_kernel(const float* __restrict__ part, int ksplit, int64_t M, int64_t oc,
                                   int64_t P, const float* __restrict__ bias, float* __restrict__ y) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over oc * M, m fastest
   if (i >= oc * M) return;
   const int64_t c = i / M, m = i - c * M;
-  float acc = 0.f;
-  for (int s = 0; s < ksplit; ++s) acc += part[(int64_t)s * oc * M + i];
+  const float acc = sum_splits(part, ksplit, oc * M, i);
   const int64_t n = m / P, p = m - n * P;
   y[(n * oc + c) * P + p] = acc + (bias ? bias[c] : 0.f);
 }
@@ -320,8 +336,7 @@ __global__ void dgrad_reduce_kernel(const float* __restrict__ part, int ksplit, 
                                     const float* __restrict__ mask, float* __restrict__ dx) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  float acc = 0.f;
-  for (int s = 0; s < ksplit; ++s) acc += part[(int64_t)s * n + i];
+  float acc = sum_splits(part, ksplit, n, i);
   if (mask && !(mask[i] > 0.f)) acc = 0.f;
   dx[i] = acc;
 }
@@ -559,9 +574,18 @@ struct ConvCsum {
   __device__ void epilogue_cta(int, int, int, double) const {}
 };
 
+// CTAs the clipped-sum launches aim for (split count = this / output tiles)
+static int csum_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("DPG_CSUM_CTAS");
+    return e ? std::atoi(e) : ctas_target();
+  }();
+  return v;
+}
+
 int csum_conv_splits(const ConvGeom& cg) {
   const int64_t tiles = ((cg.K() + BM - 1) / BM) * ((cg.oc + 127) / 128);
-  int64_t splits = (ctas_target() + tiles - 1) / tiles;
+  int64_t splits = (csum_ctas() + tiles - 1) / tiles;
   const int64_t max_by_k = std::max<int64_t>(1, (cg.b * cg.P()) / (2 * BK));
   splits = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(splits, cg.b), max_by_k));
   const int64_t spl = (cg.b + splits - 1) / splits;
@@ -694,7 +718,7 @@ struct LinCsum {
 
 int csum_linear_splits(int64_t b, int64_t mid, int64_t d, int64_t r) {
   const int64_t tiles = ((d + BM - 1) / BM) * ((r + 127) / 128);
-  int64_t splits = (ctas_target() + tiles - 1) / tiles;
+  int64_t splits = (csum_ctas() + tiles - 1) / tiles;
   const int64_t max_by_k = std::max<int64_t>(1, (b * mid) / (2 * BK));
   splits = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(splits, b), max_by_k));
   const int64_t spl = (b + splits - 1) / splits;
