@@ -294,8 +294,17 @@ void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w,
                        const ConvGeom& g, float* y, void* ws);
 void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
                          const float* mask_src, float* dx, void* ws);
+// softmax-CE epilogue of the logits-producing linear forward (one row per sample)
+struct LossFuse {
+  const float* targets;
+  float* loss;
+  float* grad;
+  int logits_relu;
+  DeviceErr* err;
+};
+bool linear_fwd_fuses_loss(int64_t d, int64_t r, const float* x, const float* w);
 void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-                       int64_t rows, int64_t d, int64_t r, float* y);
+                       int64_t rows, int64_t d, int64_t r, float* y, const LossFuse* loss = nullptr);
 void launch_linear_dgrad(dpg_ctx* ctx, const float* dy, const float* w, int64_t rows, int64_t d,
                          int64_t r, const float* mask_src, float* dx);
 void launch_embedding_fwd(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* sorted_s,

@@ -203,14 +203,18 @@ __global__ void __launch_bounds__(256) linear_fwd_narrow_kernel(const float* __r
 // chunks; every lane keeps the r weight chunks of its column in flight (coalesced 128-bit loads),
 // per-row dot products are reduced warp (fixed shuffle tree) then across the 4 warps in order.
 constexpr int kRowWarps = 4;
+__device__ __forceinline__ void softmax_ce_warp(const float* row, int logits_relu, const float* __restrict__ targets,
+                                                int64_t n, int64_t k, float* __restrict__ loss,
+                                                float* __restrict__ grad, DeviceErr* err);
 template <int RMAX>
 __global__ void __launch_bounds__(32 * kRowWarps) linear_fwd_row_kernel(const float* __restrict__ x,
                                                                        int x_relu,
                                                                        const float* __restrict__ w,
                                                                        const float* __restrict__ bias,
                                                                        int64_t d, int r,
-                                                                       float* __restrict__ y) {
+                                                                       float* __restrict__ y, LossFuse ce) {
   __shared__ float part[kRowWarps][RMAX];
+  __shared__ float logit[RMAX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = blockIdx.x;
   float acc[RMAX];
@@ -244,7 +248,13 @@ __global__ void __launch_bounds__(32 * kRowWarps) linear_fwd_row_kernel(const fl
     float t = part[0][o];
 #pragma unroll
     for (int q = 1; q < kRowWarps; ++q) t += part[q][o];
-    y[row * r + o] = (bias ? __ldg(bias + o) : 0.f) + t;
+    const float v = (bias ? __ldg(bias + o) : 0.f) + t;
+    y[row * r + o] = v;
+    logit[o] = v;
+  }
+  if (ce.grad) {  // this layer's outputs are the logits: the loss in the same launch
+    __syncthreads();
+    if (warp == 0) softmax_ce_warp(logit, ce.logits_relu, ce.targets, row, r, ce.loss, ce.grad, ce.err);
   }
 }
 
@@ -336,15 +346,26 @@ struct LinearFwdProb {
   }
 };
 
+bool linear_fwd_fuses_loss(int64_t d, int64_t r, const float* x, const float* w) {
+  return (d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(w) & 15) == 0 && r <= 64;
+}
+
 void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-                       int64_t rows, int64_t d, int64_t r, float* y) {
+                       int64_t rows, int64_t d, int64_t r, float* y, const LossFuse* loss) {
+  LossFuse ce{};
+  if (loss) {
+    if (!linear_fwd_fuses_loss(d, r, x, w)) raise(DPG_ERR_INTERNAL, "linear forward cannot fuse the loss");
+    ce = *loss;
+    ce.err = ctx->dev_err;
+  }
   if (rows == 0) return;
   const bool aligned = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(w) & 15) == 0;
   if (aligned && r <= 64) {
-    if (r <= 16) linear_fwd_row_kernel<16><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y);
-    else if (r <= 32) linear_fwd_row_kernel<32><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y);
-    else linear_fwd_row_kernel<64><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y);
+    if (r <= 16) linear_fwd_row_kernel<16><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y, ce);
+    else if (r <= 32) linear_fwd_row_kernel<32><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y, ce);
+    else linear_fwd_row_kernel<64><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y, ce);
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
@@ -430,13 +451,11 @@ void launch_embedding_fwd(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* 
 // (stage TARGET, sample n). One warp per sample: lanes own classes, max and sum by a fixed
 // shuffle tree (the fp64 sum is associated differently from the reference's loop; the float
 // outputs agree to rounding).
-__global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict__ logits, int logits_relu,
-                                                         const float* __restrict__ targets, int64_t b,
-                                                         int64_t k, float* __restrict__ loss,
-                                                         float* __restrict__ grad, DeviceErr* err) {
+// one warp: loss and logit gradient of sample n from its k logits in `row`
+__device__ __forceinline__ void softmax_ce_warp(const float* row, int logits_relu, const float* __restrict__ targets,
+                                                int64_t n, int64_t k, float* __restrict__ loss,
+                                                float* __restrict__ grad, DeviceErr* err) {
   const int lane = threadIdx.x & 31;
-  const int64_t n = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (n >= b) return;
   const double tv = (double)targets[n];
   int64_t cls = 0;
   if (!(tv >= 0.0) || tv != floor(tv) || tv >= (double)k) {
@@ -445,7 +464,6 @@ __global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict
   } else {
     cls = (int64_t)tv;
   }
-  const float* row = logits + n * k;
   double mx = -INFINITY;
   for (int64_t j = lane; j < k; j += 32) {
     const double v = (double)relu_if(row[j], logits_relu);
@@ -469,6 +487,15 @@ __global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict
     if (logits_relu && !(row[j] > 0.f)) gv = 0.f;  // relu layer after the last linear
     grad[n * k + j] = gv;
   }
+}
+
+__global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict__ logits, int logits_relu,
+                                                         const float* __restrict__ targets, int64_t b,
+                                                         int64_t k, float* __restrict__ loss,
+                                                         float* __restrict__ grad, DeviceErr* err) {
+  const int64_t n = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (n >= b) return;
+  softmax_ce_warp(logits + n * k, logits_relu, targets, n, k, loss, grad, err);
 }
 
 void launch_softmax_ce(dpg_ctx* ctx, const float* logits, int logits_relu, const float* targets,

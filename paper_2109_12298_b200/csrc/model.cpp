@@ -236,6 +236,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
   float* P = m->p_params;
   auto act = [&](int buf) -> const float* { return buf < 0 ? x : m->bufs[buf]; };
   // ---- forward (layers.hpp:576-592) ----
+  bool loss_done = false;  // softmax-CE fused into the logits-producing linear forward
   for (size_t l = 0; l < m->layers.size(); ++l) {
     LayerPlan& lp = m->layers[l];
     if (lp.param0 < 0) continue;
@@ -249,8 +250,12 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
         dpg::ProfScope ps(ctx, "fwd.linear[" + std::to_string(l) + "]",
                           io + 4.0 * m->params[lp.param0].numel,
                           2.0 * b * lp.mid * lp.d.in_features * lp.d.out_features);
+        const bool last = lp.out_buf == m->out_buf && lp.mid == 1 &&
+                          dpg::linear_fwd_fuses_loss(lp.d.in_features, lp.d.out_features, in, w);
+        const dpg::LossFuse ce{targets, loss, m->highways[m->out_buf], m->out_relu ? 1 : 0, nullptr};
         dpg::launch_linear_fwd(ctx, in, lp.in_relu, w, bias, b * lp.mid, lp.d.in_features,
-                               lp.d.out_features, out);
+                               lp.d.out_features, out, last ? &ce : nullptr);
+        loss_done = loss_done || last;
         break;
       }
       case DPG_LAYER_CONV2D: {
@@ -274,7 +279,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
   // ---- loss (layers.hpp:894-919) ----
   const float* logits = act(m->out_buf);
   float* g_last = m->highways[m->out_buf];  // highway of the last parametric layer
-  {
+  if (!loss_done) {
     dpg::ProfScope ps(ctx, "loss.softmax_ce", 4.0 * b * (2 * m->out_width + 2), 0.0);
     dpg::launch_softmax_ce(ctx, logits, m->out_relu, targets, b, m->out_width, loss, g_last);
   }
