@@ -43,7 +43,7 @@ extern "C" {
 #endif
 
 #define DPG_API __attribute__((visibility("default")))
-#define DPG_ABI_VERSION 1
+#define DPG_ABI_VERSION 2
 
 /* errors.hpp:12-72 */
 typedef enum dpg_status {
@@ -63,8 +63,8 @@ typedef enum dpg_layer_kind {
   DPG_LAYER_LINEAR = 0,
   DPG_LAYER_EMBEDDING = 1,
   DPG_LAYER_CONV2D = 2,
-  DPG_LAYER_LAYER_NORM = 3, /* no device rule (SURVEY.md §8f "next") -> DPG_ERR_REGISTRY */
-  DPG_LAYER_GROUP_NORM = 4, /* no device rule -> DPG_ERR_REGISTRY */
+  DPG_LAYER_LAYER_NORM = 3, /* over the trailing norm_size features (1-D normalized shape) */
+  DPG_LAYER_GROUP_NORM = 4, /* groups over norm_size channels of [batch, C, ...] */
   DPG_LAYER_RELU = 5,
   DPG_LAYER_FLATTEN = 6,
 } dpg_layer_kind;
@@ -76,6 +76,8 @@ typedef struct dpg_layer_desc {
   int64_t in_features, out_features; /* linear */
   int64_t vocab_size, embedding_dim; /* embedding */
   int64_t in_channels, out_channels, kernel_h, kernel_w, stride, padding; /* conv2d */
+  int64_t norm_size, groups; /* layer_norm: normalized numel; group_norm: channels, groups */
+  double eps;                /* layer_norm / group_norm (layers.hpp:128-150, default 1e-5) */
 } dpg_layer_desc;
 
 /* Conv2dSpec (layers.hpp:58-65); groups = dilation = 1 as in the reference. */
@@ -152,6 +154,20 @@ DPG_API dpg_status dpg_grad_sample_conv2d(dpg_ctx* ctx, const float* x, const fl
 DPG_API dpg_status dpg_grad_sample_embedding(dpg_ctx* ctx, const float* idx, const float* highway,
                                              int64_t b, int64_t t, int64_t vocab, int64_t dim,
                                              float* g, double* sq);
+
+/* per_sample_rule_layer_norm (grad_sample.hpp:87-108), registry "layer_norm" (:216-220):
+ *   ggamma[n,j] = sum_p highway[n,p,j] * normalized[n,p,j],  gbeta[n,j] = sum_p highway[n,p,j]
+ * normalized / highway [b, positions, m] (normalized = the forward cache's xhat); fp32 sums in
+ * ascending p as the reference (bit-identical). Either output may be NULL. */
+DPG_API dpg_status dpg_grad_sample_layer_norm(dpg_ctx* ctx, const float* normalized, const float* highway,
+                                              int64_t b, int64_t positions, int64_t m, float* ggamma,
+                                              float* gbeta, double* sq_gamma, double* sq_beta);
+/* per_sample_rule_group_norm (grad_sample.hpp:110-131), registry "group_norm" (:221-225):
+ *   ggamma[n,c] = sum_s highway[n,c,s] * normalized[n,c,s],  gbeta[n,c] = sum_s highway[n,c,s]
+ * normalized / highway [b, channels, spatial]. */
+DPG_API dpg_status dpg_grad_sample_group_norm(dpg_ctx* ctx, const float* normalized, const float* highway,
+                                              int64_t b, int64_t channels, int64_t spatial, float* ggamma,
+                                              float* gbeta, double* sq_gamma, double* sq_beta);
 
 /* clip_and_sum factors (optimizer.hpp:67-98): N_n = sqrt(sum_p sq[p, n]) summed in parameter
  * order; scale_n = (float)(C / max(N_n, C)); num_clipped = #{N_n > C}. A non-finite sq[p, n]

@@ -146,6 +146,19 @@ class _Impl:
             _I64(stride), _I64(pad), _ptr(gw), _ptr(gb)))
         return gw, gb
 
+    def rule_norm(self, normalized: np.ndarray, hw: np.ndarray, group: bool):
+        """per_sample_rule_layer_norm ([b, q, c], group=False) / _group_norm ([b, c, q]); reference only."""
+        assert self.prefix == "dpgref"
+        b = normalized.shape[0]
+        c = normalized.shape[1] if group else normalized.shape[-1]
+        q = normalized.size // (b * c)
+        gg = np.empty((b, c), dtype=normalized.dtype)
+        gb = np.empty((b, c), dtype=normalized.dtype)
+        self.check(self.fn("rule_norm", normalized.dtype)(
+            ctypes.c_int(int(group)), _ptr(np.ascontiguousarray(normalized)), _ptr(np.ascontiguousarray(hw)),
+            _I64(b), _I64(c), _I64(q), _ptr(gg), _ptr(gb)))
+        return gg, gb
+
     def rule_embedding(self, idx: np.ndarray, hw: np.ndarray, vocab: int):
         b, t = idx.shape
         dim = hw.shape[-1]

@@ -52,6 +52,7 @@ typedef struct dpgo_layer {
   int64_t in_features, out_features;  /* linear */
   int64_t vocab_size, embedding_dim;  /* embedding */
   int64_t in_channels, out_channels, kernel_h, kernel_w, stride, padding; /* conv2d */
+  int64_t norm_size, groups; double eps; /* layer_norm / group_norm (not in the restatement) */
 } dpgo_layer;
 
 /* ---- RngStream::standard (rng.cpp:15-66): std::mt19937_64 + Box-Muller with a spare ---- */

@@ -33,6 +33,8 @@ struct CLayer {  // identical layout to dpgo_layer / dpg_layer_desc
   int64_t in_features, out_features;
   int64_t vocab_size, embedding_dim;
   int64_t in_channels, out_channels, kernel_h, kernel_w, stride, padding;
+  int64_t norm_size, groups;
+  double eps;
 };
 
 int code_of(const std::exception& e) {
@@ -66,6 +68,8 @@ std::vector<LayerDescriptor> descs_of(const CLayer* layers, int n) {
         out.push_back(LayerDescriptor::conv2d(c.in_channels, c.out_channels, c.kernel_h, c.kernel_w,
                                               c.stride, c.padding, c.has_bias));
         break;
+      case 3: out.push_back(LayerDescriptor::layer_norm(Shape{(std::size_t)c.norm_size}, c.eps)); break;
+      case 4: out.push_back(LayerDescriptor::group_norm(c.groups, c.norm_size, c.eps)); break;
       case 5: out.push_back(LayerDescriptor::relu()); break;
       case 6: out.push_back(LayerDescriptor::flatten()); break;
       default: throw ParameterError("ref_shim: unsupported layer kind");
@@ -325,6 +329,23 @@ int dpgref_rng_below(uint64_t seed, int64_t n, uint64_t bound, uint64_t* out) {
       auto [gwt, gbt] = per_sample_rule_conv2d(d, cache, hwt);                                     \
       std::memcpy(gw, gwt.data(), sizeof(T) * gwt.numel());                                        \
       if (gb) std::memcpy(gb, gbt.data(), sizeof(T) * gbt.numel());                                \
+    });                                                                                            \
+  }                                                                                                \
+  /* per_sample_rule_layer_norm / _group_norm on [b, q, c] / [b, c, q] with a given cache */    \
+  int dpgref_rule_norm##SFX(int group, const T* normalized, const T* hw, int64_t b, int64_t c,     \
+                            int64_t q, T* gg, T* gb) {                                             \
+    return guarded([&] {                                                                           \
+      LayerDescriptor d = group ? LayerDescriptor::group_norm(1, c)                                \
+                                : LayerDescriptor::layer_norm(Shape{(std::size_t)c});              \
+      const Shape shp = group ? Shape{(size_t)b, (size_t)c, (size_t)q} : Shape{(size_t)b, (size_t)q, (size_t)c}; \
+      LayerCache<T> cache;                                                                         \
+      cache.valid = true;                                                                          \
+      cache.input = Tensor<T>(shp);                                                                \
+      cache.normalized = tensor_of<T>(shp, normalized);                                            \
+      Tensor<T> h = tensor_of<T>(shp, hw);                                                         \
+      auto [g1, g2] = group ? per_sample_rule_group_norm(d, cache, h) : per_sample_rule_layer_norm(d, cache, h); \
+      std::memcpy(gg, g1.data(), sizeof(T) * g1.numel());                                          \
+      std::memcpy(gb, g2.data(), sizeof(T) * g2.numel());                                          \
     });                                                                                            \
   }                                                                                                \
   int dpgref_rule_embedding##SFX(const T* idx, const T* hw, int64_t b, int64_t t, int64_t vocab,   \

@@ -33,6 +33,9 @@ class CLayerDesc(ctypes.Structure):
         ("kernel_w", ctypes.c_int64),
         ("stride", ctypes.c_int64),
         ("padding", ctypes.c_int64),
+        ("norm_size", ctypes.c_int64),
+        ("groups", ctypes.c_int64),
+        ("eps", ctypes.c_double),
     ]
 
 
@@ -50,6 +53,9 @@ class LayerDesc:
     kernel_w: int = 0
     stride: int = 1
     padding: int = 0
+    norm_size: int = 0   # layer_norm: normalized numel (1-D shape); group_norm: channels
+    groups: int = 0
+    eps: float = 1e-5
 
     # factories: LayerDescriptor::linear / embedding / conv2d / relu / flatten (layers.hpp:96-163)
     @staticmethod
@@ -73,6 +79,24 @@ class LayerDesc:
                          stride=stride, padding=padding)
 
     @staticmethod
+    def layer_norm(m: int, eps: float = 1e-5) -> "LayerDesc":
+        # LayerDescriptor::layer_norm(Shape{m}, eps) (layers.hpp:128-138), 1-D normalized shape
+        if m <= 0:
+            raise ValueError("layer_norm: normalized shape must be non-empty")
+        if eps <= 0:
+            raise ValueError("layer_norm: eps must be positive")
+        return LayerDesc(LAYER_NORM, False, norm_size=m, eps=eps)
+
+    @staticmethod
+    def group_norm(groups: int, channels: int, eps: float = 1e-5) -> "LayerDesc":
+        # LayerDescriptor::group_norm (layers.hpp:140-150)
+        if groups <= 0 or channels <= 0 or channels % groups:
+            raise ValueError("group_norm: groups must be positive and divide channels")
+        if eps <= 0:
+            raise ValueError("group_norm: eps must be positive")
+        return LayerDesc(GROUP_NORM, False, norm_size=channels, groups=groups, eps=eps)
+
+    @staticmethod
     def relu() -> "LayerDesc":
         return LayerDesc(RELU, False)
 
@@ -93,12 +117,15 @@ class LayerDesc:
             if self.has_bias:
                 s.append(("bias", (self.out_channels,)))
             return s
+        if self.kind in (LAYER_NORM, GROUP_NORM):  # build_model: gamma = 1, beta = 0
+            return [("gamma", (self.norm_size,)), ("beta", (self.norm_size,))]
         return []
 
     def to_c(self) -> CLayerDesc:
         return CLayerDesc(self.kind, int(self.has_bias), self.in_features, self.out_features,
                           self.vocab_size, self.embedding_dim, self.in_channels, self.out_channels,
-                          self.kernel_h, self.kernel_w, self.stride, self.padding)
+                          self.kernel_h, self.kernel_w, self.stride, self.padding, self.norm_size,
+                          self.groups, self.eps)
 
 
 def c_layers(layers: Sequence[LayerDesc]):

@@ -313,4 +313,21 @@ void launch_softmax_ce(dpg_ctx* ctx, const float* logits, int logits_relu, const
                        int64_t b, int64_t k, float* loss, float* grad);
 void launch_relu_mask(dpg_ctx* ctx, float* g, const float* mask_src, int64_t n);
 
+// norm.cu — layer_norm over [b, positions, m] (trailing m), group_norm over [b, C, spatial]
+void launch_layer_norm_fwd(dpg_ctx* ctx, const float* x, int relu, const float* gamma, const float* beta,
+                           int64_t b, int64_t positions, int64_t m, double eps, float* y, float* xhat,
+                           float* inv_std);
+void launch_layer_norm_dgrad(dpg_ctx* ctx, const float* gy, const float* gamma, const float* xhat,
+                             const float* inv_std, int64_t b, int64_t positions, int64_t m,
+                             const float* mask, float* gx);
+void launch_group_norm_fwd(dpg_ctx* ctx, const float* x, int relu, const float* gamma, const float* beta,
+                           int64_t b, int64_t channels, int64_t spatial, int64_t groups, double eps,
+                           float* y, float* xhat, float* inv_std);
+void launch_group_norm_dgrad(dpg_ctx* ctx, const float* gy, const float* gamma, const float* xhat,
+                             const float* inv_std, int64_t b, int64_t channels, int64_t spatial,
+                             int64_t groups, const float* mask, float* gx);
+// per-sample gamma / beta records (either may be NULL) and their squared norms [b]
+void launch_norm_rule(dpg_ctx* ctx, const float* hw, const float* xhat, int64_t b, int64_t channels,
+                      int64_t positions, bool group_layout, float* gg, float* gb, double* sq_g, double* sq_b);
+
 }  // namespace dpg

@@ -48,6 +48,11 @@ struct LayerPlan {
   int64_t mid = 1;         // linear: rows per sample
   int64_t tokens = 0;      // embedding
   int prev_param_layer = -1;  // previous parametric layer (whose output feeds this one)
+  // layer_norm / group_norm: channels C, positions per (sample, channel) Q, statistics blocks
+  // per sample; forward cache (layers.hpp:249-262): normalized input and inv_std
+  int64_t norm_c = 0, norm_q = 0, stat_blocks = 0;
+  float* xhat = nullptr;
+  float* inv_std = nullptr;
 };
 
 int64_t conv_out_extent(int64_t in, int64_t kernel, int64_t stride, int64_t pad) {
@@ -266,6 +271,19 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
         dpg::launch_conv2d_fwd(ctx, in, lp.in_relu, w, bias, g, out, m->ws);
         break;
       }
+      case DPG_LAYER_LAYER_NORM:
+      case DPG_LAYER_GROUP_NORM: {
+        const bool gn = lp.kind == DPG_LAYER_GROUP_NORM;
+        dpg::ProfScope ps(ctx, std::string(gn ? "fwd.group_norm[" : "fwd.layer_norm[") + std::to_string(l) + "]",
+                          4.0 * b * (3 * lp.in_numel + lp.stat_blocks), 0.0);
+        if (gn)
+          dpg::launch_group_norm_fwd(ctx, in, lp.in_relu, w, bias, b, lp.norm_c, lp.norm_q, lp.stat_blocks,
+                                     lp.d.eps, out, lp.xhat, lp.inv_std);
+        else
+          dpg::launch_layer_norm_fwd(ctx, in, lp.in_relu, w, bias, b, lp.norm_q, lp.norm_c, lp.d.eps, out,
+                                     lp.xhat, lp.inv_std);
+        break;
+      }
       case DPG_LAYER_EMBEDDING: {
         dpg::ProfScope ps(ctx, "fwd.embedding[" + std::to_string(l) + "]",
                           4.0 * b * lp.tokens * (1 + 2 * lp.d.embedding_dim), 0.0);
@@ -330,6 +348,16 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
         if (lp.nparams > 1) bias_rule(g.P(), g.oc, true);
         break;
       }
+      case DPG_LAYER_LAYER_NORM:
+      case DPG_LAYER_GROUP_NORM: {
+        const bool gn = lp.kind == DPG_LAYER_GROUP_NORM;
+        const ParamInfo& pb = m->params[lp.param0 + 1];
+        dpg::ProfScope ps(ctx, std::string(gn ? "gs.group_norm" : "gs.layer_norm") + ls,
+                          4.0 * b * (2 * lp.out_numel + 2 * lp.norm_c), 0.0);
+        dpg::launch_norm_rule(ctx, hw, lp.xhat, b, lp.norm_c, lp.norm_q, gn, gw, gs_ptr(o, lp.param0 + 1, b),
+                              sq_w, slab + (int64_t)pb.sq_row0 * b);
+        break;
+      }
       case DPG_LAYER_EMBEDDING: {
         dpg::ProfScope ps(ctx, "gs.embedding" + ls, 4.0 * b * lp.out_numel + gwrite, 0.0);
         dpg::launch_gs_embedding(ctx, m->sorted_v, m->sorted_s, hw, b, lp.tokens,
@@ -358,6 +386,18 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
           g.b = b;
           dpg::ProfScope ps(ctx, "dgrad.conv2d" + ls, dio, 2.0 * b * g.oc * g.K() * g.P());
           dpg::launch_conv2d_dgrad(ctx, hw, w, g, mask, dst, m->ws);
+          break;
+        }
+        case DPG_LAYER_LAYER_NORM:
+        case DPG_LAYER_GROUP_NORM: {
+          const bool gn = lp.kind == DPG_LAYER_GROUP_NORM;
+          dpg::ProfScope ps(ctx, std::string(gn ? "dgrad.group_norm" : "dgrad.layer_norm") + ls,
+                            4.0 * b * (4 * lp.in_numel + lp.stat_blocks), 0.0);
+          if (gn)
+            dpg::launch_group_norm_dgrad(ctx, hw, w, lp.xhat, lp.inv_std, b, lp.norm_c, lp.norm_q,
+                                         lp.stat_blocks, mask, dst);
+          else
+            dpg::launch_layer_norm_dgrad(ctx, hw, w, lp.xhat, lp.inv_std, b, lp.norm_q, lp.norm_c, mask, dst);
           break;
         }
         default:
@@ -585,6 +625,34 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
           if (d.has_bias) pshapes.push_back({"bias", d.out_channels});
           break;
         }
+        case DPG_LAYER_LAYER_NORM: {  // layers.hpp:468-506
+          const dpg_layer_desc& d = lp.d;
+          if (d.norm_size <= 0) raise(DPG_ERR_PARAMETER, "layer_norm: normalized shape must be non-empty");
+          if (!(d.eps > 0.0)) raise(DPG_ERR_PARAMETER, "layer_norm: eps must be positive");
+          if (shape.empty() || shape.back() != d.norm_size)
+            shape_err("trailing dims of " + shape_str(shape, 1) + " do not match normalized shape [" +
+                      std::to_string(d.norm_size) + "]");
+          lp.norm_c = d.norm_size;
+          lp.norm_q = numel / d.norm_size;
+          lp.stat_blocks = lp.norm_q;
+          pshapes.push_back({"gamma", d.norm_size});
+          pshapes.push_back({"beta", d.norm_size});
+          break;
+        }
+        case DPG_LAYER_GROUP_NORM: {  // layers.hpp:508-551
+          const dpg_layer_desc& d = lp.d;
+          if (d.groups <= 0 || d.norm_size <= 0 || d.norm_size % d.groups != 0)
+            raise(DPG_ERR_PARAMETER, "group_norm: groups must be positive and divide channels");
+          if (!(d.eps > 0.0)) raise(DPG_ERR_PARAMETER, "group_norm: eps must be positive");
+          if (shape.empty() || shape[0] != d.norm_size)
+            shape_err("expected [batch, " + std::to_string(d.norm_size) + ", ...], got " + shape_str(shape, 1));
+          lp.norm_c = d.norm_size;
+          lp.norm_q = numel / d.norm_size;
+          lp.stat_blocks = d.groups;
+          pshapes.push_back({"gamma", d.norm_size});
+          pshapes.push_back({"beta", d.norm_size});
+          break;
+        }
         case DPG_LAYER_RELU:
           cur_relu = true;
           break;
@@ -605,7 +673,9 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
           pi.numel = pshapes[k].second;
           pi.offset = offset;
           pi.name = pshapes[k].first;
-          pi.is_bias = pi.name == "bias";
+          // biases and the normalisation affine parameters: small per-sample records whose clipped
+          // sums are weighted sums of the records (launch_wsum_multi)
+          pi.is_bias = pi.name == "bias" || lp.kind == DPG_LAYER_LAYER_NORM || lp.kind == DPG_LAYER_GROUP_NORM;
           offset += pi.numel;
           m->params.push_back(pi);
         }
@@ -684,6 +754,8 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     for (size_t cs : csum_bytes) total += al(cs);
     total += 3 * (al(sizeof(float) * max_batch * m->in_numel) + al(sizeof(float) * max_batch));
     total += al(sizeof(float) * max_batch);
+    for (auto& lp : m->layers)
+      if (lp.stat_blocks) total += al(sizeof(float) * max_batch * lp.in_numel) + al(sizeof(float) * max_batch * lp.stat_blocks);
     DPG_CUDA(cudaMalloc(&m->arena, total));
     DPG_CUDA(cudaMemset(m->arena, 0, total));
     char* p = m->arena;
@@ -711,6 +783,11 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
       m->ys[q] = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
     }
     m->loss = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
+    for (auto& lp : m->layers)
+      if (lp.stat_blocks) {
+        lp.xhat = reinterpret_cast<float*>(take(sizeof(float) * max_batch * lp.in_numel));
+        lp.inv_std = reinterpret_cast<float*>(take(sizeof(float) * max_batch * lp.stat_blocks));
+      }
     std::vector<int32_t> rp;
     for (size_t q = 0; q < m->params.size(); ++q)
       for (int r = 0; r < m->params[q].sq_rows; ++r) rp.push_back((int32_t)q);

@@ -78,6 +78,34 @@ dpg_status dpg_grad_sample_conv2d(dpg_ctx* ctx, const float* x, const float* hig
   });
 }
 
+static dpg_status norm_rule(dpg_ctx* ctx, const float* normalized, const float* highway, int64_t b,
+                            int64_t channels, int64_t positions, bool group_layout, float* gg, float* gb,
+                            double* sq_g, double* sq_b, const char* who) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    need(normalized, "normalized");
+    need(highway, "highway");
+    if (b < 0 || channels <= 0 || positions <= 0)
+      raise(DPG_ERR_DIMENSION, std::string(who) + ": extents must be positive");
+    if (b == 0) return;
+    dpg::launch_norm_rule(ctx, highway, normalized, b, channels, positions, group_layout, gg, gb, sq_g, sq_b);
+  });
+}
+
+dpg_status dpg_grad_sample_layer_norm(dpg_ctx* ctx, const float* normalized, const float* highway, int64_t b,
+                                      int64_t positions, int64_t m, float* ggamma, float* gbeta,
+                                      double* sq_gamma, double* sq_beta) {
+  return norm_rule(ctx, normalized, highway, b, m, positions, false, ggamma, gbeta, sq_gamma, sq_beta,
+                   "layer_norm");
+}
+
+dpg_status dpg_grad_sample_group_norm(dpg_ctx* ctx, const float* normalized, const float* highway, int64_t b,
+                                      int64_t channels, int64_t spatial, float* ggamma, float* gbeta,
+                                      double* sq_gamma, double* sq_beta) {
+  return norm_rule(ctx, normalized, highway, b, channels, spatial, true, ggamma, gbeta, sq_gamma, sq_beta,
+                   "group_norm");
+}
+
 dpg_status dpg_grad_sample_embedding(dpg_ctx* ctx, const float* idx, const float* highway,
                                      int64_t b, int64_t t, int64_t vocab, int64_t dim, float* g,
                                      double* sq) {

@@ -133,6 +133,8 @@ _SIGS = {
     "dpg_train_step_host": (_I32, [_P, _P, _P, _I64, _P]),
     "dpg_train_step_host_async": (_I32, [_P, _P, _P, _I64, _P]),
     "dpg_train_step": (_I32, [_P, _P, _P, _I64, _P, _I32]),
+    "dpg_grad_sample_layer_norm": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P]),
+    "dpg_grad_sample_group_norm": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P]),
 }
 
 _lib = None
@@ -281,6 +283,33 @@ def per_sample_rule_embedding(ctx: Context, idx: torch.Tensor, highway: torch.Te
     _check(lib().dpg_grad_sample_embedding(ctx.h, _p(idx), _p(highway), b, t, vocab, dim, _p(g),
                                            _p(sq)), ctx.h)
     return g, sq
+
+
+def per_sample_rule_layer_norm(ctx: Context, normalized: torch.Tensor, highway: torch.Tensor):
+    """grad_sample.hpp:87-108. normalized / highway [b, ..., m] -> (ggamma [b, m], gbeta [b, m],
+    sq_gamma [b], sq_beta [b])."""
+    b, m = normalized.shape[0], normalized.shape[-1]
+    positions = normalized.numel() // max(1, b * m)
+    dev = normalized.device
+    gg, gb = _f32((b, m), dev), _f32((b, m), dev)
+    sg = torch.empty(b, dtype=torch.float64, device=dev)
+    sb = torch.empty(b, dtype=torch.float64, device=dev)
+    _check(lib().dpg_grad_sample_layer_norm(ctx.h, _p(normalized), _p(highway), b, positions, m, _p(gg),
+                                            _p(gb), _p(sg), _p(sb)), ctx.h)
+    return gg, gb, sg, sb
+
+
+def per_sample_rule_group_norm(ctx: Context, normalized: torch.Tensor, highway: torch.Tensor):
+    """grad_sample.hpp:110-131. normalized / highway [b, C, ...] -> (ggamma [b, C], gbeta [b, C], ...)."""
+    b, c = normalized.shape[0], normalized.shape[1]
+    spatial = normalized.numel() // max(1, b * c)
+    dev = normalized.device
+    gg, gb = _f32((b, c), dev), _f32((b, c), dev)
+    sg = torch.empty(b, dtype=torch.float64, device=dev)
+    sb = torch.empty(b, dtype=torch.float64, device=dev)
+    _check(lib().dpg_grad_sample_group_norm(ctx.h, _p(normalized), _p(highway), b, c, spatial, _p(gg),
+                                            _p(gb), _p(sg), _p(sb)), ctx.h)
+    return gg, gb, sg, sb
 
 
 def clip_factors(ctx: Context, sq: torch.Tensor, c: float):

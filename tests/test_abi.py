@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 def test_python_binding_covers_abi_and_loads():
     from paper_2109_12298_b200 import dpg
     assert set(dpg.exported_symbols()) == set(declared())
-    assert dpg.lib().dpg_abi_version() == 1
+    assert dpg.lib().dpg_abi_version() == 2
 
 
 def test_ctx_create_without_gpu_fails_cleanly():
@@ -55,5 +55,5 @@ def test_ctx_create_without_gpu_fails_cleanly():
 def test_layer_desc_layout_matches_header():
     import ctypes
     from paper_2109_12298_b200.configs import CLayerDesc
-    assert ctypes.sizeof(CLayerDesc) == 8 + 10 * 8
+    assert ctypes.sizeof(CLayerDesc) == 8 + 12 * 8 + 8  # + norm_size, groups, eps
     assert CLayerDesc.in_features.offset == 8 and CLayerDesc.padding.offset == 80
