@@ -2,7 +2,7 @@
 //
 // Built by oracle/Makefile against the reference sources (where /root/reference exists) and
 // libdpg.so, into oracle/_ref/adapter_parity; run on the GPU box by tests/test_gpu_adapter.py.
-// For the MNIST, CIFAR and embedding models it runs compute_grad_samples (grad_sample.hpp:328-343)
+// For the MNIST, CIFAR, embedding and a layer_norm / group_norm model it runs compute_grad_samples (grad_sample.hpp:328-343)
 // twice on the same inputs — default registry vs make_gpu_registry — then one full
 // make_private / DpOptimizer step each, and prints one JSON line with the max-scaled differences.
 #include <cmath>
@@ -36,8 +36,12 @@ static ModelGraph<float> model_for(int which) {
          LayerDescriptor::relu(),                     LayerDescriptor::conv2d(64, 64, 3, 3, 2, 1), LayerDescriptor::relu(),
          LayerDescriptor::conv2d(64, 128, 3, 3, 2, 1), LayerDescriptor::relu(),                     LayerDescriptor::flatten(),
          LayerDescriptor::linear(512, 10)};
-  } else {
+  } else if (which == 2) {
     d = {LayerDescriptor::embedding(10000, 128), LayerDescriptor::flatten(), LayerDescriptor::linear(128 * 16, 2)};
+  } else {
+    d = {LayerDescriptor::conv2d(3, 8, 3, 3, 1, 1), LayerDescriptor::group_norm(2, 8), LayerDescriptor::relu(),
+         LayerDescriptor::flatten(), LayerDescriptor::linear(8 * 6 * 6, 32), LayerDescriptor::layer_norm(Shape{32}),
+         LayerDescriptor::relu(), LayerDescriptor::linear(32, 10)};
   }
   return build_model<float>(d, rng);
 }
@@ -49,16 +53,17 @@ int main() {
     return 1;
   }
   const auto gpu_reg = dpgrad_gpu::make_gpu_registry(ctx);
-  const char* names[] = {"mnist", "cifar", "embedding"};
+  const char* names[] = {"mnist", "cifar", "embedding", "norms"};
   std::printf("{");
   double worst = 0;
-  for (int which = 0; which < 3; ++which) {
+  for (int which = 0; which < 4; ++which) {
     ModelGraph<float> m = model_for(which);
     const std::size_t b = 8;
     RngStream data = RngStream::standard(2);
     Tensor<float> x;
     if (which == 0) x = gaussian<float>({b, 1, 28, 28}, 1.0, data);
     else if (which == 1) x = gaussian<float>({b, 3, 32, 32}, 1.0, data);
+    else if (which == 3) x = gaussian<float>({b, 3, 6, 6}, 1.0, data);
     else {
       x = Tensor<float>({b, 16});
       for (std::size_t i = 0; i < x.numel(); ++i) x[i] = (float)data.below(10000);

@@ -3,7 +3,8 @@
 // The reference drives per-sample gradients through GradSamplerRegistry (grad_sample.hpp:156-238):
 // a rule key -> std::function<vector<Tensor<T>>(const Layer<T>&, const LayerCache<T>&,
 // const Tensor<T>& highway)>, looked up by the backward walk (grad_sample.hpp:291-292). This
-// header builds a registry whose "linear", "conv2d" and "embedding" rules run on the B200 through
+// header builds a registry whose "linear", "conv2d", "embedding", "layer_norm" and "group_norm"
+// rules run on the B200 through
 // the C ABI (include/dpg.h), registered with override_existing = true (grad_sample.hpp:159-167),
 // so compute_grad_samples / GradSampleModule / make_private work unchanged:
 //
@@ -131,6 +132,33 @@ inline dpgrad::GradSamplerRegistry<float> make_gpu_registry(dpg_ctx* ctx) {
         return out;
       },
       true);
+  // registry "layer_norm" / "group_norm" (grad_sample.hpp:216-225): the rules read the forward
+  // cache's normalized input (layers.hpp:249-262)
+  auto norm_rule = [ctx](bool group) {
+    return [ctx, group](const Layer<float>& layer, const LayerCache<float>& cache, const Tensor<float>& hw) {
+      const std::size_t b = cache.input.extent(0);
+      const std::size_t c = group ? layer.desc.channels : shape_numel(layer.desc.normalized_shape);
+      const std::size_t q = cache.input.numel() / (b * c);
+      DevBuf xh(cache.normalized.data(), cache.normalized.numel()), hd(hw.data(), hw.numel());
+      DevBuf gg(b * c), gb(b * c);
+      check(group ? dpg_grad_sample_group_norm(ctx, xh.p, hd.p, (int64_t)b, (int64_t)c, (int64_t)q, gg.p, gb.p,
+                                               nullptr, nullptr)
+                  : dpg_grad_sample_layer_norm(ctx, xh.p, hd.p, (int64_t)b, (int64_t)q, (int64_t)c, gg.p, gb.p,
+                                               nullptr, nullptr),
+            ctx);
+      check(dpg_ctx_sync(ctx), ctx);
+      Shape gshape = group ? Shape{layer.desc.channels} : layer.desc.normalized_shape;
+      gshape.insert(gshape.begin(), b);
+      std::vector<Tensor<float>> out;
+      out.emplace_back(gshape);
+      gg.to_host(out.back().data());
+      out.emplace_back(gshape);
+      gb.to_host(out.back().data());
+      return out;
+    };
+  };
+  reg.register_rule("layer_norm", norm_rule(false), true);
+  reg.register_rule("group_norm", norm_rule(true), true);
   return reg;
 }
 

@@ -21,6 +21,6 @@ def test_reference_engine_with_gpu_rules():
     line = out.stdout.strip().splitlines()[-1]
     res = json.loads(line)
     assert out.returncode == 0, res
-    for model in ("mnist", "cifar", "embedding"):
+    for model in ("mnist", "cifar", "embedding", "norms"):
         assert res[model]["record_maxscaled"] <= 1e-5, res
         assert res[model]["params_maxscaled"] <= 1e-5, res
