@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(256) clip_factors_kernel(const double* __restr
                                                            float* __restrict__ scale,
                                                            unsigned long long* num_clipped,
                                                            DeviceErr* err) {
+  pdl_wait();
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int clipped = 0;
   if (n < b) {
@@ -60,7 +61,7 @@ void launch_clip_factors(dpg_ctx* ctx, const double* slab, const int32_t* row_pa
                          int64_t b, double c, double* norms, float* scale, int64_t* num_clipped) {
   if (num_clipped) DPG_CUDA(cudaMemsetAsync(num_clipped, 0, sizeof(int64_t), ctx->stream));
   if (b == 0) return;
-  clip_factors_kernel<<<(unsigned)((b + 127) / 128), 128, 0, ctx->stream>>>(
+  ::dpg::launch_pdl(clip_factors_kernel, (unsigned)((b + 127) / 128), 128, 0, ctx->stream, 
       slab, row_param, rows, b, c, norms, scale, reinterpret_cast<unsigned long long*>(num_clipped),
       ctx->dev_err);
   DPG_LAUNCH_CHECK(ctx);
@@ -123,12 +124,13 @@ struct ScaleC {
 
 __global__ void __launch_bounds__(32 * kColWarps) splitk_reduce_kernel(PartV v, int splits, int64_t n,
                                                                        float* out, int accumulate) {
+  pdl_wait();
   colsum_body(v, OneC{}, splits, n, (int64_t)blockIdx.x * 32, out, accumulate);
 }
 
 static void launch_splitk_reduce(dpg_ctx* ctx, const float* part, int splits, int64_t n, float* out,
                                  int accumulate) {
-  splitk_reduce_kernel<<<(unsigned)((n + 31) / 32), 32 * kColWarps, 0, ctx->stream>>>(
+  ::dpg::launch_pdl(splitk_reduce_kernel, (unsigned)((n + 31) / 32), 32 * kColWarps, 0, ctx->stream, 
       PartV{part, n}, splits, n, out, accumulate);
   DPG_LAUNCH_CHECK(ctx);
 }
@@ -181,12 +183,14 @@ struct RecordV {  // materialised per-sample values: v(n, j) = g[n, j]
 
 __global__ void __launch_bounds__(32 * kColWarps) wsum_outer_kernel(OuterV v, const float* scale, int64_t b,
                                                                     float* out, int accumulate) {
+  pdl_wait();
   colsum_body(v, ScaleC{scale}, b, v.d * v.r, (int64_t)blockIdx.x * 32, out, accumulate);
 }
 
 // all small per-sample records (the biases) of a model in one launch: blockIdx.y = item
 __global__ void __launch_bounds__(32 * kColWarps) wsum_multi_kernel(WsumItems items, const float* scale,
                                                                     int64_t b, int accumulate) {
+  pdl_wait();
   const WsumItem& it = items.item[blockIdx.y];
   const int64_t j0 = (int64_t)blockIdx.x * 32;
   if (j0 >= it.numel) return;
@@ -199,7 +203,7 @@ void launch_wsum_multi(dpg_ctx* ctx, const WsumItems& items, const float* scale,
   int64_t maxn = 0;
   for (int i = 0; i < items.count; ++i) maxn = items.item[i].numel > maxn ? items.item[i].numel : maxn;
   dim3 grid((unsigned)((maxn + 31) / 32), (unsigned)items.count);
-  wsum_multi_kernel<<<grid, 32 * kColWarps, 0, ctx->stream>>>(items, scale, b, accumulate);
+  ::dpg::launch_pdl(wsum_multi_kernel, grid, 32 * kColWarps, 0, ctx->stream, items, scale, b, accumulate);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -246,7 +250,7 @@ void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, c
   if (mid == 1) {
     if (d * r >= (int64_t(1) << 31)) raise(DPG_ERR_DIMENSION, "linear clipped sum: d * r too large");
     OuterV v{acts, hw, d, r, acts_relu};
-    wsum_outer_kernel<<<(unsigned)((r * d + 31) / 32), 32 * kColWarps, 0, ctx->stream>>>(v, scale, b, sw, accumulate);
+    ::dpg::launch_pdl(wsum_outer_kernel, (unsigned)((r * d + 31) / 32), 32 * kColWarps, 0, ctx->stream, v, scale, b, sw, accumulate);
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
@@ -386,6 +390,7 @@ constexpr int kCsRows = 32;
 
 __global__ void embed_chunk_starts_kernel(const int32_t* __restrict__ sorted_v, int64_t t,
                                           int nchunks, int32_t* __restrict__ starts) {
+  pdl_wait();
   const int64_t n = blockIdx.x;
   const int32_t* sv = sorted_v + n * t;
   for (int c = threadIdx.x; c <= nchunks; c += blockDim.x) {
@@ -404,6 +409,7 @@ __global__ void __launch_bounds__(256) clipped_sum_embedding_kernel(
     const int32_t* __restrict__ starts, const float* __restrict__ hw,
     const float* __restrict__ scale, int64_t b, int64_t t, int64_t vocab, int64_t dim,
     int nchunks, float* __restrict__ summed, int accumulate) {
+  pdl_wait();
   extern __shared__ float acc[];  // [kCsRows][dim]
   const int c = blockIdx.x;
   const int64_t v0 = (int64_t)c * kCsRows;
@@ -453,14 +459,14 @@ void launch_clipped_sum_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const i
   const int nchunks = (int)((vocab + kCsRows - 1) / kCsRows);
   int32_t* starts = static_cast<int32_t*>(ws);
   if (b > 0) {
-    embed_chunk_starts_kernel<<<(unsigned)b, 256, 0, ctx->stream>>>(sorted_v, t, nchunks, starts);
+    ::dpg::launch_pdl(embed_chunk_starts_kernel, (unsigned)b, 256, 0, ctx->stream, sorted_v, t, nchunks, starts);
     DPG_LAUNCH_CHECK(ctx);
   }
   const size_t smem = sizeof(float) * kCsRows * (size_t)dim;
   if (smem > 48 * 1024)
     DPG_CUDA(cudaFuncSetAttribute(clipped_sum_embedding_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  clipped_sum_embedding_kernel<<<(unsigned)nchunks, 256, smem, ctx->stream>>>(
+  ::dpg::launch_pdl(clipped_sum_embedding_kernel, (unsigned)nchunks, 256, smem, ctx->stream, 
       sorted_v, sorted_s, starts, hw, scale, b, t, vocab, dim, nchunks, summed, accumulate);
   DPG_LAUNCH_CHECK(ctx);
 }
@@ -473,6 +479,7 @@ constexpr int64_t kSqChunk = 16384;
 __global__ void __launch_bounds__(256) sq_materialised_kernel(const float* __restrict__ g,
                                                               int64_t b, int64_t numel,
                                                               double* __restrict__ sq_part) {
+  pdl_wait();
   const int64_t n = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * kSqChunk;
   const int64_t c1 = c0 + kSqChunk < numel ? c0 + kSqChunk : numel;
@@ -493,7 +500,7 @@ void launch_sq_materialised(dpg_ctx* ctx, const float* g, int64_t b, int64_t num
                             double* sq_part) {
   if (b == 0) return;
   dim3 grid((unsigned)sq_rows_materialised(numel), (unsigned)b);
-  sq_materialised_kernel<<<grid, 256, 0, ctx->stream>>>(g, b, numel, sq_part);
+  ::dpg::launch_pdl(sq_materialised_kernel, grid, 256, 0, ctx->stream, g, b, numel, sq_part);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -501,6 +508,7 @@ void launch_sq_materialised(dpg_ctx* ctx, const float* g, int64_t b, int64_t num
 __global__ void weighted_sum_kernel(const float* __restrict__ g, const float* __restrict__ scale,
                                     int64_t b, int64_t numel, float* __restrict__ summed,
                                     int accumulate) {
+  pdl_wait();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= numel) return;
   float acc = 0.f;
@@ -511,7 +519,7 @@ __global__ void weighted_sum_kernel(const float* __restrict__ g, const float* __
 void launch_weighted_sum_materialised(dpg_ctx* ctx, const float* g, const float* scale, int64_t b,
                                       int64_t numel, float* summed, int accumulate) {
   if (numel == 0) return;
-  weighted_sum_kernel<<<(unsigned)((numel + 255) / 256), 256, 0, ctx->stream>>>(g, scale, b, numel, summed, accumulate);
+  ::dpg::launch_pdl(weighted_sum_kernel, (unsigned)((numel + 255) / 256), 256, 0, ctx->stream, g, scale, b, numel, summed, accumulate);
   DPG_LAUNCH_CHECK(ctx);
 }
 

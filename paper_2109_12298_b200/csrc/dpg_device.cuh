@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 #include "dpg_internal.h"
 
@@ -79,6 +81,36 @@ __device__ __forceinline__ void st_stream4(float* p, float4 v) {
 }
 __device__ __forceinline__ void st_stream(float* p, float v) {
   asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// Programmatic dependent launch: every kernel is launched with programmatic stream
+// serialization (launch_pdl), so it may start — and run its prologue — while the previous kernel
+// on the stream drains; pdl_wait() (griddepcontrol.wait) blocks until that kernel has completed
+// and its memory is visible. Every kernel calls it before touching data another kernel wrote.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Launch with programmatic stream serialization (see pdl_wait); DPG_PDL=0 launches plainly.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DPG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  (void)cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);  // errors: DPG_LAUNCH_CHECK
 }
 
 }  // namespace dpg

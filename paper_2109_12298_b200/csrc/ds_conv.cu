@@ -38,6 +38,7 @@ struct Params {
 
 template <int MODE, bool EXACT>
 __global__ void __launch_bounds__(kThreads) ds_conv_kernel(const Params p) {
+  pdl_wait();
   const int blk = blockIdx.x * kThreads + threadIdx.x;
   const bool active = blk < p.nq * p.ng;
   const int jq = active ? blk % p.nq : 0, gq = active ? blk / p.nq : 0;
@@ -197,8 +198,8 @@ void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom&
   p.out = gw;
   p.sq_part = sq_part;
   dim3 grid((unsigned)gs_rows(g), (unsigned)g.b);
-  if (p.P <= 16) ds_conv_kernel<0, true><<<grid, kThreads, 0, ctx->stream>>>(p);
-  else ds_conv_kernel<0, false><<<grid, kThreads, 0, ctx->stream>>>(p);
+  if (p.P <= 16) ::dpg::launch_pdl(ds_conv_kernel<0, true>, grid, kThreads, 0, ctx->stream, p);
+  else ::dpg::launch_pdl(ds_conv_kernel<0, false>, grid, kThreads, 0, ctx->stream, p);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -217,7 +218,7 @@ void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* 
   p.out = part;
   p.spl = (g.b + splits - 1) / splits;
   dim3 grid((unsigned)((p.nq * p.ng + kThreads - 1) / kThreads), (unsigned)splits);
-  ds_conv_kernel<1, false><<<grid, kThreads, 0, ctx->stream>>>(p);
+  ::dpg::launch_pdl(ds_conv_kernel<1, false>, grid, kThreads, 0, ctx->stream, p);
   DPG_LAUNCH_CHECK(ctx);
 }
 

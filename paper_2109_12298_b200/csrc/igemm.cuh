@@ -19,6 +19,7 @@ namespace dpg {
 
 template <int BM, int BN, int BK, class Prob>
 __global__ void __launch_bounds__(256) igemm_kernel(const Prob p) {
+  pdl_wait();
   constexpr int TM = BM / 16, TN = BN / 16;
   constexpr int A_PER = (BM * BK + 255) / 256, B_PER = (BK * BN + 255) / 256;
   __shared__ float As[BK][BM + 1];
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256) igemm_kernel(const Prob p) {
 template <int BM, int BN, int BK, class Prob>
 void launch_igemm(dpg_ctx* ctx, const Prob& p, int64_t batches) {
   dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)batches);
-  igemm_kernel<BM, BN, BK, Prob><<<grid, 256, 0, ctx->stream>>>(p);
+  ::dpg::launch_pdl(igemm_kernel<BM, BN, BK, Prob>, grid, 256, 0, ctx->stream, p);
   DPG_LAUNCH_CHECK(ctx);
 }
 

@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(256) linear_fwd_narrow_kernel(const float* __r
                                                                 const float* __restrict__ bias,
                                                                 int64_t rows, int64_t d, int r,
                                                                 float* __restrict__ y) {
+  pdl_wait();
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) linear_fwd_row_kernel(const fl
                                                                        const float* __restrict__ bias,
                                                                        int64_t d, int r,
                                                                        float* __restrict__ y, LossFuse ce) {
+  pdl_wait();
   __shared__ float part[kRowWarps][RMAX];
   __shared__ float logit[RMAX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -271,6 +273,7 @@ __global__ void __launch_bounds__(kFwdThreads) linear_fwd_rows_kernel(const floa
                                                                      const float* __restrict__ bias,
                                                                      int64_t rows, int64_t d, int r,
                                                                      float* __restrict__ y) {
+  pdl_wait();
   __shared__ float red[kFwdThreads / 32][kFwdRows * RMAX];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t row0 = (int64_t)blockIdx.x * kFwdRows;
@@ -363,26 +366,26 @@ void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w,
   const bool aligned = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(w) & 15) == 0;
   if (aligned && r <= 64) {
-    if (r <= 16) linear_fwd_row_kernel<16><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y, ce);
-    else if (r <= 32) linear_fwd_row_kernel<32><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y, ce);
-    else linear_fwd_row_kernel<64><<<(unsigned)rows, 32 * kRowWarps, 0, ctx->stream>>>(x, x_relu, w, bias, d, (int)r, y, ce);
+    if (r <= 16) ::dpg::launch_pdl(linear_fwd_row_kernel<16>, (unsigned)rows, 32 * kRowWarps, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
+    else if (r <= 32) ::dpg::launch_pdl(linear_fwd_row_kernel<32>, (unsigned)rows, 32 * kRowWarps, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
+    else ::dpg::launch_pdl(linear_fwd_row_kernel<64>, (unsigned)rows, 32 * kRowWarps, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
   if (aligned && r <= 16) {
     const unsigned g4 = (unsigned)((rows + kFwdRows - 1) / kFwdRows);
-    if (r <= 4) linear_fwd_rows_kernel<4><<<g4, kFwdThreads, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
-    else linear_fwd_rows_kernel<16><<<g4, kFwdThreads, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
+    if (r <= 4) ::dpg::launch_pdl(linear_fwd_rows_kernel<4>, g4, kFwdThreads, 0, ctx->stream, x, x_relu, w, bias, rows, d, (int)r, y);
+    else ::dpg::launch_pdl(linear_fwd_rows_kernel<16>, g4, kFwdThreads, 0, ctx->stream, x, x_relu, w, bias, rows, d, (int)r, y);
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
   const unsigned grid = (unsigned)((rows + 7) / 8);
   if (r <= 4) {
-    linear_fwd_narrow_kernel<4><<<grid, 256, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
+    ::dpg::launch_pdl(linear_fwd_narrow_kernel<4>, grid, 256, 0, ctx->stream, x, x_relu, w, bias, rows, d, (int)r, y);
   } else if (r <= 16) {
-    linear_fwd_narrow_kernel<16><<<grid, 256, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
+    ::dpg::launch_pdl(linear_fwd_narrow_kernel<16>, grid, 256, 0, ctx->stream, x, x_relu, w, bias, rows, d, (int)r, y);
   } else if (r <= 32) {
-    linear_fwd_narrow_kernel<32><<<grid, 256, 0, ctx->stream>>>(x, x_relu, w, bias, rows, d, (int)r, y);
+    ::dpg::launch_pdl(linear_fwd_narrow_kernel<32>, grid, 256, 0, ctx->stream, x, x_relu, w, bias, rows, d, (int)r, y);
   } else {
     LinearFwdProb p{x, w, bias, y, x_relu, rows, r, d};
     launch_igemm<64, 64, 16>(ctx, p, 1);
@@ -398,6 +401,7 @@ __global__ void __launch_bounds__(256) linear_dgrad_kernel(const float* __restri
                                                            int64_t rows, int64_t d, int64_t r,
                                                            const float* __restrict__ mask,
                                                            float* __restrict__ dx) {
+  pdl_wait();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * d) return;
   // 32-bit division when the index fits (the common case; int64 division is a long sequence)
@@ -413,7 +417,7 @@ void launch_linear_dgrad(dpg_ctx* ctx, const float* dy, const float* w, int64_t 
                          int64_t r, const float* mask_src, float* dx) {
   const int64_t n = rows * d;
   if (n == 0) return;
-  linear_dgrad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(dy, w, rows, d, r, mask_src, dx);
+  ::dpg::launch_pdl(linear_dgrad_kernel, (unsigned)((n + 255) / 256), 256, 0, ctx->stream, dy, w, rows, d, r, mask_src, dx);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -423,6 +427,7 @@ __global__ void __launch_bounds__(256) embedding_fwd_kernel(const int32_t* __res
                                                             const float* __restrict__ table,
                                                             int64_t total, int64_t t, int64_t dim,
                                                             float* __restrict__ out) {
+  pdl_wait();
   const int64_t tok = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (tok >= total) return;
@@ -442,7 +447,7 @@ void launch_embedding_fwd(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* 
                           const float* table, int64_t b, int64_t t, int64_t dim, float* out) {
   const int64_t total = b * t;
   if (total == 0) return;
-  embedding_fwd_kernel<<<(unsigned)((total + 7) / 8), 256, 0, ctx->stream>>>(sorted_v, sorted_s, table, total, t, dim, out);
+  ::dpg::launch_pdl(embedding_fwd_kernel, (unsigned)((total + 7) / 8), 256, 0, ctx->stream, sorted_v, sorted_s, table, total, t, dim, out);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -493,6 +498,7 @@ __global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict
                                                          const float* __restrict__ targets, int64_t b,
                                                          int64_t k, float* __restrict__ loss,
                                                          float* __restrict__ grad, DeviceErr* err) {
+  pdl_wait();
   const int64_t n = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (n >= b) return;
   softmax_ce_warp(logits + n * k, logits_relu, targets, n, k, loss, grad, err);
@@ -501,18 +507,19 @@ __global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict
 void launch_softmax_ce(dpg_ctx* ctx, const float* logits, int logits_relu, const float* targets,
                        int64_t b, int64_t k, float* loss, float* grad) {
   if (b == 0) return;
-  softmax_ce_kernel<<<(unsigned)((b + 7) / 8), 256, 0, ctx->stream>>>(logits, logits_relu, targets, b, k, loss, grad, ctx->dev_err);
+  ::dpg::launch_pdl(softmax_ce_kernel, (unsigned)((b + 7) / 8), 256, 0, ctx->stream, logits, logits_relu, targets, b, k, loss, grad, ctx->dev_err);
   DPG_LAUNCH_CHECK(ctx);
 }
 
 __global__ void relu_mask_kernel(float* __restrict__ g, const float* __restrict__ m, int64_t n) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && !(m[i] > 0.f)) g[i] = 0.f;
 }
 
 void launch_relu_mask(dpg_ctx* ctx, float* g, const float* mask_src, int64_t n) {
   if (n == 0) return;
-  relu_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(g, mask_src, n);
+  ::dpg::launch_pdl(relu_mask_kernel, (unsigned)((n + 255) / 256), 256, 0, ctx->stream, g, mask_src, n);
   DPG_LAUNCH_CHECK(ctx);
 }
 

@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(256) noise_update_kernel(
     float* __restrict__ params, const float* __restrict__ summed, float* __restrict__ grad,
     int64_t n, double std_dev, float inv_e, float lr, uint64_t seed, uint64_t step,
     const float* __restrict__ injected, const uint64_t* step_ptr, const DeviceErr* err) {
+  pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i0 = 2 * q;
   if (i0 >= n) return;
@@ -85,13 +86,14 @@ void launch_noise_update(dpg_ctx* ctx, float* params, const float* summed, float
   const float denom = (float)expected_batch;
   const float inv_e = 1.0f / denom;  // T(1) / denom (optimizer.hpp:259, 264)
   const int64_t pairs = (n + 1) / 2;
-  noise_update_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, ctx->stream>>>(
+  ::dpg::launch_pdl(noise_update_kernel, (unsigned)((pairs + 255) / 256), 256, 0, ctx->stream, 
       params, summed, grad, n, std_dev, inv_e, (float)lr, seed, step, injected, step_ptr, ctx->dev_err);
   DPG_LAUNCH_CHECK(ctx);
 }
 
 __global__ void gaussian_kernel(float* __restrict__ out, int64_t n, double std_dev, uint64_t seed,
                                 uint64_t step) {
+  pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i0 = 2 * q;
   if (i0 >= n) return;
@@ -109,7 +111,7 @@ void launch_gaussian(dpg_ctx* ctx, float* out, int64_t n, double std_dev, uint64
     return;
   }
   const int64_t pairs = (n + 1) / 2;
-  gaussian_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, ctx->stream>>>(out, n, std_dev, seed, step);
+  ::dpg::launch_pdl(gaussian_kernel, (unsigned)((pairs + 255) / 256), 256, 0, ctx->stream, out, n, std_dev, seed, step);
   DPG_LAUNCH_CHECK(ctx);
 }
 

@@ -38,6 +38,7 @@ __global__ void norm_fwd_kernel(const float* __restrict__ x, int relu, const flo
                                 const float* __restrict__ beta, NormIdx ix, int64_t b, int64_t blocks_per_sample,
                                 int64_t cnt_c, int64_t cnt_q, int gn, double eps, float* __restrict__ y,
                                 float* __restrict__ xhat, float* __restrict__ inv_std) {
+  pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= b * blocks_per_sample) return;
   const int64_t n = t / blocks_per_sample, blk = t - n * blocks_per_sample;
@@ -73,6 +74,7 @@ __global__ void norm_dgrad_kernel(const float* __restrict__ gy, const float* __r
                                   const float* __restrict__ xhat, const float* __restrict__ inv_std, NormIdx ix,
                                   int64_t b, int64_t blocks_per_sample, int64_t cnt_c, int64_t cnt_q, int gn,
                                   const float* __restrict__ mask, float* __restrict__ gx) {
+  pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= b * blocks_per_sample) return;
   const int64_t n = t / blocks_per_sample, blk = t - n * blocks_per_sample;
@@ -107,6 +109,7 @@ __global__ void __launch_bounds__(256) norm_rule_kernel(const float* __restrict_
                                                         float* __restrict__ gg, float* __restrict__ gb,
                                                         double* __restrict__ sq_g, double* __restrict__ sq_b,
                                                         int64_t b) {
+  pdl_wait();
   const int64_t n = blockIdx.x;
   double sg = 0.0, sb = 0.0;
   for (int64_t c = threadIdx.x; c < channels; c += blockDim.x) {
@@ -139,7 +142,7 @@ void launch_layer_norm_fwd(dpg_ctx* ctx, const float* x, int relu, const float* 
                            int64_t b, int64_t positions, int64_t m, double eps, float* y, float* xhat,
                            float* inv_std) {
   if (b == 0) return;
-  norm_fwd_kernel<<<blocks_for(b * positions, 128), 128, 0, ctx->stream>>>(
+  ::dpg::launch_pdl(norm_fwd_kernel, blocks_for(b * positions, 128), 128, 0, ctx->stream, 
       x, relu, gamma, beta, ln_idx(positions, m), b, positions, m, 1, 0, eps, y, xhat, inv_std);
   DPG_LAUNCH_CHECK(ctx);
 }
@@ -148,7 +151,7 @@ void launch_layer_norm_dgrad(dpg_ctx* ctx, const float* gy, const float* gamma, 
                              const float* inv_std, int64_t b, int64_t positions, int64_t m,
                              const float* mask, float* gx) {
   if (b == 0) return;
-  norm_dgrad_kernel<<<blocks_for(b * positions, 128), 128, 0, ctx->stream>>>(
+  ::dpg::launch_pdl(norm_dgrad_kernel, blocks_for(b * positions, 128), 128, 0, ctx->stream, 
       gy, gamma, xhat, inv_std, ln_idx(positions, m), b, positions, m, 1, 0, mask, gx);
   DPG_LAUNCH_CHECK(ctx);
 }
@@ -157,7 +160,7 @@ void launch_group_norm_fwd(dpg_ctx* ctx, const float* x, int relu, const float* 
                            int64_t b, int64_t channels, int64_t spatial, int64_t groups, double eps,
                            float* y, float* xhat, float* inv_std) {
   if (b == 0) return;
-  norm_fwd_kernel<<<blocks_for(b * groups, 128), 128, 0, ctx->stream>>>(
+  ::dpg::launch_pdl(norm_fwd_kernel, blocks_for(b * groups, 128), 128, 0, ctx->stream, 
       x, relu, gamma, beta, gn_idx(channels, spatial), b, groups, channels / groups, spatial, 1, eps, y,
       xhat, inv_std);
   DPG_LAUNCH_CHECK(ctx);
@@ -167,7 +170,7 @@ void launch_group_norm_dgrad(dpg_ctx* ctx, const float* gy, const float* gamma, 
                              const float* inv_std, int64_t b, int64_t channels, int64_t spatial,
                              int64_t groups, const float* mask, float* gx) {
   if (b == 0) return;
-  norm_dgrad_kernel<<<blocks_for(b * groups, 128), 128, 0, ctx->stream>>>(
+  ::dpg::launch_pdl(norm_dgrad_kernel, blocks_for(b * groups, 128), 128, 0, ctx->stream, 
       gy, gamma, xhat, inv_std, gn_idx(channels, spatial), b, groups, channels / groups, spatial, 1, mask, gx);
   DPG_LAUNCH_CHECK(ctx);
 }
@@ -176,7 +179,7 @@ void launch_norm_rule(dpg_ctx* ctx, const float* hw, const float* xhat, int64_t 
                       int64_t positions, bool group_layout, float* gg, float* gb, double* sq_g, double* sq_b) {
   if (b == 0) return;
   const NormIdx ix = group_layout ? gn_idx(channels, positions) : ln_idx(positions, channels);
-  norm_rule_kernel<<<(unsigned)b, 256, 0, ctx->stream>>>(hw, xhat, ix, channels, positions, gg, gb, sq_g,
+  ::dpg::launch_pdl(norm_rule_kernel, (unsigned)b, 256, 0, ctx->stream, hw, xhat, ix, channels, positions, gg, gb, sq_g,
                                                          sq_b, b);
   DPG_LAUNCH_CHECK(ctx);
 }

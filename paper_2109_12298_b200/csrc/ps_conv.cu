@@ -64,6 +64,7 @@ __device__ __forceinline__ double block_sum_dyn(double v, double* red /* >= 32 *
 
 template <int MODE>
 __global__ void __launch_bounds__(kMaxThreads, 3) ps_conv_kernel(const Params p) {
+  pdl_wait();
   extern __shared__ __align__(16) float sm[];
   float* hs = sm;                                             // [P][oct]
   float* xt = hs + p.P * p.oct;                               // [pc][Kc4]
@@ -324,7 +325,7 @@ static void launch(dpg_ctx* ctx, const Params& p, unsigned gy) {
                                   160 * 1024));
     attr = 160 * 1024;
   }
-  ps_conv_kernel<MODE><<<grid, p.nth, smem, ctx->stream>>>(p);
+  ::dpg::launch_pdl(ps_conv_kernel<MODE>, grid, p.nth, smem, ctx->stream, p);
   DPG_LAUNCH_CHECK(ctx);
 }
 

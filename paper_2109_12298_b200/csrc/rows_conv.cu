@@ -37,6 +37,7 @@ struct Params {
 
 template <int PT>
 __global__ void __launch_bounds__(kThreads, 4) gs_rows_kernel(const Params p) {
+  pdl_wait();
   extern __shared__ __align__(16) float sm[];
   float* xt = sm;                                          // [PT][Kc4], rows >= P are zero
   const int ostr = (p.opart + 3) & ~3;                     // row stride of the transposed tile
@@ -214,7 +215,7 @@ void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom&
       DPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
       attr = 160 * 1024;
     }
-    kern<<<grid, kThreads, smem, ctx->stream>>>(p);
+    ::dpg::launch_pdl(kern, grid, kThreads, smem, ctx->stream, p);
   };
   switch (pick_pt(p.P)) {
     case 4: go(gs_rows_kernel<4>); break;

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(256) gs_linear_outer_kernel(const float* __res
                                                               float* __restrict__ gw,
                                                               double* __restrict__ sq_part,
                                                               int64_t b) {
+  pdl_wait();
   const int n = blockIdx.y;
   const int64_t total = r * d;
   const int64_t c0 = (int64_t)blockIdx.x * kOuterChunk;
@@ -105,7 +106,7 @@ void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const floa
   if (b == 0) return;
   if (mid == 1) {
     dim3 grid((unsigned)((r * d + kOuterChunk - 1) / kOuterChunk), (unsigned)b);
-    gs_linear_outer_kernel<<<grid, 256, 0, ctx->stream>>>(acts, acts_relu, hw, d, r, gw, sq_part, b);
+    ::dpg::launch_pdl(gs_linear_outer_kernel, grid, 256, 0, ctx->stream, acts, acts_relu, hw, d, r, gw, sq_part, b);
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(256) gs_bias_kernel(const float* __restrict__ 
                                                       int64_t r, int conv_layout,
                                                       float* __restrict__ gb,
                                                       double* __restrict__ sq_part, int64_t b) {
+  pdl_wait();
   const int64_t n = blockIdx.x;
   double sq = 0.0;
   if (conv_layout) {
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(256) gs_bias_kernel(const float* __restrict__ 
 void launch_gs_bias(dpg_ctx* ctx, const float* hw, int64_t b, int64_t mid, int64_t r,
                     bool hw_layout_conv, float* gb, double* sq_part) {
   if (b == 0) return;
-  gs_bias_kernel<<<(unsigned)b, 256, 0, ctx->stream>>>(hw, mid, r, hw_layout_conv ? 1 : 0, gb, sq_part, b);
+  ::dpg::launch_pdl(gs_bias_kernel, (unsigned)b, 256, 0, ctx->stream, hw, mid, r, hw_layout_conv ? 1 : 0, gb, sq_part, b);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -302,6 +304,7 @@ __global__ void __launch_bounds__(kSortThreads) embed_sort_kernel(const float* _
                                                                   int32_t* __restrict__ sorted_v,
                                                                   int32_t* __restrict__ sorted_s,
                                                                   DeviceErr* err) {
+  pdl_wait();
   __shared__ unsigned long long keys[kMaxTokens];
   const int64_t n = blockIdx.x;
   int p2 = 1;
@@ -350,7 +353,7 @@ void launch_embed_sort(dpg_ctx* ctx, const float* idx, int64_t b, int64_t t, int
                        int32_t* sorted_v, int32_t* sorted_s) {
   if (t > kMaxTokens) raise(DPG_ERR_DIMENSION, "embedding: at most 4096 tokens per sample on device");
   if (b == 0 || t == 0) return;
-  embed_sort_kernel<<<(unsigned)b, kSortThreads, 0, ctx->stream>>>(idx, t, vocab, sorted_v, sorted_s, ctx->dev_err);
+  ::dpg::launch_pdl(embed_sort_kernel, (unsigned)b, kSortThreads, 0, ctx->stream, idx, t, vocab, sorted_v, sorted_s, ctx->dev_err);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -371,6 +374,7 @@ __global__ void __launch_bounds__(256) gs_embedding_dense_kernel(
     const int32_t* __restrict__ sorted_v, const int32_t* __restrict__ sorted_s,
     const float* __restrict__ hw, int64_t t, int64_t vocab, int64_t dim, float* __restrict__ g,
     double* __restrict__ sq_part, int64_t b) {
+  pdl_wait();
   extern __shared__ int32_t sv[];
   const int64_t n = blockIdx.y;
   const int64_t v0 = (int64_t)blockIdx.x * kEmbRows;
@@ -413,6 +417,7 @@ __global__ void __launch_bounds__(256) gs_embedding_dense_kernel(
 __global__ void __launch_bounds__(256) gs_embedding_sq_kernel(
     const int32_t* __restrict__ sorted_v, const int32_t* __restrict__ sorted_s,
     const float* __restrict__ hw, int64_t t, int64_t dim, double* __restrict__ sq_part) {
+  pdl_wait();
   const int64_t n = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t* sv = sorted_v + n * t;
@@ -445,14 +450,14 @@ void launch_gs_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* s
   if (b == 0) return;
   if (g) {
     dim3 grid((unsigned)((vocab + kEmbRows - 1) / kEmbRows), (unsigned)b);
-    gs_embedding_dense_kernel<<<grid, 256, sizeof(int32_t) * t, ctx->stream>>>(
+    ::dpg::launch_pdl(gs_embedding_dense_kernel, grid, 256, sizeof(int32_t) * t, ctx->stream, 
         sorted_v, sorted_s, hw, t, vocab, dim, g, sq_part, b);
   } else {
     // sparse mode: the norm lands in the first row; the remaining rows are zero-filled so the
     // slab layout does not depend on the mode
     const int rows = sq_rows_embedding(vocab, dim);
     if (rows > 1) DPG_CUDA(cudaMemsetAsync(sq_part + b, 0, sizeof(double) * (size_t)(rows - 1) * b, ctx->stream));
-    gs_embedding_sq_kernel<<<(unsigned)b, 256, 0, ctx->stream>>>(sorted_v, sorted_s, hw, t, dim, sq_part);
+    ::dpg::launch_pdl(gs_embedding_sq_kernel, (unsigned)b, 256, 0, ctx->stream, sorted_v, sorted_s, hw, t, dim, sq_part);
   }
   DPG_LAUNCH_CHECK(ctx);
 }
@@ -460,6 +465,7 @@ void launch_gs_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* s
 // ------------------------------------------------------------------------------------------
 __global__ void sq_reduce_kernel(const double* __restrict__ part, int rows, int64_t b,
                                  double* __restrict__ out) {
+  pdl_wait();
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= b) return;
   double acc = 0.0;
@@ -469,7 +475,7 @@ __global__ void sq_reduce_kernel(const double* __restrict__ part, int rows, int6
 
 void launch_sq_reduce(dpg_ctx* ctx, const double* part, int rows, int64_t b, double* out) {
   if (b == 0) return;
-  sq_reduce_kernel<<<(unsigned)((b + 255) / 256), 256, 0, ctx->stream>>>(part, rows, b, out);
+  ::dpg::launch_pdl(sq_reduce_kernel, (unsigned)((b + 255) / 256), 256, 0, ctx->stream, part, rows, b, out);
   DPG_LAUNCH_CHECK(ctx);
 }
 

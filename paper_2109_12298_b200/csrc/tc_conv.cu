@@ -183,6 +183,7 @@ __device__ __forceinline__ float sum_splits(const float* __restrict__ part, int 
 // Y[n][oc][p] = bias[oc] + sum_s part[s][oc][n*P + p]
 __global__ void fwd_reduce_kernel(const float* __restrict__ part, int ksplit, int64_t M, int64_t oc,
                                   int64_t P, const float* __restrict__ bias, float* __restrict__ y) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over oc * M, m fastest
   if (i >= oc * M) return;
   const int64_t c = i / M, m = i - c * M;
@@ -209,7 +210,7 @@ void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const fl
   launch_tc_auto(ctx, p, 1);
   if (p.ksplit > 1) {
     const int64_t n = p.M * p.N;
-    fwd_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(p.part, p.ksplit, p.M, p.N, p.g.P, bias, y);
+    ::dpg::launch_pdl(fwd_reduce_kernel, (unsigned)((n + 255) / 256), 256, 0, ctx->stream, p.part, p.ksplit, p.M, p.N, p.g.P, bias, y);
     DPG_LAUNCH_CHECK(ctx);
   }
 }
@@ -334,6 +335,7 @@ struct ConvDgrad {
 // dx = mask ? (sum_s part[s]) : 0 (input-shaped partials; every class writes disjoint pixels)
 __global__ void dgrad_reduce_kernel(const float* __restrict__ part, int ksplit, int64_t n,
                                     const float* __restrict__ mask, float* __restrict__ dx) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float acc = sum_splits(part, ksplit, n, i);
@@ -392,7 +394,7 @@ void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& c
   // writes its rows (zeros when its K range is empty), so the partials need no clearing
   launch_tc_auto(ctx, p, p.ncls);
   if (p.ksplit > 1) {
-    dgrad_reduce_kernel<<<(unsigned)((p.dx_numel + 255) / 256), 256, 0, ctx->stream>>>(p.part, p.ksplit, p.dx_numel, mask_src, dx);
+    ::dpg::launch_pdl(dgrad_reduce_kernel, (unsigned)((p.dx_numel + 255) / 256), 256, 0, ctx->stream, p.part, p.ksplit, p.dx_numel, mask_src, dx);
     DPG_LAUNCH_CHECK(ctx);
   }
 }

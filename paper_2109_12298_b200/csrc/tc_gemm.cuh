@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Pro
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // TMEM allocation and barrier init above overlap the previous kernel's tail
   p.setup(z, m0, n0, scratch, tid);
   tc_fence_before();
   __syncthreads();
@@ -553,6 +554,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) tc_ws_kernel(const Prob p, int 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -713,7 +715,7 @@ void launch_tc(dpg_ctx* ctx, const Prob& p, int64_t batches) {
     if (T == 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>(T, kNumSMs);
     static const int dbg = [] { const char* e = std::getenv("DPG_TC_DBG"); return e ? std::atoi(e) : 0; }();
-    tc_ws_kernel<BN, Prob><<<grid, kWsThreads, smem, ctx->stream>>>(p, mt, nt, T, dbg);
+    ::dpg::launch_pdl(tc_ws_kernel<BN, Prob>, grid, kWsThreads, smem, ctx->stream, p, mt, nt, T, dbg);
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
@@ -724,7 +726,7 @@ void launch_tc(dpg_ctx* ctx, const Prob& p, int64_t batches) {
     attr = smem;
   }
   dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)(batches * p.ksplit));
-  tc_gemm_kernel<BN, Prob><<<grid, kThreads, smem, ctx->stream>>>(p);
+  ::dpg::launch_pdl(tc_gemm_kernel<BN, Prob>, grid, kThreads, smem, ctx->stream, p);
   DPG_LAUNCH_CHECK(ctx);
 }
 

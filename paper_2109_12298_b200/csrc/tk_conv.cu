@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(kThreads) tk_gs_kernel(Geo g, const float* __r
                                                          int64_t spl, float* __restrict__ out,
                                                          double* __restrict__ sq_part, float* __restrict__ gb,
                                                          double* __restrict__ sq_b) {
+  pdl_wait();
   extern __shared__ __align__(16) float sm[];
   __shared__ double red[kThreads / 32];
   __shared__ double bred[kThreads / 32];
@@ -307,7 +308,7 @@ void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom&
   const Geo g = make(cg);
   const size_t smem = gs_smem(g);
   set_smem((const void*)tk_gs_kernel<0>, smem);
-  tk_gs_kernel<0><<<(unsigned)cg.b, kThreads, smem, ctx->stream>>>(g, x, relu, hw, nullptr, cg.b, 1, gw,
+  ::dpg::launch_pdl(tk_gs_kernel<0>, (unsigned)cg.b, kThreads, smem, ctx->stream, g, x, relu, hw, nullptr, cg.b, 1, gw,
                                                                     sq_part, gb, sq_b);
   DPG_LAUNCH_CHECK(ctx);
 }
@@ -324,7 +325,7 @@ void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* 
   const size_t smem = gs_smem(g);
   const int64_t spl = (cg.b + splits - 1) / splits;
   set_smem((const void*)tk_gs_kernel<1>, smem);
-  tk_gs_kernel<1><<<(unsigned)splits, kThreads, smem, ctx->stream>>>(g, x, relu, hw, scale, cg.b, spl, part,
+  ::dpg::launch_pdl(tk_gs_kernel<1>, (unsigned)splits, kThreads, smem, ctx->stream, g, x, relu, hw, scale, cg.b, spl, part,
                                                                       nullptr, nullptr, nullptr);
   DPG_LAUNCH_CHECK(ctx);
 }
