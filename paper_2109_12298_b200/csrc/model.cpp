@@ -303,6 +303,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
   }
   // ---- reverse walk (grad_sample.hpp:277-303) ----
   double* slab = o->slab;
+  int rule_branch = 0;
   for (int l = (int)m->layers.size() - 1; l >= 0; --l) {
     LayerPlan& lp = m->layers[l];
     if (lp.param0 < 0) continue;
@@ -313,13 +314,19 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
     double* sq_w = slab + (int64_t)pw.sq_row0 * b;
     const std::string ls = "[" + std::to_string(l) + "]";
     const double gwrite = gw ? 4.0 * b * pw.numel : 0.0;
+    // rules alternate between the two aux streams (each needs only its own highway), and a
+    // separate bias rule runs on the other one
+    const int rb = rule_branch++ & 1;
     auto bias_rule = [&](int64_t mid, int64_t r, bool conv_layout) {
-      const ParamInfo& pb = m->params[lp.param0 + 1];
-      dpg::ProfScope ps(ctx, "gs.bias" + ls, 4.0 * b * (lp.out_numel + r), 0.0);
-      dpg::launch_gs_bias(ctx, hw, b, mid, r, conv_layout, gs_ptr(o, lp.param0 + 1, b),
-                          slab + (int64_t)pb.sq_row0 * b);
+      on_branch(m, rb ^ 1, [&] {
+        const ParamInfo& pb = m->params[lp.param0 + 1];
+        dpg::ProfScope ps(ctx, "gs.bias" + ls, 4.0 * b * (lp.out_numel + r), 0.0);
+        dpg::launch_gs_bias(ctx, hw, b, mid, r, conv_layout, gs_ptr(o, lp.param0 + 1, b),
+                            slab + (int64_t)pb.sq_row0 * b);
+      });
     };
-    on_branch(m, 0, [&] {
+    struct { int64_t mid, r, conv; } pending_bias{0, 0, -1};  // a separate bias rule, forked below
+    on_branch(m, rb, [&] {
     switch (lp.kind) {
       case DPG_LAYER_LINEAR: {
         {
@@ -328,7 +335,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
           dpg::launch_gs_linear(ctx, in, lp.in_relu, hw, b, lp.mid, lp.d.in_features,
                                 lp.d.out_features, gw, sq_w);
         }
-        if (lp.nparams > 1) bias_rule(lp.mid, lp.d.out_features, false);
+        if (lp.nparams > 1) pending_bias = {lp.mid, lp.d.out_features, 0};
         break;
       }
       case DPG_LAYER_CONV2D: {
@@ -345,7 +352,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
           }
           dpg::launch_gs_conv2d(ctx, in, lp.in_relu, hw, g, gw, sq_w);
         }
-        if (lp.nparams > 1) bias_rule(g.P(), g.oc, true);
+        if (lp.nparams > 1) pending_bias = {g.P(), g.oc, 1};
         break;
       }
       case DPG_LAYER_LAYER_NORM:
@@ -366,6 +373,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
       }
     }
     });
+    if (pending_bias.conv >= 0) bias_rule(pending_bias.mid, pending_bias.r, pending_bias.conv == 1);
     // input gradient for the previous parametric layer, with the ReLU mask folded in
     if (lp.prev_param_layer >= 0) {
       const LayerPlan& prev = m->layers[lp.prev_param_layer];
