@@ -157,8 +157,14 @@ struct dpg_optimizer {
     float* loss;
     cudaGraphExec_t exec;
     int64_t kernels;  // kernels per replay (gpu_launches evidence)
+    uint64_t last_use;
   };
+  // Bounded LRU of instantiated step graphs: Poisson sampling gives a new physical batch size
+  // almost every step, so a miss re-captures and updates the least recently used executable in
+  // place (cudaGraphExecUpdate: same topology, new kernel arguments) instead of instantiating.
+  static constexpr size_t kMaxGraphs = 8;
   std::vector<Graph> graphs;
+  uint64_t graph_clock = 0;
   // pinned ring the graph replays read their Philox step from (a pageable source could make the
   // H2D wait for the stream); a slot is reused only after the copy that read it has executed
   static constexpr int kStepRing = 16;
@@ -1092,13 +1098,30 @@ dpg_status dpg_train_step(dpg_optimizer* o, const float* x, const float* targets
       }
       DPG_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
       ctx->capturing = false;
-      cudaGraphExec_t exec;
-      DPG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-      DPG_CUDA(cudaGraphDestroy(graph));
-      o->graphs.push_back({b, x, targets, loss, exec, ctx->launches - before});
+      const int64_t kernels = ctx->launches - before;
       ctx->launches = before;
-      hit = &o->graphs.back();
+      if (o->graphs.size() >= dpg_optimizer::kMaxGraphs) {
+        auto lru = std::min_element(o->graphs.begin(), o->graphs.end(),
+                                    [](const auto& a, const auto& c) { return a.last_use < c.last_use; });
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(lru->exec, graph, &info) == cudaSuccess) {
+          *lru = {b, x, targets, loss, lru->exec, kernels, 0};
+          hit = &*lru;
+        } else {
+          (void)cudaGetLastError();  // topology changed (e.g. another split-K choice): rebuild
+          DPG_CUDA(cudaGraphExecDestroy(lru->exec));
+          o->graphs.erase(lru);
+        }
+      }
+      if (!hit) {
+        cudaGraphExec_t exec;
+        DPG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        o->graphs.push_back({b, x, targets, loss, exec, kernels, 0});
+        hit = &o->graphs.back();
+      }
+      DPG_CUDA(cudaGraphDestroy(graph));
     }
+    hit->last_use = ++o->graph_clock;
     if (!o->step_ring) {
       DPG_CUDA(cudaHostAlloc(&o->step_ring, sizeof(uint64_t) * dpg_optimizer::kStepRing, cudaHostAllocDefault));
       for (auto& e : o->ring_ev) DPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

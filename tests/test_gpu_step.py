@@ -274,3 +274,24 @@ def test_degenerate_dp_equals_sgd(ctx):
         mean_grad[off:off + numel] = rec[b * off:b * (off + numel)].reshape(b, numel).astype(np.float64).mean(0)
     sgd = params - 0.1 * mean_grad
     assert maxscaled_err(p_new - params, sgd - params) < 1e-5
+
+
+def test_variable_batch_graph_cache_equals_eager(ctx):
+    """Poisson-style physical batch sizes: 14 steps over 11 distinct sizes (more than the 8-entry
+    graph cache, so executables are updated in place) give the eager path's bits."""
+    import torch
+    from paper_2109_12298_b200 import dpg
+    sizes = [32, 17, 29, 32, 9, 24, 31, 12, 20, 17, 27, 14, 32, 5]
+    w, params, x, y, m, o, cfg = _setup(ctx, "cifar_b512", 32, noise_multiplier=1.0, expected_batch_size=24.0)
+    xt, yt = _t(x), _t(y)
+    bufs = {b: (xt[:b].contiguous(), yt[:b].contiguous(), torch.zeros(b, device="cuda")) for b in set(sizes)}
+    for b in sizes:
+        o.train_step(*bufs[b], use_graph=False)
+    eager = m.store_params()
+    m.load_params(params)
+    o2 = dpg.DpOptimizer(m, **cfg)
+    for b in sizes:
+        o2.train_step(*bufs[b], use_graph=True)
+    ctx.sync()
+    assert np.array_equal(m.store_params(), eager), "graph cache replays must be bit-identical to eager"
+
