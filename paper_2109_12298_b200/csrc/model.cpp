@@ -434,25 +434,43 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
                              o->norms, o->scale, o->num_clipped);
   }
   auto act = [&](int buf) -> const float* { return buf < 0 ? x : m->bufs[buf]; };
-  // bias clipped sums: weighted sums of the per-sample bias records, all biases in one launch
-  if (!o->cfg.clipped_sum_from_record) {
-    dpg::WsumItems items{};
-    double bytes = 0;
-    for (auto& pi : m->params) {
-      if (!pi.is_bias) continue;
-      if (items.count == 16) {
-        dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
-        items.count = 0;
-      }
-      items.item[items.count++] = {gs_ptr(o, (int)(&pi - &m->params[0]), b), o->summed + pi.offset, pi.numel};
-      bytes += 4.0 * (b * pi.numel + 2 * pi.numel);
+  // A weight's clipped sum comes from its stored per-sample gradients (the reference's own pass 2,
+  // optimizer.hpp:99-114) when that record is smaller than the layer's activations + highway,
+  // which (s ⊙ B)^T A would re-read (e.g. CIFAR conv1: 1.8 MB of G vs 23 MB of x and y);
+  // otherwise from (s ⊙ B)^T A without touching G.
+  std::vector<char> from_record(m->params.size(), 0);
+  for (auto& lp : m->layers) {
+    if (lp.param0 < 0) continue;
+    for (int k = 0; k < lp.nparams; ++k) {
+      const ParamInfo& pi = m->params[lp.param0 + k];
+      from_record[lp.param0 + k] =
+          pi.is_bias || (o->cfg.materialise_grad_sample && lp.kind != DPG_LAYER_EMBEDDING &&
+                         2 * pi.numel < lp.in_numel + lp.out_numel);
     }
-    on_branch(m, 1, [&] {
-      dpg::ProfScope ps(ctx, "csum.bias[all]", bytes, 0.0);
-      dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
-    });
   }
-  int branch = 0;  // weight clipped sums round-robin over aux 0, aux 1, the caller's stream
+  // stream plan for the per-layer (s ⊙ B)^T A launches: greedy, largest first, onto the least
+  // loaded of aux 0 / aux 1 / the caller's stream (estimated cost ~ launch + flops); the record
+  // weighted sums (one launch) take the caller's stream
+  double load[3] = {0.0, 0.0, 1.0};
+  std::vector<int> stream_of(m->layers.size(), 2);
+  {
+    std::vector<std::pair<double, int>> cost;
+    for (size_t l = 0; l < m->layers.size(); ++l) {
+      const LayerPlan& lp = m->layers[l];
+      if (lp.param0 < 0 || from_record[lp.param0]) continue;
+      double fl = 0;
+      if (lp.kind == DPG_LAYER_CONV2D) fl = 2.0 * b * lp.g.oc * lp.g.K() * lp.g.P();
+      if (lp.kind == DPG_LAYER_LINEAR) fl = 2.0 * b * lp.mid * lp.d.in_features * lp.d.out_features;
+      if (lp.kind == DPG_LAYER_EMBEDDING) fl = 8.0 * b * lp.out_numel;
+      cost.push_back({1.0 + 25.0 * fl / 1e9, (int)l});
+    }
+    std::sort(cost.begin(), cost.end(), [](const auto& a, const auto& c) { return a.first > c.first; });
+    for (auto& [c, l] : cost) {
+      const int s = (int)(std::min_element(load, load + 3) - load);
+      load[s] += c;
+      stream_of[l] = s;
+    }
+  }
   for (size_t l = 0; l < m->layers.size(); ++l) {
     LayerPlan& lp = m->layers[l];
     if (lp.param0 < 0) continue;
@@ -462,7 +480,7 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       float* dst = o->summed + pi.offset;
       float* rec = gs_ptr(o, p, b);
       const std::string ls = "[" + std::to_string(l) + "]";
-      if (pi.is_bias && !o->cfg.clipped_sum_from_record) continue;  // done above
+      if (from_record[p] && !o->cfg.clipped_sum_from_record) continue;  // done above
       if (o->cfg.clipped_sum_from_record) {
         // the reference's pass 2 over the stored per-sample gradients (exact order)
         dpg::ProfScope ps(ctx, std::string(pi.is_bias ? "csum.bias" : "csum.record") + ls,
@@ -474,7 +492,7 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       const float* hw = m->highways[lp.out_buf];
       const double cio = 4.0 * (b * (lp.in_numel + lp.out_numel) + 2 * pi.numel);
       void* ws = m->csum_ws[l];
-      const int br = branch++ % (dpg_model::kAux + 1);
+      const int br = stream_of[l];
       on_branch(m, br < dpg_model::kAux ? br : -1, [&] {
       switch (lp.kind) {
         case DPG_LAYER_LINEAR: {
@@ -503,6 +521,23 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       }
       });
     }
+  }
+  // record-based clipped sums (biases, normalisation affines, small weights): weighted column sums
+  // of the per-sample records, all in one launch
+  if (!o->cfg.clipped_sum_from_record) {
+    dpg::WsumItems items{};
+    double bytes = 0;
+    for (auto& pi : m->params) {
+      if (!from_record[&pi - &m->params[0]]) continue;
+      if (items.count == 16) {
+        dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+        items.count = 0;
+      }
+      items.item[items.count++] = {gs_ptr(o, (int)(&pi - &m->params[0]), b), o->summed + pi.offset, pi.numel};
+      bytes += 4.0 * (b * pi.numel + 2 * pi.numel);
+    }
+    dpg::ProfScope ps(ctx, "csum.record[all]", bytes, 0.0);
+    dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
   }
   join_branches(m);
   o->has_summed = true;
