@@ -745,11 +745,19 @@ void launch_tc_auto(dpg_ctx* ctx, const Prob& p, int64_t batches) {
 
 // split-K factor: only when the output tiles alone leave SMs idle; then enough splits to fill
 // ctas_target() CTAs with >= 2 K stages per split
+// CTAs a split-K forward / dgrad launch aims for (DPG_KSPLIT_CTAS overrides; tuning knob)
+inline int ksplit_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("DPG_KSPLIT_CTAS");
+    return e ? std::atoi(e) : ctas_target();
+  }();
+  return v;
+}
 inline int pick_ksplit(int64_t M, int64_t N, int64_t K, int64_t batches) {
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + 127) / 128) * batches;
   if (tiles >= kNumSMs) return 1;
   const int64_t nk = (K + BK - 1) / BK;
-  int64_t ks = (ctas_target() + tiles - 1) / tiles;
+  int64_t ks = (ksplit_ctas() + tiles - 1) / tiles;
   ks = std::min<int64_t>(ks, std::max<int64_t>(1, nk / 2));
   return (int)std::max<int64_t>(1, std::min<int64_t>(ks, 16));
 }
