@@ -745,11 +745,13 @@ void launch_tc_auto(dpg_ctx* ctx, const Prob& p, int64_t batches) {
 
 // split-K factor: only when the output tiles alone leave SMs idle; then enough splits to fill
 // ctas_target() CTAs with >= 2 K stages per split
-// CTAs a split-K forward / dgrad launch aims for (DPG_KSPLIT_CTAS overrides; tuning knob)
+// CTAs a split-K forward / dgrad launch aims for (DPG_KSPLIT_CTAS overrides). Two per SM:
+// measured on the CIFAR step (fewer splits = less partial traffic for the reduce), 444 -> 296
+// CTAs took the step from 399 to 389 us (148: 390 us).
 inline int ksplit_ctas() {
   static const int v = [] {
     const char* e = std::getenv("DPG_KSPLIT_CTAS");
-    return e ? std::atoi(e) : ctas_target();
+    return e ? std::atoi(e) : (ws_enabled() ? kNumSMs : 2 * kNumSMs);
   }();
   return v;
 }
