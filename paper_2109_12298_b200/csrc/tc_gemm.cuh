@@ -40,6 +40,9 @@ constexpr int BM = 128;
 #ifndef DPG_TC_BK
 #define DPG_TC_BK 16
 #endif
+#ifndef DPG_TC_MINB
+#define DPG_TC_MINB 4  // resident CTAs per SM the 16-wide-K kernel is register-budgeted for (64 regs)
+#endif
 constexpr int BK = DPG_TC_BK;
 static_assert(BK == 16 || BK == 32, "BK: one 64 B or 128 B swizzle row");
 constexpr int kQuadsPerRow = BK / 4;                 // 16 B chunks per K-major row
@@ -47,7 +50,7 @@ constexpr int kRowBytes = BK * 4;                    // 64 or 128
 constexpr int kAtomBytes = 8 * kRowBytes;            // 8-row swizzle atom: 512 or 1024
 constexpr int kAQ = BM * kQuadsPerRow / 256;         // A quads per thread per stage: 2 or 4
 constexpr uint64_t kLayoutType = BK == 32 ? 2 : 4;   // UMMA layout: SWIZZLE_128B / SWIZZLE_64B
-constexpr int kMinBlocks = BK == 32 ? 2 : 3;         // resident CTAs per SM the kernel is built for
+constexpr int kMinBlocks = BK == 32 ? 2 : DPG_TC_MINB;         // resident CTAs per SM the kernel is built for
 constexpr int kThreads = 256;
 constexpr int kStages = 2;
 
