@@ -482,6 +482,64 @@ def cpu_baseline_linear_t64(budget_s=15.0):
                       f"thread shards, add_noise), median of {len(times)}, -O3 -march=x86-64-v3"}
 
 
+# ------------------------------------------------------------------------------ Poisson batches
+def run_poisson(args):
+    """Poisson sampling on the host (data.cpp:31-37: each of N examples joins a
+    batch with probability q = E / N), so every step has a different physical batch size; the
+    device step replays from the bounded graph cache (updated in place on a miss). E = 512 of a
+    CIFAR-10-sized dataset (N = 50000); samples/s = sum of realised batch sizes / device time."""
+    import numpy as np
+    import torch
+    from paper_2109_12298_b200 import dpg
+    from paper_2109_12298_b200.configs import WORKLOADS
+    w = WORKLOADS["cifar_b512"]
+    N, E = 50000, 512
+    q = E / N
+    rng = np.random.default_rng(7)
+    sizes = [int(v) for v in rng.binomial(N, q, size=args.warmup + args.steps)]
+    bmax = max(sizes)
+    params, _, _ = synth(w, bmax)
+    _, x, y = synth(w, bmax)
+    ctx = dpg.Context(0)
+    model = dpg.Model(ctx, w.layers, w.in_shape, max_batch=bmax)
+    model.load_params(params)
+    opt = dpg.DpOptimizer(model, noise_multiplier=args.sigma, max_grad_norm=args.max_grad_norm,
+                          learning_rate=0.1, expected_batch_size=float(E), noise_seed=3)
+    xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    loss = torch.zeros(bmax, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    for b in sizes[:args.warmup]:
+        opt.train_step(xt[:b], yt[:b], loss[:b])
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.kernel_launches
+    for i, b in enumerate(sizes[args.warmup:]):
+        flush.zero_()
+        evs[i][0].record(stream)
+        opt.train_step(xt[:b], yt[:b], loss[:b])
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ctx.sync()
+    total_ms = sum(a.elapsed_time(c) for a, c in evs)
+    timed = sizes[args.warmup:]
+    line = {
+        "metric": "DP-SGD step samples/sec (CIFAR-10 CNN, Poisson sampling, E=512)",
+        "value": sum(timed) / (total_ms / 1000.0), "unit": "samples/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cifar_poisson", "dataset": N, "expected_batch": E, "q": q,
+                   "batch_min": min(timed), "batch_max": max(timed), "distinct_batches": len(set(timed)),
+                   "graph_cache": "8 executables, LRU, updated in place on a miss",
+                   "l2": "256 MiB flush before every timed step (outside the step's events)"},
+        "gpu_launches": ctx.kernel_launches - launches0, "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -490,6 +548,10 @@ def main():
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("gloo")
+    if args.workload == "cifar_poisson" and args.impl == "ours":
+        if rank == 0:
+            run_poisson(args)
+        return
     if args.workload == "linear_t64" and args.impl == "ours":
         if rank == 0:
             run_linear_t64(args, rank, world)
