@@ -520,6 +520,22 @@ struct ConvCsum {
     const Row r = reinterpret_cast<const Row*>(s + ((4 * g.P + 15) & ~15))[row];
     const int k = (int)k64, Ki = (int)K, n_end = (int)bsz, chw = g.ic * g.h * g.w;
     float v[4];
+    if ((g.P & 3) == 0) {
+      // the quad's 4 k share one sample (k % 4 == 0, P % 4 == 0): one division, one base
+      uint32_t qq, pp;
+      g.fP.divmod((uint32_t)k, qq, pp);
+      const int n = z * (int)spl + (int)qq;
+      const float* xb = x + (n * chw + r.plane);
+      const bool in = k < Ki && n < n_end;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const PEnt t = pt[pp + e];
+        const int iy = t.y + r.ki, ix = t.x + r.kj;
+        const bool ok = in && (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
+        v[e] = ldg_or_zero(xb + (iy * g.w + ix), ok);
+      }
+      return make_float4(v[0], v[1], v[2], v[3]);
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t qq, pp;
@@ -679,6 +695,16 @@ struct LinCsum {
   __device__ float4 a_quad(int z, int64_t m0, int row, int64_t k64, const uint8_t*) const {
     const int i = (int)m0 + row, k = (int)k64, Ki = (int)K, Mi = (int)M, midi = (int)mid;
     float v[4];
+    if ((midi & 3) == 0) {  // the quad's 4 k are 4 consecutive t of one sample: one division
+      uint32_t qq, t;
+      fmid.divmod((uint32_t)k, qq, t);
+      const int n = z * (int)spl + (int)qq;
+      const float* base = acts + ((n * midi + (int)t) * Mi + i);
+      const bool in = k < Ki && n < (int)bsz;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = ldg_or_zero(base + e * Mi, in);
+      return make_float4(v[0], v[1], v[2], v[3]);
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t qq, t;
@@ -693,6 +719,16 @@ struct LinCsum {
   __device__ float4 b_quad(int z, int64_t n0, int row, int64_t k64, const uint8_t*) const {
     const int o = (int)n0 + row, k = (int)k64, Ki = (int)K, Ni = (int)N, midi = (int)mid;
     float v[4];
+    if ((midi & 3) == 0) {
+      uint32_t qq, t;
+      fmid.divmod((uint32_t)k, qq, t);
+      const int n = z * (int)spl + (int)qq;
+      const float* base = hw + ((n * midi + (int)t) * Ni + o);
+      const bool in = k < Ki && n < (int)bsz;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = ldg_or_zero(base + e * Ni, in);
+      return make_float4(v[0], v[1], v[2], v[3]);
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t qq, t;
@@ -703,6 +739,11 @@ struct LinCsum {
     return make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ float4 b_fix(int z, int64_t, int, int64_t k, const uint8_t*, float4 v) const {
+    if (((int)mid & 3) == 0) {  // one sample per quad: one scale
+      const int64_t n = (int64_t)z * spl + fmid.div((uint32_t)k);
+      const float sc = ldg_or_zero(scale + n, n < bsz);
+      return make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
+    }
     float sc[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {

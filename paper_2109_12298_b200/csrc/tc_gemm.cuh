@@ -40,6 +40,9 @@ constexpr int BM = 128;
 #ifndef DPG_TC_BK
 #define DPG_TC_BK 16
 #endif
+#ifndef DPG_TC_EXP
+#define DPG_TC_EXP 0  // timing experiments only (results wrong): 1 = skip gathers, 2 = skip stores, 4 = skip MMAs
+#endif
 #ifndef DPG_TC_MINB
 #define DPG_TC_MINB 4  // resident CTAs per SM the 16-wide-K kernel is register-budgeted for (64 regs)
 #endif
@@ -340,7 +343,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Pro
     uint8_t* st = smem + s * S::STAGE;
     const StageBufsT sb{st, st + S::A_BYTES, st + 2 * S::A_BYTES, st + 2 * S::A_BYTES + S::B_BYTES};
     if (i >= kStages) mbar_wait(&bars[s], ((i / kStages) - 1) & 1);
+#if DPG_TC_EXP & 2
+    if (i < 0)
+#endif
     stash<BN, Prob>(p, z, m0, n0, (int64_t)(ks0 + i) * BK, scratch, tid, mrows, nrows, sb, ra, rb);
+#if DPG_TC_EXP & 1
+    if (i < 0)
+#endif
     if (i + 2 < nk) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + i + 2) * BK, scratch, tid, mrows, nrows, ra, rb);
     fence_proxy_async();
     __syncthreads();
@@ -350,6 +359,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Pro
       const uint32_t sb_hi = smem_u32(sb.b_hi), sb_lo = smem_u32(sb.b_lo);
 #pragma unroll
       for (int kk = 0; kk < BK / 8; ++kk) {
+        if (DPG_TC_EXP & 4) break;
         const uint32_t off = kk * 32;  // 8 tf32 = 32 B along the swizzled row
         const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
         mma_tf32(tmem, sw_desc(sa_lo + off), sw_desc(sb_hi + off), idesc, acc0);
