@@ -125,3 +125,23 @@ def test_nonparam_models_and_ragged_layers(oracle_r, oracle_ref):
     a = oracle_r.dpsgd_step(w.layers, w.in_shape, p, x, y, 0.5, 0.8, 0.1, 7.0)
     r = oracle_ref.dpsgd_step(w.layers, w.in_shape, p, x, y, 0.5, 0.8, 0.1, 7.0)
     assert np.array_equal(a["params"], r["params"]) and np.array_equal(a["record"], r["record"])
+
+
+def test_reference_norm_rules_and_step(oracle_ref):
+    """The layer_norm / group_norm rules the GPU parity tests check against (grad_sample.hpp:87-131):
+    the reference's fp64 rules are the plain sums, and its step runs a model with both layers."""
+    from paper_2109_12298_b200.configs import LayerDesc as L, param_count
+    g = np.random.default_rng(5)
+    xh, h = g.standard_normal((3, 4, 6)), g.standard_normal((3, 4, 6))
+    gg, gb = oracle_ref.rule_norm(xh, h, False)  # layer_norm over the trailing 6
+    np.testing.assert_allclose(gg, (xh * h).sum(1), rtol=1e-14)
+    np.testing.assert_allclose(gb, h.sum(1), rtol=1e-14)
+    gg, gb = oracle_ref.rule_norm(xh, h, True)  # group_norm over [b, 4 channels, 6]
+    np.testing.assert_allclose(gg, (xh * h).sum(2), rtol=1e-14)
+    layers = (L.conv2d(3, 4, 3, 3, 1, 1), L.group_norm(2, 4), L.relu(), L.flatten(), L.linear(64, 8),
+              L.layer_norm(8), L.relu(), L.linear(8, 3))
+    p = g.standard_normal(param_count(layers)) * 0.3
+    x = g.standard_normal((5, 3, 4, 4))
+    y = g.integers(0, 3, 5).astype(np.float64)
+    r = oracle_ref.dpsgd_step(layers, (3, 4, 4), p, x, y, 0.0, 1.0, 0.1, 5.0)
+    assert np.all(np.isfinite(r["params"])) and np.all(r["norms"] > 0)
