@@ -295,3 +295,32 @@ def test_variable_batch_graph_cache_equals_eager(ctx):
     ctx.sync()
     assert np.array_equal(m.store_params(), eager), "graph cache replays must be bit-identical to eager"
 
+
+
+def test_nccl_allreduce_in_captured_step(ctx):
+    """The multi-GPU data path on one GPU: a one-rank NCCL communicator puts ncclAllReduce of the
+    clipped sum into the captured step; sum over one rank is the identity, so the
+    update must equal the communicator-free step bit for bit (eager and graph)."""
+    import torch
+    from paper_2109_12298_b200 import dpg
+    b = 16
+    w, params, x, y, m, o, cfg = _setup(ctx, "cifar_b512", b, noise_multiplier=1.0)
+    xt, yt = _t(x), _t(y)
+    loss = torch.zeros(b, device="cuda")
+    for _ in range(2):
+        o.train_step(xt, yt, loss, use_graph=True)
+    ctx.sync()
+    ref = m.store_params()
+    c2 = dpg.Context(0)
+    c2.init_comm(1, 0, dpg.Context.nccl_unique_id())
+    m2 = dpg.Model(c2, w.layers, w.in_shape, max_batch=64)
+    m2.load_params(params)
+    o2 = dpg.DpOptimizer(m2, **cfg)
+    o2.train_step(xt, yt, loss, use_graph=False)
+    o2.train_step(xt, yt, loss, use_graph=True)
+    c2.sync()
+    assert np.array_equal(m2.store_params(), ref)
+    buf = torch.arange(10, dtype=torch.float32, device="cuda")
+    c2.allreduce_sum(buf)
+    c2.sync()
+    assert torch.equal(buf, torch.arange(10, dtype=torch.float32, device="cuda"))
