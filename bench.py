@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--max-grad-norm", type=float, default=1.0)
     ap.add_argument("--no-materialise", action="store_true",
                     help="norms without storing the GradSampleRecord (not the headline)")
+    ap.add_argument("--csum-from-record", action="store_true",
+                    help="clipped sums as the reference's pass 2 over the stored record (not the headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
     return ap.parse_args()
@@ -586,7 +588,8 @@ def main():
     materialise = not args.no_materialise
     opt = dpg.DpOptimizer(model, noise_multiplier=args.sigma, max_grad_norm=args.max_grad_norm,
                           learning_rate=0.1, expected_batch_size=float(gb), noise_seed=3,
-                          materialise_grad_sample=materialise)
+                          materialise_grad_sample=materialise,
+                          clipped_sum_from_record=args.csum_from_record and materialise)
     xt = torch.from_numpy(x).cuda()
     yt = torch.from_numpy(y).cuda()
     loss = torch.zeros(b, device="cuda")
@@ -699,6 +702,7 @@ def main():
                    "parallelism": f"dp{world} (sample shards, 1 NCCL all-reduce of the clipped sum)",
                    "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
                    "materialise_grad_sample": materialise, "graph": True,
+                   "clipped_sum": "record pass 2" if (args.csum_from_record and materialise) else "(s.B)^T A",
                    "l2": "256 MiB flush before every timed step (outside the step's events)"},
         "roofline": roofline,
         "e2e": e2e,

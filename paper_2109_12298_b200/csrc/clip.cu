@@ -511,8 +511,21 @@ __global__ void weighted_sum_kernel(const float* __restrict__ g, const float* __
   pdl_wait();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= numel) return;
+  // the reference's sequential order, with 16 samples' loads in flight per round (a streaming
+  // read of the record instead of one dependent HBM latency per sample)
   float acc = 0.f;
-  for (int64_t n = 0; n < b; ++n) acc = __fadd_rn(acc, __fmul_rn(__ldg(scale + n), __ldg(g + n * numel + j)));
+  int64_t n = 0;
+  for (; n + 16 <= b; n += 16) {
+    float v[16], s[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      v[u] = __ldg(g + (n + u) * numel + j);
+      s[u] = __ldg(scale + n + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, __fmul_rn(s[u], v[u]));
+  }
+  for (; n < b; ++n) acc = __fadd_rn(acc, __fmul_rn(__ldg(scale + n), __ldg(g + n * numel + j)));
   summed[j] = accumulate ? __fadd_rn(summed[j], acc) : acc;
 }
 

@@ -471,6 +471,7 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       stream_of[l] = s;
     }
   }
+  int rr_branch = 0;
   for (size_t l = 0; l < m->layers.size(); ++l) {
     LayerPlan& lp = m->layers[l];
     if (lp.param0 < 0) continue;
@@ -482,10 +483,14 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       const std::string ls = "[" + std::to_string(l) + "]";
       if (from_record[p] && !o->cfg.clipped_sum_from_record) continue;  // done above
       if (o->cfg.clipped_sum_from_record) {
-        // the reference's pass 2 over the stored per-sample gradients (exact order)
-        dpg::ProfScope ps(ctx, std::string(pi.is_bias ? "csum.bias" : "csum.record") + ls,
-                          4.0 * (b * pi.numel + 2 * pi.numel), 2.0 * b * pi.numel);
-        dpg::launch_weighted_sum_materialised(ctx, rec, o->scale, b, pi.numel, dst, accumulate);
+        // the reference's pass 2 over the stored per-sample gradients (exact order), one launch
+        // per parameter, round-robin over the three streams
+        on_branch(m, (rr_branch % 3) < dpg_model::kAux ? rr_branch % 3 : -1, [&] {
+          dpg::ProfScope ps(ctx, std::string(pi.is_bias ? "csum.bias" : "csum.record") + ls,
+                            4.0 * (b * pi.numel + 2 * pi.numel), 2.0 * b * pi.numel);
+          dpg::launch_weighted_sum_materialised(ctx, rec, o->scale, b, pi.numel, dst, accumulate);
+        });
+        ++rr_branch;
         continue;
       }
       const float* in = act(lp.in_buf);
