@@ -55,7 +55,10 @@ constexpr int kAQ = BM * kQuadsPerRow / 256;         // A quads per thread per s
 constexpr uint64_t kLayoutType = BK == 32 ? 2 : 4;   // UMMA layout: SWIZZLE_128B / SWIZZLE_64B
 constexpr int kMinBlocks = BK == 32 ? 2 : DPG_TC_MINB;         // resident CTAs per SM the kernel is built for
 constexpr int kThreads = 256;
-constexpr int kStages = 2;
+#ifndef DPG_TC_STAGES
+#define DPG_TC_STAGES 2
+#endif
+constexpr int kStages = DPG_TC_STAGES;  // shared-memory stage ring
 
 // ---- integer division by a runtime constant (multiply-high), valid for n < 2^31 ----
 struct FastDiv {
