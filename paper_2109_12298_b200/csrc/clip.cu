@@ -404,42 +404,128 @@ __global__ void embed_chunk_starts_kernel(const int32_t* __restrict__ sorted_v, 
   }
 }
 
+// Stage 2: the chunk's work list is staged in shared memory first — per-sample entry counts
+// (from the stage-1 starts), their exclusive prefix sum, and the (row, position) pairs of every
+// sample's tokens that fall in the chunk, in sample order — so the ordered accumulation loop only
+// touches global memory for the highway rows (no dependent index loads per sample). Chunks with
+// more entries than fit fall back to reading the indices from global memory.
+constexpr int kCsMaxEntries = 4096;
+
 __global__ void __launch_bounds__(256) clipped_sum_embedding_kernel(
     const int32_t* __restrict__ sorted_v, const int32_t* __restrict__ sorted_s,
     const int32_t* __restrict__ starts, const float* __restrict__ hw,
     const float* __restrict__ scale, int64_t b, int64_t t, int64_t vocab, int64_t dim,
     int nchunks, float* __restrict__ summed, int accumulate) {
   pdl_wait();
-  extern __shared__ float acc[];  // [kCsRows][dim]
+  extern __shared__ float acc[];  // [kCsRows][dim], then the work list
+  int* cnt = reinterpret_cast<int*>(acc + kCsRows * dim);  // [b + 1] exclusive prefix of entries
+  int* ev = cnt + (b + 1);                                 // [kCsMaxEntries] row - v0
+  int* es = ev + kCsMaxEntries;                            // [kCsMaxEntries] position s
+  int* en = es + kCsMaxEntries;                            // [kCsMaxEntries] sample n
+  __shared__ int total_sh;
   const int c = blockIdx.x;
   const int64_t v0 = (int64_t)c * kCsRows;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t i = threadIdx.x; i < kCsRows * dim; i += 256) acc[i] = 0.f;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int64_t i = tid; i < kCsRows * dim; i += 256) acc[i] = 0.f;
+  // per-sample entry counts, then an exclusive scan (one thread; b <= a few thousand)
+  for (int64_t n = tid; n < b; n += 256)
+    cnt[n + 1] = starts[n * (nchunks + 1) + c + 1] - starts[n * (nchunks + 1) + c];
   __syncthreads();
-  for (int64_t n = 0; n < b; ++n) {
-    const int j0 = starts[n * (nchunks + 1) + c], j1 = starts[n * (nchunks + 1) + c + 1];
-    if (j0 == j1) continue;
-    const float w = __ldg(scale + n);
-    const int32_t* sv = sorted_v + n * t;
-    const int32_t* ss = sorted_s + n * t;
-    const float* hwn = hw + n * t * dim;
-    for (int j = j0; j < j1;) {
-      const int32_t v = sv[j];
-      int e = j + 1;
-      while (e < j1 && sv[e] == v) ++e;
-      if (((v - v0) & 7) == warp) {
-        float* arow = acc + (v - v0) * dim;
-        for (int64_t d0 = lane; d0 < dim; d0 += 32) {
-          float g = 0.f;
-          for (int q = j; q < e; ++q) g = __fadd_rn(g, __ldg(hwn + (int64_t)ss[q] * dim + d0));
-          arow[d0] = __fadd_rn(arow[d0], __fmul_rn(w, g));
-        }
+  if (tid == 0) {
+    cnt[0] = 0;
+    for (int64_t n = 0; n < b; ++n) cnt[n + 1] += cnt[n];
+    total_sh = cnt[b];
+  }
+  __syncthreads();
+  const int total = total_sh;
+  const bool staged = total <= kCsMaxEntries;
+  if (staged) {
+    for (int64_t n = warp; n < b; n += 8) {  // a warp per sample: copy its entries
+      const int j0 = starts[n * (nchunks + 1) + c], m = cnt[n + 1] - cnt[n];
+      for (int q = lane; q < m; q += 32) {
+        ev[cnt[n] + q] = sorted_v[n * t + j0 + q] - (int)v0;
+        es[cnt[n] + q] = sorted_s[n * t + j0 + q];
+        en[cnt[n] + q] = (int)n;
       }
-      j = e;
     }
   }
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < kCsRows * dim; i += 256) {
+  if (staged && kCsRows * 8 == 256 && (dim % 32) == 0 && dim <= 256) {
+    // thread (row r = tid / 8, slice = tid % 8 of dim / 8 columns): walk the chunk's entries in
+    // sample order and accumulate the ones of row r — each thread only waits on its own row's
+    // ~b t / vocab highway loads, and the 256 threads' loads are independent
+    const int r = tid >> 3, w8 = (int)(dim >> 3), d0 = (tid & 7) * w8;
+    float a[32], gsum[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) a[k] = 0.f;
+    int cur_n = -1;
+    for (int e = 0; e < total; ++e) {
+      if (ev[e] != r) continue;
+      const int n = en[e];
+      if (n != cur_n) {
+        if (cur_n >= 0) {
+          const float w = __ldg(scale + cur_n);
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (k < w8) a[k] = __fadd_rn(a[k], __fmul_rn(w, gsum[k]));
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) gsum[k] = 0.f;
+        cur_n = n;
+      }
+      const float* src = hw + ((int64_t)n * t + es[e]) * dim + d0;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4)
+        if (k < w8) {
+          const float4 h = __ldg(reinterpret_cast<const float4*>(src + k));
+          gsum[k] = __fadd_rn(gsum[k], h.x);
+          gsum[k + 1] = __fadd_rn(gsum[k + 1], h.y);
+          gsum[k + 2] = __fadd_rn(gsum[k + 2], h.z);
+          gsum[k + 3] = __fadd_rn(gsum[k + 3], h.w);
+        }
+    }
+    if (cur_n >= 0) {
+      const float w = __ldg(scale + cur_n);
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (k < w8) a[k] = __fadd_rn(a[k], __fmul_rn(w, gsum[k]));
+    }
+    if (v0 + r < vocab) {
+      float* o = summed + (v0 + r) * dim + d0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (k < w8) o[k] = accumulate ? __fadd_rn(o[k], a[k]) : a[k];
+    }
+    return;
+  }
+  for (int64_t n = 0; n < b; ++n) {
+    const int e0 = cnt[n], e1 = cnt[n + 1];
+    if (e0 == e1) continue;
+    const float w = __ldg(scale + n);
+    const int j0 = staged ? 0 : starts[n * (nchunks + 1) + c];
+    const int32_t* sv = sorted_v + n * t;
+    const int32_t* ss = sorted_s + n * t;
+    const float* hwn = hw + n * t * dim;
+    for (int e = e0; e < e1;) {
+      const int r = staged ? ev[e] : sv[j0 + e - e0] - (int)v0;
+      int f = e + 1;
+      while (f < e1 && (staged ? ev[f] : sv[j0 + f - e0] - (int)v0) == r) ++f;
+      if ((r & 7) == warp) {
+        float* arow = acc + r * dim;
+        for (int64_t d0 = lane; d0 < dim; d0 += 32) {
+          float g = 0.f;
+          for (int q = e; q < f; ++q) {
+            const int sp = staged ? es[q] : ss[j0 + q - e0];
+            g = __fadd_rn(g, __ldg(hwn + (int64_t)sp * dim + d0));
+          }
+          arow[d0] = __fadd_rn(arow[d0], __fmul_rn(w, g));
+        }
+      }
+      e = f;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = tid; i < kCsRows * dim; i += 256) {
     const int64_t v = v0 + i / dim;
     if (v >= vocab) break;
     float* o = summed + v0 * dim + i;
@@ -462,7 +548,8 @@ void launch_clipped_sum_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const i
     ::dpg::launch_pdl(embed_chunk_starts_kernel, (unsigned)b, 256, 0, ctx->stream, sorted_v, t, nchunks, starts);
     DPG_LAUNCH_CHECK(ctx);
   }
-  const size_t smem = sizeof(float) * kCsRows * (size_t)dim;
+  const size_t smem = sizeof(float) * kCsRows * (size_t)dim + sizeof(int) * ((size_t)b + 1 + 3 * kCsMaxEntries);
+  if (smem > 200 * 1024) raise(DPG_ERR_DIMENSION, "clipped_sum_embedding: batch or embedding_dim too large for one chunk");
   if (smem > 48 * 1024)
     DPG_CUDA(cudaFuncSetAttribute(clipped_sum_embedding_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

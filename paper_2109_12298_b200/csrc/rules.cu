@@ -366,8 +366,11 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t 
   return lo;
 }
 
-// Step 2 (dense): each CTA writes kEmbRows full rows of one sample's [vocab, dim] gradient —
-// the row sum over its (ascending-s) duplicates, zeros elsewhere — in one streaming pass.
+// Step 2 (dense): each CTA owns kEmbRows consecutive rows of one sample's [vocab, dim] gradient
+// (one contiguous block). The block is first zero-filled with coalesced 128-bit streaming
+// stores — >97 % of the record is zeros (a sample touches at most t of the vocab rows) — then
+// the rows the sample's tokens hit are overwritten with their sums over duplicates in ascending
+// s (grad_sample.hpp:75-79), in the same CTA after a barrier.
 constexpr int kEmbRows = 64;
 
 __global__ void __launch_bounds__(256) gs_embedding_dense_kernel(
@@ -376,37 +379,53 @@ __global__ void __launch_bounds__(256) gs_embedding_dense_kernel(
     double* __restrict__ sq_part, int64_t b) {
   pdl_wait();
   extern __shared__ int32_t sv[];
+  __shared__ int range[2];
   const int64_t n = blockIdx.y;
   const int64_t v0 = (int64_t)blockIdx.x * kEmbRows;
+  const int64_t nrows = vocab - v0 < kEmbRows ? vocab - v0 : kEmbRows;
+  float* blk = g + (n * vocab + v0) * dim;
+  const int64_t total = nrows * dim;
+  if ((dim & 3) == 0) {
+    float4* b4 = reinterpret_cast<float4*>(blk);
+    for (int64_t i = threadIdx.x; i < total / 4; i += 256) st_stream4(reinterpret_cast<float*>(b4 + i), make_float4(0.f, 0.f, 0.f, 0.f));
+  } else {
+    for (int64_t i = threadIdx.x; i < total; i += 256) st_stream(blk + i, 0.f);
+  }
   for (int s = threadIdx.x; s < t; s += 256) sv[s] = sorted_v[n * t + s];
   __syncthreads();
+  if (threadIdx.x < 2) range[threadIdx.x] = lower_bound_i32(sv, (int)t, (int32_t)(v0 + (threadIdx.x ? nrows : 0)));
+  __syncthreads();  // also orders the zero fill before the row writes below
+  const int lo = range[0], hi = range[1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t* ss = sorted_s + n * t;
   const float* hwn = hw + n * t * dim;
   double sq = 0.0;
-  for (int64_t v = v0 + warp; v < v0 + kEmbRows && v < vocab; v += 8) {
-    const int lo = lower_bound_i32(sv, (int)t, (int32_t)v);
-    int hi = lo;
-    while (hi < t && sv[hi] == v) ++hi;
-    float* row = g + (n * vocab + v) * dim;
-    if ((dim & 3) == 0) {
-      for (int64_t d0 = 4 * lane; d0 < dim; d0 += 128) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int j = lo; j < hi; ++j) {
-          const float4 h = __ldg(reinterpret_cast<const float4*>(hwn + (int64_t)ss[j] * dim + d0));
-          acc.x += h.x; acc.y += h.y; acc.z += h.z; acc.w += h.w;
+  int r = 0;  // run index: warp w takes runs w, w + 8, ...
+  for (int j0 = lo; j0 < hi; ++r) {
+    int j1 = j0 + 1;
+    while (j1 < hi && sv[j1] == sv[j0]) ++j1;
+    if ((r & 7) == warp) {
+      float* row = g + (n * vocab + sv[j0]) * dim;
+      if ((dim & 3) == 0) {
+        for (int64_t d0 = 4 * lane; d0 < dim; d0 += 128) {
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int j = j0; j < j1; ++j) {
+            const float4 h = __ldg(reinterpret_cast<const float4*>(hwn + (int64_t)ss[j] * dim + d0));
+            acc.x += h.x; acc.y += h.y; acc.z += h.z; acc.w += h.w;
+          }
+          st_stream4(row + d0, acc);
+          sq += (double)acc.x * acc.x + (double)acc.y * acc.y + (double)acc.z * acc.z + (double)acc.w * acc.w;
         }
-        st_stream4(row + d0, acc);
-        sq += (double)acc.x * acc.x + (double)acc.y * acc.y + (double)acc.z * acc.z + (double)acc.w * acc.w;
-      }
-    } else {
-      for (int64_t d0 = lane; d0 < dim; d0 += 32) {
-        float acc = 0.f;
-        for (int j = lo; j < hi; ++j) acc += __ldg(hwn + (int64_t)ss[j] * dim + d0);
-        st_stream(row + d0, acc);
-        sq += (double)acc * acc;
+      } else {
+        for (int64_t d0 = lane; d0 < dim; d0 += 32) {
+          float acc = 0.f;
+          for (int j = j0; j < j1; ++j) acc += __ldg(hwn + (int64_t)ss[j] * dim + d0);
+          st_stream(row + d0, acc);
+          sq += (double)acc * acc;
+        }
       }
     }
+    j0 = j1;
   }
   __shared__ double red[8];
   const double tot = block_sum<256>(sq, red);
