@@ -450,50 +450,75 @@ __global__ void __launch_bounds__(256) clipped_sum_embedding_kernel(
     }
   }
   __syncthreads();
-  if (staged && kCsRows * 8 == 256 && (dim % 32) == 0 && dim <= 256) {
+  if (staged && kCsRows * 8 == 256 && (dim % 32) == 0 && dim <= 128) {
     // thread (row r = tid / 8, slice = tid % 8 of dim / 8 columns): walk the chunk's entries in
     // sample order and accumulate the ones of row r — each thread only waits on its own row's
     // ~b t / vocab highway loads, and the 256 threads' loads are independent
     const int r = tid >> 3, w8 = (int)(dim >> 3), d0 = (tid & 7) * w8;
-    float a[32], gsum[32];
+    float a[16], gsum[16];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) a[k] = 0.f;
+    for (int k = 0; k < 16; ++k) {
+      a[k] = 0.f;
+      gsum[k] = 0.f;
+    }
     int cur_n = -1;
+    // matching entries are gathered in batches of kB and their highway loads issued together,
+    // then accumulated in order (runs of one sample summed first, then scaled in)
+    constexpr int kB = 4;
+    int bn[kB], bs[kB];
+    int nb = 0;
+    auto flush = [&]() {
+      float4 h[kB][4];
+#pragma unroll
+      for (int q = 0; q < kB; ++q)
+        if (q < nb) {
+          const float* src = hw + ((int64_t)bn[q] * t + bs[q]) * dim + d0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (4 * k < w8) h[q][k] = __ldg(reinterpret_cast<const float4*>(src + 4 * k));
+        }
+#pragma unroll
+      for (int q = 0; q < kB; ++q)
+        if (q < nb) {
+          if (bn[q] != cur_n) {
+            if (cur_n >= 0) {
+              const float w = __ldg(scale + cur_n);
+#pragma unroll
+              for (int k = 0; k < 16; ++k)
+                if (k < w8) a[k] = __fadd_rn(a[k], __fmul_rn(w, gsum[k]));
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) gsum[k] = 0.f;
+            cur_n = bn[q];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (4 * k < w8) {
+              gsum[4 * k] = __fadd_rn(gsum[4 * k], h[q][k].x);
+              gsum[4 * k + 1] = __fadd_rn(gsum[4 * k + 1], h[q][k].y);
+              gsum[4 * k + 2] = __fadd_rn(gsum[4 * k + 2], h[q][k].z);
+              gsum[4 * k + 3] = __fadd_rn(gsum[4 * k + 3], h[q][k].w);
+            }
+        }
+      nb = 0;
+    };
     for (int e = 0; e < total; ++e) {
       if (ev[e] != r) continue;
-      const int n = en[e];
-      if (n != cur_n) {
-        if (cur_n >= 0) {
-          const float w = __ldg(scale + cur_n);
-#pragma unroll
-          for (int k = 0; k < 32; ++k)
-            if (k < w8) a[k] = __fadd_rn(a[k], __fmul_rn(w, gsum[k]));
-        }
-#pragma unroll
-        for (int k = 0; k < 32; ++k) gsum[k] = 0.f;
-        cur_n = n;
-      }
-      const float* src = hw + ((int64_t)n * t + es[e]) * dim + d0;
-#pragma unroll
-      for (int k = 0; k < 32; k += 4)
-        if (k < w8) {
-          const float4 h = __ldg(reinterpret_cast<const float4*>(src + k));
-          gsum[k] = __fadd_rn(gsum[k], h.x);
-          gsum[k + 1] = __fadd_rn(gsum[k + 1], h.y);
-          gsum[k + 2] = __fadd_rn(gsum[k + 2], h.z);
-          gsum[k + 3] = __fadd_rn(gsum[k + 3], h.w);
-        }
+      bn[nb] = en[e];
+      bs[nb] = es[e];
+      if (++nb == kB) flush();
     }
+    flush();
     if (cur_n >= 0) {
       const float w = __ldg(scale + cur_n);
 #pragma unroll
-      for (int k = 0; k < 32; ++k)
+      for (int k = 0; k < 16; ++k)
         if (k < w8) a[k] = __fadd_rn(a[k], __fmul_rn(w, gsum[k]));
     }
     if (v0 + r < vocab) {
       float* o = summed + (v0 + r) * dim + d0;
 #pragma unroll
-      for (int k = 0; k < 32; ++k)
+      for (int k = 0; k < 16; ++k)
         if (k < w8) o[k] = accumulate ? __fadd_rn(o[k], a[k]) : a[k];
     }
     return;
