@@ -411,7 +411,7 @@ __global__ void embed_chunk_starts_kernel(const int32_t* __restrict__ sorted_v, 
 // more entries than fit fall back to reading the indices from global memory.
 constexpr int kCsMaxEntries = 4096;
 
-__global__ void __launch_bounds__(256) clipped_sum_embedding_kernel(
+__global__ void __launch_bounds__(256, 3) clipped_sum_embedding_kernel(
     const int32_t* __restrict__ sorted_v, const int32_t* __restrict__ sorted_s,
     const int32_t* __restrict__ starts, const float* __restrict__ hw,
     const float* __restrict__ scale, int64_t b, int64_t t, int64_t vocab, int64_t dim,
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(256) clipped_sum_embedding_kernel(
     int cur_n = -1;
     // matching entries are gathered in batches of kB and their highway loads issued together,
     // then accumulated in order (runs of one sample summed first, then scaled in)
-    constexpr int kB = 4;
+    constexpr int kB = 2;
     int bn[kB], bs[kB];
     int nb = 0;
     auto flush = [&]() {

@@ -203,19 +203,18 @@ __global__ void __launch_bounds__(256) linear_fwd_narrow_kernel(const float* __r
 // Narrow outputs (r <= 64) with d % 4 == 0: one CTA per row, its 4 warps split the row's 16-byte
 // chunks; every lane keeps the r weight chunks of its column in flight (coalesced 128-bit loads),
 // per-row dot products are reduced warp (fixed shuffle tree) then across the 4 warps in order.
-constexpr int kRowWarps = 4;
 __device__ __forceinline__ void softmax_ce_warp(const float* row, int logits_relu, const float* __restrict__ targets,
                                                 int64_t n, int64_t k, float* __restrict__ loss,
                                                 float* __restrict__ grad, DeviceErr* err);
-template <int RMAX>
-__global__ void __launch_bounds__(32 * kRowWarps) linear_fwd_row_kernel(const float* __restrict__ x,
+template <int RMAX, int NW>  // NW warps per row: 8 for long rows (e.g. 32768 features), else 4
+__global__ void __launch_bounds__(32 * NW) linear_fwd_row_kernel(const float* __restrict__ x,
                                                                        int x_relu,
                                                                        const float* __restrict__ w,
                                                                        const float* __restrict__ bias,
                                                                        int64_t d, int r,
                                                                        float* __restrict__ y, LossFuse ce) {
   pdl_wait();
-  __shared__ float part[kRowWarps][RMAX];
+  __shared__ float part[NW][RMAX];
   __shared__ float logit[RMAX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = blockIdx.x;
@@ -224,7 +223,8 @@ __global__ void __launch_bounds__(32 * kRowWarps) linear_fwd_row_kernel(const fl
   for (int o = 0; o < RMAX; ++o) acc[o] = 0.f;
   const float4* xr = reinterpret_cast<const float4*>(x + row * d);
   const int64_t d4 = d >> 2;
-  for (int64_t c = (int64_t)warp * 32 + lane; c < d4; c += 32 * kRowWarps) {
+#pragma unroll 4
+  for (int64_t c = (int64_t)warp * 32 + lane; c < d4; c += 32 * NW) {
     float4 xv = __ldg(xr + c);
     xv = make_float4(relu_if(xv.x, x_relu), relu_if(xv.y, x_relu), relu_if(xv.z, x_relu), relu_if(xv.w, x_relu));
 #pragma unroll
@@ -246,10 +246,10 @@ __global__ void __launch_bounds__(32 * kRowWarps) linear_fwd_row_kernel(const fl
     }
   }
   __syncthreads();
-  for (int o = threadIdx.x; o < r; o += 32 * kRowWarps) {
+  for (int o = threadIdx.x; o < r; o += 32 * NW) {
     float t = part[0][o];
 #pragma unroll
-    for (int q = 1; q < kRowWarps; ++q) t += part[q][o];
+    for (int q = 1; q < NW; ++q) t += part[q][o];
     const float v = (bias ? __ldg(bias + o) : 0.f) + t;
     y[row * r + o] = v;
     logit[o] = v;
@@ -366,9 +366,11 @@ void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w,
   const bool aligned = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(w) & 15) == 0;
   if (aligned && r <= 64) {
-    if (r <= 16) ::dpg::launch_pdl(linear_fwd_row_kernel<16>, (unsigned)rows, 32 * kRowWarps, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
-    else if (r <= 32) ::dpg::launch_pdl(linear_fwd_row_kernel<32>, (unsigned)rows, 32 * kRowWarps, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
-    else ::dpg::launch_pdl(linear_fwd_row_kernel<64>, (unsigned)rows, 32 * kRowWarps, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
+    if (d >= 8192 && r <= 16)
+      ::dpg::launch_pdl(linear_fwd_row_kernel<16, 8>, (unsigned)rows, 256, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
+    else if (r <= 16) ::dpg::launch_pdl(linear_fwd_row_kernel<16, 4>, (unsigned)rows, 128, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
+    else if (r <= 32) ::dpg::launch_pdl(linear_fwd_row_kernel<32, 4>, (unsigned)rows, 128, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
+    else ::dpg::launch_pdl(linear_fwd_row_kernel<64, 4>, (unsigned)rows, 128, 0, ctx->stream, x, x_relu, w, bias, d, (int)r, y, ce);
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
@@ -413,10 +415,56 @@ __global__ void __launch_bounds__(256) linear_dgrad_kernel(const float* __restri
   dx[e] = acc;
 }
 
+// d % 4 == 0, r <= RMAX: blockIdx.y = row, each thread 4 consecutive j (128-bit loads of W and the
+// mask, one 128-bit store), the row's r highway values in registers
+template <int RMAX>
+__global__ void __launch_bounds__(256) linear_dgrad_vec_kernel(const float* __restrict__ dy,
+                                                               const float* __restrict__ w, int64_t d,
+                                                               int r, const float* __restrict__ mask,
+                                                               float* __restrict__ dx) {
+  pdl_wait();
+  const int64_t row = blockIdx.y;
+  const int64_t j = 4 * ((int64_t)blockIdx.x * 256 + threadIdx.x);
+  if (j >= d) return;
+  float dv[RMAX];
+#pragma unroll
+  for (int o = 0; o < RMAX; ++o) dv[o] = o < r ? __ldg(dy + row * r + o) : 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int o = 0; o < RMAX; ++o) {
+    if (o >= r) break;
+    const float4 wv = __ldg(reinterpret_cast<const float4*>(w + (int64_t)o * d + j));
+    acc.x = fmaf(dv[o], wv.x, acc.x);
+    acc.y = fmaf(dv[o], wv.y, acc.y);
+    acc.z = fmaf(dv[o], wv.z, acc.z);
+    acc.w = fmaf(dv[o], wv.w, acc.w);
+  }
+  if (mask) {
+    const float4 mv = __ldg(reinterpret_cast<const float4*>(mask + row * d + j));
+    if (!(mv.x > 0.f)) acc.x = 0.f;
+    if (!(mv.y > 0.f)) acc.y = 0.f;
+    if (!(mv.z > 0.f)) acc.z = 0.f;
+    if (!(mv.w > 0.f)) acc.w = 0.f;
+  }
+  *reinterpret_cast<float4*>(dx + row * d + j) = acc;
+}
+
 void launch_linear_dgrad(dpg_ctx* ctx, const float* dy, const float* w, int64_t rows, int64_t d,
                          int64_t r, const float* mask_src, float* dx) {
   const int64_t n = rows * d;
   if (n == 0) return;
+  const bool aligned = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(dx) & 15) == 0 &&
+                       (!mask_src || (reinterpret_cast<uintptr_t>(mask_src) & 15) == 0);
+  if (aligned && r <= 16 && rows < 65536) {
+    const dim3 grid((unsigned)((d / 4 + 255) / 256), (unsigned)rows);
+    if (r <= 4)
+      ::dpg::launch_pdl(linear_dgrad_vec_kernel<4>, grid, 256, 0, ctx->stream, dy, w, d, (int)r, mask_src, dx);
+    else
+      ::dpg::launch_pdl(linear_dgrad_vec_kernel<16>, grid, 256, 0, ctx->stream, dy, w, d, (int)r, mask_src, dx);
+    DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
   ::dpg::launch_pdl(linear_dgrad_kernel, (unsigned)((n + 255) / 256), 256, 0, ctx->stream, dy, w, rows, d, r, mask_src, dx);
   DPG_LAUNCH_CHECK(ctx);
 }
