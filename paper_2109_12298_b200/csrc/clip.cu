@@ -31,7 +31,17 @@ __global__ void __launch_bounds__(256) clip_factors_kernel(const double* __restr
     double sq = 0.0;
     int bad = -1;
     int r = 0;
-    for (; r + 8 <= rows; r += 8) {  // 8 independent loads in flight, summed in row order
+    for (; r + 32 <= rows; r += 32) {  // 32 independent loads in flight, summed in row order
+      double v[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) v[u] = slab[(int64_t)(r + u) * b + n];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        if (bad < 0 && !isfinite(v[u])) bad = row_param ? row_param[r + u] : 0;
+        sq += v[u];
+      }
+    }
+    for (; r + 8 <= rows; r += 8) {
       double v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = slab[(int64_t)(r + u) * b + n];
@@ -61,7 +71,7 @@ void launch_clip_factors(dpg_ctx* ctx, const double* slab, const int32_t* row_pa
                          int64_t b, double c, double* norms, float* scale, int64_t* num_clipped) {
   if (num_clipped) DPG_CUDA(cudaMemsetAsync(num_clipped, 0, sizeof(int64_t), ctx->stream));
   if (b == 0) return;
-  ::dpg::launch_pdl(clip_factors_kernel, (unsigned)((b + 127) / 128), 128, 0, ctx->stream, 
+  ::dpg::launch_pdl(clip_factors_kernel, (unsigned)((b + 63) / 64), 64, 0, ctx->stream, 
       slab, row_param, rows, b, c, norms, scale, reinterpret_cast<unsigned long long*>(num_clipped),
       ctx->dev_err);
   DPG_LAUNCH_CHECK(ctx);
