@@ -437,25 +437,43 @@ __global__ void __launch_bounds__(256, 3) clipped_sum_embedding_kernel(
   const int64_t v0 = (int64_t)c * kCsRows;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int64_t i = tid; i < kCsRows * dim; i += 256) acc[i] = 0.f;
-  // per-sample entry counts, then an exclusive scan (one thread; b <= a few thousand)
-  for (int64_t n = tid; n < b; n += 256)
-    cnt[n + 1] = starts[n * (nchunks + 1) + c + 1] - starts[n * (nchunks + 1) + c];
-  __syncthreads();
-  if (tid == 0) {
-    cnt[0] = 0;
-    for (int64_t n = 0; n < b; ++n) cnt[n + 1] += cnt[n];
-    total_sh = cnt[b];
+  // per-sample entry counts, then an exclusive scan: each thread sums a contiguous block of
+  // samples, the 256 block sums are scanned by warp shuffles, then each block is re-walked
+  __shared__ int wsum[8];
+  const int64_t per = (b + 255) / 256, nb0 = tid * per, nb1 = nb0 + per < b ? nb0 + per : b;
+  int mine = 0;
+  for (int64_t n = nb0; n < nb1; ++n) {
+    const int m = starts[n * (nchunks + 1) + c + 1] - starts[n * (nchunks + 1) + c];
+    cnt[n + 1] = m;
+    mine += m;
   }
+  int incl = mine;  // inclusive warp scan of the per-thread sums
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < warp; ++w) base += wsum[w];
+  int run = base + incl - mine;  // exclusive prefix of this thread's block
+  if (tid == 0) cnt[0] = 0;
+  for (int64_t n = nb0; n < nb1; ++n) {
+    run += cnt[n + 1];
+    cnt[n + 1] = run;
+  }
+  if (tid == 255) total_sh = run;
   __syncthreads();
   const int total = total_sh;
   const bool staged = total <= kCsMaxEntries;
   if (staged) {
-    for (int64_t n = warp; n < b; n += 8) {  // a warp per sample: copy its entries
-      const int j0 = starts[n * (nchunks + 1) + c], m = cnt[n + 1] - cnt[n];
-      for (int q = lane; q < m; q += 32) {
-        ev[cnt[n] + q] = sorted_v[n * t + j0 + q] - (int)v0;
-        es[cnt[n] + q] = sorted_s[n * t + j0 + q];
-        en[cnt[n] + q] = (int)n;
+    for (int64_t n = tid; n < b; n += 256) {  // a thread per sample: copy its (few) entries
+      const int j0 = starts[n * (nchunks + 1) + c], e0 = cnt[n], m = cnt[n + 1] - e0;
+      for (int q = 0; q < m; ++q) {
+        ev[e0 + q] = sorted_v[n * t + j0 + q] - (int)v0;
+        es[e0 + q] = sorted_s[n * t + j0 + q];
+        en[e0 + q] = (int)n;
       }
     }
   }
