@@ -21,7 +21,10 @@ std::string& thread_err() {
   return s;
 }
 
-void sync_ctx(dpg_ctx* ctx) { DPG_CUDA(cudaStreamSynchronize(ctx->stream)); }
+void sync_ctx(dpg_ctx* ctx) {
+  DPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (cudaStream_t s : ctx->extra_streams) DPG_CUDA(cudaStreamSynchronize(s));  // e.g. host read-backs
+}
 
 static std::string fmt_value(uint64_t bits) {
   float f;

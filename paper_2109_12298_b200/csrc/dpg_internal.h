@@ -72,6 +72,9 @@ struct dpg_ctx {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   bool capturing = false;
+  // streams owned by models of this context whose work a dpg_ctx_sync must also cover (the
+  // pipelined host path's copy stream: loss read-backs)
+  std::vector<cudaStream_t> extra_streams;
 
   // scratch space for operator-ABI calls (grows outside capture only)
   void* workspace(size_t bytes);

@@ -121,8 +121,11 @@ struct dpg_model {
   float* xs[2] = {nullptr, nullptr};
   float* ys[2] = {nullptr, nullptr};
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t read_stream = nullptr;  // loss read-backs (a separate queue: H2D never waits on them)
   cudaEvent_t copied[2] = {nullptr, nullptr};   // slot's H2D done
   cudaEvent_t consumed[2] = {nullptr, nullptr}; // step that read the slot done
+  float* losses[2] = {nullptr, nullptr};         // per-slot loss buffers: their D2H runs on the copy stream
+  cudaEvent_t loss_read[2] = {nullptr, nullptr}; // that D2H done (the slot's next step may overwrite)
   int64_t async_calls = 0;
 };
 
@@ -807,7 +810,7 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     total += al(ws);
     for (size_t cs : csum_bytes) total += al(cs);
     total += 3 * (al(sizeof(float) * max_batch * m->in_numel) + al(sizeof(float) * max_batch));
-    total += al(sizeof(float) * max_batch);
+    total += 3 * al(sizeof(float) * max_batch);
     for (auto& lp : m->layers)
       if (lp.stat_blocks) total += al(sizeof(float) * max_batch * lp.in_numel) + al(sizeof(float) * max_batch * lp.stat_blocks);
     DPG_CUDA(cudaMalloc(&m->arena, total));
@@ -837,6 +840,7 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
       m->ys[q] = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
     }
     m->loss = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
+    for (auto& lb : m->losses) lb = reinterpret_cast<float*>(take(sizeof(float) * max_batch));
     for (auto& lp : m->layers)
       if (lp.stat_blocks) {
         lp.xhat = reinterpret_cast<float*>(take(sizeof(float) * max_batch * lp.in_numel));
@@ -862,7 +866,11 @@ void dpg_model_destroy(dpg_model* m) {
   cudaStreamSynchronize(m->ctx->stream);
   if (m->copy_stream) {
     cudaStreamSynchronize(m->copy_stream);
+    cudaStreamSynchronize(m->read_stream);
+    auto& xs = m->ctx->extra_streams;
+    xs.erase(std::remove(xs.begin(), xs.end(), m->read_stream), xs.end());
     cudaStreamDestroy(m->copy_stream);
+    cudaStreamDestroy(m->read_stream);
   }
   for (auto& st : m->aux)
     if (st) {
@@ -872,6 +880,7 @@ void dpg_model_destroy(dpg_model* m) {
   for (auto& e : m->evs)
     if (e) cudaEventDestroy(e);
   for (int q = 0; q < 2; ++q) {
+    if (m->loss_read[q]) cudaEventDestroy(m->loss_read[q]);
     if (m->copied[q]) cudaEventDestroy(m->copied[q]);
     if (m->consumed[q]) cudaEventDestroy(m->consumed[q]);
   }
@@ -1223,13 +1232,19 @@ dpg_status dpg_train_step_host_async(dpg_optimizer* o, const float* x_host, cons
     if (!x_host || !targets_host) raise(DPG_ERR_PARAMETER, "input and targets must not be NULL");
     if (!m->copy_stream) {
       DPG_CUDA(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+      DPG_CUDA(cudaStreamCreateWithFlags(&m->read_stream, cudaStreamNonBlocking));
+      ctx->extra_streams.push_back(m->read_stream);
       for (int q = 0; q < 2; ++q) {
         DPG_CUDA(cudaEventCreateWithFlags(&m->copied[q], cudaEventDisableTiming));
         DPG_CUDA(cudaEventCreateWithFlags(&m->consumed[q], cudaEventDisableTiming));
+        DPG_CUDA(cudaEventCreateWithFlags(&m->loss_read[q], cudaEventDisableTiming));
       }
     }
     slot = (int)(m->async_calls & 1);
-    if (m->async_calls >= 2) DPG_CUDA(cudaStreamWaitEvent(m->copy_stream, m->consumed[slot], 0));
+    if (m->async_calls >= 2) {
+      DPG_CUDA(cudaStreamWaitEvent(m->copy_stream, m->consumed[slot], 0));
+      DPG_CUDA(cudaStreamWaitEvent(ctx->stream, m->loss_read[slot], 0));  // slot's loss copied out
+    }
     DPG_CUDA(cudaMemcpyAsync(m->xs[slot], x_host, sizeof(float) * b * m->in_numel, cudaMemcpyHostToDevice, m->copy_stream));
     DPG_CUDA(cudaMemcpyAsync(m->ys[slot], targets_host, sizeof(float) * b, cudaMemcpyHostToDevice, m->copy_stream));
     DPG_CUDA(cudaEventRecord(m->copied[slot], m->copy_stream));
@@ -1237,12 +1252,16 @@ dpg_status dpg_train_step_host_async(dpg_optimizer* o, const float* x_host, cons
     ++m->async_calls;
   });
   if (st != DPG_OK) return st;
-  const dpg_status st2 = dpg_train_step(o, m->xs[slot], m->ys[slot], b, m->loss, 1);
+  const dpg_status st2 = dpg_train_step(o, m->xs[slot], m->ys[slot], b, m->losses[slot], 1);
   if (st2 != DPG_OK) return st2;
   return guard(ctx, [&] {
     DPG_CUDA(cudaEventRecord(m->consumed[slot], ctx->stream));
+    // the loss read-back rides on the copy stream, off the compute stream's step-to-step path
+    DPG_CUDA(cudaStreamWaitEvent(m->read_stream, m->consumed[slot], 0));
     if (loss_host)
-      DPG_CUDA(cudaMemcpyAsync(loss_host, m->loss, sizeof(float) * b, cudaMemcpyDeviceToHost, ctx->stream));
+      DPG_CUDA(cudaMemcpyAsync(loss_host, m->losses[slot], sizeof(float) * b, cudaMemcpyDeviceToHost,
+                               m->read_stream));
+    DPG_CUDA(cudaEventRecord(m->loss_read[slot], m->read_stream));
   });
 }
 
