@@ -669,9 +669,45 @@ __global__ void weighted_sum_kernel(const float* __restrict__ g, const float* __
   summed[j] = accumulate ? __fadd_rn(summed[j], acc) : acc;
 }
 
+// Narrow parameters (a few thousand columns): the record is staged through shared memory in
+// 64-sample chunks loaded by the whole CTA (every load in flight at once), then each thread
+// sums its column over the chunk in sample order — same order and roundings as above.
+constexpr int kWsCols = 128, kWsChunk = 64;
+__global__ void __launch_bounds__(256) weighted_sum_narrow_kernel(const float* __restrict__ g,
+                                                                  const float* __restrict__ scale, int64_t b,
+                                                                  int64_t numel, float* __restrict__ summed,
+                                                                  int accumulate) {
+  pdl_wait();
+  __shared__ float tile[kWsChunk][kWsCols];
+  __shared__ float sc[kWsChunk];
+  const int64_t j0 = (int64_t)blockIdx.x * kWsCols;
+  const int tid = threadIdx.x;
+  float acc = 0.f;
+  for (int64_t n0 = 0; n0 < b; n0 += kWsChunk) {
+    const int nn = (int)(b - n0 < kWsChunk ? b - n0 : kWsChunk);
+    for (int i = tid; i < kWsChunk * kWsCols; i += 256) {
+      const int q = i / kWsCols, c = i - q * kWsCols;
+      tile[q][c] = (q < nn && j0 + c < numel) ? __ldg(g + (n0 + q) * numel + j0 + c) : 0.f;
+    }
+    if (tid < kWsChunk) sc[tid] = tid < nn ? __ldg(scale + n0 + tid) : 0.f;
+    __syncthreads();
+    if (tid < kWsCols)
+      for (int q = 0; q < nn; ++q) acc = __fadd_rn(acc, __fmul_rn(sc[q], tile[q][tid]));
+    __syncthreads();
+  }
+  const int64_t j = j0 + tid;
+  if (tid < kWsCols && j < numel) summed[j] = accumulate ? __fadd_rn(summed[j], acc) : acc;
+}
+
 void launch_weighted_sum_materialised(dpg_ctx* ctx, const float* g, const float* scale, int64_t b,
                                       int64_t numel, float* summed, int accumulate) {
   if (numel == 0) return;
+  if (numel <= 8192) {
+    ::dpg::launch_pdl(weighted_sum_narrow_kernel, (unsigned)((numel + kWsCols - 1) / kWsCols), 256, 0, ctx->stream,
+                      g, scale, b, numel, summed, accumulate);
+    DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
   ::dpg::launch_pdl(weighted_sum_kernel, (unsigned)((numel + 255) / 256), 256, 0, ctx->stream, g, scale, b, numel, summed, accumulate);
   DPG_LAUNCH_CHECK(ctx);
 }

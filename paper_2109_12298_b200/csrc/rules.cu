@@ -273,7 +273,15 @@ __global__ void __launch_bounds__(256) gs_bias_kernel(const float* __restrict__ 
     for (int64_t o = threadIdx.x; o < r; o += 256) {
       double acc = 0.0;
       const float* col = hw + n * mid * r + o;
-      for (int64_t m = 0; m < mid; ++m) acc += (double)__ldg(col + m * r);
+      int64_t m = 0;
+      for (; m + 16 <= mid; m += 16) {  // 16 loads in flight, summed in order
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = __ldg(col + (m + u) * r);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc += (double)v[u];
+      }
+      for (; m < mid; ++m) acc += (double)__ldg(col + m * r);
       const float v = (float)acc;
       if (gb) gb[n * r + o] = v;
       sq += (double)v * v;
