@@ -37,7 +37,7 @@ struct Params {
 
 template <int PT>
 __global__ void __launch_bounds__(kThreads, 4) gs_rows_kernel(const Params p) {
-  pdl_wait();
+  
   extern __shared__ __align__(16) float sm[];
   float* xt = sm;                                          // [PT][Kc4], rows >= P are zero
   const int ostr = (p.opart + 3) & ~3;                     // row stride of the transposed tile
@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(kThreads, 4) gs_rows_kernel(const Params p) {
     }
     kt[k] = e;
   }
+  pdl_wait();  // the tap table above is geometry only
   // highway rows of this part: contiguous [nrow][P] in B[n]
   const float* hrow = p.hw + ((int64_t)n * p.oc + o_begin) * p.P;
   for (int i = tid; i < ostr * PT; i += kThreads) {

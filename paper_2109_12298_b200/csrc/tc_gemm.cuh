@@ -322,11 +322,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Pro
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  pdl_wait();  // TMEM allocation and barrier init above overlap the previous kernel's tail
-  p.setup(z, m0, n0, scratch, tid);
+  p.setup(z, m0, n0, scratch, tid);  // index tables: geometry only, no upstream data
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // TMEM allocation, barrier init and the tables above overlap the previous kernel's tail
   const uint32_t tmem = *tmem_slot;
 
   const int nk_all = (int)((Kz + BK - 1) / BK);
