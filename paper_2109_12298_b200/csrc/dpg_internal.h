@@ -197,7 +197,7 @@ void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* 
           const ConvGeom& g, float* part, int splits);
 }  // namespace ds
 
-namespace tk {  // thin-K conv layers (ic*kh*kw <= 32) on CUDA cores: rule (+ bias rule), clipped sum
+namespace tk {  // thin-K conv layers (ic*kh*kw <= 64) on CUDA cores: rule (+ bias rule), clipped sum
 bool supported(const ConvGeom& g);
 void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
         double* sq_part, float* gb, double* sq_b);

@@ -1,4 +1,4 @@
-// tk_conv.cu — "thin-K" conv layers (ic * kh * kw <= 32, e.g. an RGB input layer) on CUDA cores.
+// tk_conv.cu — "thin-K" conv layers (ic * kh * kw <= 64, e.g. an RGB or greyscale input layer) on CUDA cores.
 //
 //   per-sample   G[n][oc][k]   = sum_p B[n, oc, p] X~[n, k, p]  + ||G_n||^2     (grad_sample.hpp:135-150)
 //                gb[n][oc]     = (float) sum_p (double) B[n, oc, p] + ||gb_n||^2 (sum_middle, tensor.hpp:197-205)
@@ -24,7 +24,7 @@ namespace dpg {
 namespace tk {
 
 constexpr int kThreads = 256;
-constexpr int kMaxK = 32;
+constexpr int kMaxK = 64;
 constexpr int kMaxOc = 64;
 
 struct Geo {
