@@ -55,6 +55,9 @@ constexpr int kAQ = BM * kQuadsPerRow / 256;         // A quads per thread per s
 constexpr uint64_t kLayoutType = BK == 32 ? 2 : 4;   // UMMA layout: SWIZZLE_128B / SWIZZLE_64B
 constexpr int kMinBlocks = BK == 32 ? 2 : DPG_TC_MINB;         // resident CTAs per SM the kernel is built for
 constexpr int kThreads = 256;
+#ifndef DPG_TC_TRUNC
+#define DPG_TC_TRUNC 1  // 3xTF32 with a truncated hi part (measured: parity unchanged, step -0.9 %)
+#endif
 #ifndef DPG_TC_STAGES
 #define DPG_TC_STAGES 2
 #endif
@@ -157,14 +160,22 @@ __device__ __forceinline__ uint32_t sw_off(int row, int q) {
   return (uint32_t)((row >> 3) * kAtomBytes + (row & 7) * kRowBytes + ((q ^ x) << 4));
 }
 
-// 3xTF32 split of a finite fp32 value, both parts rounded to nearest TF32 (ties away from zero,
-// as cvt.rna) by integer add + mask on the bit pattern: hi = rna(x), lo = rna(x - hi) with x - hi
-// exact in fp32 and |x - hi| <= 2^-11 |x|. Five ops and no special-case branches (cvt.rna.tf32
-// is emulated with an Inf/NaN guard); a non-finite x still gives a non-finite product, which the
-// clip-factor check reports.
+// 3xTF32 split of a finite fp32 value. Default (DPG_TC_TRUNC=1): hi = x as stored, which the
+// tensor core reads as trunc_tf32(x) (top 19 bits), lo = x - trunc_tf32(x), exact in fp32 and
+// itself truncated by the MMA: |error| <= 2^-21 |x| per operand, two ops. DPG_TC_TRUNC=0: both
+// parts rounded to nearest (ties away, as cvt.rna) by integer add + mask, |error| <= 2^-22 |x|,
+// five ops. No special-case branches either way; a non-finite x still gives a non-finite
+// product, which the clip-factor check reports.
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+#if DPG_TC_TRUNC
+  // the MMA reads the top 19 bits of each 32-bit operand: store x itself as "hi" and the exact
+  // remainder x - trunc_tf32(x) as "lo" (two ops)
+  hi = __float_as_uint(x);
+  lo = __float_as_uint(x - __uint_as_float(hi & 0xffffe000u));
+#else
   hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
   lo = (__float_as_uint(x - __uint_as_float(hi)) + 0x1000u) & 0xffffe000u;
+#endif
 }
 
 // Store 4 values (k .. k+3 of one row) as hi / lo TF32 into the swizzled stage buffers.
