@@ -57,13 +57,18 @@ def parse():
     ap.add_argument("--csum-from-record", action="store_true",
                     help="clipped sums as the reference's pass 2 over the stored record (not the headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: clipped-sum exchange over peer memory inside the update kernel "
+                         "(dpg_optimizer_set_peers) or one NCCL all-reduce")
     ap.add_argument("--profile-steps", type=int, default=5)
     return ap.parse_args()
 
 
 def dist_env():
-    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
-            int(os.environ.get("LOCAL_RANK", "0")))
+    # DPG_BENCH_DEVICE pins every rank to one device: a protocol check of the N > 1 path on a
+    # one-GPU box (the peer exchange works between processes sharing a GPU); not a measurement
+    local = int(os.environ.get("DPG_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), local
 
 
 def peaks():
@@ -572,7 +577,7 @@ def main():
 
     torch.cuda.set_device(local)
     ctx = dpg.Context(local)
-    if world > 1:
+    if world > 1 and args.exchange == "nccl":
         import torch.distributed as dist
         obj = [dpg.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -590,6 +595,10 @@ def main():
                           learning_rate=0.1, expected_batch_size=float(gb), noise_seed=3,
                           materialise_grad_sample=materialise,
                           clipped_sum_from_record=args.csum_from_record and materialise)
+    if world > 1 and args.exchange == "p2p":
+        handles = [None] * world
+        torch.distributed.all_gather_object(handles, opt.peer_handle())
+        opt.set_peers(rank, handles)
     xt = torch.from_numpy(x).cuda()
     yt = torch.from_numpy(y).cuda()
     loss = torch.zeros(b, device="cuda")
@@ -611,10 +620,18 @@ def main():
     for _ in range(max(3, args.warmup)):
         opt.train_step(xt, yt, loss)
     ctx.sync()
-    t_soak = time.perf_counter() + 0.5  # bring SM clocks up before the timed region
-    while time.perf_counter() < t_soak:
-        opt.train_step(xt, yt, loss)
+    # bring SM clocks up before the timed region; rank 0's clock decides when to stop, so every
+    # rank runs the same number of steps (each step's exchange pairs across ranks)
+    t_soak = time.perf_counter() + 0.5
+    while True:
+        for _ in range(10):
+            opt.train_step(xt, yt, loss)
         torch.cuda.synchronize()
+        done = torch.tensor([int(time.perf_counter() >= t_soak)])
+        if world > 1:
+            torch.distributed.broadcast(done, src=0)
+        if done.item():
+            break
     barrier()
     torch.cuda.synchronize()
 
@@ -701,7 +718,9 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": w.name, "global_batch": gb, "per_rank_batch": b,
-                   "parallelism": f"dp{world} (sample shards, 1 NCCL all-reduce of the clipped sum)",
+                   "parallelism": f"dp{world} (sample shards, " + (
+                       "clipped sums summed over peer memory inside the update kernel)" if args.exchange == "p2p"
+                       else "1 NCCL all-reduce of the clipped sum)"),
                    "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
                    "materialise_grad_sample": materialise, "graph": True,
                    "clipped_sum": "record pass 2" if (args.csum_from_record and materialise) else "(s.B)^T A",

@@ -262,6 +262,21 @@ DPG_API dpg_status dpg_optimizer_create(dpg_model* model, const dpg_optimizer_co
                                         dpg_optimizer** out);
 DPG_API void dpg_optimizer_destroy(dpg_optimizer* opt);
 
+/* The clipped-sum exchange over peer memory instead of NCCL: every
+ * rank maps the other ranks' optimizer state (CUDA IPC; NVLink P2P between GPUs) and step()
+ * sums the W clipped sums straight from peer memory inside the noise + update kernel, in rank
+ * order (identical on every rank), with device-side flags ordering the ranks — no all-reduce
+ * launch, no host synchronisation. After step(), the summed buffer holds the all-rank sum, as
+ * with dpg_allreduce_sum. Replaces ncclAllReduce (the reference's W = 1 analogue is the
+ * virtual-step fold, optimizer.hpp:240-254).
+ *   dpg_optimizer_peer_handle  writes this rank's DPG_PEER_HANDLE_BYTES-byte handle;
+ *   dpg_optimizer_set_peers    takes all W handles (rank order, this rank's included); W = 1
+ *                              turns the exchange off. Every rank must then call step() the
+ *                              same number of times (a rank waits for its peers' clipped sums). */
+#define DPG_PEER_HANDLE_BYTES 128
+DPG_API dpg_status dpg_optimizer_peer_handle(dpg_optimizer* opt, void* handle);
+DPG_API dpg_status dpg_optimizer_set_peers(dpg_optimizer* opt, int rank, int world, const void* handles);
+
 /* GradSampleModule::forward_backward (optimizer.hpp:369-372) -> compute_grad_samples
  * (grad_sample.hpp:328-343) followed by DpOptimizer::set_grad_sample (optimizer.hpp:147-161):
  * one forward, softmax cross-entropy (layers.hpp:894-919), one backward walk with the device

@@ -288,6 +288,18 @@ void launch_noise_update(dpg_ctx* ctx, float* params, const float* summed, float
                          uint64_t step, const float* injected, const uint64_t* step_ptr);
 void launch_gaussian(dpg_ctx* ctx, float* out, int64_t n, double std_dev, uint64_t seed,
                      uint64_t step);
+// the clipped-sum exchange over peer memory (noise.cu): rank r's optimizer arena mapped by every
+// rank; flags[r] points at rank r's three 128-byte flag lines (signal, ack, local CTA counter)
+constexpr int kMaxPeers = 8;
+struct PeerSet {
+  static constexpr int kSig = 0, kAck = 16, kCount = 32;  // in u64 units (128-byte lines)
+  int world = 0, rank = 0;
+  const float* summed[kMaxPeers] = {};
+  unsigned long long* flags[kMaxPeers] = {};
+};
+void launch_noise_update_p2p(dpg_ctx* ctx, const PeerSet& ps, float* params, float* summed, float* reduced,
+                             float* grad, int64_t n, double sigma, double c, double expected_batch, double lr,
+                             uint64_t seed, uint64_t step, const float* injected, const uint64_t* step_ptr);
 
 // layers.cu — supporting forward / backward
 // ws: split-K scratch of at least conv_fwd_ws_bytes / conv_dgrad_ws_bytes (nullable: no split)

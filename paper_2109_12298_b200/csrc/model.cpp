@@ -143,6 +143,11 @@ struct dpg_optimizer {
   float* scale = nullptr;
   int64_t* num_clipped = nullptr;
   uint64_t* step_dev = nullptr;
+  // clipped-sum exchange over peer memory (dpg_optimizer_set_peers): world = 0 when unused
+  dpg::PeerSet peers;
+  float* reduced = nullptr;               // [L] the rank-order sum, copied into summed at the end
+  unsigned long long* xflags = nullptr;   // this rank's flag lines (PeerSet::flags[rank])
+  std::vector<void*> peer_maps;           // IPC mappings of the peers' arenas
   // GradientState (optimizer.hpp:47-57)
   bool has_grad_sample = false, consumed = false, has_summed = false, has_grad = false;
   int64_t accumulated = 0;
@@ -558,6 +563,16 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
 void finish_impl(dpg_optimizer* o, bool graph_mode) {
   dpg_model* m = o->m;
   dpg_ctx* ctx = m->ctx;
+  if (o->peers.world > 1) {
+    dpg::ProfScope ps(ctx, "noise_update", 16.0 * m->L + 4.0 * o->peers.world * m->L, 0.0);
+    dpg::launch_noise_update_p2p(ctx, o->peers, m->p_params, o->summed, o->reduced, o->grad, m->L,
+                                 o->cfg.noise_multiplier, o->cfg.max_grad_norm, o->cfg.expected_batch_size,
+                                 o->cfg.learning_rate, o->cfg.noise_seed, o->steps, o->injected,
+                                 graph_mode ? o->step_dev : nullptr);
+    if (!graph_mode) ++o->steps;
+    o->has_grad = true;
+    return;
+  }
   if (ctx->comm) {
     dpg::ProfScope ps(ctx, "allreduce", 8.0 * m->L, 0.0);
     DPG_NCCL(ncclAllReduce(o->summed, o->summed, (size_t)m->L, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
@@ -944,7 +959,8 @@ dpg_status dpg_optimizer_create(dpg_model* m, const dpg_optimizer_config* cfg, d
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t rec = cfg->materialise_grad_sample ? sizeof(float) * (size_t)(B * L) : sizeof(float) * (size_t)(B * bias_numel);
     size_t total = 2 * al(sizeof(float) * L) + al(rec) + al(sizeof(double) * m->sq_rows * B) +
-                   al(sizeof(double) * B) + al(sizeof(float) * B) + al(sizeof(int64_t)) + al(sizeof(uint64_t));
+                   al(sizeof(double) * B) + al(sizeof(float) * B) + al(sizeof(int64_t)) + al(sizeof(uint64_t)) +
+                   al(sizeof(float) * L) + al(3 * 128);
     DPG_CUDA(cudaMalloc(&o->arena, total));
     DPG_CUDA(cudaMemset(o->arena, 0, total));
     char* p = o->arena;
@@ -962,6 +978,8 @@ dpg_status dpg_optimizer_create(dpg_model* m, const dpg_optimizer_config* cfg, d
     o->scale = reinterpret_cast<float*>(take(sizeof(float) * B));
     o->num_clipped = reinterpret_cast<int64_t*>(take(sizeof(int64_t)));
     o->step_dev = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t)));
+    o->reduced = reinterpret_cast<float*>(take(sizeof(float) * L));
+    o->xflags = reinterpret_cast<unsigned long long*>(take(3 * 128));
   });
   if (st != DPG_OK) {
     if (o->arena) cudaFree(o->arena);
@@ -980,8 +998,74 @@ void dpg_optimizer_destroy(dpg_optimizer* o) {
   for (auto e : o->ring_ev)
     if (e) cudaEventDestroy(e);
   if (o->step_ring) cudaFreeHost(o->step_ring);
+  for (void* p : o->peer_maps) cudaIpcCloseMemHandle(p);
   if (o->arena) cudaFree(o->arena);
   delete o;
+}
+
+namespace {
+struct PeerHandle {
+  cudaIpcMemHandle_t arena;
+  int64_t summed_off, flags_off, L;
+};
+static_assert(sizeof(PeerHandle) <= DPG_PEER_HANDLE_BYTES, "peer handle");
+}  // namespace
+
+dpg_status dpg_optimizer_peer_handle(dpg_optimizer* o, void* handle) {
+  if (!o || !handle) return DPG_ERR_PARAMETER;
+  return guard(o->m->ctx, [&] {
+    DPG_CUDA(cudaSetDevice(o->m->ctx->device));
+    PeerHandle h{};
+    DPG_CUDA(cudaIpcGetMemHandle(&h.arena, o->arena));
+    h.summed_off = reinterpret_cast<char*>(o->summed) - o->arena;
+    h.flags_off = reinterpret_cast<char*>(o->xflags) - o->arena;
+    h.L = o->m->L;
+    std::memset(handle, 0, DPG_PEER_HANDLE_BYTES);
+    std::memcpy(handle, &h, sizeof(h));
+  });
+}
+
+dpg_status dpg_optimizer_set_peers(dpg_optimizer* o, int rank, int world, const void* handles) {
+  if (!o) return DPG_ERR_PARAMETER;
+  return guard(o->m->ctx, [&] {
+    DPG_CUDA(cudaSetDevice(o->m->ctx->device));
+    if (world < 1 || world > dpg::kMaxPeers || rank < 0 || rank >= world)
+      raise(DPG_ERR_PARAMETER, "peer exchange: need 0 <= rank < world <= " + std::to_string(dpg::kMaxPeers));
+    if (world > 1 && !handles) raise(DPG_ERR_PARAMETER, "peer exchange: handles must not be NULL");
+    DPG_CUDA(cudaStreamSynchronize(o->m->ctx->stream));
+    dpg::PeerSet ps;
+    std::vector<void*> maps;
+    if (world > 1) {
+      ps.world = world;
+      ps.rank = rank;
+      for (int r = 0; r < world; ++r) {
+        PeerHandle h;
+        std::memcpy(&h, static_cast<const char*>(handles) + (size_t)r * DPG_PEER_HANDLE_BYTES, sizeof(h));
+        if (h.L != o->m->L) raise(DPG_ERR_DIMENSION, "peer exchange: rank " + std::to_string(r) + " has " +
+                                                         std::to_string(h.L) + " parameters, this rank " +
+                                                         std::to_string(o->m->L));
+        char* base = o->arena;
+        if (r != rank) {
+          void* p = nullptr;
+          const cudaError_t e = cudaIpcOpenMemHandle(&p, h.arena, cudaIpcMemLazyEnablePeerAccess);
+          if (e != cudaSuccess) {
+            for (void* q : maps) cudaIpcCloseMemHandle(q);
+            raise(DPG_ERR_CUDA, std::string("peer exchange: cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+          }
+          maps.push_back(p);
+          base = static_cast<char*>(p);
+        }
+        ps.summed[r] = reinterpret_cast<const float*>(base + h.summed_off);
+        ps.flags[r] = reinterpret_cast<unsigned long long*>(base + h.flags_off);
+      }
+    }
+    for (void* p : o->peer_maps) cudaIpcCloseMemHandle(p);
+    o->peer_maps = maps;
+    o->peers = ps;
+    // captured steps bake the exchange in or out
+    for (auto& g : o->graphs) cudaGraphExecDestroy(g.exec);
+    o->graphs.clear();
+  });
 }
 
 dpg_status dpg_forward_backward(dpg_optimizer* o, const float* x, const float* targets, int64_t b,

@@ -71,10 +71,19 @@ __device__ __forceinline__ void build_ktab(const Geo& g, KEnt* t, int tid, int K
   }
 }
 __device__ __forceinline__ void build_ptab(const Geo& g, PEnt* t, int tid) {
-  for (int p = tid; p < g.P; p += kThreads) {
+  for (int p = tid; p < ((g.P + 3) & ~3); p += kThreads) {
     const int oy = p / g.ow, ox = p - oy * g.ow;
-    t[p] = PEnt{(short)(oy * g.stride - g.pad), (short)(ox * g.stride - g.pad)};
+    // the padding up to a multiple of 4 holds sentinels, so a quad is one 16-byte load
+    t[p] = p < g.P ? PEnt{(short)(oy * g.stride - g.pad), (short)(ox * g.stride - g.pad)}
+                   : PEnt{(short)kBad, (short)kBad};
   }
+}
+__device__ __forceinline__ void ptab_quad(const PEnt* pt, int p, PEnt (&t)[4]) {
+  const int4 q = *reinterpret_cast<const int4*>(pt + p);
+  t[0] = *reinterpret_cast<const PEnt*>(&q.x);
+  t[1] = *reinterpret_cast<const PEnt*>(&q.y);
+  t[2] = *reinterpret_cast<const PEnt*>(&q.z);
+  t[3] = *reinterpret_cast<const PEnt*>(&q.w);
 }
 
 // The gathers use 32-bit element offsets: every tensor a contraction reads must have < 2^31
@@ -436,11 +445,13 @@ struct ConvGs {
     const Row r = reinterpret_cast<const Row*>(s + ((4 * Ki + 15) & ~15))[row];
     const int base = z * (g.ic * g.h * g.w) + r.plane;  // < 2^31 (launch check)
     float v[4];
+    if (k >= Ki) return make_float4(0.f, 0.f, 0.f, 0.f);
+    PEnt t[4];
+    ptab_quad(pt, k, t);  // k % 4 == 0; entries in [Ki, Ki rounded up to 4) are sentinels
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const PEnt t = pt[min(k + e, Ki - 1)];
-      const int iy = t.y + r.ki, ix = t.x + r.kj;
-      const bool ok = k + e < Ki && (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
+      const int iy = t[e].y + r.ki, ix = t[e].x + r.kj;
+      const bool ok = (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
       v[e] = ldg_or_zero(x + (base + iy * g.w + ix), ok);
     }
     return make_float4(v[0], v[1], v[2], v[3]);
@@ -527,9 +538,11 @@ struct ConvCsum {
       const int n = z * (int)spl + (int)qq;
       const float* xb = x + (n * chw + r.plane);
       const bool in = k < Ki && n < n_end;
+      PEnt t4[4];
+      ptab_quad(pt, (int)pp, t4);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const PEnt t = pt[pp + e];
+        const PEnt t = t4[e];
         const int iy = t.y + r.ki, ix = t.x + r.kj;
         const bool ok = in && (unsigned)iy < (unsigned)g.h && (unsigned)ix < (unsigned)g.w;
         v[e] = ldg_or_zero(xb + (iy * g.w + ix), ok);

@@ -116,6 +116,8 @@ _SIGS = {
     "dpg_model_store_params": (_I32, [_P, _P]),
     "dpg_model_output_width": (_I64, [_P]),
     "dpg_optimizer_create": (_I32, [_P, _P, ctypes.POINTER(_P)]),
+    "dpg_optimizer_peer_handle": (_I32, [_P, _P]),
+    "dpg_optimizer_set_peers": (_I32, [_P, ctypes.c_int, ctypes.c_int, _P]),
     "dpg_optimizer_destroy": (None, [_P]),
     "dpg_forward_backward": (_I32, [_P, _P, _P, _I64, _P]),
     "dpg_virtual_step": (_I32, [_P]),
@@ -475,6 +477,21 @@ class DpOptimizer:
         self._b = x.shape[0]
         self._x, self._y = x, targets  # keep alive until the fold
         _check(lib().dpg_forward_backward(self.h, _p(x), _p(targets), x.shape[0], _p(loss)), self.ctx.h)
+
+    PEER_HANDLE_BYTES = 128  # DPG_PEER_HANDLE_BYTES
+
+    def peer_handle(self) -> bytes:
+        """This rank's handle for the peer-memory clipped-sum exchange (dpg_optimizer_peer_handle)."""
+        buf = ctypes.create_string_buffer(self.PEER_HANDLE_BYTES)
+        _check(lib().dpg_optimizer_peer_handle(self.h, ctypes.cast(buf, _P)), self.ctx.h)
+        return buf.raw
+
+    def set_peers(self, rank: int, handles) -> None:
+        """Sum the clipped sums of all ranks over peer memory inside step() (instead of NCCL).
+        `handles`: every rank's peer_handle() in rank order; a single handle turns it off."""
+        blob = b"".join(handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        _check(lib().dpg_optimizer_set_peers(self.h, rank, len(handles), ctypes.cast(buf, _P)), self.ctx.h)
 
     def virtual_step(self):
         _check(lib().dpg_virtual_step(self.h), self.ctx.h)

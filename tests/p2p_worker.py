@@ -1,0 +1,72 @@
+"""One rank of the peer-memory exchange test (test_gpu_p2p.py); run as a subprocess.
+
+usage: python p2p_worker.py RANK WORLD PORT OUT_NPZ
+Every rank takes its contiguous slice of each step's batch (SURVEY.md §8e partitioning), swaps
+peer handles over a gloo group, and runs STEPS train steps (the first eager, the rest CUDA-graph
+replays) with the exchange inside step(). Writes its final parameters and last summed gradient.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+
+STEPS = 3
+PER_RANK = 24
+
+
+def problem(world):
+    """Deterministic model, parameters and batches shared by the workers and the single-process run."""
+    from paper_2109_12298_b200.configs import CIFAR_LAYERS, param_count
+    g = np.random.default_rng(7)
+    L = param_count(CIFAR_LAYERS)
+    params = (0.05 * g.standard_normal(L)).astype(np.float32)
+    b = PER_RANK * world
+    xs = [g.standard_normal((b, 3, 32, 32)).astype(np.float32) for _ in range(STEPS)]
+    ys = [g.integers(0, 10, b).astype(np.float32) for _ in range(STEPS)]
+    return CIFAR_LAYERS, (3, 32, 32), params, xs, ys
+
+
+def run(rank, world, data_world, handles_fn=None):
+    """Train STEPS steps on rank `rank`'s slice of the data_world-sized batches; world = 1 is the
+    single-process run on the full batch."""
+    import torch
+    from paper_2109_12298_b200 import dpg
+    layers, in_shape, params, xs, ys = problem(data_world)
+    total = xs[0].shape[0]
+    per = total // world
+    ctx = dpg.Context(0)
+    m = dpg.Model(ctx, layers, in_shape, max_batch=per)
+    m.load_params(params)
+    o = dpg.DpOptimizer(m, noise_multiplier=1.0, max_grad_norm=1.0, learning_rate=0.1,
+                        expected_batch_size=float(total), noise_seed=11)
+    if handles_fn:
+        o.set_peers(rank, handles_fn(o.peer_handle()))
+    for s in range(STEPS):
+        x = torch.from_numpy(xs[s][rank * per:(rank + 1) * per]).cuda()
+        y = torch.from_numpy(ys[s][rank * per:(rank + 1) * per]).cuda()
+        o.train_step(x, y, torch.zeros(per, device="cuda"), use_graph=s > 0)
+    ctx.sync()
+    return m.store_params(), o.summed_grad().cpu().numpy().copy()
+
+
+def main():
+    rank, world, port, out = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+
+    def gather(h):
+        hs = [None] * world
+        dist.all_gather_object(hs, h)
+        return hs
+
+    p, summed = run(rank, world, world, gather)
+    np.savez(out, params=p, summed=summed)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
