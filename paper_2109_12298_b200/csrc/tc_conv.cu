@@ -100,7 +100,7 @@ static void check_i32_linear(int64_t b, int64_t mid, int64_t d, int64_t r) {
 }
 
 // ------------------------------------------------------------------------------ forward
-struct ConvFwd {
+struct ConvFwd : TileRows {
   static constexpr bool kCtaReduce = false;
   Geo g;
   const float* x;
@@ -234,7 +234,7 @@ struct DClass {
   int64_t M, K;
 };
 
-struct ConvDgrad {
+struct ConvDgrad : TileRows {
   static constexpr bool kCtaReduce = false;
   Geo g;
   const float* dy;
@@ -409,7 +409,7 @@ void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& c
 }
 
 // ------------------------------------------------------------------------------ per-sample conv
-struct ConvGs {
+struct ConvGs : TileRows {
   static constexpr bool kCtaReduce = true;
   Geo g;
   const float* x;
@@ -496,7 +496,7 @@ void conv_gs(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const Co
 }
 
 // ------------------------------------------------------------------------------ clipped conv sum
-struct ConvCsum {
+struct ConvCsum : TileRows {
   static constexpr bool kCtaReduce = false;
   Geo g;
   const float* x;
@@ -637,7 +637,7 @@ void conv_csum(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const 
 }
 
 // ------------------------------------------------------------------------------ linear, mid > 1
-struct LinGs {
+struct LinGs : TileRows {
   static constexpr bool kCtaReduce = true;
   const float* acts;
   int relu;
@@ -686,11 +686,11 @@ int gs_linear_rows(int64_t d, int64_t r) {
 void linear_gs(dpg_ctx* ctx, const float* acts, int relu, const float* hw, int64_t b, int64_t mid,
                int64_t d, int64_t r, float* gw, double* sq_part) {
   check_i32_linear(b, mid, d, r);
-  LinGs p{acts, relu, hw, gw, sq_part, d, r, mid, b, 1, 0};
+  LinGs p{{}, acts, relu, hw, gw, sq_part, d, r, mid, b, 1, 0};
   launch_tc_auto(ctx, p, b);
 }
 
-struct LinCsum {
+struct LinCsum : TileRows {
   static constexpr bool kCtaReduce = false;
   const float* acts;
   int relu;

@@ -35,6 +35,10 @@ namespace dpg {
 namespace tc {
 
 constexpr int BM = 128;
+// every problem carries its rows per CTA tile (<= BM; set by launch_tc)
+struct TileRows {
+  int mstep = BM;
+};
 // K per stage: 16 fp32 = one 64 B swizzle row (SWIZZLE_64B) keeps a stage at 24 KB for BN = 64, so
 // three CTAs fit an SM (shared memory and registers); DPG_TC_BK=32 selects 128 B rows (SWIZZLE_128B).
 #ifndef DPG_TC_BK
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Pro
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int z = blockIdx.z / p.ksplit, split = blockIdx.z % p.ksplit;
-  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  const int64_t m0 = (int64_t)blockIdx.x * p.mstep, n0 = (int64_t)blockIdx.y * BN;
   constexpr uint32_t kCols = tmem_cols<BN>();
   const int64_t Mz = p.mdim(z), Kz = p.kdim(z);
   if (m0 >= Mz) return;  // ragged batches (e.g. dgrad parity classes): whole CTA idle
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Pro
   // Two register sets: the operands of stage i + 2 are requested while stage i is stored, so each
   // gather has a full stage period (store + barrier + MMA issue of the previous stage) to land.
   float4 ra0[kAQ], rb0[Frag<BN>::BQ], ra1[kAQ], rb1[Frag<BN>::BQ];
-  const int mrows = (int)std::min<int64_t>(BM, Mz - m0);
+  const int mrows = (int)std::min<int64_t>(p.mstep, Mz - m0);
   const int nrows = (int)std::min<int64_t>(BN, p.N - n0);
   if (nk > 0) fetch<BN>(p, z, m0, n0, (int64_t)ks0 * BK, scratch, tid, mrows, nrows, ra0, rb0);
   if (nk > 1) fetch<BN>(p, z, m0, n0, (int64_t)(ks0 + 1) * BK, scratch, tid, mrows, nrows, ra1, rb1);
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Pro
   // epilogue: warp w -> TMEM lanes [32 (w % 4), +32), columns [(w / 4) BN / 2, +BN / 2)
   const int lane_base = 32 * (warp & 3);
   const int64_t m = m0 + lane_base + (tid & 31);
-  const bool row_ok = m < Mz;
+  const bool row_ok = lane_base + (tid & 31) < mrows;
   constexpr int HALF = BN / 2 >= 16 ? BN / 2 : 16;
   const int c_begin = (warp >> 2) * HALF;
   double sq = 0.0;
@@ -728,9 +732,27 @@ inline bool ws_enabled() {
 // CTAs a launch should fill: one persistent CTA per SM (warp-specialised), else kMinBlocks per SM
 inline int ctas_target() { return ws_enabled() ? kNumSMs : kMinBlocks * kNumSMs; }
 
+// Rows per CTA tile: the UMMA tile is always BM = 128 rows, but an M that is not a multiple of
+// 128 is split into equal tiles (M = 288: 3 x 96 instead of 128 + 128 + 32), so the gathers —
+// the CTA's critical path — are balanced across the launch. DPG_TC_BAL=0: plain 128-row tiles.
+inline bool balanced_tiles() {
+  static const bool on = [] {
+    const char* e = std::getenv("DPG_TC_BAL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+inline int tile_rows(int64_t M) {
+  if (!balanced_tiles() || M <= 0) return BM;
+  const int64_t t = (M + BM - 1) / BM;
+  return (int)((M + t - 1) / t);
+}
+
 template <int BN, class Prob>
-void launch_tc(dpg_ctx* ctx, const Prob& p, int64_t batches) {
-  const int mt = (int)((p.M + BM - 1) / BM), nt = (int)((p.N + BN - 1) / BN);
+void launch_tc(dpg_ctx* ctx, const Prob& p_in, int64_t batches) {
+  Prob p = p_in;
+  p.mstep = ws_enabled() ? BM : tile_rows(p.M);
+  const int mt = (int)((p.M + p.mstep - 1) / p.mstep), nt = (int)((p.N + BN - 1) / BN);
   if (ws_enabled()) {
     const int smem = ws_stages<BN>() * Smem<BN>::STAGE + 256 + 2 * ((p.scratch + 127) & ~127) + 1024;
     static int attr = 0;
