@@ -217,7 +217,7 @@ void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
 // one warp per row with a fixed fp64 tree; linear layout [mid][r]: sequential in mid, coalesced
 // over o. One CTA per sample; norm partial = one row.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) gs_bias_kernel(const float* __restrict__ hw, int64_t mid,
+__global__ void __launch_bounds__(256, 4) gs_bias_kernel(const float* __restrict__ hw, int64_t mid,
                                                       int64_t r, int conv_layout,
                                                       float* __restrict__ gb,
                                                       double* __restrict__ sq_part, int64_t b) {
@@ -231,7 +231,40 @@ __global__ void __launch_bounds__(256) gs_bias_kernel(const float* __restrict__ 
     // in rare rounding-boundary cases, within the 1e-7 bias tolerance)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t o = warp;
-    if (mid <= 256) {
+    if (mid <= 64) {
+      // short rows (e.g. an 8x8 feature map): 8 rows per warp, all 16 loads issued first and the
+      // 8 shuffle trees interleaved (same association as below)
+      constexpr int RW = 8;
+      for (; o < r; o += 8 * RW) {
+        float v[RW][2];
+#pragma unroll
+        for (int q = 0; q < RW; ++q)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int64_t m = lane + 32 * i, oq = o + 8 * q;
+            v[q][i] = (oq < r && m < mid) ? __ldg(hw + (n * r + oq) * mid + m) : 0.f;
+          }
+        double acc[RW];
+#pragma unroll
+        for (int q = 0; q < RW; ++q) {
+          acc[q] = 0.0;
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            if (lane + 32 * i < mid) acc[q] += (double)v[q][i];
+        }
+#pragma unroll
+        for (int q = 0; q < RW; ++q) acc[q] = warp_sum(acc[q]);
+#pragma unroll
+        for (int q = 0; q < RW; ++q) {
+          const int64_t oq = o + 8 * q;
+          const float fv = (float)acc[q];
+          if (lane == 0 && oq < r) {
+            if (gb) gb[n * r + oq] = fv;
+            sq += (double)fv * fv;
+          }
+        }
+      }
+    } else if (mid <= 256) {
       // 4 rows at a time, every lane's loads issued before the sums (same association)
       for (; o + 24 < r; o += 32) {
         float v[4][8];
