@@ -30,31 +30,18 @@ __global__ void __launch_bounds__(256) clip_factors_kernel(const double* __restr
   if (n < b) {
     double sq = 0.0;
     int bad = -1;
-    int r = 0;
-    for (; r + 32 <= rows; r += 32) {  // 32 independent loads in flight, summed in row order
+    // every row's load of a 32-row batch issued before the in-order sum (a short tail of rows
+    // must not become a chain of dependent loads)
+    for (int r = 0; r < rows; r += 32) {
       double v[32];
 #pragma unroll
-      for (int u = 0; u < 32; ++u) v[u] = slab[(int64_t)(r + u) * b + n];
+      for (int u = 0; u < 32; ++u) v[u] = r + u < rows ? slab[(int64_t)(r + u) * b + n] : 0.0;
 #pragma unroll
       for (int u = 0; u < 32; ++u) {
+        if (r + u >= rows) break;
         if (bad < 0 && !isfinite(v[u])) bad = row_param ? row_param[r + u] : 0;
         sq += v[u];
       }
-    }
-    for (; r + 8 <= rows; r += 8) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = slab[(int64_t)(r + u) * b + n];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (bad < 0 && !isfinite(v[u])) bad = row_param ? row_param[r + u] : 0;
-        sq += v[u];
-      }
-    }
-    for (; r < rows; ++r) {
-      const double v = slab[(int64_t)r * b + n];
-      if (bad < 0 && !isfinite(v)) bad = row_param ? row_param[r] : 0;
-      sq += v;
     }
     if (bad >= 0) report_error(err, err_key(ERR_STAGE_NONFINITE, (uint64_t)bad, (uint64_t)n), 0);
     const double norm = sqrt(sq);
