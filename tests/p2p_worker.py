@@ -1,6 +1,6 @@
 """One rank of the peer-memory exchange test (test_gpu_p2p.py); run as a subprocess.
 
-usage: python p2p_worker.py RANK WORLD PORT OUT_NPZ
+usage: python p2p_worker.py RANK WORLD PORT OUT_NPZ [ragged]
 Every rank takes its contiguous slice of each step's batch (SURVEY.md §8e partitioning), swaps
 peer handles over a gloo group, and runs STEPS train steps (the first eager, the rest CUDA-graph
 replays) with the exchange inside step(). Writes its final parameters and last summed gradient.
@@ -29,31 +29,49 @@ def problem(world):
     return CIFAR_LAYERS, (3, 32, 32), params, xs, ys
 
 
-def run(rank, world, data_world, handles_fn=None):
+# ragged shards of the 2-rank batches (48 samples): step 1 leaves rank 1 empty (noise-only
+# step_empty_batch there, optimizer.hpp:197-213, while rank 0 steps all 48 samples)
+RAGGED = [(30, 18), (48, 0), (20, 28)]
+
+
+def shard(s, rank, world, total, ragged):
+    if not ragged:
+        per = total // world
+        return rank * per, (rank + 1) * per
+    cuts = [0, RAGGED[s][0], total] if world == 2 else [0, total]
+    return cuts[rank], cuts[rank + 1]
+
+
+def run(rank, world, data_world, handles_fn=None, ragged=False):
     """Train STEPS steps on rank `rank`'s slice of the data_world-sized batches; world = 1 is the
     single-process run on the full batch."""
     import torch
     from paper_2109_12298_b200 import dpg
     layers, in_shape, params, xs, ys = problem(data_world)
     total = xs[0].shape[0]
-    per = total // world
     ctx = dpg.Context(0)
-    m = dpg.Model(ctx, layers, in_shape, max_batch=per)
+    m = dpg.Model(ctx, layers, in_shape, max_batch=total if ragged else total // world)
     m.load_params(params)
     o = dpg.DpOptimizer(m, noise_multiplier=1.0, max_grad_norm=1.0, learning_rate=0.1,
                         expected_batch_size=float(total), noise_seed=11)
     if handles_fn:
         o.set_peers(rank, handles_fn(o.peer_handle()))
     for s in range(STEPS):
-        x = torch.from_numpy(xs[s][rank * per:(rank + 1) * per]).cuda()
-        y = torch.from_numpy(ys[s][rank * per:(rank + 1) * per]).cuda()
-        o.train_step(x, y, torch.zeros(per, device="cuda"), use_graph=s > 0)
+        a, b = shard(s, rank, world, total, ragged)
+        if b == a:
+            o.zero_grad()
+            o.step_empty_batch()
+            continue
+        x = torch.from_numpy(xs[s][a:b]).cuda()
+        y = torch.from_numpy(ys[s][a:b]).cuda()
+        o.train_step(x, y, torch.zeros(b - a, device="cuda"), use_graph=s > 0)
     ctx.sync()
     return m.store_params(), o.summed_grad().cpu().numpy().copy()
 
 
 def main():
     rank, world, port, out = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+    ragged = len(sys.argv) > 5 and sys.argv[5] == "ragged"
     import torch.distributed as dist
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
 
@@ -62,7 +80,7 @@ def main():
         dist.all_gather_object(hs, h)
         return hs
 
-    p, summed = run(rank, world, world, gather)
+    p, summed = run(rank, world, world, gather, ragged)
     np.savez(out, params=p, summed=summed)
     dist.barrier()
     dist.destroy_process_group()

@@ -26,12 +26,16 @@ def _port():
         return s.getsockname()[1]
 
 
-def test_peer_exchange_two_ranks_match_single_process(tmp_path, ctx):
+@pytest.mark.parametrize("ragged", [False, True])
+def test_peer_exchange_two_ranks_match_single_process(tmp_path, ctx, ragged):
+    """ragged: unequal shards, and one step where rank 1 has no samples (step_empty_batch)."""
     sys.path.insert(0, HERE)
     import p2p_worker
     port = _port()
     outs = [str(tmp_path / f"r{r}.npz") for r in range(2)]
-    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "p2p_worker.py"), str(r), "2", str(port), outs[r]],
+    extra = ["ragged"] if ragged else []
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "p2p_worker.py"), str(r), "2", str(port), outs[r]]
+                              + extra,
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, start_new_session=True)
              for r in range(2)]
     logs = []
@@ -48,7 +52,7 @@ def test_peer_exchange_two_ranks_match_single_process(tmp_path, ctx):
     r0, r1 = np.load(outs[0]), np.load(outs[1])
     assert np.array_equal(r0["params"], r1["params"])
     assert np.array_equal(r0["summed"], r1["summed"])
-    p_single, s_single = p2p_worker.run(0, 1, 2)
+    p_single, s_single = p2p_worker.run(0, 1, 2, ragged=ragged)
     _, _, params0, _, _ = p2p_worker.problem(2)
     assert maxscaled_err(r0["summed"], s_single) <= 1e-5
     assert maxscaled_err(r0["params"] - params0, p_single - params0) <= 1e-5
