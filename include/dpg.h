@@ -203,6 +203,20 @@ DPG_API dpg_status dpg_clip_and_sum_materialised(dpg_ctx* ctx, const float* cons
                                                  float* scale, int64_t* num_clipped,
                                                  int accumulate);
 
+/* Workspace: the operators above take scratch (norm partials, split-K partials, sort keys)
+ * from one per-context device arena that grows on first use. To keep every hot call
+ * allocation-free, query the largest size the caller will use and reserve it
+ * once. A query returns 0 for invalid extents (the call itself reports the error). */
+DPG_API size_t dpg_grad_sample_linear_workspace_size(int64_t b, int64_t mid, int64_t d, int64_t r);
+DPG_API size_t dpg_grad_sample_conv2d_workspace_size(int64_t b, int64_t h, int64_t w,
+                                                     const dpg_conv2d_spec* spec);
+DPG_API size_t dpg_grad_sample_embedding_workspace_size(int64_t b, int64_t t, int64_t vocab, int64_t dim);
+DPG_API size_t dpg_clipped_sum_linear_workspace_size(int64_t b, int64_t mid, int64_t d, int64_t r);
+DPG_API size_t dpg_clipped_sum_conv2d_workspace_size(int64_t b, int64_t h, int64_t w,
+                                                     const dpg_conv2d_spec* spec);
+DPG_API size_t dpg_clipped_sum_embedding_workspace_size(int64_t b, int64_t t, int64_t vocab, int64_t dim);
+DPG_API dpg_status dpg_ctx_reserve_workspace(dpg_ctx* ctx, size_t bytes);
+
 /* add_noise + finish_step (optimizer.hpp:120-133, 256-271), fused, over n flat elements:
  *   noised = summed + (float)(N(0,1) * sigma * C)      sigma == 0: no noise
  *   grad   = noised * (1.0f / (float)E)                 (scale(), tensor.hpp:155-159)

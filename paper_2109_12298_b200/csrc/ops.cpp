@@ -39,6 +39,34 @@ void need_ctx(dpg_ctx* ctx) {
   DPG_CUDA(cudaSetDevice(ctx->device));
 }
 
+// Workspace each operator takes from the context arena (the dpg_*_workspace_size queries return
+// these, so a caller can dpg_ctx_reserve_workspace once and no hot call allocates).
+size_t ws_gs_linear(int64_t b, int64_t mid, int64_t d, int64_t r) {
+  return sizeof(double) * (size_t)dpg::sq_rows_linear(mid, d, r) * (size_t)b;
+}
+size_t ws_gs_conv2d(const ConvGeom& g) { return sizeof(double) * (size_t)dpg::sq_rows_conv2d(g) * (size_t)g.b; }
+size_t ws_embed_sort(int64_t b, int64_t t) { return sizeof(int32_t) * 2 * (size_t)(b * t); }
+size_t ws_gs_embedding(int64_t b, int64_t t, int64_t vocab, int64_t dim) {
+  return ws_embed_sort(b, t) + sizeof(double) * (size_t)dpg::sq_rows_embedding(vocab, dim) * (size_t)b;
+}
+size_t ws_cs_linear(int64_t b, int64_t mid, int64_t d, int64_t r) {
+  return dpg::clipped_sum_ws_linear(b, mid, d, r) + sizeof(float) * (size_t)(b * r);
+}
+size_t ws_cs_conv2d(const ConvGeom& g) { return dpg::clipped_sum_ws_conv2d(g) + sizeof(float) * (size_t)(g.b * g.oc); }
+size_t ws_cs_embedding(int64_t b, int64_t t, int64_t vocab) {
+  return ws_embed_sort(b, t) + dpg::clipped_sum_ws_embedding(b, vocab);
+}
+
+// a query never raises: invalid extents report 0
+template <class F>
+size_t ws_query(F&& f) {
+  try {
+    return f();
+  } catch (...) {
+    return 0;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -54,7 +82,7 @@ dpg_status dpg_grad_sample_linear(dpg_ctx* ctx, const float* acts, const float* 
       raise(DPG_ERR_DIMENSION, "batched_outer: extents must be positive");
     if (b == 0) return;
     const int rows = dpg::sq_rows_linear(mid, d, r);
-    double* part = sq_w ? static_cast<double*>(ctx->workspace(sizeof(double) * rows * b)) : nullptr;
+    double* part = sq_w ? static_cast<double*>(ctx->workspace(ws_gs_linear(b, mid, d, r))) : nullptr;
     dpg::launch_gs_linear(ctx, acts, 0, highway, b, mid, d, r, gw, part);
     if (sq_w) dpg::launch_sq_reduce(ctx, part, rows, b, sq_w);
     if (gb || sq_b) dpg::launch_gs_bias(ctx, highway, b, mid, r, false, gb, sq_b);
@@ -71,7 +99,7 @@ dpg_status dpg_grad_sample_conv2d(dpg_ctx* ctx, const float* x, const float* hig
     const ConvGeom g = conv_geom(b, h, w, spec);
     if (b == 0) return;
     const int rows = dpg::sq_rows_conv2d(g);
-    double* part = sq_w ? static_cast<double*>(ctx->workspace(sizeof(double) * rows * b)) : nullptr;
+    double* part = sq_w ? static_cast<double*>(ctx->workspace(ws_gs_conv2d(g))) : nullptr;
     dpg::launch_gs_conv2d(ctx, x, 0, highway, g, gw, part);
     if (sq_w) dpg::launch_sq_reduce(ctx, part, rows, b, sq_w);
     if (gb || sq_b) dpg::launch_gs_bias(ctx, highway, b, g.P(), g.oc, true, gb, sq_b);
@@ -116,9 +144,8 @@ dpg_status dpg_grad_sample_embedding(dpg_ctx* ctx, const float* idx, const float
     if (vocab <= 0 || dim <= 0) raise(DPG_ERR_PARAMETER, "embedding: extents must be positive");
     if (b == 0 || t == 0) return;
     const int rows = dpg::sq_rows_embedding(vocab, dim);
-    const size_t sort_bytes = sizeof(int32_t) * 2 * (size_t)(b * t);
-    const size_t part_bytes = sizeof(double) * (size_t)rows * b;
-    char* ws = static_cast<char*>(ctx->workspace(sort_bytes + part_bytes));
+    const size_t sort_bytes = ws_embed_sort(b, t);
+    char* ws = static_cast<char*>(ctx->workspace(ws_gs_embedding(b, t, vocab, dim)));
     int32_t* sv = reinterpret_cast<int32_t*>(ws);
     int32_t* ss = sv + b * t;
     double* part = reinterpret_cast<double*>(ws + sort_bytes);
@@ -157,7 +184,7 @@ dpg_status dpg_clipped_sum_linear(dpg_ctx* ctx, const float* acts, const float* 
     need(scale, "scale");
     need(sw, "sw");
     if (b <= 0) raise(DPG_ERR_PARAMETER, "clip_and_sum on an empty batch");
-    void* ws = ctx->workspace(dpg::clipped_sum_ws_linear(b, mid, d, r) + sizeof(float) * b * r);
+    void* ws = ctx->workspace(ws_cs_linear(b, mid, d, r));
     dpg::launch_clipped_sum_linear(ctx, acts, 0, highway, scale, b, mid, d, r, sw, sb, accumulate, ws);
     if (sb) {
       // bias: weighted sum of the per-sample bias sums (bit-exact with the reference)
@@ -181,7 +208,7 @@ dpg_status dpg_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, const float* hig
     const ConvGeom g = conv_geom(b, h, w, spec);
     if (b <= 0) raise(DPG_ERR_PARAMETER, "clip_and_sum on an empty batch");
     const size_t wsz = dpg::clipped_sum_ws_conv2d(g);
-    void* ws = ctx->workspace(wsz + sizeof(float) * b * g.oc);
+    void* ws = ctx->workspace(ws_cs_conv2d(g));
     dpg::launch_clipped_sum_conv2d(ctx, x, 0, highway, scale, g, sw, sb, accumulate, ws);
     if (sb) {
       float* gb = reinterpret_cast<float*>(static_cast<char*>(ws) + wsz);
@@ -201,8 +228,8 @@ dpg_status dpg_clipped_sum_embedding(dpg_ctx* ctx, const float* idx, const float
     need(scale, "scale");
     need(summed, "summed");
     if (b <= 0) raise(DPG_ERR_PARAMETER, "clip_and_sum on an empty batch");
-    const size_t sort_bytes = sizeof(int32_t) * 2 * (size_t)(b * t);
-    char* ws = static_cast<char*>(ctx->workspace(sort_bytes + dpg::clipped_sum_ws_embedding(b, vocab)));
+    const size_t sort_bytes = ws_embed_sort(b, t);
+    char* ws = static_cast<char*>(ctx->workspace(ws_cs_embedding(b, t, vocab)));
     int32_t* sv = reinterpret_cast<int32_t*>(ws);
     int32_t* ss = sv + b * t;
     dpg::launch_embed_sort(ctx, idx, b, t, vocab, sv, ss);
@@ -267,4 +294,30 @@ dpg_status dpg_gaussian(dpg_ctx* ctx, float* out, int64_t n, double std_dev, uin
   });
 }
 
+
+size_t dpg_grad_sample_linear_workspace_size(int64_t b, int64_t mid, int64_t d, int64_t r) {
+  return ws_query([&] { return (b > 0 && mid > 0 && d > 0 && r > 0) ? ws_gs_linear(b, mid, d, r) : size_t(0); });
+}
+size_t dpg_grad_sample_conv2d_workspace_size(int64_t b, int64_t h, int64_t w, const dpg_conv2d_spec* spec) {
+  return ws_query([&] { return b > 0 ? ws_gs_conv2d(conv_geom(b, h, w, spec)) : size_t(0); });
+}
+size_t dpg_grad_sample_embedding_workspace_size(int64_t b, int64_t t, int64_t vocab, int64_t dim) {
+  return ws_query([&] { return (b > 0 && t > 0 && vocab > 0 && dim > 0) ? ws_gs_embedding(b, t, vocab, dim) : size_t(0); });
+}
+size_t dpg_clipped_sum_linear_workspace_size(int64_t b, int64_t mid, int64_t d, int64_t r) {
+  return ws_query([&] { return (b > 0 && mid > 0 && d > 0 && r > 0) ? ws_cs_linear(b, mid, d, r) : size_t(0); });
+}
+size_t dpg_clipped_sum_conv2d_workspace_size(int64_t b, int64_t h, int64_t w, const dpg_conv2d_spec* spec) {
+  return ws_query([&] { return b > 0 ? ws_cs_conv2d(conv_geom(b, h, w, spec)) : size_t(0); });
+}
+size_t dpg_clipped_sum_embedding_workspace_size(int64_t b, int64_t t, int64_t vocab, int64_t dim) {
+  return ws_query([&] { return (b > 0 && t > 0 && vocab > 0 && dim > 0) ? ws_cs_embedding(b, t, vocab) : size_t(0); });
+}
+
+dpg_status dpg_ctx_reserve_workspace(dpg_ctx* ctx, size_t bytes) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    ctx->workspace(bytes);
+  });
+}
 }  // extern "C"

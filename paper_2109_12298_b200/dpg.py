@@ -117,6 +117,13 @@ _SIGS = {
     "dpg_model_output_width": (_I64, [_P]),
     "dpg_optimizer_create": (_I32, [_P, _P, ctypes.POINTER(_P)]),
     "dpg_optimizer_peer_handle": (_I32, [_P, _P]),
+    "dpg_grad_sample_linear_workspace_size": (ctypes.c_size_t, [_I64, _I64, _I64, _I64]),
+    "dpg_grad_sample_conv2d_workspace_size": (ctypes.c_size_t, [_I64, _I64, _I64, _P]),
+    "dpg_grad_sample_embedding_workspace_size": (ctypes.c_size_t, [_I64, _I64, _I64, _I64]),
+    "dpg_clipped_sum_linear_workspace_size": (ctypes.c_size_t, [_I64, _I64, _I64, _I64]),
+    "dpg_clipped_sum_conv2d_workspace_size": (ctypes.c_size_t, [_I64, _I64, _I64, _P]),
+    "dpg_clipped_sum_embedding_workspace_size": (ctypes.c_size_t, [_I64, _I64, _I64, _I64]),
+    "dpg_ctx_reserve_workspace": (_I32, [_P, ctypes.c_size_t]),
     "dpg_optimizer_set_peers": (_I32, [_P, ctypes.c_int, ctypes.c_int, _P]),
     "dpg_optimizer_destroy": (None, [_P]),
     "dpg_forward_backward": (_I32, [_P, _P, _P, _I64, _P]),
@@ -199,6 +206,10 @@ class Context:
     def sync(self):
         _check(lib().dpg_ctx_sync(self.h), self.h)
 
+    def reserve_workspace(self, nbytes: int):
+        """Pre-size the operator workspace arena (dpg_ctx_reserve_workspace)."""
+        _check(lib().dpg_ctx_reserve_workspace(self.h, nbytes), self.h)
+
     @property
     def kernel_launches(self) -> int:
         return int(lib().dpg_ctx_kernel_launches(self.h))
@@ -257,6 +268,17 @@ def per_sample_rule_linear(ctx: Context, acts: torch.Tensor, highway: torch.Tens
 
 def _spec(ic, oc, kh, kw, stride, pad):
     return dpg_conv2d_spec(ic, oc, kh, kw, stride, pad)
+
+
+def workspace_size(op: str, *extents) -> int:
+    """Context-arena bytes an operator takes (dpg_<op>_workspace_size; host-only, no GPU needed).
+    conv2d ops take (b, h, w, ic, oc, kh, kw, stride, pad), the others their ABI extents."""
+    fn = getattr(lib(), f"dpg_{op}_workspace_size")
+    if op.endswith("conv2d"):
+        b, h, w, ic, oc, kh, kw, stride, pad = extents
+        spec = _spec(ic, oc, kh, kw, stride, pad)
+        return int(fn(b, h, w, ctypes.byref(spec)))
+    return int(fn(*extents))
 
 
 def per_sample_rule_conv2d(ctx: Context, x: torch.Tensor, highway: torch.Tensor, kh: int, kw: int,

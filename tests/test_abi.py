@@ -57,3 +57,22 @@ def test_layer_desc_layout_matches_header():
     from paper_2109_12298_b200.configs import CLayerDesc
     assert ctypes.sizeof(CLayerDesc) == 8 + 12 * 8 + 8  # + norm_size, groups, eps
     assert CLayerDesc.in_features.offset == 8 and CLayerDesc.padding.offset == 80
+
+
+def test_workspace_queries_on_host():
+    """dpg_*_workspace_size (size the arena once, no allocation in hot calls) are
+    host-only: sizes for the CIFAR layers, 0 for invalid extents."""
+    from paper_2109_12298_b200 import dpg
+    conv = (512, 16, 16, 32, 64, 3, 3, 2, 1)  # conv2 of the CIFAR model
+    gs = dpg.workspace_size("grad_sample_conv2d", *conv)
+    cs = dpg.workspace_size("clipped_sum_conv2d", *conv)
+    assert gs >= 8 * 512 and gs % 8 == 0
+    assert cs >= 4 * 512 * 64  # at least the per-sample bias sums
+    assert dpg.workspace_size("grad_sample_linear", 512, 1, 512, 10) >= 8 * 512
+    assert dpg.workspace_size("clipped_sum_linear", 256, 64, 512, 512) > 0
+    assert dpg.workspace_size("grad_sample_embedding", 512, 256, 10000, 128) >= 8 * 512 * 256
+    assert dpg.workspace_size("clipped_sum_embedding", 512, 256, 10000, 128) > 0
+    # invalid extents: 0, no exception across the ABI
+    assert dpg.workspace_size("grad_sample_conv2d", 512, 2, 2, 32, 64, 3, 3, 1, 0) == 0  # kernel > input
+    assert dpg.workspace_size("grad_sample_conv2d", 4, 8, 8, 0, 4, 3, 3, 1, 1) == 0
+    assert dpg.workspace_size("grad_sample_linear", 4, 0, 3, 3) == 0

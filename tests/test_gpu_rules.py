@@ -118,6 +118,23 @@ def test_conv_rule(ctx, oracle_r, case):
     np.testing.assert_allclose(_n(sb), (_n(gb).astype(np.float64) ** 2).sum(1), rtol=1e-12)
 
 
+def test_reserved_workspace_covers_the_call(ctx, oracle_r):
+    """Reserve the queried workspace, then the call runs from it and gives the same records."""
+    from paper_2109_12298_b200 import dpg
+    b, ic, h, w, oc, kh, kw, s, p = 16, 32, 16, 16, 64, 3, 3, 2, 1
+    need = max(dpg.workspace_size("grad_sample_conv2d", b, h, w, ic, oc, kh, kw, s, p),
+               dpg.workspace_size("clipped_sum_conv2d", b, h, w, ic, oc, kh, kw, s, p))
+    assert need > 0
+    c2 = dpg.Context(0)
+    c2.reserve_workspace(need)
+    g = _rng(5)
+    x = g.standard_normal((b, ic, h, w)).astype(np.float32)
+    hw = g.standard_normal((b, oc, 8, 8)).astype(np.float32)
+    gw, gb, _, _ = dpg.per_sample_rule_conv2d(c2, _t(x), _t(hw), kh, kw, s, p)
+    gw1, gb1, _, _ = dpg.per_sample_rule_conv2d(ctx, _t(x), _t(hw), kh, kw, s, p)
+    assert np.array_equal(_n(gw), _n(gw1)) and np.array_equal(_n(gb), _n(gb1))
+
+
 def test_conv_identity_kernel_kat(ctx):
     """1x1 identity kernel case hand-checkable; zero input -> zero."""
     from paper_2109_12298_b200 import dpg
