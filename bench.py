@@ -577,11 +577,6 @@ def main():
 
     torch.cuda.set_device(local)
     ctx = dpg.Context(local)
-    if world > 1 and args.exchange == "nccl":
-        import torch.distributed as dist
-        obj = [dpg.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx.init_comm(world, rank, obj[0])
 
     w = WORKLOADS[args.workload]
     b = w.batch
@@ -595,10 +590,27 @@ def main():
                           learning_rate=0.1, expected_batch_size=float(gb), noise_seed=3,
                           materialise_grad_sample=materialise,
                           clipped_sum_from_record=args.csum_from_record and materialise)
-    if world > 1 and args.exchange == "p2p":
+    exchange = args.exchange if world > 1 else None
+    if exchange == "p2p":
         handles = [None] * world
         torch.distributed.all_gather_object(handles, opt.peer_handle())
-        opt.set_peers(rank, handles)
+        err = ""
+        try:
+            opt.set_peers(rank, handles)
+        except dpg.DpgError as e:  # e.g. no peer access between these GPUs
+            err = str(e)
+        errs = [None] * world
+        torch.distributed.all_gather_object(errs, err)
+        if any(errs):  # every rank must take the same path
+            if not err:
+                opt.set_peers(rank, [handles[rank]])
+            if rank == 0:
+                print(f"peer exchange unavailable ({next(e for e in errs if e)}); using NCCL", file=sys.stderr)
+            exchange = "nccl"
+    if exchange == "nccl":
+        obj = [dpg.Context.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        ctx.init_comm(world, rank, obj[0])
     xt = torch.from_numpy(x).cuda()
     yt = torch.from_numpy(y).cuda()
     loss = torch.zeros(b, device="cuda")
@@ -718,8 +730,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": w.name, "global_batch": gb, "per_rank_batch": b,
-                   "parallelism": f"dp{world} (sample shards, " + (
-                       "clipped sums summed over peer memory inside the update kernel)" if args.exchange == "p2p"
+                   "parallelism": "dp1 (one GPU)" if world == 1 else f"dp{world} (sample shards, " + (
+                       "clipped sums summed over peer memory inside the update kernel)" if exchange == "p2p"
                        else "1 NCCL all-reduce of the clipped sum)"),
                    "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
                    "materialise_grad_sample": materialise, "graph": True,

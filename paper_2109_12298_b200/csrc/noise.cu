@@ -114,9 +114,20 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded: a peer that never arrives (a rank died, or ranks disagree on the number of steps)
+// traps after 120 s, failing the launch with an error instead of hanging the device.
 __device__ __forceinline__ void wait_all(const PeerSet& ps, int slot, unsigned long long e) {
+  const unsigned long long t0 = global_ns();
   for (int r = 0; r < ps.world; ++r)
-    while (ld_acquire_sys(ps.flags[r] + slot) < e) __nanosleep(64);
+    while (ld_acquire_sys(ps.flags[r] + slot) < e) {
+      __nanosleep(256);
+      if (global_ns() - t0 > 120ull * 1000000000ull) __trap();
+    }
 }
 
 __global__ void xch_signal_kernel(PeerSet ps, uint64_t step, const uint64_t* step_ptr) {
