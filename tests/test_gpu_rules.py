@@ -95,6 +95,8 @@ CONV_CASES = [
     (2, 5, 9, 7, 7, 3, 3, 1, 0),       # ragged, stride 1
     (2, 2, 6, 6, 3, 1, 1, 1, 0),       # 1x1
     (2, 3, 10, 10, 4, 5, 5, 3, 2),     # stride 3, pad 2
+    (3, 16, 9, 9, 8, 3, 3, 2, 1),      # K = 144: two equal 72-row tiles
+    (2, 24, 12, 12, 16, 3, 3, 1, 1),   # K = 216: two equal 108-row tiles, P = 144
 ]
 
 
