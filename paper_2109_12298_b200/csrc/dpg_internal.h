@@ -316,7 +316,13 @@ struct LossFuse {
   float* grad;
   int logits_relu;
   DeviceErr* err;
+  // optional: the layer's input gradient in the same launch (dx = W^T grad, ReLU mask of the
+  // previous layer's pre-activation folded in), bit-identical to launch_linear_dgrad's vector path
+  float* dx = nullptr;
+  const float* dmask = nullptr;
 };
+// can the logits layer's forward launch also produce its input gradient (launch_linear_fwd + LossFuse::dx)?
+bool linear_fwd_fuses_dgrad(int64_t d, int64_t r, const float* dx, const float* mask);
 bool linear_fwd_fuses_loss(int64_t d, int64_t r, const float* x, const float* w);
 void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
                        int64_t rows, int64_t d, int64_t r, float* y, const LossFuse* loss = nullptr);

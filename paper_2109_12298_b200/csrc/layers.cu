@@ -257,6 +257,33 @@ __global__ void __launch_bounds__(32 * NW) linear_fwd_row_kernel(const float* __
   if (ce.grad) {  // this layer's outputs are the logits: the loss in the same launch
     __syncthreads();
     if (warp == 0) softmax_ce_warp(logit, ce.logits_relu, ce.targets, row, r, ce.loss, ce.grad, ce.err);
+    if (ce.dx) {  // and the input gradient: linear_dgrad_vec_kernel's arithmetic, in its order
+      __syncthreads();
+      __shared__ float g[RMAX];
+      if (threadIdx.x < r) g[threadIdx.x] = ce.grad[row * r + threadIdx.x];
+      __syncthreads();
+      for (int64_t c = threadIdx.x; c < d4; c += 32 * NW) {
+        const int64_t j = 4 * c;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int o = 0; o < RMAX; ++o) {
+          if (o >= r) break;
+          const float4 wv = __ldg(reinterpret_cast<const float4*>(w + (int64_t)o * d + j));
+          a.x = fmaf(g[o], wv.x, a.x);
+          a.y = fmaf(g[o], wv.y, a.y);
+          a.z = fmaf(g[o], wv.z, a.z);
+          a.w = fmaf(g[o], wv.w, a.w);
+        }
+        if (ce.dmask) {
+          const float4 mv = __ldg(reinterpret_cast<const float4*>(ce.dmask + row * d + j));
+          if (!(mv.x > 0.f)) a.x = 0.f;
+          if (!(mv.y > 0.f)) a.y = 0.f;
+          if (!(mv.z > 0.f)) a.z = 0.f;
+          if (!(mv.w > 0.f)) a.w = 0.f;
+        }
+        *reinterpret_cast<float4*>(ce.dx + row * d + j) = a;
+      }
+    }
   }
 }
 
@@ -349,6 +376,11 @@ struct LinearFwdProb {
   }
 };
 
+bool linear_fwd_fuses_dgrad(int64_t d, int64_t r, const float* dx, const float* mask) {
+  return (d & 3) == 0 && r <= 16 && (reinterpret_cast<uintptr_t>(dx) & 15) == 0 &&
+         (!mask || (reinterpret_cast<uintptr_t>(mask) & 15) == 0);
+}
+
 bool linear_fwd_fuses_loss(int64_t d, int64_t r, const float* x, const float* w) {
   return (d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
          (reinterpret_cast<uintptr_t>(w) & 15) == 0 && r <= 64;
@@ -359,6 +391,8 @@ void launch_linear_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w,
   LossFuse ce{};
   if (loss) {
     if (!linear_fwd_fuses_loss(d, r, x, w)) raise(DPG_ERR_INTERNAL, "linear forward cannot fuse the loss");
+    if (loss->dx && !linear_fwd_fuses_dgrad(d, r, loss->dx, loss->dmask))
+      raise(DPG_ERR_INTERNAL, "linear forward cannot fuse the input gradient");
     ce = *loss;
     ce.err = ctx->dev_err;
   }

@@ -256,6 +256,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
   auto act = [&](int buf) -> const float* { return buf < 0 ? x : m->bufs[buf]; };
   // ---- forward (layers.hpp:576-592) ----
   bool loss_done = false;  // softmax-CE fused into the logits-producing linear forward
+  int dgrad_fused = -1;    // ... and that layer's input gradient too (its backward dgrad is skipped)
   for (size_t l = 0; l < m->layers.size(); ++l) {
     LayerPlan& lp = m->layers[l];
     if (lp.param0 < 0) continue;
@@ -271,7 +272,18 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
                           2.0 * b * lp.mid * lp.d.in_features * lp.d.out_features);
         const bool last = lp.out_buf == m->out_buf && lp.mid == 1 &&
                           dpg::linear_fwd_fuses_loss(lp.d.in_features, lp.d.out_features, in, w);
-        const dpg::LossFuse ce{targets, loss, m->highways[m->out_buf], m->out_relu ? 1 : 0, nullptr};
+        dpg::LossFuse ce{targets, loss, m->highways[m->out_buf], m->out_relu ? 1 : 0, nullptr};
+        if (last && lp.prev_param_layer >= 0) {
+          // the backward's first input gradient (dgrad of this layer) in the same launch
+          const LayerPlan& prev = m->layers[lp.prev_param_layer];
+          float* dst = m->highways[prev.out_buf];
+          const float* mask = lp.in_relu ? m->bufs[prev.out_buf] : nullptr;
+          if (dpg::linear_fwd_fuses_dgrad(lp.d.in_features, lp.d.out_features, dst, mask)) {
+            ce.dx = dst;
+            ce.dmask = mask;
+            dgrad_fused = l;
+          }
+        }
         dpg::launch_linear_fwd(ctx, in, lp.in_relu, w, bias, b * lp.mid, lp.d.in_features,
                                lp.d.out_features, out, last ? &ce : nullptr);
         loss_done = loss_done || last;
@@ -389,7 +401,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
     });
     if (pending_bias.conv >= 0) bias_rule(pending_bias.mid, pending_bias.r, pending_bias.conv == 1);
     // input gradient for the previous parametric layer, with the ReLU mask folded in
-    if (lp.prev_param_layer >= 0) {
+    if (lp.prev_param_layer >= 0 && l != dgrad_fused) {
       const LayerPlan& prev = m->layers[lp.prev_param_layer];
       float* dst = m->highways[prev.out_buf];
       const float* mask = lp.in_relu ? m->bufs[prev.out_buf] : nullptr;
