@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256) clip_factors_kernel(const double* __restr
                                                            double* __restrict__ norms,
                                                            float* __restrict__ scale,
                                                            unsigned long long* num_clipped,
-                                                           DeviceErr* err) {
+                                                           DeviceErr* err, unsigned long long* sync) {
   pdl_wait();
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int clipped = 0;
@@ -50,17 +50,29 @@ __global__ void __launch_bounds__(256) clip_factors_kernel(const double* __restr
     scale[n] = (float)s;
     clipped = norm > c ? 1 : 0;
   }
+  // num_clipped without a memset launch before the kernel: CTAs add into a context accumulator;
+  // the last CTA to take a ticket publishes the total and resets the accumulator and the ticket
   const int cnt = __syncthreads_count(clipped);
-  if (threadIdx.x == 0 && num_clipped && cnt) atomicAdd(num_clipped, (unsigned long long)cnt);
+  if (threadIdx.x == 0 && num_clipped) {
+    if (cnt) atomicAdd(&sync[0], (unsigned long long)cnt);
+    __threadfence();
+    if (atomicAdd(&sync[1], 1ull) == gridDim.x - 1) {
+      __threadfence();
+      *num_clipped = atomicExch(&sync[0], 0ull);
+      atomicExch(&sync[1], 0ull);
+    }
+  }
 }
 
 void launch_clip_factors(dpg_ctx* ctx, const double* slab, const int32_t* row_param, int rows,
                          int64_t b, double c, double* norms, float* scale, int64_t* num_clipped) {
-  if (num_clipped) DPG_CUDA(cudaMemsetAsync(num_clipped, 0, sizeof(int64_t), ctx->stream));
-  if (b == 0) return;
+  if (b == 0) {
+    if (num_clipped) DPG_CUDA(cudaMemsetAsync(num_clipped, 0, sizeof(int64_t), ctx->stream));
+    return;
+  }
   ::dpg::launch_pdl(clip_factors_kernel, (unsigned)((b + 63) / 64), 64, 0, ctx->stream, 
       slab, row_param, rows, b, c, norms, scale, reinterpret_cast<unsigned long long*>(num_clipped),
-      ctx->dev_err);
+      ctx->dev_err, ctx->clip_sync);
   DPG_LAUNCH_CHECK(ctx);
 }
 

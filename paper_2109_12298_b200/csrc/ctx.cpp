@@ -138,6 +138,8 @@ dpg_status dpg_ctx_create(int device, void* stream, dpg_ctx** out) {
       ctx->own_stream = true;
     }
     DPG_CUDA(cudaMalloc(&ctx->dev_err, sizeof(dpg::DeviceErr)));
+    DPG_CUDA(cudaMalloc(&ctx->clip_sync, 2 * sizeof(unsigned long long)));
+    DPG_CUDA(cudaMemset(ctx->clip_sync, 0, 2 * sizeof(unsigned long long)));
     DPG_CUDA(cudaMallocHost(&ctx->host_err, sizeof(dpg::DeviceErr)));
     dpg::DeviceErr clear{dpg::ERR_NONE, 0};
     *ctx->host_err = clear;
@@ -158,6 +160,7 @@ void dpg_ctx_destroy(dpg_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->dev_err) cudaFree(ctx->dev_err);
+  if (ctx->clip_sync) cudaFree(ctx->clip_sync);
   if (ctx->host_err) cudaFreeHost(ctx->host_err);
   for (auto& r : ctx->prof_pending) {
     cudaEventDestroy(r.a);

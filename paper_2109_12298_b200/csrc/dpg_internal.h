@@ -66,6 +66,7 @@ struct dpg_ctx {
   std::string err;
   int64_t launches = 0;
   dpg::DeviceErr* dev_err = nullptr;  // device
+  unsigned long long* clip_sync = nullptr;  // device [2]: clip_factors' clipped count + CTA ticket (self-resetting)
   dpg::DeviceErr* host_err = nullptr; // pinned mirror
   void* ws = nullptr;
   size_t ws_bytes = 0;
