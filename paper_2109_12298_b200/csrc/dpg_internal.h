@@ -286,7 +286,8 @@ void launch_weighted_sum_materialised(dpg_ctx* ctx, const float* g, const float*
 // noise.cu
 void launch_noise_update(dpg_ctx* ctx, float* params, const float* summed, float* grad, int64_t n,
                          double sigma, double c, double expected_batch, double lr, uint64_t seed,
-                         uint64_t step, const float* injected, const uint64_t* step_ptr);
+                         uint64_t step, const float* injected, uint64_t* step_ptr,
+                         unsigned long long* advance = nullptr);
 void launch_gaussian(dpg_ctx* ctx, float* out, int64_t n, double std_dev, uint64_t seed,
                      uint64_t step);
 // the clipped-sum exchange over peer memory (noise.cu): rank r's optimizer arena mapped by every
@@ -300,7 +301,8 @@ struct PeerSet {
 };
 void launch_noise_update_p2p(dpg_ctx* ctx, const PeerSet& ps, float* params, float* summed, float* reduced,
                              float* grad, int64_t n, double sigma, double c, double expected_batch, double lr,
-                             uint64_t seed, uint64_t step, const float* injected, const uint64_t* step_ptr);
+                             uint64_t seed, uint64_t step, const float* injected, uint64_t* step_ptr,
+                             unsigned long long* advance);
 
 // layers.cu — supporting forward / backward
 // ws: split-K scratch of at least conv_fwd_ws_bytes / conv_dgrad_ws_bytes (nullable: no split)

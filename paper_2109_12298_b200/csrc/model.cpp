@@ -143,6 +143,11 @@ struct dpg_optimizer {
   float* scale = nullptr;
   int64_t* num_clipped = nullptr;
   uint64_t* step_dev = nullptr;
+  unsigned long long* step_tick = nullptr;  // ticket of the kernel that advances step_dev in a replay
+  // step_dev == dev_step_next when dev_step_known: the previous replay advanced it on the device,
+  // so the next replay needs no host-to-device copy of the step
+  bool dev_step_known = false;
+  uint64_t dev_step_next = 0;
   // clipped-sum exchange over peer memory (dpg_optimizer_set_peers): world = 0 when unused
   dpg::PeerSet peers;
   float* reduced = nullptr;               // [L] the rank-order sum, copied into summed at the end
@@ -580,8 +585,11 @@ void finish_impl(dpg_optimizer* o, bool graph_mode) {
     dpg::launch_noise_update_p2p(ctx, o->peers, m->p_params, o->summed, o->reduced, o->grad, m->L,
                                  o->cfg.noise_multiplier, o->cfg.max_grad_norm, o->cfg.expected_batch_size,
                                  o->cfg.learning_rate, o->cfg.noise_seed, o->steps, o->injected,
-                                 graph_mode ? o->step_dev : nullptr);
-    if (!graph_mode) ++o->steps;
+                                 graph_mode ? o->step_dev : nullptr, graph_mode ? o->step_tick : nullptr);
+    if (!graph_mode) {
+      ++o->steps;
+      o->dev_step_known = false;
+    }
     o->has_grad = true;
     return;
   }
@@ -593,8 +601,11 @@ void finish_impl(dpg_optimizer* o, bool graph_mode) {
   dpg::launch_noise_update(ctx, m->p_params, o->summed, o->grad, m->L, o->cfg.noise_multiplier,
                            o->cfg.max_grad_norm, o->cfg.expected_batch_size,
                            o->cfg.learning_rate, o->cfg.noise_seed, o->steps, o->injected,
-                           graph_mode ? o->step_dev : nullptr);
-  if (!graph_mode) ++o->steps;
+                           graph_mode ? o->step_dev : nullptr, graph_mode ? o->step_tick : nullptr);
+  if (!graph_mode) {
+    ++o->steps;
+    o->dev_step_known = false;
+  }
   o->has_grad = true;
 }
 
@@ -972,7 +983,7 @@ dpg_status dpg_optimizer_create(dpg_model* m, const dpg_optimizer_config* cfg, d
     const size_t rec = cfg->materialise_grad_sample ? sizeof(float) * (size_t)(B * L) : sizeof(float) * (size_t)(B * bias_numel);
     size_t total = 2 * al(sizeof(float) * L) + al(rec) + al(sizeof(double) * m->sq_rows * B) +
                    al(sizeof(double) * B) + al(sizeof(float) * B) + al(sizeof(int64_t)) + al(sizeof(uint64_t)) +
-                   al(sizeof(float) * L) + al(3 * 128);
+                   al(sizeof(float) * L) + al(3 * 128) + al(sizeof(unsigned long long));
     DPG_CUDA(cudaMalloc(&o->arena, total));
     DPG_CUDA(cudaMemset(o->arena, 0, total));
     char* p = o->arena;
@@ -992,6 +1003,7 @@ dpg_status dpg_optimizer_create(dpg_model* m, const dpg_optimizer_config* cfg, d
     o->step_dev = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t)));
     o->reduced = reinterpret_cast<float*>(take(sizeof(float) * L));
     o->xflags = reinterpret_cast<unsigned long long*>(take(3 * 128));
+    o->step_tick = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long)));
   });
   if (st != DPG_OK) {
     if (o->arena) cudaFree(o->arena);
@@ -1271,15 +1283,19 @@ dpg_status dpg_train_step(dpg_optimizer* o, const float* x, const float* targets
       DPG_CUDA(cudaHostAlloc(&o->step_ring, sizeof(uint64_t) * dpg_optimizer::kStepRing, cudaHostAllocDefault));
       for (auto& e : o->ring_ev) DPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    const int slot = (int)(o->steps % dpg_optimizer::kStepRing);
-    if (o->ring_used[slot]) DPG_CUDA(cudaEventSynchronize(o->ring_ev[slot]));
-    o->step_ring[slot] = o->steps;
-    DPG_CUDA(cudaMemcpyAsync(o->step_dev, &o->step_ring[slot], sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
-    DPG_CUDA(cudaEventRecord(o->ring_ev[slot], ctx->stream));
-    o->ring_used[slot] = true;
+    if (!o->dev_step_known || o->dev_step_next != o->steps) {
+      const int slot = (int)(o->steps % dpg_optimizer::kStepRing);
+      if (o->ring_used[slot]) DPG_CUDA(cudaEventSynchronize(o->ring_ev[slot]));
+      o->step_ring[slot] = o->steps;
+      DPG_CUDA(cudaMemcpyAsync(o->step_dev, &o->step_ring[slot], sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+      DPG_CUDA(cudaEventRecord(o->ring_ev[slot], ctx->stream));
+      o->ring_used[slot] = true;
+    }
     DPG_CUDA(cudaGraphLaunch(hit->exec, ctx->stream));
     ctx->launches += hit->kernels;
     ++o->steps;
+    o->dev_step_known = true;  // the replay's update kernel wrote steps + 1 ... i.e. the new o->steps
+    o->dev_step_next = o->steps;
     mark_done();
   });
 }

@@ -47,18 +47,34 @@ __device__ __forceinline__ void normal_pair(uint64_t seed, uint64_t step, uint64
   z1 = rad * s;
 }
 
+// Graph replays keep the Philox step on the device: every CTA reads it first, and the last CTA
+// to take a ticket (self-resetting counter) writes step + 1 for the next replay — no host-to-device
+// copy per step. Called by every thread of the CTA before any early return.
+__device__ __forceinline__ void advance_step(uint64_t* step_ptr, uint64_t step, unsigned long long* ticket) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ticket, 1ull) == gridDim.x - 1) {
+      atomicExch(ticket, 0ull);
+      *step_ptr = step + 1;
+    }
+  }
+}
+
 // One thread per element pair. If an earlier stage flagged an error (NumericError etc.) the
 // update is skipped: the reference throws before touching the parameters.
 __global__ void __launch_bounds__(256) noise_update_kernel(
     float* __restrict__ params, const float* __restrict__ summed, float* __restrict__ grad,
     int64_t n, double std_dev, float inv_e, float lr, uint64_t seed, uint64_t step,
-    const float* __restrict__ injected, const uint64_t* step_ptr, const DeviceErr* err) {
+    const float* __restrict__ injected, uint64_t* step_ptr, const DeviceErr* err,
+    unsigned long long* advance) {
   pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i0 = 2 * q;
+  if (step_ptr) step = *step_ptr;
+  if (advance) advance_step(step_ptr, step, advance);  // after every CTA has read it
   if (i0 >= n) return;
   if (error_pending(err)) return;
-  if (step_ptr) step = *step_ptr;
   float nz[2] = {0.f, 0.f};
   if (injected) {
     nz[0] = injected[i0];
@@ -82,14 +98,15 @@ __global__ void __launch_bounds__(256) noise_update_kernel(
 
 void launch_noise_update(dpg_ctx* ctx, float* params, const float* summed, float* grad, int64_t n,
                          double sigma, double c, double expected_batch, double lr, uint64_t seed,
-                         uint64_t step, const float* injected, const uint64_t* step_ptr) {
+                         uint64_t step, const float* injected, uint64_t* step_ptr,
+                         unsigned long long* advance) {
   if (n == 0) return;
   const double std_dev = sigma * c;
   const float denom = (float)expected_batch;
   const float inv_e = 1.0f / denom;  // T(1) / denom (optimizer.hpp:259, 264)
   const int64_t pairs = (n + 1) / 2;
   ::dpg::launch_pdl(noise_update_kernel, (unsigned)((pairs + 255) / 256), 256, 0, ctx->stream, 
-      params, summed, grad, n, std_dev, inv_e, (float)lr, seed, step, injected, step_ptr, ctx->dev_err);
+      params, summed, grad, n, std_dev, inv_e, (float)lr, seed, step, injected, step_ptr, ctx->dev_err, advance);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -189,9 +206,10 @@ __global__ void __launch_bounds__(256) noise_update_p2p_kernel(
 }
 
 __global__ void xch_complete_kernel(PeerSet ps, const float* __restrict__ reduced, float* __restrict__ summed,
-                                    int64_t n, uint64_t step, const uint64_t* step_ptr) {
+                                    int64_t n, uint64_t step, uint64_t* step_ptr, unsigned long long* advance) {
   pdl_wait();
   if (step_ptr) step = *step_ptr;
+  if (advance) advance_step(step_ptr, step, advance);
   if (threadIdx.x == 0) wait_all(ps, PeerSet::kAck, step + 1);
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -200,7 +218,8 @@ __global__ void xch_complete_kernel(PeerSet ps, const float* __restrict__ reduce
 
 void launch_noise_update_p2p(dpg_ctx* ctx, const PeerSet& ps, float* params, float* summed, float* reduced,
                              float* grad, int64_t n, double sigma, double c, double expected_batch, double lr,
-                             uint64_t seed, uint64_t step, const float* injected, const uint64_t* step_ptr) {
+                             uint64_t seed, uint64_t step, const float* injected, uint64_t* step_ptr,
+                             unsigned long long* advance) {
   ::dpg::launch_pdl(xch_signal_kernel, 1u, 32, 0, ctx->stream, ps, step, step_ptr);
   DPG_LAUNCH_CHECK(ctx);
   const double std_dev = sigma * c;
@@ -210,7 +229,7 @@ void launch_noise_update_p2p(dpg_ctx* ctx, const PeerSet& ps, float* params, flo
                     reduced, grad, n, std_dev, inv_e, (float)lr, seed, step, injected, step_ptr, ctx->dev_err, ps);
   DPG_LAUNCH_CHECK(ctx);
   ::dpg::launch_pdl(xch_complete_kernel, (unsigned)std::min<int64_t>(kNumSMs, (n + 255) / 256 + 1), 256, 0,
-                    ctx->stream, ps, (const float*)reduced, summed, n, step, step_ptr);
+                    ctx->stream, ps, (const float*)reduced, summed, n, step, step_ptr, advance);
   DPG_LAUNCH_CHECK(ctx);
 }
 

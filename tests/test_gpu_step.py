@@ -231,6 +231,13 @@ def test_graph_replay_equals_eager(ctx):
         o2.train_step(xt, yt, loss, use_graph=True)
     ctx.sync()
     assert np.array_equal(m.store_params(), eager), "graph replay must be bit-identical to eager"
+    # replays advance the Philox step on the device; an eager step in between must resynchronise it
+    m.load_params(params)
+    o5 = dpg.DpOptimizer(m, **cfg)
+    for graph in (True, False, True):
+        o5.train_step(xt, yt, loss, use_graph=graph)
+    ctx.sync()
+    assert np.array_equal(m.store_params(), eager), "graph / eager / graph must equal three eager steps"
     # host-buffer path == device path
     m.load_params(params)
     o3 = dpg.DpOptimizer(m, **cfg)
