@@ -88,6 +88,9 @@ __device__ __forceinline__ void st_stream(float* p, float v) {
 // on the stream drains; pdl_wait() (griddepcontrol.wait) blocks until that kernel has completed
 // and its memory is visible. Every kernel calls it before touching data another kernel wrote.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next kernel on the stream launch before this one finishes (its own pdl_wait still
+// waits for this grid's completion and memory)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Launch with programmatic stream serialization (see pdl_wait); DPG_PDL=0 launches plainly.
 inline bool pdl_enabled() {

@@ -193,6 +193,7 @@ __device__ __forceinline__ float sum_splits(const float* __restrict__ part, int 
 __global__ void fwd_reduce_kernel(const float* __restrict__ part, int ksplit, int64_t M, int64_t oc,
                                   int64_t P, const float* __restrict__ bias, float* __restrict__ y) {
   pdl_wait();
+  pdl_trigger();  // the next GEMM's CTAs may start their prologue beside this short pass
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over oc * M, m fastest
   if (i >= oc * M) return;
   const int64_t c = i / M, m = i - c * M;
@@ -345,6 +346,7 @@ struct ConvDgrad : TileRows {
 __global__ void dgrad_reduce_kernel(const float* __restrict__ part, int ksplit, int64_t n,
                                     const float* __restrict__ mask, float* __restrict__ dx) {
   pdl_wait();
+  pdl_trigger();  // the next GEMM's CTAs may start their prologue beside this short pass
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float acc = sum_splits(part, ksplit, n, i);

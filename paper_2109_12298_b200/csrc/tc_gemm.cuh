@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Pro
   if (nk > 0) mbar_wait(&bars[(nk - 1) % kStages], ((nk - 1) / kStages) & 1);
   tc_fence_after();
   // the main loop is done: the next kernel may launch during the epilogues
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  pdl_trigger();
 
   // epilogue: warp w -> TMEM lanes [32 (w % 4), +32), columns [(w / 4) BN / 2, +BN / 2)
   const int lane_base = 32 * (warp & 3);
