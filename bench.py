@@ -57,9 +57,11 @@ def parse():
     ap.add_argument("--csum-from-record", action="store_true",
                     help="clipped sums as the reference's pass 2 over the stored record (not the headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
-                    help="N > 1: clipped-sum exchange over peer memory inside the update kernel "
-                         "(dpg_optimizer_set_peers) or one NCCL all-reduce")
+    ap.add_argument("--exchange", default="nccl", choices=["p2p", "nccl"],
+                    help="N > 1: one NCCL all-reduce of the clipped sum (default), or the exchange "
+                         "over peer memory inside the update kernel (dpg_optimizer_set_peers)")
+    ap.add_argument("--no-strong", action="store_true",
+                    help="skip the strong-scaling cfg5 line (global batch 4096 split over the ranks)")
     ap.add_argument("--profile-steps", type=int, default=5)
     return ap.parse_args()
 
@@ -69,6 +71,24 @@ def dist_env():
     # one-GPU box (the peer exchange works between processes sharing a GPU); not a measurement
     local = int(os.environ.get("DPG_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), local
+
+
+def spawn_ranks(nranks: int) -> int:
+    """`bench.py --gpus N` started without torchrun: re-launch this command as N ranks under
+    torch.distributed.run on 127.0.0.1 (the driver's own form); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nranks}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def config_for(workload_name: str, global_batch: int, per_rank: int, world: int, detail: dict) -> dict:
+    """The `config` object, with the same keys in both arms (detail: arm-specific settings)."""
+    return {"workload": workload_name, "global_batch": global_batch, "per_rank_batch": per_rank,
+            "parallelism": f"dp{world} (sample shards)" if world > 1 else "dp1 (one GPU)", "detail": detail}
 
 
 def peaks():
@@ -243,7 +263,9 @@ def pick_sample(workload, nthreads, budget_s):
     return max(b, want), kind, cores
 
 
-def cpu_baseline(workload, budget_s=15.0):
+def cpu_baseline(workload, budget_s=15.0, single_thread=True):
+    """The reference on this box's host cores: sample-sharded over all threads (the headline
+    baseline) and, as BASELINE.md §3.1 item 5 asks, the reference as-is on one thread."""
     nthreads = cpu_threads()
     b, kind, cores = pick_sample(workload, nthreads, budget_s / 3)
     times = []
@@ -254,10 +276,16 @@ def cpu_baseline(workload, budget_s=15.0):
         if time.perf_counter() > t_end or len(times) >= 10:
             break
     med = statistics.median(times)
-    return {"value": b / med, "unit": "samples/s", "cores": cores, "kind": kind,
-            "sample": f"{workload.name}: full DP-SGD step of the reference over {b} samples, "
-                      f"median of {len(times)} steps, {'-O3 -march=x86-64-v3 ' if kind == 'reference' else ''}"
-                      f"{cores} host threads (sample-sharded, virtual-step semantics)"}
+    out = {"value": b / med, "unit": "samples/s", "cores": cores, "kind": kind,
+           "sample": f"{workload.name}: full DP-SGD step of the reference over {b} samples, "
+                     f"median of {len(times)} steps, {'-O3 -march=x86-64-v3 ' if kind == 'reference' else ''}"
+                     f"{cores} host threads (sample-sharded, virtual-step semantics)"}
+    if single_thread and cores > 1:
+        b1, kind1, _ = pick_sample(workload, 1, 2.0)
+        t1 = [reference_sample_step(workload, b1, 1)[0] for _ in range(3)]
+        out["single_thread"] = {"value": b1 / statistics.median(t1), "unit": "samples/s", "cores": 1,
+                                "kind": kind1, "sample": f"{b1} samples per step, median of 3 steps, one thread"}
+    return out
 
 
 def run_reference(args, rank, world):
@@ -290,7 +318,8 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": w.name, "global_batch": w.batch * args.gpus, "per_step_sample": b},
+        "config": config_for(w.name, w.batch * args.gpus, w.batch, args.gpus,
+                             {"arm": "reference CPU path", "per_step_sample": b}),
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
                          "sample": f"{b} samples of {w.name} per step, {cores} host threads"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -550,10 +579,14 @@ def run_poisson(args):
 # ------------------------------------------------------------------------------ our arm
 def main():
     args = parse()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     rank, world, local = dist_env()
-    if world > 1 or args.gpus > 1:
+    if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines name the N ranks
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("gloo")
     if args.workload == "cifar_poisson" and args.impl == "ours":
         if rank == 0:
@@ -575,6 +608,10 @@ def main():
     from paper_2109_12298_b200 import dpg
     from paper_2109_12298_b200.configs import WORKLOADS
 
+    ndev = torch.cuda.device_count()
+    shared = world > ndev  # more ranks than GPUs (a 1-GPU box): ranks share devices, protocol check only
+    if shared:
+        local = local % ndev
     torch.cuda.set_device(local)
     ctx = dpg.Context(local)
 
@@ -591,26 +628,36 @@ def main():
                           materialise_grad_sample=materialise,
                           clipped_sum_from_record=args.csum_from_record and materialise)
     exchange = args.exchange if world > 1 else None
-    if exchange == "p2p":
-        handles = [None] * world
-        torch.distributed.all_gather_object(handles, opt.peer_handle())
-        err = ""
-        try:
-            opt.set_peers(rank, handles)
-        except dpg.DpgError as e:  # e.g. no peer access between these GPUs
-            err = str(e)
-        errs = [None] * world
-        torch.distributed.all_gather_object(errs, err)
-        if any(errs):  # every rank must take the same path
-            if not err:
-                opt.set_peers(rank, [handles[rank]])
-            if rank == 0:
-                print(f"peer exchange unavailable ({next(e for e in errs if e)}); using NCCL", file=sys.stderr)
-            exchange = "nccl"
-    if exchange == "nccl":
-        obj = [dpg.Context.nccl_unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(obj, src=0)
-        ctx.init_comm(world, rank, obj[0])
+    if shared and exchange == "nccl":
+        exchange = "p2p"  # NCCL refuses two ranks on one device; CUDA IPC within a device works
+
+    def setup_exchange(o, exchange):
+        """Wire optimizer o into the chosen exchange; returns the exchange actually used."""
+        if exchange == "p2p":
+            handles = [None] * world
+            torch.distributed.all_gather_object(handles, o.peer_handle())
+            err = ""
+            try:
+                o.set_peers(rank, handles)
+            except dpg.DpgError as e:  # e.g. no peer access between these GPUs
+                err = str(e)
+            errs = [None] * world
+            torch.distributed.all_gather_object(errs, err)
+            if any(errs):  # every rank must take the same path
+                if not err:
+                    o.set_peers(rank, [handles[rank]])
+                if rank == 0:
+                    print(f"peer exchange unavailable ({next(e for e in errs if e)}); using NCCL", file=sys.stderr)
+                exchange = "nccl"
+        if exchange == "nccl" and not comm_ready[0]:
+            obj = [dpg.Context.nccl_unique_id() if rank == 0 else None]
+            torch.distributed.broadcast_object_list(obj, src=0)
+            ctx.init_comm(world, rank, obj[0])
+            comm_ready[0] = True
+        return exchange
+
+    comm_ready = [False]
+    exchange = setup_exchange(opt, exchange)
     xt = torch.from_numpy(x).cuda()
     yt = torch.from_numpy(y).cuda()
     loss = torch.zeros(b, device="cuda")
@@ -706,17 +753,22 @@ def main():
     achieved = (d["bytes"] / d["count"]) / (dom_ms * 1e6)  # GB/s
     # DRAM bytes of the dominant stage from the committed ncu --set full capture of the same
     # step (tools/ncu_stages.py), per launch; null when that stage is not in the capture
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{w.name}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            t = json.load(f).get(dom)
+            tj = json.load(f)
+        t = tj.get(dom)
         traffic = t["traffic"] if t else None
+        if t:
+            traffic_src = (f"committed capture {os.path.relpath(tpath, ROOT)} ({tj.get('_source', 'ncu --set full')}); "
+                           "not measured in this run")
     hot, full = step_bytes(w, b, materialise)
     eager_step_ms = sum(v["ms"] for v in prof.values()) / args.profile_steps
     ms_per_step = total_ms / args.steps
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic,
+                "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                "stage_timing": "eager profiled pass (per-stage CUDA events, one stream); value is the graph replay",
                 "algorithmic_bytes_per_launch": d["bytes"] / d["count"], "launch_ms": dom_ms,
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured" else "fallback",
                 "step": {"bytes_full": full, "bytes_hot": hot,
@@ -725,23 +777,65 @@ def main():
                 "stages_ms": {k: round(v["ms"], 5) for k, v in sorted(stages.items(), key=lambda kv: -kv[1]["ms"])},
                 "eager_stage_sum_ms": eager_step_ms}
 
+    # ---- strong scaling, BASELINE configs[4]: global batch 4096 split over the ranks ----
+    strong = None
+    if not args.no_strong and w.name == "cifar_b512" and 4096 % world == 0:
+        w5 = WORKLOADS["cifar_b4096"]
+        from paper_2109_12298_b200.sharding import shard_range
+        lo5, hi5 = shard_range(w5.batch, world, rank)  # contiguous sample shard of ONE global batch
+        per5 = hi5 - lo5
+        p5, x5, y5 = synth(w5, w5.batch)
+        x5, y5 = x5[lo5:hi5], y5[lo5:hi5]
+        m5 = dpg.Model(ctx, w5.layers, w5.in_shape, max_batch=per5)
+        m5.load_params(p5)
+        o5 = dpg.DpOptimizer(m5, noise_multiplier=args.sigma, max_grad_norm=args.max_grad_norm,
+                             learning_rate=0.1, expected_batch_size=float(w5.batch), noise_seed=3,
+                             materialise_grad_sample=materialise)
+        ex5 = setup_exchange(o5, exchange) if world > 1 else None
+        x5t, y5t = torch.from_numpy(x5).cuda(), torch.from_numpy(y5).cuda()
+        l5 = torch.zeros(per5, device="cuda")
+        for _ in range(max(3, args.warmup)):
+            o5.train_step(x5t, y5t, l5)
+        steps5 = max(20, min(args.steps, 200))
+        ev5 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps5)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(steps5):
+            flush.zero_()
+            ev5[i][0].record(stream)
+            o5.train_step(x5t, y5t, l5)
+            ev5[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ctx.sync()
+        t5 = max_over_ranks(sum(a.elapsed_time(c) for a, c in ev5))
+        strong = {"workload": "cifar_b4096", "scaling": "strong", "global_batch": w5.batch, "per_rank_batch": per5,
+                  "n_gpus": world, "steps": steps5, "value": w5.batch * steps5 / (t5 / 1000.0), "unit": "samples/s",
+                  "ms_per_step": t5 / steps5, "exchange": ex5,
+                  "timing": "device (CUDA events), max over ranks, L2 flushed before every step"}
+        del o5, m5
+
     line = {
         "metric": METRICS.get(w.name, METRIC), "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": w.name, "global_batch": gb, "per_rank_batch": b,
-                   "parallelism": "dp1 (one GPU)" if world == 1 else f"dp{world} (sample shards, " + (
-                       "clipped sums summed over peer memory inside the update kernel)" if exchange == "p2p"
-                       else "1 NCCL all-reduce of the clipped sum)"),
-                   "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
-                   "materialise_grad_sample": materialise, "graph": True,
-                   "clipped_sum": "record pass 2" if (args.csum_from_record and materialise) else "(s.B)^T A",
-                   "l2": "256 MiB flush before every timed step (outside the step's events)"},
+        "config": config_for(w.name, gb, b, world, {
+            "arm": "B200 (libdpg.so, CUDA graph per step)",
+            "exchange": None if world == 1 else (
+                "clipped sums summed over peer memory inside the update kernel" if exchange == "p2p"
+                else "1 NCCL all-reduce of the clipped sum (+ status lane)"),
+            "ranks_share_devices": bool(shared),
+            "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
+            "materialise_grad_sample": materialise,
+            "clipped_sum": "record pass 2" if (args.csum_from_record and materialise) else "(s.B)^T A",
+            "l2": "256 MiB flush before every timed step (outside the step's events)"}),
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": gpu_launches,
         "clocks": clk,
     }
+    if strong:
+        line["strong_scaling_cfg5"] = strong
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     if rank == 0:

@@ -7,7 +7,6 @@
 //                  are deterministic and identical on every replay.
 //   materialised : the reference's own pass 2 over a stored record, in its exact order.
 #include "conv_common.cuh"
-#include "igemm.cuh"
 
 namespace dpg {
 
@@ -144,33 +143,6 @@ static void launch_splitk_reduce(dpg_ctx* ctx, const float* part, int splits, in
   DPG_LAUNCH_CHECK(ctx);
 }
 
-struct SplitKStore {
-  float* part;
-  int64_t M, N;
-  template <int TM, int TN>
-  __device__ void store(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
-        if (m < M && n < N) part[((int64_t)z * M + m) * N + n] = acc[i][j];
-      }
-  }
-};
-
-// Choose samples per split so that tiles x splits fills the GPU about twice.
-static int pick_splits(int64_t b, int64_t tiles, int64_t per_sample_k) {
-  int64_t want = (2 * kNumSMs + tiles - 1) / tiles;
-  if (want > b) want = b;
-  // keep at least ~64 k-steps per split
-  const int64_t max_by_k = (b * per_sample_k) / 64;
-  if (want > max_by_k) want = max_by_k;
-  if (want < 1) want = 1;
-  const int64_t spl = (b + want - 1) / want;
-  return (int)((b + spl - 1) / spl);  // every split non-empty
-}
-
 // ------------------------------------------------------------------------------------------
 // Weighted sums over samples with few outputs: out[j] (+)= sum_n s_n v(n, j) (colsum_body).
 // ------------------------------------------------------------------------------------------
@@ -217,39 +189,9 @@ void launch_wsum_multi(dpg_ctx* ctx, const WsumItems& items, const float* scale,
 }
 
 // Linear weight, mid > 1: split-K GEMM over (n, t).
-struct CsLinearProb : SplitKStore {
-  static constexpr bool kAMajorM = true;
-  static constexpr bool kBMajorN = true;
-  static constexpr bool kExact = false;
-  const float* acts;
-  const float* hw;
-  const float* scale;
-  int acts_relu;
-  int64_t K;        // per split: spl * mid
-  int64_t spl, mid, bsz;
-  __device__ float init(int, int64_t, int64_t) const { return 0.f; }
-  __device__ float a(int z, int64_t m, int64_t k) const {
-    const int64_t n = z * spl + k / mid, t = k - (k / mid) * mid;
-    if (n >= bsz) return 0.f;
-    return __ldg(scale + n) * __ldg(hw + (n * mid + t) * M + m);
-  }
-  __device__ float b(int z, int64_t k, int64_t col) const {
-    const int64_t n = z * spl + k / mid, t = k - (k / mid) * mid;
-    if (n >= bsz) return 0.f;
-    return relu_if(__ldg(acts + (n * mid + t) * N + col), acts_relu);
-  }
-  template <int TM, int TN>
-  __device__ void epilogue(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
-    store<TM, TN>(z, m0, n0, tx, ty, acc);
-  }
-};
-
 size_t clipped_sum_ws_linear(int64_t b, int64_t mid, int64_t d, int64_t r) {
   if (mid == 1) return 0;
-  if (use_tc()) return sizeof(float) * (size_t)tc::csum_linear_splits(b, mid, d, r) * (size_t)(r * d);
-  const int64_t tiles = ((r + 63) / 64) * ((d + 63) / 64);
-  const int splits = pick_splits(b, tiles, mid);
-  return sizeof(float) * (size_t)splits * (size_t)(r * d);
+  return sizeof(float) * (size_t)tc::csum_linear_splits(b, mid, d, r) * (size_t)(r * d);
 }
 
 void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw,
@@ -263,77 +205,18 @@ void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, c
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
-  if (use_tc()) {
-    const int splits = tc::csum_linear_splits(b, mid, d, r);
-    tc::linear_csum(ctx, acts, acts_relu, hw, scale, b, mid, d, r, static_cast<float*>(ws), splits);
-    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, r * d, sw, accumulate);
-    return;
-  }
-  const int64_t tiles = ((r + 63) / 64) * ((d + 63) / 64);
-  const int splits = pick_splits(b, tiles, mid);
-  const int64_t spl = (b + splits - 1) / splits;
-  CsLinearProb p;
-  p.part = static_cast<float*>(ws);
-  p.M = r;
-  p.N = d;
-  p.acts = acts;
-  p.hw = hw;
-  p.scale = scale;
-  p.acts_relu = acts_relu;
-  p.K = spl * mid;
-  p.spl = spl;
-  p.mid = mid;
-  p.bsz = b;
-  launch_igemm<64, 64, 16>(ctx, p, splits);
-  launch_splitk_reduce(ctx, p.part, splits, r * d, sw, accumulate);
+  const int splits = tc::csum_linear_splits(b, mid, d, r);
+  tc::linear_csum(ctx, acts, acts_relu, hw, scale, b, mid, d, r, static_cast<float*>(ws), splits);
+  launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, r * d, sw, accumulate);
 }
 
 // ------------------------------------------------------------------------------------------
 // Conv weight: S[oc, k] = sum_{n, p} (scale_n * B[n, oc, p]) * X~[n, k, p] — the conv weight
 // gradient of the clip-scaled highway; split-K over samples.
 // ------------------------------------------------------------------------------------------
-struct CsConvProb : SplitKStore {
-  static constexpr bool kAMajorM = false;
-  static constexpr bool kBMajorN = false;
-  static constexpr bool kExact = false;
-  Im2col xc;
-  const float* hw;
-  const float* scale;
-  int64_t K, spl, P, bsz;
-  __device__ float init(int, int64_t, int64_t) const { return 0.f; }
-  __device__ float a(int z, int64_t m, int64_t k) const {
-    const int64_t q = k / P;
-    const int64_t n = z * spl + q, p = k - q * P;
-    if (n >= bsz) return 0.f;
-    return __ldg(scale + n) * __ldg(hw + (n * M + m) * P + p);
-  }
-  __device__ float b(int z, int64_t k, int64_t col) const {
-    const int64_t q = k / P;
-    const int64_t n = z * spl + q, p = k - q * P;
-    if (n >= bsz) return 0.f;
-    return xc(n, (int)col, (int)p);
-  }
-  template <int TM, int TN>
-  __device__ void epilogue(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
-    store<TM, TN>(z, m0, n0, tx, ty, acc);
-  }
-};
-
-static void cs_conv_tiles(const ConvGeom& g, int& bm, int& bn) {
-  bm = g.oc <= 32 ? 32 : 64;
-  bn = g.K() <= 32 ? 32 : 64;
-}
-
 size_t clipped_sum_ws_conv2d(const ConvGeom& g) {
-  if (ds::enabled()) return sizeof(float) * (size_t)ds::csum_splits(g) * (size_t)(g.oc * g.K());
   if (tk::supported(g)) return sizeof(float) * (size_t)tk::csum_splits(g) * (size_t)(g.oc * g.K());
-  if (ps::supported_csum(g)) return sizeof(float) * (size_t)ps::csum_splits(g) * (size_t)(g.oc * g.K());
-  if (use_tc()) return sizeof(float) * (size_t)tc::csum_conv_splits(g) * (size_t)(g.oc * g.K());
-  int bm, bn;
-  cs_conv_tiles(g, bm, bn);
-  const int64_t tiles = ((g.oc + bm - 1) / bm) * ((g.K() + bn - 1) / bn);
-  const int splits = pick_splits(g.b, tiles, g.P());
-  return sizeof(float) * (size_t)splits * (size_t)(g.oc * g.K());
+  return sizeof(float) * (size_t)tc::csum_conv_splits(g) * (size_t)(g.oc * g.K());
 }
 
 void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
@@ -341,51 +224,15 @@ void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const f
                                int accumulate, void* ws) {
   (void)sb;  // the bias clipped sum is a weighted sum of the bias records (launch_wsum_multi)
   const int64_t nw = g.oc * g.K();
-  if (ds::enabled()) {
-    const int splits = ds::csum_splits(g);
-    ds::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
-    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
-    return;
-  }
   if (tk::supported(g)) {
     const int splits = tk::csum_splits(g);
     tk::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
     launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
     return;
   }
-  if (ps::supported_csum(g)) {
-    const int splits = ps::csum_splits(g);
-    ps::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
-    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
-    return;
-  }
-  if (use_tc()) {
-    const int splits = tc::csum_conv_splits(g);
-    tc::conv_csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
-    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
-    return;
-  }
-  int bm, bn;
-  cs_conv_tiles(g, bm, bn);
-  const int64_t tiles = ((g.oc + bm - 1) / bm) * ((g.K() + bn - 1) / bn);
-  const int splits = pick_splits(g.b, tiles, g.P());
-  const int64_t spl = (g.b + splits - 1) / splits;
-  CsConvProb p;
-  p.part = static_cast<float*>(ws);
-  p.M = g.oc;
-  p.N = g.K();
-  p.xc = make_im2col(x, x_relu, g);
-  p.hw = hw;
-  p.scale = scale;
-  p.K = spl * g.P();
-  p.spl = spl;
-  p.P = g.P();
-  p.bsz = g.b;
-  if (bm == 32 && bn == 32) launch_igemm<32, 32, 16>(ctx, p, splits);
-  else if (bm == 32) launch_igemm<32, 64, 16>(ctx, p, splits);
-  else if (bn == 32) launch_igemm<64, 32, 16>(ctx, p, splits);
-  else launch_igemm<64, 64, 16>(ctx, p, splits);
-  launch_splitk_reduce(ctx, p.part, splits, g.oc * g.K(), sw, accumulate);
+  const int splits = tc::csum_conv_splits(g);
+  tc::conv_csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
+  launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -603,8 +450,7 @@ void launch_clipped_sum_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const i
   const size_t smem = sizeof(float) * kCsRows * (size_t)dim + sizeof(int) * ((size_t)b + 1 + 3 * kCsMaxEntries);
   if (smem > 200 * 1024) raise(DPG_ERR_DIMENSION, "clipped_sum_embedding: batch or embedding_dim too large for one chunk");
   if (smem > 48 * 1024)
-    DPG_CUDA(cudaFuncSetAttribute(clipped_sum_embedding_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_smem_attr(reinterpret_cast<const void*>(clipped_sum_embedding_kernel), (int)smem);
   ::dpg::launch_pdl(clipped_sum_embedding_kernel, (unsigned)nchunks, 256, smem, ctx->stream, 
       sorted_v, sorted_s, starts, hw, scale, b, t, vocab, dim, nchunks, summed, accumulate);
   DPG_LAUNCH_CHECK(ctx);

@@ -2,18 +2,24 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "dpg_internal.h"
 
 namespace dpg {
 
-bool use_tc() {
-  static const bool on = [] {
-    const char* e = std::getenv("DPG_SIMT");
-    return !(e && e[0] == '1');
-  }();
-  return on;
+void ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  DPG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{dev, fn}];
+  if (bytes <= have) return;
+  DPG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
 }
 
 std::string& thread_err() {
@@ -57,6 +63,9 @@ void throw_device_error(dpg_ctx* ctx, ErrNamer names, const void* user) {
       raise(DPG_ERR_NUMERIC, "non-finite per-sample gradient in " +
                                  (who.empty() ? "parameter " + std::to_string(major) : who) +
                                  " (sample " + std::to_string(minor) + ")");
+    case ERR_STAGE_REMOTE:
+      raise(DPG_ERR_NUMERIC, "another rank of the sample-sharded step reported an error; the update "
+                             "was skipped on every rank");
     default:
       raise(DPG_ERR_INTERNAL, "unknown device error record");
   }
@@ -246,6 +255,7 @@ dpg_status dpg_ctx_init_comm(dpg_ctx* ctx, int nranks, int rank, const unsigned 
     }
     ncclUniqueId uid;
     std::memcpy(uid.internal, id, 128);
+    ++ctx->comm_gen;  // (also when the init below fails: graphs holding the old comm are stale)
     DPG_NCCL(ncclCommInitRank(&ctx->comm, nranks, uid, rank));
     ctx->nranks = nranks;
     ctx->rank = rank;

@@ -64,9 +64,20 @@ __device__ __forceinline__ float4 ldg4_or_zero(const float* p, bool ok) {
   return __ldg(reinterpret_cast<const float4*>(q));
 }
 
+// Record (key, aux) if key precedes the recorded key. Key and aux change together under a lock
+// word, so the aux always belongs to the recorded key (errors are rare: the lock is off the fast
+// path, which is one relaxed read).
 __device__ __forceinline__ void report_error(DeviceErr* err, uint64_t key, uint64_t aux) {
-  const unsigned long long old = atomicMin(&err->key, (unsigned long long)key);
-  if (key < old) atomicExch(&err->aux, (unsigned long long)aux);
+  if (key >= *(volatile unsigned long long*)&err->key) return;
+  while (atomicCAS(&err->lock, 0u, 1u) != 0u) __nanosleep(32);
+  __threadfence();
+  if (key < *(volatile unsigned long long*)&err->key) {
+    *(volatile unsigned long long*)&err->aux = aux;
+    __threadfence();
+    *(volatile unsigned long long*)&err->key = key;
+  }
+  __threadfence();
+  atomicExch(&err->lock, 0u);
 }
 
 __device__ __forceinline__ bool error_pending(const DeviceErr* err) {

@@ -46,6 +46,7 @@ enum ErrStage : uint64_t {
   ERR_STAGE_EMBED_INDEX = 1,  // layers.hpp:425-426 (forward gather)
   ERR_STAGE_TARGET = 2,       // layers.hpp:905
   ERR_STAGE_NONFINITE = 3,    // optimizer.hpp:77-83
+  ERR_STAGE_REMOTE = 4,       // another rank of the sample-sharded step reported an error
 };
 __host__ __device__ inline uint64_t err_key(uint64_t stage, uint64_t major, uint64_t sample) {
   return (stage << 56) | ((major & 0xFFFFFFull) << 32) | (sample & 0xFFFFFFFFull);
@@ -55,6 +56,8 @@ constexpr uint64_t ERR_NONE = ~0ull;
 struct DeviceErr {
   unsigned long long key;  // ERR_NONE when clear
   unsigned long long aux;  // stage-specific detail (e.g. the raw index bits)
+  unsigned int lock;       // report_error's writer lock (key and aux are updated together)
+  unsigned int pad;
 };
 
 }  // namespace dpg
@@ -66,7 +69,8 @@ struct dpg_ctx {
   std::string err;
   int64_t launches = 0;
   dpg::DeviceErr* dev_err = nullptr;  // device
-  unsigned long long* clip_sync = nullptr;  // device [2]: clip_factors' clipped count + CTA ticket (self-resetting)
+  unsigned long long* clip_sync = nullptr;
+  uint64_t comm_gen = 0;  // bumped by dpg_ctx_init_comm: captured steps of an older communicator are stale  // device [2]: clip_factors' clipped count + CTA ticket (self-resetting)
   dpg::DeviceErr* host_err = nullptr; // pinned mirror
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -109,6 +113,11 @@ namespace dpg {
 using ErrNamer = std::string (*)(const void* user, uint64_t stage, uint64_t major);
 void throw_device_error(dpg_ctx* ctx, ErrNamer names, const void* user);
 void sync_ctx(dpg_ctx* ctx);
+
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the current device.
+// Attributes are per (device, function), so the record is keyed on both and guarded by a mutex:
+// several host threads may each drive their own GPU (one context per thread).
+void ensure_smem_attr(const void* fn, int bytes);
 
 inline void count_launch(dpg_ctx* ctx) { ++ctx->launches; }
 
@@ -162,10 +171,6 @@ struct ConvGeom {
   int64_t P() const { return oh * ow; }
 };
 
-// Kernel family selection: tcgen05 (default) or the SIMT implicit-GEMM path (DPG_SIMT=1,
-// kept for A/B measurements). Read once per process.
-bool use_tc();
-
 namespace tc {
 size_t fwd_ws_bytes(const ConvGeom& cg);
 void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
@@ -188,16 +193,6 @@ void linear_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, con
                  int64_t b, int64_t mid, int64_t d, int64_t r, float* part, int splits);
 }  // namespace tc
 
-namespace ds {
-bool enabled();
-int gs_rows(const ConvGeom& g);
-void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
-        double* sq_part);
-int csum_splits(const ConvGeom& g);
-void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* scale,
-          const ConvGeom& g, float* part, int splits);
-}  // namespace ds
-
 namespace tk {  // thin-K conv layers (ic*kh*kw <= 64) on CUDA cores: rule (+ bias rule), clipped sum
 bool supported(const ConvGeom& g);
 void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
@@ -213,17 +208,6 @@ int gs_rows(const ConvGeom& g);
 void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
         double* sq_part, float* gb = nullptr, double* sq_b = nullptr);
 }  // namespace rs
-
-namespace ps {
-bool supported(const ConvGeom& g);       // per-sample gradient path
-bool supported_csum(const ConvGeom& g);  // clipped-sum path (A/B only)
-int gs_rows(const ConvGeom& g);
-void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
-        double* sq_part, float* gb = nullptr, double* sq_b = nullptr);
-int csum_splits(const ConvGeom& g);
-void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* scale,
-          const ConvGeom& g, float* part, int splits);
-}  // namespace ps
 
 // rules.cu — per-sample gradients
 int sq_rows_linear(int64_t mid, int64_t d, int64_t r);
@@ -287,7 +271,9 @@ void launch_weighted_sum_materialised(dpg_ctx* ctx, const float* g, const float*
 void launch_noise_update(dpg_ctx* ctx, float* params, const float* summed, float* grad, int64_t n,
                          double sigma, double c, double expected_batch, double lr, uint64_t seed,
                          uint64_t step, const float* injected, uint64_t* step_ptr,
-                         unsigned long long* advance = nullptr);
+                         unsigned long long* advance = nullptr, const float* status = nullptr);
+// multi-rank steps: lane = error_pending ? 1 : 0, exchanged with the clipped sum (noise.cu)
+void launch_status_lane(dpg_ctx* ctx, float* lane);
 void launch_gaussian(dpg_ctx* ctx, float* out, int64_t n, double std_dev, uint64_t seed,
                      uint64_t step);
 // the clipped-sum exchange over peer memory (noise.cu): rank r's optimizer arena mapped by every

@@ -9,57 +9,21 @@
 namespace dpg {
 
 // ------------------------------------------------------------------------------------------
-// conv2d forward (layers.hpp:432-467): Y[n, oc, p] = bias[oc] + sum_k W[oc, k] X~[n, k, p];
-// GEMM M = oc, N = b*P, K = ic*kh*kw; the accumulator starts from the bias as the reference's
-// does (layers.hpp:458).
+// conv2d forward (layers.hpp:432-467) and dgrad (:630-649): tcgen05 implicit GEMMs (tc_conv.cu);
+// a SIMT gather-form dgrad remains for geometries the tcgen05 tap tables do not cover
+// (stride > 4, output extents >= 255).
 // ------------------------------------------------------------------------------------------
-struct ConvFwdProb {
-  static constexpr bool kAMajorM = false;  // W[oc, k] contiguous in k
-  static constexpr bool kBMajorN = true;   // consecutive n -> consecutive output positions
-  static constexpr bool kExact = false;
-  Im2col xc;
-  const float* w;
-  const float* bias;
-  float* y;
-  int64_t M, N, K, P;
-  __device__ float init(int, int64_t m, int64_t) const { return (bias && m < M) ? __ldg(bias + m) : 0.f; }
-  __device__ float a(int, int64_t m, int64_t k) const { return __ldg(w + m * K + k); }
-  __device__ float b(int, int64_t k, int64_t nn) const {
-    const int64_t n = nn / P, p = nn - n * P;
-    return xc(n, (int)k, (int)p);
-  }
-  template <int TM, int TN>
-  __device__ void epilogue(int, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int64_t m = m0 + ty + 16 * i, nn = n0 + tx + 16 * j;
-        if (m < M && nn < N) {
-          const int64_t n = nn / P, p = nn - n * P;
-          y[(n * M + m) * P + p] = acc[i][j];
-        }
-      }
-  }
-};
-
 size_t conv_fwd_ws_bytes(const ConvGeom& g) {
-  return use_tc() ? tc::fwd_ws_bytes(g) : 0;
+  return tc::fwd_ws_bytes(g);
 }
 size_t conv_dgrad_ws_bytes(const ConvGeom& g) {
-  return (use_tc() && tc::dgrad_supported(g)) ? tc::dgrad_ws_bytes(g) : 0;
+  return tc::dgrad_supported(g) ? tc::dgrad_ws_bytes(g) : 0;
 }
 
 void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
                        const ConvGeom& g, float* y, void* ws) {
   if (g.b == 0) return;
-  if (use_tc()) {
-    tc::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws);
-    return;
-  }
-  ConvFwdProb p{make_im2col(x, x_relu, g), w, bias, y, g.oc, g.b * g.P(), g.K(), g.P()};
-  if (g.oc <= 32) launch_igemm<32, 128, 16>(ctx, p, 1);
-  else launch_igemm<64, 64, 16>(ctx, p, 1);
+  tc::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -129,7 +93,7 @@ struct ConvDgradProb {
 void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
                          const float* mask_src, float* dx, void* ws) {
   if (g.b == 0) return;
-  if (use_tc() && tc::dgrad_supported(g)) {
+  if (tc::dgrad_supported(g)) {
     tc::conv_dgrad(ctx, dy, w, g, mask_src, dx, ws);
     return;
   }

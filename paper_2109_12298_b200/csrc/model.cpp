@@ -178,6 +178,7 @@ struct dpg_optimizer {
   static constexpr size_t kMaxGraphs = 8;
   std::vector<Graph> graphs;
   uint64_t graph_clock = 0;
+  uint64_t graph_comm_gen = 0;  // ctx->comm_gen the cached graphs were captured under
   // pinned ring the graph replays read their Philox step from (a pageable source could make the
   // H2D wait for the stream); a slot is reused only after the copy that read it has executed
   static constexpr int kStepRing = 16;
@@ -580,6 +581,9 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
 void finish_impl(dpg_optimizer* o, bool graph_mode) {
   dpg_model* m = o->m;
   dpg_ctx* ctx = m->ctx;
+  // multi-rank: the status lane summed[L] travels with the clipped sum, so an error on any rank
+  // skips the update on every rank (see noise.cu)
+  if (o->peers.world > 1 || ctx->comm) dpg::launch_status_lane(ctx, o->summed + m->L);
   if (o->peers.world > 1) {
     dpg::ProfScope ps(ctx, "noise_update", 16.0 * m->L + 4.0 * o->peers.world * m->L, 0.0);
     dpg::launch_noise_update_p2p(ctx, o->peers, m->p_params, o->summed, o->reduced, o->grad, m->L,
@@ -595,13 +599,14 @@ void finish_impl(dpg_optimizer* o, bool graph_mode) {
   }
   if (ctx->comm) {
     dpg::ProfScope ps(ctx, "allreduce", 8.0 * m->L, 0.0);
-    DPG_NCCL(ncclAllReduce(o->summed, o->summed, (size_t)m->L, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
+    DPG_NCCL(ncclAllReduce(o->summed, o->summed, (size_t)m->L + 1, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
   }
   dpg::ProfScope ps(ctx, "noise_update", 16.0 * m->L, 0.0);
   dpg::launch_noise_update(ctx, m->p_params, o->summed, o->grad, m->L, o->cfg.noise_multiplier,
                            o->cfg.max_grad_norm, o->cfg.expected_batch_size,
                            o->cfg.learning_rate, o->cfg.noise_seed, o->steps, o->injected,
-                           graph_mode ? o->step_dev : nullptr, graph_mode ? o->step_tick : nullptr);
+                           graph_mode ? o->step_dev : nullptr, graph_mode ? o->step_tick : nullptr,
+                           ctx->comm ? o->summed + m->L : nullptr);
   if (!graph_mode) {
     ++o->steps;
     o->dev_step_known = false;
@@ -981,9 +986,10 @@ dpg_status dpg_optimizer_create(dpg_model* m, const dpg_optimizer_config* cfg, d
       if (pi.is_bias) bias_numel = std::max(bias_numel, pi.offset + pi.numel);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t rec = cfg->materialise_grad_sample ? sizeof(float) * (size_t)(B * L) : sizeof(float) * (size_t)(B * bias_numel);
-    size_t total = 2 * al(sizeof(float) * L) + al(rec) + al(sizeof(double) * m->sq_rows * B) +
+    // summed / reduced: L clipped-sum elements + the multi-rank status lane (noise.cu)
+    size_t total = al(sizeof(float) * (L + 1)) + al(sizeof(float) * L) + al(rec) + al(sizeof(double) * m->sq_rows * B) +
                    al(sizeof(double) * B) + al(sizeof(float) * B) + al(sizeof(int64_t)) + al(sizeof(uint64_t)) +
-                   al(sizeof(float) * L) + al(3 * 128) + al(sizeof(unsigned long long));
+                   al(sizeof(float) * (L + 1)) + al(3 * 128) + al(sizeof(unsigned long long));
     DPG_CUDA(cudaMalloc(&o->arena, total));
     DPG_CUDA(cudaMemset(o->arena, 0, total));
     char* p = o->arena;
@@ -992,7 +998,7 @@ dpg_status dpg_optimizer_create(dpg_model* m, const dpg_optimizer_config* cfg, d
       p += al(bytes);
       return r;
     };
-    o->summed = reinterpret_cast<float*>(take(sizeof(float) * L));
+    o->summed = reinterpret_cast<float*>(take(sizeof(float) * (L + 1)));
     o->grad = reinterpret_cast<float*>(take(sizeof(float) * L));
     float* r = reinterpret_cast<float*>(take(rec));
     if (cfg->materialise_grad_sample) o->record = r; else o->bias_scratch = r;
@@ -1001,7 +1007,7 @@ dpg_status dpg_optimizer_create(dpg_model* m, const dpg_optimizer_config* cfg, d
     o->scale = reinterpret_cast<float*>(take(sizeof(float) * B));
     o->num_clipped = reinterpret_cast<int64_t*>(take(sizeof(int64_t)));
     o->step_dev = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t)));
-    o->reduced = reinterpret_cast<float*>(take(sizeof(float) * L));
+    o->reduced = reinterpret_cast<float*>(take(sizeof(float) * (L + 1)));
     o->xflags = reinterpret_cast<unsigned long long*>(take(3 * 128));
     o->step_tick = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long)));
   });
@@ -1232,6 +1238,14 @@ dpg_status dpg_train_step(dpg_optimizer* o, const float* x, const float* targets
       o->pending_x = x;
       step_impl(o, x, false);
       return;
+    }
+    if (o->graph_comm_gen != ctx->comm_gen) {
+      // the communicator changed (dpg_ctx_init_comm): graphs captured with the old one (or with
+      // none) would all-reduce on a destroyed communicator or not at all
+      DPG_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (auto& g : o->graphs) cudaGraphExecDestroy(g.exec);
+      o->graphs.clear();
+      o->graph_comm_gen = ctx->comm_gen;
     }
     dpg_optimizer::Graph* hit = nullptr;
     for (auto& g : o->graphs)

@@ -61,20 +61,45 @@ __device__ __forceinline__ void advance_step(uint64_t* step_ptr, uint64_t step, 
   }
 }
 
+// Multi-rank steps carry one status lane after the L clipped-sum elements: each rank writes 1 when
+// it has an error pending (non-finite per-sample gradient, bad target / index), the exchange
+// sums the lanes with the clipped sums, and every rank skips the update when the sum is
+// non-zero — the reference's step throws before touching any parameter, on every rank alike.
+__global__ void status_lane_kernel(float* __restrict__ lane, const DeviceErr* err) {
+  pdl_wait();
+  if (threadIdx.x == 0) *lane = error_pending(err) ? 1.f : 0.f;
+}
+
+void launch_status_lane(dpg_ctx* ctx, float* lane) {
+  ::dpg::launch_pdl(status_lane_kernel, 1u, 32, 0, ctx->stream, lane, (const DeviceErr*)ctx->dev_err);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+// true when the step must not update: a local error, or (status lane) an error on another rank,
+// which is then recorded locally so the host surfaces it here too
+__device__ __forceinline__ bool skip_update(DeviceErr* err, float status) {
+  if (error_pending(err)) return true;
+  if (status != 0.f) {
+    report_error(err, err_key(ERR_STAGE_REMOTE, 0, 0), 0);
+    return true;
+  }
+  return false;
+}
+
 // One thread per element pair. If an earlier stage flagged an error (NumericError etc.) the
 // update is skipped: the reference throws before touching the parameters.
 __global__ void __launch_bounds__(256) noise_update_kernel(
     float* __restrict__ params, const float* __restrict__ summed, float* __restrict__ grad,
     int64_t n, double std_dev, float inv_e, float lr, uint64_t seed, uint64_t step,
-    const float* __restrict__ injected, uint64_t* step_ptr, const DeviceErr* err,
-    unsigned long long* advance) {
+    const float* __restrict__ injected, uint64_t* step_ptr, DeviceErr* err,
+    unsigned long long* advance, const float* status) {
   pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i0 = 2 * q;
   if (step_ptr) step = *step_ptr;
   if (advance) advance_step(step_ptr, step, advance);  // after every CTA has read it
   if (i0 >= n) return;
-  if (error_pending(err)) return;
+  if (skip_update(err, status ? *status : 0.f)) return;
   float nz[2] = {0.f, 0.f};
   if (injected) {
     nz[0] = injected[i0];
@@ -99,14 +124,15 @@ __global__ void __launch_bounds__(256) noise_update_kernel(
 void launch_noise_update(dpg_ctx* ctx, float* params, const float* summed, float* grad, int64_t n,
                          double sigma, double c, double expected_batch, double lr, uint64_t seed,
                          uint64_t step, const float* injected, uint64_t* step_ptr,
-                         unsigned long long* advance) {
+                         unsigned long long* advance, const float* status) {
   if (n == 0) return;
   const double std_dev = sigma * c;
   const float denom = (float)expected_batch;
   const float inv_e = 1.0f / denom;  // T(1) / denom (optimizer.hpp:259, 264)
   const int64_t pairs = (n + 1) / 2;
   ::dpg::launch_pdl(noise_update_kernel, (unsigned)((pairs + 255) / 256), 256, 0, ctx->stream, 
-      params, summed, grad, n, std_dev, inv_e, (float)lr, seed, step, injected, step_ptr, ctx->dev_err, advance);
+      params, summed, grad, n, std_dev, inv_e, (float)lr, seed, step, injected, step_ptr, ctx->dev_err, advance,
+      status);
   DPG_LAUNCH_CHECK(ctx);
 }
 
@@ -157,11 +183,18 @@ __global__ void xch_signal_kernel(PeerSet ps, uint64_t step, const uint64_t* ste
 __global__ void __launch_bounds__(256) noise_update_p2p_kernel(
     float* __restrict__ params, float* __restrict__ reduced, float* __restrict__ grad, int64_t n,
     double std_dev, float inv_e, float lr, uint64_t seed, uint64_t step, const float* __restrict__ injected,
-    const uint64_t* step_ptr, const DeviceErr* err, PeerSet ps) {
+    const uint64_t* step_ptr, DeviceErr* err, PeerSet ps) {
   pdl_wait();
   if (step_ptr) step = *step_ptr;
   const unsigned long long e = step + 1;
-  if (threadIdx.x == 0) wait_all(ps, PeerSet::kSig, e);
+  __shared__ float status;  // sum of the W status lanes (element n of every clipped-sum buffer)
+  if (threadIdx.x == 0) {
+    wait_all(ps, PeerSet::kSig, e);
+    float st = 0.f;
+    for (int r = 0; r < ps.world; ++r) st += __ldcg(ps.summed[r] + n);
+    status = st;
+    if (blockIdx.x == 0) reduced[n] = st;
+  }
   __syncthreads();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i0 = 2 * q;
@@ -181,7 +214,7 @@ __global__ void __launch_bounds__(256) noise_update_p2p_kernel(
       nz[0] = (float)(z0 * std_dev);
       nz[1] = (float)(z1 * std_dev);
     }
-    const bool skip = error_pending(err);  // still takes part in the exchange: peers wait on us
+    const bool skip = skip_update(err, status);  // still takes part in the exchange: peers wait on us
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int64_t i = i0 + k;
@@ -212,8 +245,8 @@ __global__ void xch_complete_kernel(PeerSet ps, const float* __restrict__ reduce
   if (advance) advance_step(step_ptr, step, advance);
   if (threadIdx.x == 0) wait_all(ps, PeerSet::kAck, step + 1);
   __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    summed[i] = reduced[i];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    summed[i] = reduced[i];  // (element n: the summed status lane)
 }
 
 void launch_noise_update_p2p(dpg_ctx* ctx, const PeerSet& ps, float* params, float* summed, float* reduced,

@@ -190,11 +190,7 @@ static size_t smem_bytes(const Params& p) {
 }
 
 bool supported(const ConvGeom& g) {
-  static const bool off = [] {
-    const char* e = std::getenv("DPG_RS");
-    return e && e[0] == '0';
-  }();
-  if (off || g.P() > kMaxP || g.kh >= 32 || g.kw >= 32 || g.ic >= (1 << 21)) return false;
+  if (g.P() > kMaxP || g.kh >= 32 || g.kw >= 32 || g.ic >= (1 << 21)) return false;
   return smem_bytes(make_params(nullptr, 0, nullptr, g)) <= 160 * 1024;
 }
 
@@ -211,11 +207,7 @@ void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom&
   const size_t smem = smem_bytes(p);
   dim3 grid((unsigned)p.osplit, (unsigned)g.b);
   auto go = [&](auto kern) {
-    static int attr = 0;
-    if ((int)smem > attr) {
-      DPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-      attr = 160 * 1024;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), (int)smem);
     ::dpg::launch_pdl(kern, grid, kThreads, smem, ctx->stream, p);
   };
   switch (pick_pt(p.P)) {

@@ -9,7 +9,6 @@
 // Norm partials go to a [rows, b] double slab (one row per output tile); clip_factors sums the
 // rows in parameter order (optimizer.hpp:67-89).
 #include "conv_common.cuh"
-#include "igemm.cuh"
 
 namespace dpg {
 
@@ -60,45 +59,9 @@ __global__ void __launch_bounds__(256) gs_linear_outer_kernel(const float* __res
   if (threadIdx.x == 0 && sq_part) sq_part[(int64_t)blockIdx.x * b + n] = t;
 }
 
-// Linear, mid > 1 (cfg2, T = 64): per-sample GEMM G[n] = B[n]^T A[n], M = r, N = d, K = mid.
-struct GsLinearProb {
-  static constexpr bool kAMajorM = true;   // hw[n, t, o]: contiguous along o (= m)
-  static constexpr bool kBMajorN = true;   // acts[n, t, i]: contiguous along i (= n)
-  static constexpr bool kExact = false;
-  const float* acts;
-  const float* hw;
-  float* gw;
-  double* sq_part;
-  int acts_relu;
-  int64_t M, N, K, bsz;
-  __device__ float init(int, int64_t, int64_t) const { return 0.f; }
-  __device__ float a(int z, int64_t m, int64_t k) const { return __ldg(hw + ((int64_t)z * K + k) * M + m); }
-  __device__ float b(int z, int64_t k, int64_t n) const {
-    return relu_if(__ldg(acts + ((int64_t)z * K + k) * N + n), acts_relu);
-  }
-  template <int TM, int TN>
-  __device__ void epilogue(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
-    double sq = 0.0;
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
-        if (m < M && n < N) {
-          if (gw) st_stream(gw + ((int64_t)z * M + m) * N + n, acc[i][j]);
-          sq += (double)acc[i][j] * acc[i][j];
-        }
-      }
-    tile_sq_store<TM, TN>(sq, sq_part, bsz, z);
-  }
-};
-
-constexpr int kLinBM = 64, kLinBN = 64, kLinBK = 16;
-
 int sq_rows_linear(int64_t mid, int64_t d, int64_t r) {
   if (mid == 1) return (int)((r * d + kOuterChunk - 1) / kOuterChunk);
-  if (use_tc()) return tc::gs_linear_rows(d, r);
-  return (int)(((r + kLinBM - 1) / kLinBM) * ((d + kLinBN - 1) / kLinBN));
+  return tc::gs_linear_rows(d, r);
 }
 
 void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw, int64_t b,
@@ -110,71 +73,25 @@ void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const floa
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
-  if (use_tc()) {
-    tc::linear_gs(ctx, acts, acts_relu, hw, b, mid, d, r, gw, sq_part);
-    return;
-  }
-  GsLinearProb p{acts, hw, gw, sq_part, acts_relu, r, d, mid, b};
-  launch_igemm<kLinBM, kLinBN, kLinBK>(ctx, p, b);
+  tc::linear_gs(ctx, acts, acts_relu, hw, b, mid, d, r, gw, sq_part);
 }
 
 // ------------------------------------------------------------------------------------------
 // Conv2d: G[n, oc, k] = sum_p B[n, oc, p] * X~[n, k, p], X~ = im2col(x) gathered on the fly
 // (layers.hpp:290-324 index map: k = (c*kh + ki)*kw + kj, p = oy*ow + ox).
 // ------------------------------------------------------------------------------------------
-struct GsConvProb {
-  static constexpr bool kAMajorM = false;  // hw[n, oc, p]: contiguous along p (= k)
-  static constexpr bool kBMajorN = false;  // X~[n, kcol, p]: walk p fastest
-  static constexpr bool kExact = false;
-  Im2col xc;
-  const float* hw;
-  float* gw;
-  double* sq_part;
-  int64_t M, N, K, bsz;  // M = oc, N = ic*kh*kw, K = P
-  __device__ float init(int, int64_t, int64_t) const { return 0.f; }
-  __device__ float a(int z, int64_t m, int64_t k) const { return __ldg(hw + ((int64_t)z * M + m) * K + k); }
-  __device__ float b(int z, int64_t k, int64_t n) const { return xc((int64_t)z, (int)n, (int)k); }
-  template <int TM, int TN>
-  __device__ void epilogue(int z, int64_t m0, int64_t n0, int tx, int ty, float (&acc)[TM][TN]) const {
-    double sq = 0.0;
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
-        if (m < M && n < N) {
-          if (gw) st_stream(gw + ((int64_t)z * M + m) * N + n, acc[i][j]);
-          sq += (double)acc[i][j] * acc[i][j];
-        }
-      }
-    tile_sq_store<TM, TN>(sq, sq_part, bsz, z);
-  }
-};
-
-static void conv_tiles(const ConvGeom& g, int& bm, int& bn) {
-  bm = g.oc <= 32 ? 32 : 64;
-  bn = g.K() <= 32 ? 32 : 64;
-}
-
 int sq_rows_conv2d(const ConvGeom& g) {
-  if (ds::enabled()) return ds::gs_rows(g);
   if (tk::supported(g)) return 1;
-  if (rs::supported(g)) return rs::gs_rows(g);  // (ds is opt-in and overrides both)
-  if (ps::supported(g)) return ps::gs_rows(g);
-  if (use_tc()) return tc::gs_conv_rows(g);
-  int bm, bn;
-  conv_tiles(g, bm, bn);
-  return (int)(((g.oc + bm - 1) / bm) * ((g.K() + bn - 1) / bn));
+  if (rs::supported(g)) return rs::gs_rows(g);
+  return tc::gs_conv_rows(g);
 }
 
 bool gs_conv2d_fuses_bias(const ConvGeom& g) {
-  return !ds::enabled() && (tk::supported(g) || rs::supported(g) || ps::supported(g));
+  return tk::supported(g) || rs::supported(g);
 }
 int sq_rows_conv2d_bias(const ConvGeom& g) {
-  if (ds::enabled()) return 1;
   if (tk::supported(g)) return 1;
   if (rs::supported(g)) return rs::gs_rows(g);
-  if (ps::supported(g)) return ps::gs_rows(g);
   return 1;
 }
 
@@ -182,34 +99,16 @@ void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
                       float* gw, double* sq_part, float* gb, double* sq_b) {
   if (g.b == 0) return;
   const bool bias = gb || sq_b;
-  if (!ds::enabled() && tk::supported(g)) {
+  if (tk::supported(g)) {
     tk::gs(ctx, x, x_relu, hw, g, gw, sq_part, gb, sq_b);
     return;
   }
-  if (!ds::enabled() && rs::supported(g)) {
+  if (rs::supported(g)) {
     rs::gs(ctx, x, x_relu, hw, g, gw, sq_part, gb, sq_b);
     return;
   }
-  if (!ds::enabled() && ps::supported(g)) {
-    ps::gs(ctx, x, x_relu, hw, g, gw, sq_part, gb, sq_b);
-    return;
-  }
   if (bias) launch_gs_bias(ctx, hw, g.b, g.P(), g.oc, true, gb, sq_b);
-  if (ds::enabled()) {
-    ds::gs(ctx, x, x_relu, hw, g, gw, sq_part);
-    return;
-  }
-  if (use_tc()) {
-    tc::conv_gs(ctx, x, x_relu, hw, g, gw, sq_part);
-    return;
-  }
-  GsConvProb p{make_im2col(x, x_relu, g), hw, gw, sq_part, g.oc, g.K(), g.P(), g.b};
-  int bm, bn;
-  conv_tiles(g, bm, bn);
-  if (bm == 32 && bn == 32) launch_igemm<32, 32, 16>(ctx, p, g.b);
-  else if (bm == 32) launch_igemm<32, 64, 16>(ctx, p, g.b);
-  else if (bn == 32) launch_igemm<64, 32, 16>(ctx, p, g.b);
-  else launch_igemm<64, 64, 16>(ctx, p, g.b);
+  tc::conv_gs(ctx, x, x_relu, hw, g, gw, sq_part);
 }
 
 // ------------------------------------------------------------------------------------------

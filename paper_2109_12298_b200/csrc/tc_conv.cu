@@ -607,14 +607,8 @@ struct ConvCsum : TileRows {
   __device__ void epilogue_cta(int, int, int, double) const {}
 };
 
-// CTAs the clipped-sum launches aim for (split count = this / output tiles)
-static int csum_ctas() {
-  static const int v = [] {
-    const char* e = std::getenv("DPG_CSUM_CTAS");
-    return e ? std::atoi(e) : (ws_enabled() ? kNumSMs : 3 * kNumSMs);  // measured best: 3 per SM
-  }();
-  return v;
-}
+// CTAs the clipped-sum launches aim for (split count = this / output tiles; measured best: 3 per SM)
+static int csum_ctas() { return 3 * kNumSMs; }
 
 int csum_conv_splits(const ConvGeom& cg) {
   const int64_t tiles = ((cg.K() + BM - 1) / BM) * ((cg.oc + 127) / 128);

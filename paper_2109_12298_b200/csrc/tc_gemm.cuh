@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "dpg_device.cuh"
 
@@ -431,321 +432,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) tc_gemm_kernel(const Pro
   }
 }
 
-// ============================================================================================
-// Persistent warp-specialised variant (opt-in: DPG_TC_WS=1). Measured SLOWER than the kernel
-// above on the CIFAR contractions (e.g. conv1 per-sample 28 -> 100 us): with one CTA per SM its
-// 8 producer warps cannot keep enough gathers in flight, and tools/micro/skel.cu shows the
-// store / fence / arrive skeleton alone costs ~500 cycles per 16-wide K stage.
-//
-//   warps 0-7   producers: gather stage g + 2 into registers while stage g is split / stored into
-//               a ring of kWsStages shared-memory stages; every producer thread arrives on
-//               full[s] after its stores (fence.proxy.async first); they wait on empty[s]
-//               before reusing a slot. Index tables (Prob::setup) are double-buffered per tile
-//               and rebuilt between producer-only named barriers, so the gathers of the next
-//               tile start while the current one is still being stored.
-//   warps 8-11  epilogue: warp 8 + q reads TMEM lanes [32 q, +32) of the finished accumulator,
-//               hands rows to Prob::epilogue_row, releases the accumulator (tmem_empty) and
-//               reduces the tile's norm partial over its 128 threads (fixed order).
-//   warp 12     TMEM allocation; lane 0 issues the MMAs (3xTF32 per K=8 slice) of every stage,
-//               commits each stage to empty[s] and each tile to tmem_full[acc].
-// Two TMEM accumulators let tile i + 1's MMAs run while tile i is drained. Each CTA walks tiles
-// t = blockIdx.x + i * gridDim.x, t -> (m tile fastest, n tile, batch * ksplit).
-// Every barrier wait is bounded (trap after ~10 s) so a protocol fault fails the launch instead
-// of hanging the device.
-// ============================================================================================
-constexpr int kProdWarps = 8;
-constexpr int kEpiWarps = 4;
-constexpr int kMmaWarp = kProdWarps + kEpiWarps;
-constexpr int kWsThreads = (kProdWarps + kEpiWarps + 1) * 32;
-static_assert(kProdWarps * 32 == kThreads, "producers are the Prob's 256 threads");
-template <int BN>
-constexpr int ws_stages() { return BN >= 128 ? 4 : 6; }
-
-__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(done)
-      : "r"(smem_u32(bar)), "r"(phase)
-      : "memory");
-  if (done) return;
-  const long long t0 = clock64();
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-    if (done) return;
-    if (clock64() - t0 > 20000000000ll) __trap();
-  }
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// One tile of the persistent walk.
-struct WsTile {
-  int z, split, nk, ks0, mrows, nrows, tile_mn;
-  int64_t m0, n0, Mz;
-  bool live;  // m0 < Mz (ragged batches leave whole tiles empty: skipped by every role)
-};
-template <int BN, class Prob>
-__device__ __forceinline__ WsTile ws_tile(const Prob& p, int64_t t, int mt, int nt) {
-  WsTile w;
-  const int mi = (int)(t % mt);
-  const int64_t r = t / mt;
-  const int ni = (int)(r % nt);
-  const int zs = (int)(r / nt);
-  w.z = zs / p.ksplit;
-  w.split = zs % p.ksplit;
-  w.tile_mn = ni * mt + mi;
-  w.m0 = (int64_t)mi * BM;
-  w.n0 = (int64_t)ni * BN;
-  w.Mz = p.mdim(w.z);
-  w.live = w.m0 < w.Mz;
-  const int64_t Kz = p.kdim(w.z);
-  const int nk_all = (int)((Kz + BK - 1) / BK);
-  w.ks0 = (int)((int64_t)w.split * nk_all / p.ksplit);
-  w.nk = (int)((int64_t)(w.split + 1) * nk_all / p.ksplit) - w.ks0;
-  w.mrows = (int)std::min<int64_t>(BM, w.Mz - w.m0);
-  w.nrows = (int)std::min<int64_t>(BN, p.N - w.n0);
-  return w;
-}
-
-// Cursor over this CTA's (tile, stage) sequence, skipping tiles without stages.
-template <int BN, class Prob>
-struct WsCursor {
-  int64_t t, T;
-  int mt, nt, j, ord;  // ord: ordinal of the current tile among tiles with stages
-  WsTile w;
-  bool valid;
-  __device__ void seek(const Prob& p) {  // from tile t forward to a tile with stages
-    while (t < T) {
-      w = ws_tile<BN>(p, t, mt, nt);
-      if (w.live && w.nk > 0) {
-        valid = true;
-        return;
-      }
-      t += gridDim.x;
-    }
-    valid = false;
-  }
-  __device__ void init(const Prob& p, int64_t T_, int mt_, int nt_) {
-    t = blockIdx.x; T = T_; mt = mt_; nt = nt_; j = 0; ord = 0;
-    seek(p);
-  }
-  // returns true when the advance entered a new tile
-  __device__ bool advance(const Prob& p) {
-    if (++j < w.nk) return false;
-    j = 0;
-    ++ord;
-    t += gridDim.x;
-    seek(p);
-    return true;
-  }
-};
-
-template <int BN, class Prob>
-__global__ void __launch_bounds__(kWsThreads, 1) tc_ws_kernel(const Prob p, int mt, int nt, int64_t T, int dbg) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  using S = Smem<BN>;
-  constexpr int NS = ws_stages<BN>();
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * S::STAGE);
-  uint64_t* empty = full + NS;
-  uint64_t* tfull = empty + NS;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  double* red = reinterpret_cast<double*>(tempty + 4);  // [kEpiWarps]
-  uint8_t* scratch0 = smem + NS * S::STAGE + 256;
-  const int scr_stride = (p.scratch + 127) & ~127;
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr uint32_t kCols = tmem_cols<BN>();
-
-  if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * kCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], kThreads);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  pdl_wait();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp < kProdWarps) {
-    // ---------------------------------------------------------------- producers
-    WsCursor<BN, Prob> cs, cf;  // stash cursor, fetch cursor (two stages ahead)
-    cs.init(p, T, mt, nt);
-    cf = cs;
-    float4 ra0[kAQ], rb0[Frag<BN>::BQ], ra1[kAQ], rb1[Frag<BN>::BQ];
-    auto scr = [&](int ord) { return scratch0 + (ord & 1) * scr_stride; };
-    auto kstage = [&](const WsCursor<BN, Prob>& c) { return (int64_t)(c.w.ks0 + c.j) * BK; };
-    if (cf.valid) {
-      p.setup(cf.w.z, cf.w.m0, cf.w.n0, scr(cf.ord), tid);
-      named_bar(1, kThreads);
-      fetch<BN>(p, cf.w.z, cf.w.m0, cf.w.n0, kstage(cf), scr(cf.ord), tid, cf.w.mrows, cf.w.nrows, ra0, rb0);
-      if (cf.advance(p) && cf.valid) {
-        p.setup(cf.w.z, cf.w.m0, cf.w.n0, scr(cf.ord), tid);
-        named_bar(1, kThreads);
-      }
-      if (cf.valid)
-        fetch<BN>(p, cf.w.z, cf.w.m0, cf.w.n0, kstage(cf), scr(cf.ord), tid, cf.w.mrows, cf.w.nrows, ra1, rb1);
-    }
-    auto body = [&](int g, float4 (&ra)[kAQ], float4 (&rb)[Frag<BN>::BQ]) {
-      const int s = g % NS;
-      if (g >= NS) mbar_wait_bounded(&empty[s], ((g / NS) - 1) & 1);
-      uint8_t* st = smem + s * S::STAGE;
-      const StageBufsT sb{st, st + S::A_BYTES, st + 2 * S::A_BYTES, st + 2 * S::A_BYTES + S::B_BYTES};
-      stash<BN, Prob>(p, cs.w.z, cs.w.m0, cs.w.n0, kstage(cs), scr(cs.ord), tid, cs.w.mrows, cs.w.nrows, sb, ra, rb);
-      fence_proxy_async();
-      mbar_arrive(&full[s]);
-      cs.advance(p);
-      // the fetch cursor moves to stage g + 2; a new tile's tables go into the buffer of the
-      // tile two back, whose stages every producer has stored by now (barrier before the rebuild)
-      if (cf.valid && cf.advance(p) && cf.valid) {
-        named_bar(1, kThreads);
-        p.setup(cf.w.z, cf.w.m0, cf.w.n0, scr(cf.ord), tid);
-        named_bar(1, kThreads);
-      }
-      if (cf.valid && !(dbg & 2))
-        fetch<BN>(p, cf.w.z, cf.w.m0, cf.w.n0, kstage(cf), scr(cf.ord), tid, cf.w.mrows, cf.w.nrows, ra, rb);
-    };
-    int g = 0;
-#pragma unroll 1
-    while (cs.valid) {
-      body(g++, ra0, rb0);
-      if (!cs.valid) break;
-      body(g++, ra1, rb1);
-    }
-  } else if (warp < kMmaWarp) {
-    // ---------------------------------------------------------------- epilogue
-    const int q = warp & 3;
-    int i = 0;
-#pragma unroll 1
-    for (int64_t t = blockIdx.x; t < T; t += gridDim.x) {
-      const WsTile w = ws_tile<BN>(p, t, mt, nt);
-      if (!w.live) continue;
-      const int a = i & 1;
-      mbar_wait_bounded(&tfull[a], (i >> 1) & 1);
-      tc_fence_after();
-      const int64_t m = w.m0 + 32 * q + lane;
-      const bool row_ok = m < w.Mz;
-      double sq = 0.0;
-      float v[16];
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        if (dbg & 4) break;
-        if (w.nk > 0) {
-          tmem_ld16(tmem + a * kCols + ((uint32_t)(32 * q) << 16) + (uint32_t)c0, v);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) v[e] = 0.f;
-        }
-        const int64_t nrem = p.N - (w.n0 + c0);
-        const int nv = nrem >= 16 ? 16 : (nrem > 0 ? (int)nrem : 0);
-        if (row_ok && nv > 0) p.epilogue_row(w.z, w.split, m, w.n0 + c0, v, nv, sq);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[a]);
-      if (Prob::kCtaReduce) {
-        sq = warp_sum(sq);
-        if (lane == 0) red[q] = sq;
-        named_bar(2, kEpiWarps * 32);
-        if (q == 0 && lane == 0) {
-          double tot = 0.0;
-          for (int e = 0; e < kEpiWarps; ++e) tot += red[e];
-          p.epilogue_cta(w.z, w.split, w.tile_mn, tot);
-        }
-        named_bar(2, kEpiWarps * 32);
-      }
-      ++i;
-    }
-  } else if (lane == 0) {
-    // ---------------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = idesc_tf32(BN);
-    int g = 0, i = 0;
-#pragma unroll 1
-    for (int64_t t = blockIdx.x; t < T; t += gridDim.x) {
-      const WsTile w = ws_tile<BN>(p, t, mt, nt);
-      if (!w.live) continue;
-      const int a = i & 1;
-      if (i >= 2) mbar_wait_bounded(&tempty[a], ((i >> 1) - 1) & 1);
-      tc_fence_after();
-      const uint32_t acc = tmem + a * kCols;
-#pragma unroll 1
-      for (int j = 0; j < w.nk; ++j, ++g) {
-        const int s = g % NS;
-        mbar_wait_bounded(&full[s], (g / NS) & 1);
-        tc_fence_after();
-        uint8_t* st = smem + s * S::STAGE;
-        const uint32_t sa_hi = smem_u32(st), sa_lo = smem_u32(st + S::A_BYTES);
-        const uint32_t sb_hi = smem_u32(st + 2 * S::A_BYTES), sb_lo = smem_u32(st + 2 * S::A_BYTES + S::B_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          if (dbg & 1) break;
-          const uint32_t off = kk * 32;
-          mma_tf32(acc, sw_desc(sa_lo + off), sw_desc(sb_hi + off), idesc, (j > 0 || kk > 0) ? 1u : 0u);
-          mma_tf32(acc, sw_desc(sa_hi + off), sw_desc(sb_lo + off), idesc, 1u);
-          mma_tf32(acc, sw_desc(sa_hi + off), sw_desc(sb_hi + off), idesc, 1u);
-        }
-        mma_commit(&empty[s]);
-      }
-      mma_commit(&tfull[a]);
-      ++i;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kCols));
-  }
-}
-
-inline bool ws_enabled() {
-  static const int on = [] {
-    const char* e = std::getenv("DPG_TC_WS");
-    return (e && e[0] == '1') ? 1 : 0;
-  }();
-  return on != 0;
-}
-// CTAs a launch should fill: one persistent CTA per SM (warp-specialised), else kMinBlocks per SM
-inline int ctas_target() { return ws_enabled() ? kNumSMs : kMinBlocks * kNumSMs; }
+// CTAs a launch should fill: kMinBlocks per SM
+inline int ctas_target() { return kMinBlocks * kNumSMs; }
 
 // Rows per CTA tile: the UMMA tile is always BM = 128 rows, but an M that is not a multiple of
 // 128 is split into equal tiles (M = 288: 3 x 96 instead of 128 + 128 + 32), so the gathers —
-// the CTA's critical path — are balanced across the launch. DPG_TC_BAL=0: plain 128-row tiles.
-inline bool balanced_tiles() {
-  static const bool on = [] {
-    const char* e = std::getenv("DPG_TC_BAL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+// the CTA's critical path — are balanced across the launch.
 inline int tile_rows(int64_t M) {
-  if (!balanced_tiles() || M <= 0) return BM;
+  if (M <= 0) return BM;
   const int64_t t = (M + BM - 1) / BM;
   return (int)((M + t - 1) / t);
 }
@@ -753,29 +447,10 @@ inline int tile_rows(int64_t M) {
 template <int BN, class Prob>
 void launch_tc(dpg_ctx* ctx, const Prob& p_in, int64_t batches) {
   Prob p = p_in;
-  p.mstep = ws_enabled() ? BM : tile_rows(p.M);
+  p.mstep = tile_rows(p.M);
   const int mt = (int)((p.M + p.mstep - 1) / p.mstep), nt = (int)((p.N + BN - 1) / BN);
-  if (ws_enabled()) {
-    const int smem = ws_stages<BN>() * Smem<BN>::STAGE + 256 + 2 * ((p.scratch + 127) & ~127) + 1024;
-    static int attr = 0;
-    if (smem > attr) {
-      DPG_CUDA(cudaFuncSetAttribute(tc_ws_kernel<BN, Prob>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = smem;
-    }
-    const int64_t T = (int64_t)mt * nt * batches * p.ksplit;
-    if (T == 0) return;
-    const unsigned grid = (unsigned)std::min<int64_t>(T, kNumSMs);
-    static const int dbg = [] { const char* e = std::getenv("DPG_TC_DBG"); return e ? std::atoi(e) : 0; }();
-    ::dpg::launch_pdl(tc_ws_kernel<BN, Prob>, grid, kWsThreads, smem, ctx->stream, p, mt, nt, T, dbg);
-    DPG_LAUNCH_CHECK(ctx);
-    return;
-  }
   const int smem = Smem<BN>::FIXED + 1024 + p.scratch;
-  static int attr = 0;  // per template instance: largest dynamic smem configured so far
-  if (smem > attr) {
-    DPG_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<BN, Prob>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = smem;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(tc_gemm_kernel<BN, Prob>), smem);
   dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)(batches * p.ksplit));
   ::dpg::launch_pdl(tc_gemm_kernel<BN, Prob>, grid, kThreads, smem, ctx->stream, p);
   DPG_LAUNCH_CHECK(ctx);
@@ -795,20 +470,20 @@ void launch_tc_auto(dpg_ctx* ctx, const Prob& p, int64_t batches) {
 }
 
 // split-K factor: only when the output tiles alone leave SMs idle; then enough splits to fill
-// ctas_target() CTAs with >= 2 K stages per split
-// CTAs a split-K forward / dgrad launch aims for (DPG_KSPLIT_CTAS overrides). Two per SM:
-// measured on the CIFAR step (fewer splits = less partial traffic for the reduce), 444 -> 296
-// CTAs took the step from 399 to 389 us (148: 390 us).
+// ksplit_ctas() CTAs with >= 2 K stages per split.
+// CTAs a split-K forward / dgrad launch aims for. Two per SM: measured on the CIFAR step (fewer
+// splits = less partial traffic for the reduce), 444 -> 296 CTAs took the step from 399 to
+// 389 us (148: 390 us). DPG_KSPLIT=off disables split-K (the parity suite runs both ways).
 inline int ksplit_ctas() {
   static const int v = [] {
-    const char* e = std::getenv("DPG_KSPLIT_CTAS");
-    return e ? std::atoi(e) : (ws_enabled() ? kNumSMs : 2 * kNumSMs);
+    const char* e = std::getenv("DPG_KSPLIT");
+    return (e && std::strcmp(e, "off") == 0) ? 0 : 2 * kNumSMs;
   }();
   return v;
 }
 inline int pick_ksplit(int64_t M, int64_t N, int64_t K, int64_t batches) {
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + 127) / 128) * batches;
-  if (tiles >= kNumSMs) return 1;
+  if (tiles >= kNumSMs || ksplit_ctas() == 0) return 1;
   const int64_t nk = (K + BK - 1) / BK;
   int64_t ks = (ksplit_ctas() + tiles - 1) / tiles;
   ks = std::min<int64_t>(ks, std::max<int64_t>(1, nk / 2));

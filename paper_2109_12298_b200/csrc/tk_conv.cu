@@ -291,17 +291,11 @@ __global__ void __launch_bounds__(kThreads) tk_gs_kernel(Geo g, const float* __r
 }
 
 bool supported(const ConvGeom& cg) {
-  static const bool off = [] {
-    const char* e = std::getenv("DPG_TK");
-    return e && e[0] == '0';
-  }();
-  if (off || cg.K() > kMaxK || cg.oc > kMaxOc || cg.oc % 4 != 0 || cg.P() <= 0) return false;
+  if (cg.K() > kMaxK || cg.oc > kMaxOc || cg.oc % 4 != 0 || cg.P() <= 0) return false;
   return gs_smem(make(cg)) <= 160 * 1024;
 }
 
-static void set_smem(const void* fn, size_t bytes) {
-  DPG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
+static void set_smem(const void* fn, size_t bytes) { ensure_smem_attr(fn, (int)bytes); }
 
 void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& cg, float* gw,
         double* sq_part, float* gb, double* sq_b) {

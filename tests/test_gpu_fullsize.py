@@ -1,0 +1,244 @@
+"""Parity at the five BASELINE.json configurations, at the batch sizes they are quoted on.
+
+The small-batch suites (test_gpu_step.py, test_gpu_rules.py) pin every rule and the lifecycle;
+these tests pin the launches the headline configurations actually execute (tile counts, split-K
+choices, epilogue variants and stream plans all depend on b):
+
+  cfg1  MNIST CNN, b = 64                      whole step vs the fp64 oracle (record included)
+  cfg2  Linear 512->512, T = 64, b = 256       rule -> clip factors -> (s.B)^T A -> noise + update
+  cfg3  CIFAR CNN, b = 512 (headline)          whole step, C = 1.48 (both clip branches)
+  cfg4  Embedding 10000x128 + Linear, b = 512  norms / summed / update, sampled record rows
+  cfg5  CIFAR CNN, b = 4096 on one GPU         norms / summed / update, sampled record rows
+
+Reference entry points: grad_sample.hpp:328-343 (compute_grad_samples), optimizer.hpp:62-116
+(clip_and_sum), optimizer.hpp:120-133 (add_noise), optimizer.hpp:256-271 (finish_step).
+Criterion: per tensor max|gpu - ref64| / max|ref64| <= 1e-5, norms rtol 1e-5.
+The per-sample gradients of sample n depend only on sample n, so the record rows of a few
+samples are checked against the oracle run on those samples alone where the whole record
+(2.2-2.8 GB, 4.4-5.5 GB in fp64) is too large to compare.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import ROOT, maxscaled_err
+from paper_2109_12298_b200.configs import LINEAR_T64, WORKLOADS, params_meta
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def _n(t):
+    return t.detach().cpu().numpy()
+
+
+def _oracle(w, params, x, y, cfg, dtype, **kw):
+    return oracle.restatement().dpsgd_step(
+        w.layers, w.in_shape, params.astype(dtype), x.astype(dtype), y.astype(dtype), cfg["sigma"], cfg["c"],
+        cfg["lr"], cfg["e"], noise_seed=3, **kw)
+
+
+def _device_step(ctx, w, b, cfg, materialise=True):
+    from paper_2109_12298_b200 import dpg
+    params, x, y = oracle.synth_inputs(w, b=b)
+    m = dpg.Model(ctx, w.layers, w.in_shape, max_batch=b)
+    m.load_params(params)
+    o = dpg.DpOptimizer(m, noise_multiplier=cfg["sigma"], max_grad_norm=cfg["c"], learning_rate=cfg["lr"],
+                        expected_batch_size=cfg["e"], noise_seed=3, materialise_grad_sample=materialise)
+    loss = _t(np.zeros(b))
+    o.forward_backward(_t(x), _t(y), loss)
+    rec = o.grad_sample()
+    o.step()
+    norms, scales, nclip = o.last_clip_summary()
+    out = dict(params0=params, x=x, y=y, loss=_n(loss), rec=rec, norms=norms, scales=scales, nclip=nclip,
+               summed=_n(o.summed_grad()), grad=_n(o.grad()), params=m.store_params())
+    return out, m, o
+
+
+def _check_step(w, dev, r64, r32=None, tol=TOL):
+    def cmp(got, key, sl=slice(None), what=""):
+        e = maxscaled_err(got, r64[key][sl])
+        assert e <= tol, f"{w.name} {what or key}: {e:.3e} vs fp64"
+        if r32 is not None:
+            e32 = maxscaled_err(r32[key][sl], r64[key][sl])
+            assert e <= 50 * e32 + 5e-6, f"{w.name} {what or key}: {e:.3e} vs reference fp32 error {e32:.3e}"
+    np.testing.assert_allclose(dev["loss"], r64["loss"], rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(dev["norms"], r64["norms"], rtol=tol)
+    np.testing.assert_allclose(dev["scales"], r64["scales"], rtol=tol)
+    for (li, k, pname, shape, numel, off) in params_meta(w.layers):
+        sl = slice(off, off + numel)
+        cmp(dev["summed"][sl], "summed", sl, f"summed layer {li} {pname}")
+    cmp(dev["grad"], "grad")
+    p0 = dev["params0"]
+    e = maxscaled_err(dev["params"] - p0, r64["params"] - p0)
+    assert e <= tol, f"{w.name} update: {e:.3e}"
+    nref = (r32 or r64)["num_clipped"]
+    assert abs(dev["nclip"] - nref) <= 1
+
+
+def _check_record_full(w, b, rec, r64, r32):
+    for (li, k, pname, shape, numel, off) in params_meta(w.layers):
+        sl = slice(b * off, b * (off + numel))
+        got = rec[sl]
+        e = maxscaled_err(got, r64["record"][sl])
+        e32 = maxscaled_err(r32["record"][sl], r64["record"][sl])
+        assert e <= TOL, f"{w.name} record layer {li} {pname}: {e:.3e}"
+        assert e <= 50 * e32 + 5e-6, f"{w.name} record layer {li} {pname}: {e:.3e} vs fp32 {e32:.3e}"
+
+
+def _check_record_rows(w, b, rec_dev, params, x, y, rows):
+    """Record rows of `rows` (sample indices) vs the fp64 oracle run on those samples alone."""
+    cfg = dict(sigma=0.0, c=1.0, lr=0.1, e=float(len(rows)))
+    r64 = _oracle(w, params, x[rows], y[rows], cfg, np.float64)
+    nb = len(rows)
+    for (li, k, pname, shape, numel, off) in params_meta(w.layers):
+        ref = r64["record"][nb * off: nb * (off + numel)].reshape(nb, numel)
+        for j, n in enumerate(rows):
+            got = _n(rec_dev[b * off + n * numel: b * off + (n + 1) * numel])
+            e = maxscaled_err(got, ref[j])
+            assert e <= TOL, f"{w.name} record layer {li} {pname} sample {n}: {e:.3e}"
+
+
+def test_cfg1_mnist_b64(ctx):
+    w = WORKLOADS["mnist_b64"]
+    for c in (1.0, 2.4):
+        cfg = dict(sigma=0.0, c=c, lr=0.1, e=64.0)
+        dev, m, o = _device_step(ctx, w, 64, cfg)
+        r32 = _oracle(w, dev["params0"], dev["x"], dev["y"], cfg, np.float32)
+        r64 = _oracle(w, dev["params0"], dev["x"], dev["y"], cfg, np.float64)
+        _check_step(w, dev, r64, r32)
+        _check_record_full(w, 64, _n(dev["rec"]), r64, r32)
+
+
+@pytest.mark.parametrize("c", [1.0, 1.48])
+def test_cfg3_cifar_b512(ctx, c):
+    """The headline: every launch at the sizes the bench runs (no-split conv1/conv2 forward and
+    dgrad epilogues, split-K conv3/conv4, the thin-K and few-positions rule kernels)."""
+    w = WORKLOADS["cifar_b512"]
+    cfg = dict(sigma=0.0, c=c, lr=0.1, e=512.0)
+    dev, m, o = _device_step(ctx, w, 512, cfg)
+    r32 = _oracle(w, dev["params0"], dev["x"], dev["y"], cfg, np.float32)
+    r64 = _oracle(w, dev["params0"], dev["x"], dev["y"], cfg, np.float64)
+    _check_step(w, dev, r64, r32)
+    _check_record_full(w, 512, _n(dev["rec"]), r64, r32)
+    if c != 1.0:
+        assert 0 < dev["nclip"] < 512, "C = 1.48 must exercise both clip branches"
+
+
+def test_cfg3_cifar_b512_norms_only(ctx):
+    """materialise_grad_sample = False (no record): norms, clipped sums and update unchanged."""
+    w = WORKLOADS["cifar_b512"]
+    cfg = dict(sigma=0.0, c=1.48, lr=0.1, e=512.0)
+    dev, m, o = _device_step(ctx, w, 512, cfg, materialise=False)
+    assert dev["rec"] is None
+    r64 = _oracle(w, dev["params0"], dev["x"], dev["y"], cfg, np.float64, want_record=False)
+    _check_step(w, dev, r64)
+
+
+def test_cfg3_cifar_b512_injected_noise(ctx):
+    """sigma = 1 with the oracle's own mt19937_64 noise injected: the update tracks the reference."""
+    import torch
+    from paper_2109_12298_b200 import dpg
+    w = WORKLOADS["cifar_b512"]
+    b = 512
+    params, x, y = oracle.synth_inputs(w, b=b)
+    m = dpg.Model(ctx, w.layers, w.in_shape, max_batch=b)
+    m.load_params(params)
+    o = dpg.DpOptimizer(m, noise_multiplier=1.0, max_grad_norm=1.0, learning_rate=0.1,
+                        expected_batch_size=float(b), noise_seed=3)
+    noise = oracle.restatement().gaussian(3, m.L, 1.0)
+    o.set_injected_noise(_t(noise))
+    loss = torch.zeros(b, device="cuda")
+    o.train_step(_t(x), _t(y), loss, use_graph=True)
+    ctx.sync()
+    cfg = dict(sigma=1.0, c=1.0, lr=0.1, e=float(b))
+    r64 = _oracle(w, params, x, y, cfg, np.float64, injected_noise=noise.astype(np.float64), want_record=False)
+    e = maxscaled_err(m.store_params() - params, r64["params"] - params)
+    assert e <= TOL, f"graph step with injected noise: {e:.3e}"
+
+
+def test_cfg4_embed_b512(ctx):
+    w = WORKLOADS["embed_b512"]
+    b = 512
+    cfg = dict(sigma=0.0, c=132.0, lr=0.1, e=float(b))
+    dev, m, o = _device_step(ctx, w, b, cfg)
+    r64 = _oracle(w, dev["params0"], dev["x"], dev["y"], cfg, np.float64, want_record=False)
+    _check_step(w, dev, r64)
+    assert 0 < dev["nclip"] < b
+    _check_record_rows(w, b, dev["rec"], dev["params0"], dev["x"], dev["y"], [0, 1, 255, 511])
+
+
+def test_cfg5_cifar_b4096_one_gpu(ctx):
+    w = WORKLOADS["cifar_b4096"]
+    b = 4096
+    cfg = dict(sigma=0.0, c=1.48, lr=0.1, e=float(b))
+    dev, m, o = _device_step(ctx, w, b, cfg)
+    r64 = _oracle(w, dev["params0"], dev["x"], dev["y"], cfg, np.float64, want_record=False)
+    _check_step(w, dev, r64)
+    _check_record_rows(w, b, dev["rec"], dev["params0"], dev["x"], dev["y"], [0, 1, 2047, 4095])
+
+
+def test_cfg2_linear_t64_pipeline(ctx):
+    """cfg2 as bench.py runs it (operator ABI): per_sample_rule_linear on A, B [256, 64, 512] with
+    fused norms and the bias rule -> clip factors -> (s.B)^T A + bias sums -> noise + update (the
+    oracle's own noise stream injected, so the whole pipeline is compared)."""
+    import torch
+    from paper_2109_12298_b200 import dpg
+    b, t, d, r = LINEAR_T64["b"], LINEAR_T64["t"], LINEAR_T64["d"], LINEAR_T64["r"]
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((b, t, d)).astype(np.float32)
+    B = rng.standard_normal((b, t, r)).astype(np.float32) * np.float32(0.01)
+    L = r * d + r
+    params = ((rng.random(L) - 0.5) / np.sqrt(d)).astype(np.float32)
+    c = 0.8
+    Ad, Bd = _t(A), _t(B)
+    gw, gb, sw, sb = dpg.per_sample_rule_linear(ctx, Ad, Bd)
+    sq = torch.stack([sw, sb])
+    norms, scale, nclip = dpg.clip_factors(ctx, sq, c)
+    summed = torch.empty(L, device="cuda")
+    dpg.clipped_sum_linear(ctx, Ad, Bd, scale, out_w=summed[:r * d].view(r, d), out_b=summed[r * d:])
+    R = oracle.restatement()
+    noise = R.gaussian(3, L, 1.0 * c)
+    pd = _t(params)
+    dpg.noise_update(ctx, pd, summed, 1.0, c, float(b), 0.1, 3, 0, injected=_t(noise))
+    ctx.sync()
+    # oracle (fp64 and fp32): rule, clip_and_sum, add_noise with the same stream, finish_step
+    res = {}
+    for dt in (np.float64, np.float32):
+        g_w, g_b = R.rule_linear(A.astype(dt), B.astype(dt))
+        s, n64, sc, ncl = R.clip_and_sum([g_w, g_b], c)
+        flat = np.concatenate([s[0].ravel(), s[1].ravel()])
+        noised = flat + noise.astype(dt)
+        g = noised * dt(1.0 / b)
+        res[dt] = dict(gw=g_w, gb=g_b, summed=flat, norms=n64, nclip=ncl, params=params.astype(dt) - g * dt(0.1))
+    r64, r32 = res[np.float64], res[np.float32]
+    for key, got in (("gw", _n(gw)), ("gb", _n(gb)), ("summed", _n(summed))):
+        e = maxscaled_err(got, r64[key])
+        e32 = maxscaled_err(r32[key], r64[key])
+        assert e <= TOL and e <= 50 * e32 + 5e-6, f"cfg2 {key}: {e:.3e} (fp32 ref {e32:.3e})"
+    np.testing.assert_allclose(_n(norms), r64["norms"], rtol=TOL)
+    assert 0 < int(_n(nclip)[0]) < b, "the chosen C must exercise both clip branches"
+    e = maxscaled_err(_n(pd).astype(np.float64) - params, r64["params"] - params)
+    assert e <= TOL, f"cfg2 update: {e:.3e}"
+
+
+@pytest.mark.parametrize("split", ["off"])
+def test_small_batch_steps_without_split_k(split):
+    """Both sides of the split-K threshold at small b: the step suite re-run in a fresh process
+    with split-K disabled (DPG_KSPLIT=off), so the no-split forward / dgrad epilogues also run
+    at the sizes the small-b tests use."""
+    env = dict(os.environ, DPG_KSPLIT=split)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_step.py"), "-k", "matches_oracle or virtual"],
+                       env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

@@ -58,6 +58,34 @@ def test_peer_exchange_two_ranks_match_single_process(tmp_path, ctx, ragged):
     assert maxscaled_err(r0["params"] - params0, p_single - params0) <= 1e-5
 
 
+def test_error_on_one_rank_skips_the_update_on_every_rank(tmp_path, ctx):
+    """A NaN input on rank 1 (NumericError there) must stop the update on rank 0 too: the status
+    lane travels with the clipped sums, both ranks raise for that step, keep their parameters,
+    and stay bitwise identical afterwards (the reference's step throws before any update)."""
+    port = _port()
+    outs = [str(tmp_path / f"n{r}.npz") for r in range(2)]
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "p2p_worker.py"), str(r), "2", str(port), outs[r],
+                               "nan"], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, start_new_session=True)
+             for r in range(2)]
+    logs = []
+    try:
+        for p in procs:
+            out, _ = p.communicate(timeout=300)
+            logs.append(out.decode(errors="replace")[-3000:])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                os.killpg(p.pid, 9)
+    for p, log in zip(procs, logs):
+        assert p.returncode == 0, log
+    r0, r1 = np.load(outs[0]), np.load(outs[1])
+    e0, e1 = list(r0["errors"]), list(r1["errors"])
+    assert e0[0] == "" and e1[0] == "" and e0[2] == "" and e1[2] == "", (e0, e1)
+    assert "non-finite per-sample gradient" in e1[1], e1
+    assert "another rank" in e0[1], e0
+    assert np.array_equal(r0["params"], r1["params"])
+
+
 def test_peer_exchange_argument_errors(ctx):
     from paper_2109_12298_b200 import dpg
     from paper_2109_12298_b200.configs import LayerDesc as L

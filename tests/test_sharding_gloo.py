@@ -73,3 +73,29 @@ def test_shard_ranges_cover_batch():
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             sizes = [h - l for l, h in rs]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_bench_spawns_its_own_ranks_without_torchrun():
+    """`python bench.py --gpus 2` (the driver's plain form, no torchrun) re-launches itself as two
+    ranks on 127.0.0.1 over gloo; under N > 1 rank 0 alone runs the reference arm and prints ONE
+    JSON line with the shared config keys, and every rank exits 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import oracle
+    if not (oracle.reference_available(fast=True) or os.path.exists(oracle.RESTATEMENT_SO)):
+        pytest.skip("oracle not built")
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--workload", "mnist_b64", "--steps", "1", "--warmup", "0"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert set(line["config"]) == {"workload", "global_batch", "per_rank_batch", "parallelism", "detail"}
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
