@@ -181,6 +181,28 @@ def _p(t: Optional[torch.Tensor]):
     return ctypes.c_void_p(t.data_ptr())
 
 
+class _Handle:
+    """A native handle shared by its Python owner and the owner's parent, so the handles of a
+    garbage cycle (context <- model <- optimizer, collected in arbitrary order) are still
+    destroyed children first: whichever finaliser runs first destroys the handle and its
+    children, the other finds it dead."""
+
+    def __init__(self, h, destroy: str):
+        self.h = h
+        self.destroy_fn = destroy
+        self.children: List["_Handle"] = []
+
+    def destroy(self):
+        if self.h is None:
+            return
+        for c in reversed(self.children):
+            c.destroy()
+        self.children = []
+        if _lib is not None:
+            getattr(_lib, self.destroy_fn)(self.h)
+        self.h = None
+
+
 class Context:
     """dpg_ctx on one GPU, bound to torch's current stream so ordering with torch ops holds."""
 
@@ -197,10 +219,11 @@ class Context:
         h = _P()
         _check(lib().dpg_ctx_create(device, ctypes.c_void_p(s.cuda_stream), ctypes.byref(h)))
         self.h = h
+        self._handle = _Handle(h, "dpg_ctx_destroy")
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
-            _lib.dpg_ctx_destroy(self.h)
+        if getattr(self, "_handle", None) is not None:
+            self._handle.destroy()
             self.h = None
 
     def sync(self):
@@ -427,12 +450,14 @@ class Model:
         _check(lib().dpg_model_create(ctx.h, self._cl, len(layers), shp, len(in_shape), max_batch,
                                       ctypes.byref(h)), ctx.h)
         self.h = h
+        self._handle = _Handle(h, "dpg_model_destroy")
+        ctx._handle.children.append(self._handle)
         self.L = int(lib().dpg_model_parameter_count(h))
         self.meta = params_meta(layers)
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
-            _lib.dpg_model_destroy(self.h)
+        if getattr(self, "_handle", None) is not None:
+            self._handle.destroy()
             self.h = None
 
     def parameter_count(self) -> int:
@@ -487,11 +512,13 @@ class DpOptimizer:
         h = _P()
         _check(lib().dpg_optimizer_create(model.h, ctypes.byref(cfg), ctypes.byref(h)), self.ctx.h)
         self.h = h
+        self._handle = _Handle(h, "dpg_optimizer_destroy")
+        model._handle.children.append(self._handle)
         self._b = 0
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
-            _lib.dpg_optimizer_destroy(self.h)
+        if getattr(self, "_handle", None) is not None:
+            self._handle.destroy()
             self.h = None
 
     def forward_backward(self, x: torch.Tensor, targets: torch.Tensor, loss: Optional[torch.Tensor] = None):
