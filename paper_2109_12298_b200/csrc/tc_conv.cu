@@ -610,9 +610,15 @@ struct ConvCsum : TileRows {
 // CTAs the clipped-sum launches aim for (split count = this / output tiles; measured best: 3 per SM)
 static int csum_ctas() { return 3 * kNumSMs; }
 
+// Products one split accumulates in TMEM, at most. The tensor core's fp32 accumulation is not
+// round-to-nearest: its error grows with the accumulation chain (measured, CIFAR conv2 clipped sum
+// recomputed in fp64 from the device's own record: 1.4e-6 max-scaled at 256 products per split,
+// 1.0e-5 at 1,792), so long sums (b = 4096) get more splits instead of longer chains.
+constexpr int64_t kCsumChain = 512;
+
 int csum_conv_splits(const ConvGeom& cg) {
   const int64_t tiles = ((cg.K() + BM - 1) / BM) * ((cg.oc + 127) / 128);
-  int64_t splits = (csum_ctas() + tiles - 1) / tiles;
+  int64_t splits = std::max((csum_ctas() + tiles - 1) / tiles, (cg.b * cg.P() + kCsumChain - 1) / kCsumChain);
   const int64_t max_by_k = std::max<int64_t>(1, (cg.b * cg.P()) / (2 * BK));
   splits = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(splits, cg.b), max_by_k));
   const int64_t spl = (cg.b + splits - 1) / splits;
@@ -770,7 +776,7 @@ struct LinCsum : TileRows {
 
 int csum_linear_splits(int64_t b, int64_t mid, int64_t d, int64_t r) {
   const int64_t tiles = ((d + BM - 1) / BM) * ((r + 127) / 128);
-  int64_t splits = (csum_ctas() + tiles - 1) / tiles;
+  int64_t splits = std::max((csum_ctas() + tiles - 1) / tiles, (b * mid + kCsumChain - 1) / kCsumChain);
   const int64_t max_by_k = std::max<int64_t>(1, (b * mid) / (2 * BK));
   splits = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(splits, b), max_by_k));
   const int64_t spl = (b + splits - 1) / splits;

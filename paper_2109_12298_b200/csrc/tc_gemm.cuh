@@ -61,7 +61,12 @@ constexpr uint64_t kLayoutType = BK == 32 ? 2 : 4;   // UMMA layout: SWIZZLE_128
 constexpr int kMinBlocks = BK == 32 ? 2 : DPG_TC_MINB;         // resident CTAs per SM the kernel is built for
 constexpr int kThreads = 256;
 #ifndef DPG_TC_TRUNC
-#define DPG_TC_TRUNC 1  // 3xTF32 with a truncated hi part (measured: parity unchanged, step -0.9 %)
+// 3xTF32 with a truncated hi part: step -0.9 %, but biased. With hi = trunc(x), lo has the sign
+// of x and |lo| < 2^-10 |x|, so the dropped lo*lo product (up to 2^-20 |x w|) shrinks every
+// product toward zero; a long cancelling sum accumulates that linearly (b = 4096 conv2 clipped
+// sum: 1.28e-5 max-scaled vs fp64, against the fp32 reference's own 2.2e-6). Rounded parts
+// leave a zero-mean lo*lo of <= 2^-22 |x w|: the default.
+#define DPG_TC_TRUNC 0
 #endif
 #ifndef DPG_TC_STAGES
 #define DPG_TC_STAGES 2
@@ -165,9 +170,9 @@ __device__ __forceinline__ uint32_t sw_off(int row, int q) {
   return (uint32_t)((row >> 3) * kAtomBytes + (row & 7) * kRowBytes + ((q ^ x) << 4));
 }
 
-// 3xTF32 split of a finite fp32 value. Default (DPG_TC_TRUNC=1): hi = x as stored, which the
+// 3xTF32 split of a finite fp32 value. DPG_TC_TRUNC=1: hi = x as stored, which the
 // tensor core reads as trunc_tf32(x) (top 19 bits), lo = x - trunc_tf32(x), exact in fp32 and
-// itself truncated by the MMA: |error| <= 2^-21 |x| per operand, two ops. DPG_TC_TRUNC=0: both
+// itself truncated by the MMA: |error| <= 2^-21 |x| per operand, two ops. DPG_TC_TRUNC=0 (default): both
 // parts rounded to nearest (ties away, as cvt.rna) by integer add + mask, |error| <= 2^-22 |x|,
 // five ops. No special-case branches either way; a non-finite x still gives a non-finite
 // product, which the clip-factor check reports.

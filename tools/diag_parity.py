@@ -27,6 +27,10 @@ def main():
     c = float(sys.argv[3]) if len(sys.argv) > 3 else 1.48
     w = WORKLOADS[name]
     params, x, y = oracle.synth_inputs(w, b=b)
+    if os.environ.get("DIAG_REDRAW"):
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from kinks import redraw_kinks
+        x, _ = redraw_kinks(w, params, x)
     ctx = dpg.Context(0)
     m = dpg.Model(ctx, w.layers, w.in_shape, max_batch=b)
     m.load_params(params)
@@ -39,6 +43,16 @@ def main():
     norms, scales, nclip = o.last_clip_summary()
     summed = o.summed_grad().cpu().numpy()
     ctx.sync()
+    if os.environ.get("DIAG_ISOLATE"):
+        # clipped sums recomputed in fp64 from the device's own record and scales: isolates the
+        # clipped-sum kernels from upstream (forward / dgrad / rule) error
+        sc = np.asarray(scales, dtype=np.float32).astype(np.float64)
+        for (li, k, pname, shape, numel, off) in params_meta(w.layers):
+            g = rec[b * off: b * (off + numel)].reshape(b, numel).astype(np.float64)
+            ref = sc @ g
+            print(f"  isolated csum layer {li} {pname}: {maxscaled_err(summed[off:off + numel], ref):.3e}")
+        if os.environ.get("DIAG_ISOLATE") == "only":
+            return
     r64 = oracle.restatement().dpsgd_step(w.layers, w.in_shape, params.astype(np.float64), x.astype(np.float64),
                                           y.astype(np.float64), 0.0, c, 0.1, float(b), noise_seed=3)
     r32 = oracle.restatement().dpsgd_step(w.layers, w.in_shape, params, x, y, 0.0, c, 0.1, float(b), noise_seed=3)
