@@ -337,6 +337,14 @@ DPG_API dpg_status dpg_train_step_host_async(dpg_optimizer* opt, const float* x_
 DPG_API dpg_status dpg_train_step(dpg_optimizer* opt, const float* x, const float* targets,
                                   int64_t b, float* loss, int use_graph);
 
+/* ======================================================================================
+ * Diagnostics (no reference counterpart): unit test of the TMA-fed tcgen05 GEMM core that the
+ * convolution contractions are built on. D[m][n] = sum_k A[m][k] B[n][k], row-major fp32 device
+ * buffers, 3xTF32; bn in {32, 64, 128} output columns per tile, bk in {16, 32} K per stage
+ * (K a multiple of 4). */
+DPG_API dpg_status dpg_tg_gemm_selftest(dpg_ctx* ctx, const float* a, const float* b, float* d,
+                                        int64_t m, int64_t n, int64_t k, int bn, int bk);
+
 #ifdef __cplusplus
 }
 #endif

@@ -171,10 +171,32 @@ struct ConvGeom {
   int64_t P() const { return oh * ow; }
 };
 
+// TMA-fed contractions (tg_conv.cu): NHWC activations / highways beside the NCHW buffers
+struct TgPrepItem {
+  const float* w;  // reference layout [O][C][kh][kw]
+  float* wf;       // [O][kh][kw][C] (NHWC forward), nullable
+  float* wd;       // [kh][kw][C][O] (dgrad), nullable
+  int O, C, kh, kw;
+};
+struct TgPrepItems {
+  TgPrepItem item[8];
+  int count = 0;
+};
+namespace tg {
+bool fwd_nhwc_ok(const ConvGeom& g);
+bool dgrad_nhwc_ok(const ConvGeom& g);
+void conv_fwd_nhwc(dpg_ctx* ctx, const float* xh, const float* wf, const float* bias, const ConvGeom& g, float* y,
+                   float* yh, int relu_out);
+void conv_dgrad_nhwc(dpg_ctx* ctx, const float* hh, const float* wd, const ConvGeom& g, const float* mask_h,
+                     float* dx, float* dxh);
+void prep_weights(dpg_ctx* ctx, const TgPrepItems& items);
+void nchw_to_nhwc(dpg_ctx* ctx, const float* src, int relu, int64_t b, int64_t C, int64_t P, float* dst);
+}  // namespace tg
+
 namespace tc {
 size_t fwd_ws_bytes(const ConvGeom& cg);
 void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-              const ConvGeom& cg, float* y, void* ws);
+              const ConvGeom& cg, float* y, void* ws, float* yh = nullptr, int relu_out = 0);
 bool dgrad_supported(const ConvGeom& cg);
 size_t dgrad_ws_bytes(const ConvGeom& cg);
 void conv_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& cg,
@@ -295,7 +317,8 @@ void launch_noise_update_p2p(dpg_ctx* ctx, const PeerSet& ps, float* params, flo
 size_t conv_fwd_ws_bytes(const ConvGeom& g);
 size_t conv_dgrad_ws_bytes(const ConvGeom& g);
 void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-                       const ConvGeom& g, float* y, void* ws);
+                       const ConvGeom& g, float* y, void* ws, float* yh = nullptr,
+                       int relu_out = 0);
 void launch_conv2d_dgrad(dpg_ctx* ctx, const float* dy, const float* w, const ConvGeom& g,
                          const float* mask_src, float* dx, void* ws);
 // softmax-CE epilogue of the logits-producing linear forward (one row per sample)

@@ -21,9 +21,9 @@ size_t conv_dgrad_ws_bytes(const ConvGeom& g) {
 }
 
 void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-                       const ConvGeom& g, float* y, void* ws) {
+                       const ConvGeom& g, float* y, void* ws, float* yh, int relu_out) {
   if (g.b == 0) return;
-  tc::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws);
+  tc::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws, yh, relu_out);
 }
 
 // ------------------------------------------------------------------------------------------

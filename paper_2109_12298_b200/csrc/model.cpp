@@ -53,7 +53,27 @@ struct LayerPlan {
   int64_t norm_c = 0, norm_q = 0, stat_blocks = 0;
   float* xhat = nullptr;
   float* inv_std = nullptr;
+  // TMA-fed contractions (tg_conv.cu). tg_fwd: 0 = register-gather kernels (thin first layers:
+  // C % 16 != 0), 1 = NHWC implicit im2col (input copy xh). tg_dgrad: the input gradient from the
+  // NHWC highway copy hh. The producers write these copies in their epilogues
+  // (xh_by_prev / hh_by_next); otherwise a transpose launch fills them.
+  int tg_fwd = 0;
+  bool tg_dgrad = false;
+  bool xh_by_prev = false, hh_by_next = false;
+  int next_param_layer = -1;
+  float* xh = nullptr;    // [b][H][W][C] of the layer input (ReLU applied)
+  float* hh = nullptr;    // [b][OH][OW][O] of the layer's highway
+  float* wf = nullptr;    // [2][O][kh][kw][C] (TF32 hi, lo)
+  float* wd = nullptr;    // [2][kh][kw][C][O]
 };
+
+bool tg_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DPG_TG");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int64_t conv_out_extent(int64_t in, int64_t kernel, int64_t stride, int64_t pad) {
   const int64_t padded = in + 2 * pad;
@@ -260,6 +280,25 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
   dpg_ctx* ctx = m->ctx;
   float* P = m->p_params;
   auto act = [&](int buf) -> const float* { return buf < 0 ? x : m->bufs[buf]; };
+  // ---- per-step weight layouts of the TMA-fed convolutions: on a branch, beside the first
+  // layers' forward; joined before the first launch that reads them ----
+  bool prep_pending = false;
+  {
+    dpg::TgPrepItems items;
+    for (auto& lp : m->layers) {
+      if (!lp.wf && !lp.wd) continue;
+      if (items.count == 8) raise(DPG_ERR_DIMENSION, "more than 8 TMA-fed convolution layers");
+      items.item[items.count++] = {P + m->params[lp.param0].offset, lp.wf, lp.wd, (int)lp.g.oc, (int)lp.g.ic,
+                                   (int)lp.g.kh, (int)lp.g.kw};
+    }
+    if (items.count) {
+      on_branch(m, 0, [&] {
+        dpg::ProfScope ps(ctx, "prep.weights", 8.0 * 2 * 135306, 0.0);
+        dpg::tg::prep_weights(ctx, items);
+      });
+      prep_pending = true;
+    }
+  }
   // ---- forward (layers.hpp:576-592) ----
   bool loss_done = false;  // softmax-CE fused into the logits-producing linear forward
   int dgrad_fused = -1;    // ... and that layer's input gradient too (its backward dgrad is skipped)
@@ -298,9 +337,30 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
       case DPG_LAYER_CONV2D: {
         ConvGeom g = lp.g;
         g.b = b;
+        // NHWC copy of this layer's output for a TMA-fed consumer (ReLU as the consumer applies it)
+        float* yh = nullptr;
+        int relu_out = 0;
+        if (lp.next_param_layer >= 0) {
+          const LayerPlan& nx = m->layers[lp.next_param_layer];
+          if (nx.tg_fwd) {
+            yh = nx.xh;
+            relu_out = nx.in_relu ? 1 : 0;
+          }
+        }
+        if (lp.tg_fwd && !lp.xh_by_prev) {
+          dpg::ProfScope ps(ctx, "nhwc.x[" + std::to_string(l) + "]", 8.0 * b * lp.in_numel, 0.0);
+          dpg::tg::nchw_to_nhwc(ctx, in, lp.in_relu, b, g.ic, g.h * g.w, lp.xh);
+        }
+        if (lp.tg_fwd && prep_pending) {
+          join_branches(m);
+          prep_pending = false;
+        }
         dpg::ProfScope ps(ctx, "fwd.conv2d[" + std::to_string(l) + "]",
                           io + 4.0 * m->params[lp.param0].numel, 2.0 * b * g.oc * g.K() * g.P());
-        dpg::launch_conv2d_fwd(ctx, in, lp.in_relu, w, bias, g, out, m->ws);
+        if (lp.tg_fwd)
+          dpg::tg::conv_fwd_nhwc(ctx, lp.xh, lp.wf, bias, g, out, yh, relu_out);
+        else
+          dpg::launch_conv2d_fwd(ctx, in, lp.in_relu, w, bias, g, out, m->ws, yh, relu_out);
         break;
       }
       case DPG_LAYER_LAYER_NORM:
@@ -424,6 +484,16 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
         case DPG_LAYER_CONV2D: {
           ConvGeom g = lp.g;
           g.b = b;
+          if (lp.tg_dgrad) {
+            if (!lp.hh_by_next) {
+              dpg::ProfScope ps(ctx, "nhwc.hw" + ls, 8.0 * b * lp.out_numel, 0.0);
+              dpg::tg::nchw_to_nhwc(ctx, hw, 0, b, g.oc, g.P(), lp.hh);
+            }
+            dpg::ProfScope ps(ctx, "dgrad.conv2d" + ls, dio, 2.0 * b * g.oc * g.K() * g.P());
+            dpg::tg::conv_dgrad_nhwc(ctx, lp.hh, lp.wd, g, lp.in_relu ? lp.xh : nullptr, dst,
+                                     prev.tg_dgrad ? prev.hh : nullptr);
+            break;
+          }
           dpg::ProfScope ps(ctx, "dgrad.conv2d" + ls, dio, 2.0 * b * g.oc * g.K() * g.P());
           dpg::launch_conv2d_dgrad(ctx, hw, w, g, mask, dst, m->ws);
           break;
@@ -799,6 +869,19 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     m->out_relu = cur_relu;
     m->L = offset;
     // the first parametric layer gets no input gradient (grad_sample.hpp:300)
+    // ---- TMA-fed convolution plan ----
+    for (size_t l = 0; l < m->layers.size(); ++l) {
+      LayerPlan& lp = m->layers[l];
+      if (lp.prev_param_layer >= 0) m->layers[lp.prev_param_layer].next_param_layer = (int)l;
+      if (lp.kind != DPG_LAYER_CONV2D || !tg_enabled()) continue;
+      if (dpg::tg::fwd_nhwc_ok(lp.g)) lp.tg_fwd = 1;
+      lp.tg_dgrad = lp.tg_fwd && lp.prev_param_layer >= 0 && dpg::tg::dgrad_nhwc_ok(lp.g);
+    }
+    for (auto& lp : m->layers) {
+      // every conv forward writes its consumer's NHWC copy in the epilogue
+      if (lp.tg_fwd && lp.prev_param_layer >= 0) lp.xh_by_prev = m->layers[lp.prev_param_layer].kind == DPG_LAYER_CONV2D;
+      if (lp.tg_dgrad && lp.next_param_layer >= 0) lp.hh_by_next = m->layers[lp.next_param_layer].tg_dgrad;
+    }
     // ---- norm-partial rows (one row per producer output tile) ----
     int rows = 0;
     for (auto& lp : m->layers) {
@@ -856,6 +939,18 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     total += 3 * al(sizeof(float) * max_batch);
     for (auto& lp : m->layers)
       if (lp.stat_blocks) total += al(sizeof(float) * max_batch * lp.in_numel) + al(sizeof(float) * max_batch * lp.stat_blocks);
+    auto tg_sizes = [&](const LayerPlan& lp, size_t* sz) {  // xh, hh, wf, wd
+      const int64_t wn = lp.g.oc * lp.g.K();
+      sz[0] = lp.tg_fwd == 1 ? sizeof(float) * max_batch * lp.in_numel : 0;
+      sz[1] = lp.tg_dgrad ? sizeof(float) * max_batch * lp.out_numel : 0;
+      sz[2] = lp.tg_fwd == 1 ? 2 * sizeof(float) * wn : 0;  // TF32 hi and lo planes
+      sz[3] = lp.tg_dgrad ? 2 * sizeof(float) * wn : 0;
+    };
+    for (auto& lp : m->layers) {
+      size_t sz[4];
+      tg_sizes(lp, sz);
+      for (size_t z : sz) total += z ? al(z) : 0;
+    }
     DPG_CUDA(cudaMalloc(&m->arena, total));
     DPG_CUDA(cudaMemset(m->arena, 0, total));
     char* p = m->arena;
@@ -889,6 +984,13 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
         lp.xhat = reinterpret_cast<float*>(take(sizeof(float) * max_batch * lp.in_numel));
         lp.inv_std = reinterpret_cast<float*>(take(sizeof(float) * max_batch * lp.stat_blocks));
       }
+    for (auto& lp : m->layers) {
+      size_t sz[4];
+      tg_sizes(lp, sz);
+      float** dst[4] = {&lp.xh, &lp.hh, &lp.wf, &lp.wd};
+      for (int q = 0; q < 4; ++q)
+        if (sz[q]) *dst[q] = reinterpret_cast<float*>(take(sz[q]));
+    }
     std::vector<int32_t> rp;
     for (size_t q = 0; q < m->params.size(); ++q)
       for (int r = 0; r < m->params[q].sq_rows; ++r) rp.push_back((int32_t)q);

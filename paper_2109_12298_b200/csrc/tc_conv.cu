@@ -108,6 +108,8 @@ struct ConvFwd : TileRows {
   const float* wt;
   const float* bias;
   float* y;
+  float* yh;     // NHWC [b][P][oc] of relu_if(y, relu_out) for a TMA-fed consumer (nullable)
+  int relu_out;
   float* part;  // split-K partials [ksplit][oc][M] (ksplit > 1)
   int64_t M, N, K;
   int ksplit, scratch;
@@ -169,7 +171,22 @@ struct ConvFwd : TileRows {
     uint32_t n, p;
     g.fP.divmod((uint32_t)m, n, p);
     float* out = y + (int64_t)n * g.oc * g.P + p;
-    for (int j = 0; j < nv; ++j) out[(n0 + j) * g.P] = v[j] + (bias ? __ldg(bias + n0 + j) : 0.f);
+    float val[16];
+    for (int j = 0; j < nv; ++j) {
+      val[j] = v[j] + (bias ? __ldg(bias + n0 + j) : 0.f);
+      out[(n0 + j) * g.P] = val[j];
+    }
+    if (yh) {
+      float* outh = yh + (int64_t)m * g.oc + n0;
+      if (nv == 16 && (g.oc & 3) == 0) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(outh + j) = make_float4(relu_if(val[j], relu_out), relu_if(val[j + 1], relu_out),
+                                                             relu_if(val[j + 2], relu_out), relu_if(val[j + 3], relu_out));
+      } else {
+        for (int j = 0; j < nv; ++j) outh[j] = relu_if(val[j], relu_out);
+      }
+    }
   }
   __device__ void epilogue_cta(int, int, int, double) const {}
 };
@@ -191,7 +208,8 @@ __device__ __forceinline__ float sum_splits(const float* __restrict__ part, int 
 
 // Y[n][oc][p] = bias[oc] + sum_s part[s][oc][n*P + p]
 __global__ void fwd_reduce_kernel(const float* __restrict__ part, int ksplit, int64_t M, int64_t oc,
-                                  int64_t P, const float* __restrict__ bias, float* __restrict__ y) {
+                                  int64_t P, const float* __restrict__ bias, float* __restrict__ y,
+                                  float* __restrict__ yh, int relu_out) {
   pdl_wait();
   pdl_trigger();  // the next GEMM's CTAs may start their prologue beside this short pass
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over oc * M, m fastest
@@ -199,7 +217,9 @@ __global__ void fwd_reduce_kernel(const float* __restrict__ part, int ksplit, in
   const int64_t c = i / M, m = i - c * M;
   const float acc = sum_splits(part, ksplit, oc * M, i);
   const int64_t n = m / P, p = m - n * P;
-  y[(n * oc + c) * P + p] = acc + (bias ? bias[c] : 0.f);
+  const float val = acc + (bias ? bias[c] : 0.f);
+  y[(n * oc + c) * P + p] = val;
+  if (yh) yh[m * oc + c] = relu_if(val, relu_out);
 }
 
 size_t fwd_ws_bytes(const ConvGeom& cg) {
@@ -208,11 +228,11 @@ size_t fwd_ws_bytes(const ConvGeom& cg) {
 }
 
 void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
-              const ConvGeom& cg, float* y, void* ws) {
+              const ConvGeom& cg, float* y, void* ws, float* yh, int relu_out) {
   check_i32(cg);
   ConvFwd p;
   p.g = make_geo(cg);
-  p.x = x; p.relu = x_relu; p.wt = w; p.bias = bias; p.y = y;
+  p.x = x; p.relu = x_relu; p.wt = w; p.bias = bias; p.y = y; p.yh = yh; p.relu_out = relu_out;
   p.M = cg.b * cg.P(); p.N = cg.oc; p.K = cg.K();
   p.ksplit = ws ? pick_ksplit(p.M, p.N, p.K, 1) : 1;
   p.part = static_cast<float*>(ws);
@@ -220,7 +240,7 @@ void conv_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const fl
   launch_tc_auto(ctx, p, 1);
   if (p.ksplit > 1) {
     const int64_t n = p.M * p.N;
-    ::dpg::launch_pdl(fwd_reduce_kernel, (unsigned)((n + 255) / 256), 256, 0, ctx->stream, p.part, p.ksplit, p.M, p.N, p.g.P, bias, y);
+    ::dpg::launch_pdl(fwd_reduce_kernel, (unsigned)((n + 255) / 256), 256, 0, ctx->stream, p.part, p.ksplit, p.M, p.N, p.g.P, bias, y, yh, relu_out);
     DPG_LAUNCH_CHECK(ctx);
   }
 }

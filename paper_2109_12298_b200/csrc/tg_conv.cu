@@ -1,0 +1,447 @@
+// tg_conv.cu — the TMA-fed tcgen05 contractions (tg_gemm.cuh): tensor-map construction and the
+// plain row-major GEMM the core is unit-tested through (dpg_tg_gemm_selftest).
+#include <mutex>
+
+#include "tg_gemm.cuh"
+
+namespace dpg {
+namespace tg {
+
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encoder() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  });
+  if (!fn) raise(DPG_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable (driver too old for TMA)");
+  return fn;
+}
+}  // namespace
+
+CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                     const uint32_t* box, const uint32_t* estr, CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  cuuint64_t d[5], s[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = estr ? estr[i] : 1;
+    if (i + 1 < rank) s[i] = strides[i];
+  }
+  const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base), d, s,
+                               bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(DPG_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+// ---- D[M][N] = A[M][K] B[N][K]^T, all row-major (the core's unit test) ----
+template <int BN, int BK>
+struct Gemm2D {
+  static constexpr bool kScaleA = false, kBPreSplit = false, kCtaReduce = false;
+  static constexpr int kStaging = 0, kEpiIn = 0;
+  CUtensorMap ma, mb;
+  float* d;
+  int M, N, K;
+  __device__ int nkb(int) const { return (K + BK - 1) / BK; }
+  __device__ uint32_t stage_bytes() const { return (uint32_t)((BM + BN) * BK * 4); }
+  __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t, uint32_t bar, int mt, int nt, int) const {
+    tma2(sa, &ma, bar, kb * BK, mt * BM);
+    tma2(sb, &mb, bar, kb * BK, nt * BN);
+  }
+  __device__ float scale(int, int, int, int) const { return 1.f; }
+  __device__ bool has_epi_in() const { return false; }
+  __device__ uint32_t epi_in_bytes() const { return 0; }
+  __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
+  __device__ void epilogue(int mt, int nt, int, int row, int c0, const float (&v)[16], double&, uint8_t*,
+                           const uint8_t*) const {
+    const int m = mt * BM + row;
+    if (m >= M) return;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int n = nt * BN + c0 + j;
+      if (n < N) d[(int64_t)m * N + n] = v[j];
+    }
+  }
+  __device__ void epi_store(int, int, int, int, uint32_t) const {}
+  __device__ void finish(int, int, int, double) const {}
+};
+
+template <int BN, int BK>
+void gemm2d(dpg_ctx* ctx, const float* a, const float* b, float* d, int M, int N, int K) {
+  const uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N};
+  const uint64_t sa[1] = {(uint64_t)K * 4}, sb[1] = {(uint64_t)K * 4};
+  const uint32_t ba[2] = {BK, BM}, bb[2] = {BK, BN};
+  Gemm2D<BN, BK> p;
+  p.ma = make_map(a, 2, da, sa, ba, nullptr, KLay<BK>::TMA_SWIZZLE);
+  p.mb = make_map(b, 2, db, sb, bb, nullptr, KLay<BK>::TMA_SWIZZLE);
+  p.d = d; p.M = M; p.N = N; p.K = K;
+  launch<BN, BK, stages_for<BN, BK>()>(ctx, p, dim3((M + BM - 1) / BM, (N + BN - 1) / BN, 1));
+}
+
+// =============================================================================================
+// Convolution contractions. Activations and highways that feed a TMA operand are kept on the
+// device in NHWC ("channels last") beside the reference-layout NCHW buffers: a (tap, channel
+// block) of the implicit im2col is then one box — channels innermost (one swizzled 64 / 128 B
+// row per output position), output positions walked with the convolution stride as the box's
+// traversal stride, padding from the out-of-bounds fill. Weights are re-laid and split once per
+// step by tg::prep_weights: wf[hi|lo][o][ki][kj][c] (forward, K = (tap, c)) and
+// wd[hi|lo][ki][kj][c][o] (dgrad), TF32-rounded hi and lo parts, loaded as the B operand as is.
+// Outputs leave through shared memory as TMA bulk stores (NCHW and NHWC copies of a 16-channel
+// chunk per store pair), so the epilogue threads issue no per-element global traffic.
+// =============================================================================================
+
+// ---- forward: Y[(n, p), o] = bias[o] + sum_(tap, c) X[n, p @ tap, c] W[o, c, tap] ----
+// rows of a tile: spt whole samples (spt P <= 128)
+template <int BN, int BK>
+struct ConvFwdT {
+  static constexpr bool kScaleA = false, kBPreSplit = true, kCtaReduce = false;
+  static constexpr int kStaging = 2 * 8192, kEpiIn = 0;  // NCHW [spt][16][P] | NHWC [128][16] (SW64)
+  CUtensorMap ma, mb, my, myh;
+  int b, O, P, kw, s, pad, spt, cpt, nk, has_yh, relu_out;
+  uint32_t bytes;
+  const float* bias;
+  __device__ int nkb(int) const { return nk; }
+  __device__ uint32_t stage_bytes() const { return bytes; }
+  __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t sblo, uint32_t bar, int mt, int nt, int) const {
+    const int tap = kb / cpt, cb = kb - tap * cpt;
+    const int ki = tap / kw, kj = tap - ki * kw;
+    tma4(sa, &ma, bar, cb * BK, kj - pad, ki - pad, mt * spt);
+    tma3(sb, &mb, bar, kb * BK, nt * BN, 0);
+    tma3(sblo, &mb, bar, kb * BK, nt * BN, 1);
+  }
+  __device__ float scale(int, int, int, int) const { return 1.f; }
+  __device__ bool has_epi_in() const { return false; }
+  __device__ uint32_t epi_in_bytes() const { return 0; }
+  __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
+  __device__ void epilogue(int, int nt, int, int row, int c0, const float (&v)[16], double&, uint8_t* stg,
+                           const uint8_t*) const {
+    if (row >= spt * P) return;
+    const int r = row / P, pp = row - r * P;
+    const int o0 = nt * BN + c0;
+    float out[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) out[j] = v[j] + ((bias && o0 + j < O) ? __ldg(bias + o0 + j) : 0.f);
+    float* nchw = reinterpret_cast<float*>(stg) + r * 16 * P + pp;  // [spt][16][P]
+#pragma unroll
+    for (int j = 0; j < 16; ++j) nchw[j * P] = out[j];
+    if (has_yh) {
+      uint8_t* nhwc = stg + 8192;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<float4*>(nhwc + sw64_off(row, c)) =
+            make_float4(relu_if(out[4 * c], relu_out), relu_if(out[4 * c + 1], relu_out),
+                        relu_if(out[4 * c + 2], relu_out), relu_if(out[4 * c + 3], relu_out));
+    }
+  }
+  __device__ void epi_store(int mt, int nt, int, int c0, uint32_t stg) const {
+    const int o0 = nt * BN + c0;
+    tma_st3(&my, stg, 0, o0, mt * spt);
+    if (has_yh) tma_st2(&myh, stg + 8192, o0, mt * spt * P);
+  }
+  __device__ void finish(int, int, int, double) const {}
+};
+
+// ---- dgrad: dX[n, c, iy, ix] = sum_(o, tap) dY[n, o, (iy + pad - ki) / s, ...] W[o, c, tap] ----
+// one launch slice (z) per stride-parity class (py, px) of input pixels; a class only meets the
+// taps ki = (py + pad) mod s (+ s ...), each a unit-stride box of the NHWC highway at offset
+// (py + pad - ki) / s. Rows of a tile: spt samples x the class grid (QH x QW, the largest class;
+// box rows beyond a smaller class's grid fall outside the tensor and are neither loaded nor
+// stored). The ReLU mask of the layer input comes in as a TMA box of the NHWC input copy; the
+// NHWC result leaves as a TMA store with the class's stride; the NCHW result is stored directly.
+template <int BN, int BK>
+struct ConvDgradT {
+  static constexpr bool kScaleA = false, kBPreSplit = true, kCtaReduce = false;
+  static constexpr int kStaging = 8192, kEpiIn = 8192;  // NHWC [spt][QH][QW][16] (SW64) out / mask in
+  CUtensorMap ma, mb, mdxh, mmask;
+  int b, C, H, W, kh, kw, s, pad, QH, QW, spt, ocb, has_mask, has_dxh;
+  uint32_t bytes;
+  float* dx;  // NCHW [b][C][H][W]
+  __device__ int first_tap(int ph) const { return (ph + pad) % s; }
+  __device__ int taps(int k0, int kdim) const { return k0 < kdim ? (kdim - k0 + s - 1) / s : 0; }
+  __device__ int nkb(int z) const {
+    const int py = z / s, px = z - py * s;
+    return taps(first_tap(py), kh) * taps(first_tap(px), kw) * ocb;
+  }
+  __device__ uint32_t stage_bytes() const { return bytes; }
+  __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t sblo, uint32_t bar, int mt, int nt, int z) const {
+    const int py = z / s, px = z - py * s;
+    const int t = kb / ocb, ob = kb - t * ocb;
+    const int ky0 = first_tap(py), kx0 = first_tap(px);
+    const int nkx = taps(kx0, kw);
+    const int ti = t / nkx, tj = t - ti * nkx;
+    const int ki = ky0 + ti * s, kj = kx0 + tj * s;
+    const int dy = (py + pad - ki) / s, dxo = (px + pad - kj) / s;  // exact (multiples of s)
+    tma4(sa, &ma, bar, ob * BK, dxo, dy, mt * spt);
+    const int brow = (ki * kw + kj) * C + nt * BN;
+    tma3(sb, &mb, bar, ob * BK, brow, 0);
+    tma3(sblo, &mb, bar, ob * BK, brow, 1);
+  }
+  __device__ float scale(int, int, int, int) const { return 1.f; }
+  __device__ bool has_epi_in() const { return has_mask != 0; }
+  __device__ uint32_t epi_in_bytes() const { return (uint32_t)(spt * QH * QW * 16 * 4); }
+  __device__ void epi_load(int mt, int nt, int z, int c0, uint32_t dst, uint32_t bar) const {
+    const int py = z / s, px = z - py * s;
+    tma4(dst, &mmask, bar, nt * BN + c0, px, py, mt * spt);
+  }
+  __device__ void epilogue(int mt, int nt, int z, int row, int c0, const float (&v)[16], double&, uint8_t* stg,
+                           const uint8_t* in) const {
+    const int q = QH * QW;
+    if (row >= spt * q) return;
+    const int r = row / q, rr = row - r * q;
+    const int n = mt * spt + r;
+    const int qy = rr / QW, qx = rr - qy * QW;
+    const int py = z / s, px = z - py * s;
+    const int iy = s * qy + py, ix = s * qx + px;
+    float out[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float4 m = make_float4(1.f, 1.f, 1.f, 1.f);
+      if (has_mask) m = *reinterpret_cast<const float4*>(in + sw64_off(row, c));
+      out[4 * c] = m.x > 0.f ? v[4 * c] : 0.f;
+      out[4 * c + 1] = m.y > 0.f ? v[4 * c + 1] : 0.f;
+      out[4 * c + 2] = m.z > 0.f ? v[4 * c + 2] : 0.f;
+      out[4 * c + 3] = m.w > 0.f ? v[4 * c + 3] : 0.f;
+      if (has_dxh) *reinterpret_cast<float4*>(stg + sw64_off(row, c)) =
+          make_float4(out[4 * c], out[4 * c + 1], out[4 * c + 2], out[4 * c + 3]);
+    }
+    if (n >= b || iy >= H || ix >= W) return;
+    const int cb0 = nt * BN + c0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (cb0 + j < C) dx[(((int64_t)n * C + cb0 + j) * H + iy) * W + ix] = out[j];
+  }
+  __device__ void epi_store(int mt, int nt, int z, int c0, uint32_t stg) const {
+    if (!has_dxh) return;
+    const int py = z / s, px = z - py * s;
+    tma_st4(&mdxh, stg, nt * BN + c0, px, py, mt * spt);
+  }
+  __device__ void finish(int, int, int, double) const {}
+};
+
+// ---- helper kernels ----
+// per-step weight layouts of one conv layer, TF32-split: wf[h][o][(ki kw + kj) C + c] and
+// wd[h][((ki kw + kj) C + c) O + o], h = 0: rna_tf32(w), h = 1: rna_tf32(w - hi)
+__global__ void prep_weights_kernel(TgPrepItems items) {
+  pdl_wait();
+  const TgPrepItem& it = items.item[blockIdx.y];
+  const int K = it.C * it.kh * it.kw, khw = it.kh * it.kw;
+  const int64_t n = (int64_t)it.O * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(i / K), k = (int)(i - (int64_t)o * K);
+    const int c = k / khw, t = k - c * khw;
+    const float v = __ldg(it.w + i);
+    const float hi = __uint_as_float(rna_tf32(__float_as_uint(v)));
+    const float lo = __uint_as_float(rna_tf32(__float_as_uint(v - hi)));
+    if (it.wf) {
+      const int64_t d = (int64_t)o * K + t * it.C + c;
+      it.wf[d] = hi;
+      it.wf[n + d] = lo;
+    }
+    if (it.wd) {
+      const int64_t d = ((int64_t)t * it.C + c) * it.O + o;
+      it.wd[d] = hi;
+      it.wd[n + d] = lo;
+    }
+  }
+  pdl_trigger();
+}
+
+// NCHW [b][C][P] -> NHWC [b][P][C] (optionally ReLU'd), one sample plane per block through smem
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, int relu, int C, int P, float* __restrict__ dst) {
+  extern __shared__ float tile[];
+  pdl_wait();
+  const int64_t base = (int64_t)blockIdx.x * C * P;
+  for (int i = threadIdx.x; i < C * P; i += blockDim.x) {
+    const int c = i / P, p = i - c * P;
+    tile[p * (C + 1) + c] = relu_if(__ldg(src + base + i), relu);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < C * P; i += blockDim.x) {
+    const int p = i / C, c = i - p * C;
+    dst[base + i] = tile[p * (C + 1) + c];
+  }
+  pdl_trigger();
+}
+
+// ---- host launchers ----
+namespace {
+// NHWC [b][H][W][C] tiles: box (bc channels, bw x bh positions walked with stride s, bn samples)
+CUtensorMap nhwc_map(const float* base, int b, int H, int W, int C, int bc, int bw, int bh, int bn, int s,
+                     CUtensorMapSwizzle swz) {
+  const uint64_t dims[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)b};
+  const uint64_t str[3] = {(uint64_t)C * 4, (uint64_t)W * C * 4, (uint64_t)H * W * C * 4};
+  const uint32_t box[4] = {(uint32_t)bc, (uint32_t)(bw * s), (uint32_t)(bh * s), (uint32_t)bn};
+  const uint32_t es[4] = {1, (uint32_t)s, (uint32_t)s, 1};
+  return make_map(base, 4, dims, str, box, es, swz);
+}
+// [2][rows][k] (TF32 hi and lo planes): box (bk, box_rows, 1)
+CUtensorMap split_rows_map(const float* base, int64_t rows, int64_t k, int bk, int box_rows, CUtensorMapSwizzle swz) {
+  const uint64_t dims[3] = {(uint64_t)k, (uint64_t)rows, 2};
+  const uint64_t str[2] = {(uint64_t)k * 4, (uint64_t)(rows * k * 4)};
+  const uint32_t box[3] = {(uint32_t)bk, (uint32_t)box_rows, 1};
+  return make_map(base, 3, dims, str, box, nullptr, swz);
+}
+// output columns per tile: the widest of 128 / 64 / 32 that still gives >= one CTA per SM
+int pick_bn(int n, int64_t mtiles) {
+  for (int bn : {128, 64, 32})
+    if (bn <= ((n + 15) / 16) * 16 + 15 && mtiles * ((n + bn - 1) / bn) >= kNumSMs) return bn;
+  return 32;
+}
+template <class F>
+void with_bn(int bn, F&& f) {
+  switch (bn) {
+    case 128: f(std::integral_constant<int, 128>{}); break;
+    case 64: f(std::integral_constant<int, 64>{}); break;
+    default: f(std::integral_constant<int, 32>{}); break;
+  }
+}
+template <class F>
+void with_bk(int bk, F&& f) {
+  if (bk == 32) f(std::integral_constant<int, 32>{});
+  else f(std::integral_constant<int, 16>{});
+}
+}  // namespace
+
+bool fwd_nhwc_ok(const ConvGeom& g) {
+  return g.ic % 16 == 0 && g.oc % 4 == 0 && g.P() <= BM && g.P() % 4 == 0 && g.ow * g.stride <= 256 &&
+         g.oh * g.stride <= 256;
+}
+bool dgrad_nhwc_ok(const ConvGeom& g) {
+  const int64_t qh = (g.h + g.stride - 1) / g.stride, qw = (g.w + g.stride - 1) / g.stride;
+  return g.oc % 16 == 0 && g.ic % 16 == 0 && qh * qw <= BM && qw * g.stride <= 256 && qh * g.stride <= 256;
+}
+
+void conv_fwd_nhwc(dpg_ctx* ctx, const float* xh, const float* wf, const float* bias, const ConvGeom& g, float* y,
+                   float* yh, int relu_out) {
+  const int b = (int)g.b, P = (int)g.P();
+  const int spt = BM / P;
+  const int64_t mtiles = (b + spt - 1) / spt;
+  const int bk = g.ic % 32 == 0 ? 32 : 16;
+  const int bn = pick_bn((int)g.oc, mtiles);
+  with_bk(bk, [&](auto BKc) {
+    constexpr int BK = decltype(BKc)::value;
+    with_bn(bn, [&](auto BNc) {
+      constexpr int BN = decltype(BNc)::value;
+      using Pr = ConvFwdT<BN, BK>;
+      Pr p;
+      p.ma = nhwc_map(xh, b, (int)g.h, (int)g.w, (int)g.ic, BK, (int)g.ow, (int)g.oh, spt, (int)g.stride,
+                      KLay<BK>::TMA_SWIZZLE);
+      p.mb = split_rows_map(wf, g.oc, g.K(), BK, BN, KLay<BK>::TMA_SWIZZLE);
+      {  // NCHW y [b][O][P]: box (P, 16 channels, spt samples)
+        const uint64_t dims[3] = {(uint64_t)P, (uint64_t)g.oc, (uint64_t)b};
+        const uint64_t str[2] = {(uint64_t)P * 4, (uint64_t)(g.oc * P * 4)};
+        const uint32_t box[3] = {(uint32_t)P, 16, (uint32_t)spt};
+        p.my = make_map(y, 3, dims, str, box, nullptr, CU_TENSOR_MAP_SWIZZLE_NONE);
+      }
+      p.has_yh = yh != nullptr;
+      if (yh) {  // NHWC yh [b P][O]: box (16 channels, spt P rows), 64-byte swizzled staging rows
+        const uint64_t dims[2] = {(uint64_t)g.oc, (uint64_t)b * P};
+        const uint64_t str[1] = {(uint64_t)g.oc * 4};
+        const uint32_t box[2] = {16, (uint32_t)(spt * P)};
+        p.myh = make_map(yh, 2, dims, str, box, nullptr, CU_TENSOR_MAP_SWIZZLE_64B);
+      }
+      p.b = b; p.O = (int)g.oc; p.P = P; p.kw = (int)g.kw; p.s = (int)g.stride; p.pad = (int)g.pad;
+      p.spt = spt; p.cpt = (int)g.ic / BK; p.nk = (int)(g.kh * g.kw) * p.cpt; p.relu_out = relu_out;
+      p.bytes = (uint32_t)((spt * P + 2 * BN) * BK * 4);
+      p.bias = bias;
+      launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn>()>(
+          ctx, p, dim3((unsigned)mtiles, (unsigned)((g.oc + BN - 1) / BN), 1));
+    });
+  });
+}
+
+void conv_dgrad_nhwc(dpg_ctx* ctx, const float* hh, const float* wd, const ConvGeom& g, const float* mask_h,
+                     float* dx, float* dxh) {
+  const int b = (int)g.b, s = (int)g.stride;
+  const int QH = (int)((g.h + s - 1) / s), QW = (int)((g.w + s - 1) / s);
+  const int spt = BM / (QH * QW);
+  const int64_t mtiles = (b + spt - 1) / spt;
+  const int bk = g.oc % 32 == 0 ? 32 : 16;
+  const int bn = pick_bn((int)g.ic, mtiles * s * s);
+  with_bk(bk, [&](auto BKc) {
+    constexpr int BK = decltype(BKc)::value;
+    with_bn(bn, [&](auto BNc) {
+      constexpr int BN = decltype(BNc)::value;
+      using Pr = ConvDgradT<BN, BK>;
+      Pr p;
+      // unit-stride boxes over the highway (NHWC [b][OH][OW][O])
+      p.ma = nhwc_map(hh, b, (int)g.oh, (int)g.ow, (int)g.oc, BK, QW, QH, spt, 1, KLay<BK>::TMA_SWIZZLE);
+      p.mb = split_rows_map(wd, g.kh * g.kw * g.ic, g.oc, BK, BN, KLay<BK>::TMA_SWIZZLE);
+      p.has_mask = mask_h != nullptr;
+      p.has_dxh = dxh != nullptr;
+      // 16-channel boxes of the input-side NHWC tensors, the class grid walked with stride s
+      if (mask_h) p.mmask = nhwc_map(mask_h, b, (int)g.h, (int)g.w, (int)g.ic, 16, QW, QH, spt, s, CU_TENSOR_MAP_SWIZZLE_64B);
+      if (dxh) p.mdxh = nhwc_map(dxh, b, (int)g.h, (int)g.w, (int)g.ic, 16, QW, QH, spt, s, CU_TENSOR_MAP_SWIZZLE_64B);
+      p.b = b; p.C = (int)g.ic; p.H = (int)g.h; p.W = (int)g.w; p.kh = (int)g.kh; p.kw = (int)g.kw;
+      p.s = s; p.pad = (int)g.pad; p.QH = QH; p.QW = QW; p.spt = spt; p.ocb = (int)g.oc / BK;
+      p.bytes = (uint32_t)((spt * QH * QW + 2 * BN) * BK * 4);
+      p.dx = dx;
+      launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn>()>(
+          ctx, p, dim3((unsigned)mtiles, (unsigned)((g.ic + BN - 1) / BN), (unsigned)(s * s)));
+    });
+  });
+}
+
+void prep_weights(dpg_ctx* ctx, const TgPrepItems& items) {
+  if (items.count == 0) return;
+  ::dpg::launch_pdl(prep_weights_kernel, dim3(2 * kNumSMs / items.count + 1, (unsigned)items.count), 256, 0,
+                    ctx->stream, items);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+void nchw_to_nhwc(dpg_ctx* ctx, const float* src, int relu, int64_t b, int64_t C, int64_t P, float* dst) {
+  const int smem = (int)(sizeof(float) * P * (C + 1));
+  if (smem > 96 * 1024) raise(DPG_ERR_DIMENSION, "nchw_to_nhwc: sample plane too large");
+  ensure_smem_attr(reinterpret_cast<const void*>(nchw_to_nhwc_kernel), smem);
+  ::dpg::launch_pdl(nchw_to_nhwc_kernel, (unsigned)b, 256, smem, ctx->stream, src, relu, (int)C, (int)P, dst);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace tg
+}  // namespace dpg
+
+#ifdef DPG_TG_TRACE
+// trace builds only (tools/tg_trace_step.py): read the traced launch's timeline
+extern "C" __attribute__((visibility("default"))) void dpg_tg_trace_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, dpg::tg::g_tg_trace, sizeof(unsigned long long) * 8 * 256);
+}
+#endif
+
+using dpg::guard;
+using dpg::raise;
+
+dpg_status dpg_tg_gemm_selftest(dpg_ctx* ctx, const float* a, const float* b, float* d, int64_t m, int64_t n,
+                                int64_t k, int bn, int bk) {
+  return guard(ctx, [&] {
+    if (!ctx) raise(DPG_ERR_PARAMETER, "null context");
+    if (m <= 0 || n <= 0 || k <= 0 || (k * 4) % 16 != 0 || m >= (1 << 30) || n >= (1 << 30) || k >= (1 << 30))
+      raise(DPG_ERR_DIMENSION, "tg_gemm_selftest: extents must be positive, K a multiple of 4");
+    const int M = (int)m, N = (int)n, K = (int)k;
+    if (bk == 32) {
+      switch (bn) {
+        case 32: dpg::tg::gemm2d<32, 32>(ctx, a, b, d, M, N, K); break;
+        case 64: dpg::tg::gemm2d<64, 32>(ctx, a, b, d, M, N, K); break;
+        case 128: dpg::tg::gemm2d<128, 32>(ctx, a, b, d, M, N, K); break;
+        default: raise(DPG_ERR_PARAMETER, "tg_gemm_selftest: bn must be 32, 64 or 128");
+      }
+    } else if (bk == 16) {
+      switch (bn) {
+        case 32: dpg::tg::gemm2d<32, 16>(ctx, a, b, d, M, N, K); break;
+        case 64: dpg::tg::gemm2d<64, 16>(ctx, a, b, d, M, N, K); break;
+        default: raise(DPG_ERR_PARAMETER, "tg_gemm_selftest: bn must be 32 or 64 with bk 16");
+      }
+    } else {
+      raise(DPG_ERR_PARAMETER, "tg_gemm_selftest: bk must be 16 or 32");
+    }
+  });
+}

@@ -1,0 +1,540 @@
+// tg_gemm.cuh — TMA-fed, warp-specialised tcgen05 GEMM, 3xTF32 fp32-faithful.
+//
+//   D[z][m][n] = sum_k A(z, m, k) * B(z, n, k)            (both operands K-major in shared memory)
+//
+// Operand tiles are moved by the Tensor Memory Accelerator (cp.async.bulk.tensor, tiled mode):
+// the implicit im2col of a convolution is one box per (tap, channel block), whose traversal
+// strides walk the convolution stride and whose out-of-bounds fill supplies the zero padding, so
+// no thread computes an address or touches an operand element on its way from HBM/L2 to shared
+// memory. The box lands in the canonical swizzled K-major UMMA layout (SWIZZLE_64B / 128B rows).
+//
+// Persistent: a CTA walks the output tiles blockIdx.x, + gridDim.x, ... (one CTA per SM), so the
+// TMA producer streams the next tile's operands while the current tile's epilogue drains; the
+// accumulator is double-buffered in TMEM. Warp roles (320 threads):
+//   warp 0      TMA producer (one elected thread): waits for a free stage, arms its mbarrier with
+//               the stage's transaction bytes, issues the boxes (Prob::issue)
+//   warp 1      MMA issuer (one elected thread; also allocates TMEM): waits for a converted
+//               stage, issues 3 tcgen05.mma.kind::tf32 per K = 8 slice (A_lo B_hi + A_hi B_lo +
+//               A_hi B_hi) into the tile's TMEM accumulator — A read from TMEM, B from shared
+//               memory — tcgen05.commit frees the stage and, after the tile's last stage, hands
+//               the accumulator to the epilogue
+//   warps 2-5   converters: every value of the landed fp32 tiles is split into hi = rna_tf32(x)
+//               and lo = rna_tf32(x - hi), optionally scaled first (the clip factor s_n of a
+//               clipped sum). A: thread = tile row (its TMEM lane), the row's BK values read from
+//               the swizzled tile and written as two TMEM column blocks (tcgen05.st); B: split in
+//               place, lo into a second buffer at the same swizzled offset
+//
+// Why A goes through TMEM: with 3 MMAs per K slice each re-reading both operands, a 128 x 64 x 32
+// stage moved ~168 KB through shared memory (TMA write, converter read + 2 writes, 12 MMA operand
+// reads) — bandwidth-bound at ~620 ns per stage (measured, tools/micro/tg_trace.cu). With A in
+// TMEM only the TMA write, the converter's reads and B's hi/lo and MMA reads remain.
+//   warps 6-9   epilogue: tcgen05.ld of TMEM lanes [32 (w % 4), +32) -> Prob::epilogue, then free
+//               the accumulator buffer
+//
+// Rounded parts leave a zero-mean dropped lo*lo term of <= 2^-22 |x w| per product (tc_gemm.cuh's
+// note on the truncated split: that one is biased and a long sum accumulates it).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "dpg_device.cuh"
+
+namespace dpg {
+namespace tg {
+
+constexpr int BM = 128;          // UMMA M: TMEM lanes = tile rows
+constexpr int kConvThreads = 128;
+
+// Timeline trace of CTA 0 (tools/micro/tg_trace.cu builds with -DDPG_TG_TRACE): globaltimer
+// stamps per role and iteration into g_tg_trace[event][iteration].
+#ifdef DPG_TG_TRACE
+__device__ unsigned long long g_tg_trace[8][256];
+__device__ int g_tg_trace_on;  // set by the host for the one launch it traces
+__device__ __forceinline__ void tg_trace(int ev, int i) {
+  if (g_tg_trace_on && blockIdx.x == 0 && i < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tg_trace[ev][i] = t;
+  }
+}
+#else
+__device__ __forceinline__ void tg_trace(int, int) {}
+#endif
+
+// ---- PTX wrappers ----
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+// bounded: a protocol slip (e.g. a transaction count that never completes) traps after ~2^30
+// polls (tens of seconds) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  for (uint32_t n = 0;; ++n) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    if (done) return;
+    if (n == (1u << 30)) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ void tma2(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma4(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_st2(const CUtensorMap* m, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void tma_st3(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void tma_st4(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// 16-byte chunk c of row r in a SWIZZLE_64B staging tile of 64-byte rows (matches TMA's layout)
+__device__ __forceinline__ uint32_t sw64_off(int r, int c) { return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4)); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major swizzled layout of BK fp32 per row: BK = 32 -> 128 B rows (SWIZZLE_128B, UMMA layout 2),
+// BK = 16 -> 64 B rows (SWIZZLE_64B, UMMA layout 4); 8-row atoms.
+template <int BK>
+struct KLay {
+  static_assert(BK == 16 || BK == 32, "BK: one 64 B or 128 B swizzle row");
+  static constexpr int ROW = BK * 4;
+  static constexpr int ATOM = 8 * ROW;
+  static constexpr uint64_t TYPE = BK == 32 ? 2 : 4;
+  static constexpr CUtensorMapSwizzle TMA_SWIZZLE = BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  __device__ static uint64_t desc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(ATOM >> 4) << 32) |
+           ((uint64_t)1 << 46) | (TYPE << 61);
+  }
+};
+
+// kind::tf32: D f32, A/B tf32, both K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// this thread's TMEM lane, 16 consecutive columns from taddr
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] B[smem]^T (A K-major in TMEM: lane = row, one column per tf32 element)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// round to nearest TF32 (ties away from zero, as cvt.rna.tf32.f32)
+__device__ __forceinline__ uint32_t rna_tf32(uint32_t u) { return (u + 0x1000u) & 0xffffe000u; }
+
+// split 16 bytes in place: hi = rna(s x) (overwrites the landed value), lo = rna(s x - hi)
+template <bool kScale>
+__device__ __forceinline__ void split16(uint8_t* hi, uint8_t* lo, float s) {
+  float4 v = *reinterpret_cast<const float4*>(hi);
+  if (kScale) {
+    v.x *= s; v.y *= s; v.z *= s; v.w *= s;
+  }
+  uint4 h, l;
+  h.x = rna_tf32(__float_as_uint(v.x)); l.x = rna_tf32(__float_as_uint(v.x - __uint_as_float(h.x)));
+  h.y = rna_tf32(__float_as_uint(v.y)); l.y = rna_tf32(__float_as_uint(v.y - __uint_as_float(h.y)));
+  h.z = rna_tf32(__float_as_uint(v.z)); l.z = rna_tf32(__float_as_uint(v.z - __uint_as_float(h.z)));
+  h.w = rna_tf32(__float_as_uint(v.w)); l.w = rna_tf32(__float_as_uint(v.w - __uint_as_float(h.w)));
+  *reinterpret_cast<uint4*>(hi) = h;
+  *reinterpret_cast<uint4*>(lo) = l;
+}
+
+template <int BN, int BK, int ST, int STG, int EIN>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE = A_BYTES + 2 * B_BYTES;  // A (raw), B, B_lo
+  static constexpr int STG_OFF = ST * STAGE;           // 2 epilogue staging buffers of STG bytes
+  static constexpr int EIN_OFF = STG_OFF + 2 * STG;     // 2 epilogue input buffers of EIN bytes
+  static constexpr int BAR_OFF = EIN_OFF + 2 * EIN;
+  static constexpr int BARS = (3 * ST + 6) * 8;
+  static constexpr int TOTAL = BAR_OFF + BARS + 16 + 1024;  // + alignment slack
+};
+
+// TMEM: two accumulator buffers of BN columns, then per stage A_hi and A_lo (BK columns each)
+template <int BN, int BK>
+constexpr int tmem_stage_cap() {
+  return (512 - 2 * BN) / (2 * BK);
+}
+// deepest ring (<= 6 stages) that fits the 227 KB a CTA may use and the 512 TMEM columns
+template <int BN, int BK, int STG = 0, int EIN = 0>
+constexpr int stages_for() {
+  constexpr int st = Smem<BN, BK, 1, STG, EIN>::STAGE;
+  constexpr int fixed = 2 * STG + 2 * EIN + 4096;
+  constexpr int lim = 227 * 1024 - fixed;
+  constexpr int by_smem = (6 * st <= lim) ? 6 : (5 * st <= lim) ? 5 : (4 * st <= lim) ? 4 : (3 * st <= lim) ? 3 : 2;
+  return by_smem < tmem_stage_cap<BN, BK>() ? by_smem : tmem_stage_cap<BN, BK>();
+}
+constexpr uint32_t kTmemCols = 512;
+
+// Tile space of a launch: mt fastest, then nt, then z.
+struct Tiles {
+  int m, n, z;
+  __device__ int count() const { return m * n * z; }
+  __device__ void at(int t, int& mt, int& nt, int& zz) const {
+    mt = t % m;
+    const int r = t / m;
+    nt = r % n;
+    zz = r / n;
+  }
+};
+
+// Prob interface (all __device__ const members; the Prob is a __grid_constant__ kernel parameter,
+// so tensor maps it holds are addressable by TMA):
+//   static constexpr bool kScaleA;     converters multiply the A tile by scale(...)
+//   static constexpr bool kBPreSplit;  issue() loads B_hi and B_lo (both TF32-rounded in global);
+//                                      otherwise converters split the landed B in place
+//   static constexpr bool kCtaReduce;  per-tile reduction of the epilogue's acc -> finish()
+//   static constexpr int kStaging;     bytes of one epilogue staging buffer (per 16 columns; 0 =
+//                                      the epilogue stores directly)
+//   static constexpr int kEpiIn;       bytes of one epilogue input chunk loaded by TMA (0 = none)
+//   int  nkb(int z) const;             K blocks of a tile of launch slice z (may be 0)
+//   uint32_t stage_bytes() const;      TMA transaction bytes per stage
+//   void issue(int kb, uint32_t sa, uint32_t sb, uint32_t sblo, uint32_t bar, int mt, int nt, int z) const;
+//   float scale(int kb, int mt, int nt, int z) const;
+//   bool has_epi_in() const;           this launch loads epilogue inputs (kEpiIn > 0)
+//   uint32_t epi_in_bytes() const;     bytes one epi_load moves (<= kEpiIn)
+//   void epi_load(int mt, int nt, int z, int c0, uint32_t dst, uint32_t bar) const;   kEpiIn bytes
+//   void epilogue(int mt, int nt, int z, int row, int c0, const float (&v)[16], double& acc,
+//                 uint8_t* stage, const uint8_t* in) const;   row < 128, columns c0 .. c0+15
+//   void epi_store(int mt, int nt, int z, int c0, uint32_t stage) const;   one thread (kStaging)
+//   void finish(int mt, int nt, int z, double acc_sum) const;               (kCtaReduce)
+constexpr int kThreads2 = 320;
+template <int BN, int BK, int ST, class Prob>
+__global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant__ Prob p, const Tiles tiles) {
+  constexpr int STG = Prob::kStaging, EIN = Prob::kEpiIn;
+  using S = Smem<BN, BK, ST, STG, EIN>;
+  using Lay = KLay<BK>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = su32(smem);
+  const uint32_t bar0 = sbase + S::BAR_OFF;  // full[ST], conv[ST], empty[ST], tfull[2], tempty[2], ein[2]
+  auto full = [&](int s) { return bar0 + 8u * s; };
+  auto conv = [&](int s) { return bar0 + 8u * (ST + s); };
+  auto empty = [&](int s) { return bar0 + 8u * (2 * ST + s); };
+  auto tfull = [&](int a) { return bar0 + 8u * (3 * ST + a); };
+  auto tempty = [&](int a) { return bar0 + 8u * (3 * ST + 2 + a); };
+  auto ein = [&](int a) { return bar0 + 8u * (3 * ST + 4 + a); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::BAR_OFF + S::BARS);
+  auto sA = [&](int s) { return sbase + s * S::STAGE; };
+  auto sB = [&](int s) { return sbase + s * S::STAGE + S::A_BYTES; };
+  auto sBlo = [&](int s) { return sbase + s * S::STAGE + S::A_BYTES + S::B_BYTES; };
+  // TMEM columns of stage s's A_hi / A_lo (after the two accumulator buffers)
+  auto tA = [&](int s) { return (uint32_t)(2 * BN + s * 2 * BK); };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = tiles.count();
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(conv(s), kConvThreads);
+      mbar_init(empty(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), kConvThreads);
+      mbar_init(ein(a), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();  // barrier init and TMEM allocation overlap the previous kernel's tail
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int mt, nt, z;
+        tiles.at(t, mt, nt, z);
+        const int nkb = p.nkb(z);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % ST;
+          if (it >= ST) mbar_wait(empty(s), ((it / ST) - 1) & 1);
+          tg_trace(0, it);
+          mbar_expect_tx(full(s), p.stage_bytes());
+          p.issue(kb, sA(s), sB(s), sBlo(s), full(s), mt, nt, z);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(BN);
+      int it = 0, j = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+        int mt, nt, z;
+        tiles.at(t, mt, nt, z);
+        const int nkb = p.nkb(z);
+        const int a = j & 1;
+        if (j >= 2) mbar_wait(tempty(a), ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(a * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(conv(s), (it / ST) & 1);
+          tg_trace(3, it);
+          tc_fence_after();
+          const uint32_t ahi = tmem + tA(s), alo = ahi + BK;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t off = kk * 32;  // 8 tf32 = 32 B along the swizzled row
+            const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32_ts(acc, alo + kk * 8, Lay::desc(sB(s) + off), idesc, acc0);
+            mma_tf32_ts(acc, ahi + kk * 8, Lay::desc(sBlo(s) + off), idesc, 1u);
+            mma_tf32_ts(acc, ahi + kk * 8, Lay::desc(sB(s) + off), idesc, 1u);
+          }
+          mma_commit(empty(s));
+        }
+        mma_commit(tfull(a));
+      }
+    }
+  } else if (warp < 6) {
+    // converters. A: thread = row 32 (w % 4) + lane of the tile (its TMEM lane)
+    const int tc = threadIdx.x - 64;
+    const int q = warp & 3;
+    const int r = 32 * q + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(32 * q) << 16);
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int mt, nt, z;
+      tiles.at(t, mt, nt, z);
+      const int nkb = p.nkb(z);
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % ST;
+        mbar_wait(full(s), (it / ST) & 1);
+        if (tc == 0) tg_trace(1, it);
+        float sc = 1.f;
+        if (Prob::kScaleA) sc = p.scale(kb, mt, nt, z);
+        const uint8_t* arow = smem + s * S::STAGE + r * Lay::ROW;
+        const int sw = Lay::ROW == 128 ? (r & 7) : ((r >> 1) & 3);
+#pragma unroll
+        for (int h = 0; h < BK / 16; ++h) {  // 16 columns (4 chunks) at a time
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float4 v = *reinterpret_cast<const float4*>(arow + (((4 * h + c) ^ sw) << 4));
+            if (Prob::kScaleA) {
+              v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+            }
+            const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              hi[4 * c + u] = rna_tf32(__float_as_uint(e[u]));
+              lo[4 * c + u] = rna_tf32(__float_as_uint(e[u] - __uint_as_float(hi[4 * c + u])));
+            }
+          }
+          tmem_st16(lane_addr + tA(s) + 16 * h, hi);
+          tmem_st16(lane_addr + tA(s) + BK + 16 * h, lo);
+        }
+        if (!Prob::kBPreSplit) {
+          uint8_t* b = smem + s * S::STAGE + S::A_BYTES;
+#pragma unroll 4
+          for (int i = tc * 16; i < S::B_BYTES; i += kConvThreads * 16) split16<false>(b + i, b + S::B_BYTES + i, 1.f);
+          fence_proxy_async();
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        if (tc == 0) tg_trace(2, it);
+        mbar_arrive(conv(s));
+      }
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes [32 (w % 4), +32) of the tile's accumulator buffer;
+    // outputs staged in shared memory go out as TMA bulk stores issued by one thread
+    const int q = warp & 3;
+    const int row = 32 * q + lane;
+    const bool leader = warp == 6 && lane == 0;
+    int j = 0, g = 0;  // tile and chunk counters of this CTA
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      int mt, nt, z;
+      tiles.at(t, mt, nt, z);
+      const int nkb = p.nkb(z);
+      const int a = j & 1;
+      const bool epi_in = EIN > 0 && p.has_epi_in();
+      if (epi_in && leader) {  // epilogue inputs of the tile's first chunk
+        mbar_expect_tx(ein(g & 1), p.epi_in_bytes());
+        p.epi_load(mt, nt, z, 0, sbase + S::EIN_OFF + (g & 1) * EIN, ein(g & 1));
+      }
+      mbar_wait(tfull(a), (j >> 1) & 1);
+      if (row == 0) tg_trace(4, j);
+      tc_fence_after();
+      if (t + (int)gridDim.x >= ntiles) pdl_trigger();  // last tile: the next kernel may launch
+      double acc = 0.0;
+      float v[16];
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16, ++g) {
+        if (epi_in && leader && c0 + 16 < BN) {  // prefetch the next chunk's inputs
+          mbar_expect_tx(ein((g + 1) & 1), p.epi_in_bytes());
+          p.epi_load(mt, nt, z, c0 + 16, sbase + S::EIN_OFF + ((g + 1) & 1) * EIN, ein((g + 1) & 1));
+        }
+        if (nkb > 0) {
+          tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), v);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
+        }
+        if (row == 0) tg_trace(6, j * 8 + c0 / 16);
+        if (c0 + 16 >= BN) {  // every TMEM read of this buffer is done: release it to the MMA warp
+          tc_fence_before();
+          mbar_arrive(tempty(a));
+        }
+        const uint8_t* in = nullptr;
+        if (epi_in) {
+          mbar_wait(ein(g & 1), (g >> 1) & 1);
+          in = smem + S::EIN_OFF + (g & 1) * EIN;
+        }
+        uint8_t* stg = STG > 0 ? smem + S::STG_OFF + (g & 1) * STG : nullptr;
+        p.epilogue(mt, nt, z, row, c0, v, acc, stg, in);
+        if (STG > 0) {
+          fence_proxy_async();
+          if (leader) bulk_wait_read<0>();  // the previous chunk's stores have read their buffer
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (leader) {
+            p.epi_store(mt, nt, z, c0, sbase + S::STG_OFF + (g & 1) * STG);
+            bulk_commit();
+          }
+        } else if (epi_in) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // the input buffer may be refilled
+        }
+        if (row == 0) tg_trace(7, j * 8 + c0 / 16);
+      }
+      if (row == 0) tg_trace(5, j);
+      if (Prob::kCtaReduce) {
+        __shared__ double red[2][4];
+        acc = warp_sum(acc);
+        if (lane == 0) red[a][q] = acc;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) p.finish(mt, nt, z, red[a][0] + red[a][1] + red[a][2] + red[a][3]);
+      }
+    }
+    if (STG > 0 && leader) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+// ---- host side: tensor maps ----
+// Tiled fp32 tensor map. dims / strides innermost first (strides in bytes, for dims 1..rank-1);
+// box and traversal strides (estr: 1, or the convolution stride) per dim.
+CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                     const uint32_t* box, const uint32_t* estr, CUtensorMapSwizzle swz);
+
+#ifdef DPG_TG_TRACE
+inline int& trace_launch_count() {
+  static int n = 0;
+  return n;
+}
+#endif
+
+// grid: the tile space (m tiles, n tiles, slices); the launch is persistent, min(tiles, #SMs) CTAs
+template <int BN, int BK, int ST, class Prob>
+void launch(dpg_ctx* ctx, const Prob& p, dim3 grid) {
+  const int smem = Smem<BN, BK, ST, Prob::kStaging, Prob::kEpiIn>::TOTAL;
+  ensure_smem_attr(reinterpret_cast<const void*>(tg_kernel<BN, BK, ST, Prob>), smem);
+  const Tiles tiles{(int)grid.x, (int)grid.y, (int)grid.z};
+  const int64_t nt = (int64_t)grid.x * grid.y * grid.z;
+  const unsigned ctas = (unsigned)std::min<int64_t>(nt, kNumSMs);
+#ifdef DPG_TG_TRACE
+  {  // trace only the DPG_TG_TRACE_AT-th TMA-fed launch of the process
+    const int at = std::getenv("DPG_TG_TRACE_AT") ? std::atoi(std::getenv("DPG_TG_TRACE_AT")) : -1;
+    const int on = trace_launch_count()++ == at ? 1 : 0;
+    cudaMemcpyToSymbolAsync(g_tg_trace_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+  }
+#endif
+  ::dpg::launch_pdl(tg_kernel<BN, BK, ST, Prob>, dim3(ctas), kThreads2, smem, ctx->stream, p, tiles);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace tg
+}  // namespace dpg

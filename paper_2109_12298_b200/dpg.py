@@ -85,6 +85,7 @@ class dpg_optimizer_config(ctypes.Structure):
 # exported symbols and their argument types (everything include/dpg.h declares)
 _SIGS = {
     "dpg_abi_version": (ctypes.c_int, []),
+    "dpg_tg_gemm_selftest": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32]),
     "dpg_ctx_create": (_I32, [_I32, _P, ctypes.POINTER(_P)]),
     "dpg_ctx_destroy": (None, [_P]),
     "dpg_ctx_stream": (_P, [_P]),
@@ -619,3 +620,12 @@ class DpOptimizer:
         self._b = b
         _check(lib().dpg_train_step_host(self.h, hp(x_host), hp(targets_host), b, hp(loss_host)),
                self.ctx.h)
+
+
+def tg_gemm_selftest(ctx: Context, a: torch.Tensor, b: torch.Tensor, bn: int = 64, bk: int = 32) -> torch.Tensor:
+    """D = A B^T through the TMA-fed tcgen05 GEMM core (dpg_tg_gemm_selftest; diagnostics)."""
+    m, k = a.shape
+    n = b.shape[0]
+    d = torch.empty(m, n, device=a.device, dtype=torch.float32)
+    _check(lib().dpg_tg_gemm_selftest(ctx.h, _p(a), _p(b), _p(d), m, n, k, bn, bk), ctx.h)
+    return d

@@ -1,0 +1,32 @@
+"""The TMA-fed tcgen05 GEMM core (csrc/tg_gemm.cuh) on its own: D = A B^T against fp64.
+
+Every convolution contraction of the step is built on this core (TMA boxes -> in-place 3xTF32
+split -> tcgen05.mma -> TMEM epilogue), so its numerics are pinned here on plain row-major
+operands, with ragged M / N / K (TMA out-of-bounds fill) and the longest K a convolution of the
+step contracts (576). Longer chains are not fp32-faithful: the tensor core's fp32 accumulation
+error grows with the chain (K = 4096 measured 2.7e-5 max-scaled), which is why the clipped sums
+bound their chains (tc_conv.cu kCsumChain)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("m,n,k,bn,bk", [
+    (128, 64, 32, 64, 32), (300, 100, 200, 64, 32), (300, 100, 200, 32, 16), (257, 130, 576, 128, 32),
+    (1000, 32, 64, 32, 32), (64, 64, 16, 64, 16)])
+def test_tg_gemm_matches_fp64(ctx, m, n, k, bn, bk):
+    import torch
+    from paper_2109_12298_b200 import dpg
+    rng = np.random.default_rng(m + n + k)
+    a = rng.standard_normal((m, k)).astype(np.float32)
+    b = rng.standard_normal((n, k)).astype(np.float32)
+    d = dpg.tg_gemm_selftest(ctx, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), bn, bk)
+    ctx.sync()
+    ref = a.astype(np.float64) @ b.astype(np.float64).T
+    got = d.cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    # fp32-faithful: the fp32 product sum itself is ~sqrt(k) 2^-24 off
+    assert err < 2e-6, f"max-scaled error {err:.3e}"
+    # and no bias: mean signed error tiny relative to the spread
+    assert abs((got - ref).mean()) < 1e-6 * np.abs(ref).max()
