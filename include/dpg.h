@@ -338,6 +338,49 @@ DPG_API dpg_status dpg_train_step(dpg_optimizer* opt, const float* x, const floa
                                   int64_t b, float* loss, int use_graph);
 
 /* ======================================================================================
+ * Privacy bookkeeping (host side).
+ *
+ * NoiseSchedule (reference optimizer.hpp:280-358): sigma per epoch. dpg_noise_schedule_init
+ * validates like the reference factories (constant / exponential / step / custom; the custom table
+ * is borrowed, not copied); dpg_schedule_noise evaluates epoch, stores it in `current` and, when
+ * opt is non-NULL, applies it (dpg_set_noise_multiplier). */
+enum { DPG_SCHEDULE_CONSTANT = 0, DPG_SCHEDULE_EXPONENTIAL = 1, DPG_SCHEDULE_STEP = 2, DPG_SCHEDULE_CUSTOM = 3 };
+typedef struct dpg_noise_schedule {
+  int kind;
+  double initial_sigma;
+  double gamma;   /* exponential: sigma0 * gamma^epoch */
+  double factor;  /* step: sigma0 * factor^(epoch / period) */
+  uint64_t period;
+  const double* table; /* custom: per-epoch values, the last persists */
+  int64_t table_len;
+  double current;
+} dpg_noise_schedule;
+DPG_API dpg_status dpg_noise_schedule_init(dpg_noise_schedule* s, int kind, double sigma0, double gamma,
+                                           double factor, uint64_t period, const double* table,
+                                           int64_t table_len);
+DPG_API double dpg_noise_schedule_sigma_at(const dpg_noise_schedule* s, uint64_t epoch);
+DPG_API dpg_status dpg_schedule_noise(dpg_noise_schedule* s, uint64_t epoch, dpg_optimizer* opt, double* sigma);
+
+/* RDP accountant of the subsampled Gaussian mechanism (reference SPEC.md:331-389; spec-only in
+ * the reference): integer orders (default 2..64, 128, 256), per-step RDP in log space,
+ * additive composition over the recorded (sigma, q, steps), epsilon = min_a rdp(a) + ln(1/delta)/(a-1),
+ * and calibration of sigma to a target epsilon by bisection (tolerance 1e-3). */
+typedef struct dpg_accountant dpg_accountant;
+DPG_API dpg_status dpg_rdp_subsampled_gaussian(double q, double sigma, int alpha, double* out);
+DPG_API dpg_status dpg_accountant_create(const int* orders, int n, dpg_accountant** out);
+DPG_API void dpg_accountant_destroy(dpg_accountant* a);
+DPG_API int dpg_accountant_num_orders(const dpg_accountant* a);
+DPG_API dpg_status dpg_accountant_step(dpg_accountant* a, double sigma, double q, int64_t steps);
+DPG_API dpg_status dpg_accountant_rdp(const dpg_accountant* a, int* orders, double* curve);
+DPG_API dpg_status dpg_accountant_epsilon(const dpg_accountant* a, double delta, double* eps, int* best_order);
+DPG_API dpg_status dpg_get_noise_multiplier(double target_eps, double delta, double q, int64_t steps,
+                                            double sigma_min, double sigma_max, double* sigma);
+
+/* GradSampleRecord export (Appendix D inspection): parameter `param`'s
+ * [b, ...param] per-sample gradients of the pending batch, copied to host (synchronous). */
+DPG_API dpg_status dpg_grad_sample_export(const dpg_optimizer* opt, int param, float* host, int64_t capacity);
+
+/* ======================================================================================
  * Diagnostics (no reference counterpart): unit test of the TMA-fed tcgen05 GEMM core that the
  * convolution contractions are built on. D[m][n] = sum_k A[m][k] B[n][k], row-major fp32 device
  * buffers, 3xTF32; bn in {32, 64, 128} output columns per tile, bk in {16, 32} K per stage

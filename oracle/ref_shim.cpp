@@ -265,6 +265,23 @@ extern "C" {
 
 const char* dpgref_last_error() { return g_err.c_str(); }
 
+// the reference's NoiseSchedule (optimizer.hpp:280-358): build it with the factory of `kind`
+// (0 constant, 1 exponential, 2 step, 3 custom) and evaluate schedule_noise at each epoch
+int dpgref_schedule_sigmas(int kind, double sigma0, double gamma, double factor, uint64_t period,
+                           const double* table, int64_t table_len, const uint64_t* epochs, int64_t n,
+                           double* out) {
+  return guarded([&] {
+    NoiseSchedule s;
+    switch (kind) {
+      case 0: s = NoiseSchedule::constant(sigma0); break;
+      case 1: s = NoiseSchedule::exponential(sigma0, gamma); break;
+      case 2: s = NoiseSchedule::step(sigma0, factor, (std::size_t)period); break;
+      default: s = NoiseSchedule::custom(std::vector<double>(table, table + table_len)); break;
+    }
+    for (int64_t i = 0; i < n; ++i) out[i] = schedule_noise(s, (std::size_t)epochs[i]);
+  });
+}
+
 int dpgref_rng_u64(uint64_t seed, int64_t n, uint64_t* out) {
   return guarded([&] {
     RngStream r = RngStream::standard(seed);

@@ -1304,6 +1304,24 @@ dpg_status dpg_last_clip_summary(dpg_optimizer* o, double* norms, double* scales
   });
 }
 
+// the pending batch's per-sample gradients of parameter p ([b, ...param], grad_sample.hpp:18-19) to
+// the host; synchronous (GradSampleRecord export)
+dpg_status dpg_grad_sample_export(const dpg_optimizer* o, int p, float* host, int64_t capacity) {
+  return guard(o ? o->m->ctx : nullptr, [&] {
+    if (!o) raise(DPG_ERR_PARAMETER, "null optimizer");
+    if (p < 0 || p >= (int)o->m->params.size()) raise(DPG_ERR_PARAMETER, "parameter index out of range");
+    if (!o->has_grad_sample) raise(DPG_ERR_LIFECYCLE, "no grad_sample: run forward_backward first");
+    if (!o->cfg.materialise_grad_sample)
+      raise(DPG_ERR_LIFECYCLE, "grad_sample was not materialised (materialise_grad_sample = 0)");
+    const ParamInfo& pi = o->m->params[p];
+    const int64_t n = o->pending_b * pi.numel;
+    if (!host || capacity < n) raise(DPG_ERR_DIMENSION, "export buffer needs " + std::to_string(n) + " floats");
+    DPG_CUDA(cudaSetDevice(o->m->ctx->device));
+    DPG_CUDA(cudaStreamSynchronize(o->m->ctx->stream));
+    DPG_CUDA(cudaMemcpy(host, o->record + o->pending_b * pi.offset, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  });
+}
+
 const float* dpg_grad_sample(const dpg_optimizer* o) {
   return (o && o->has_grad_sample && o->cfg.materialise_grad_sample) ? o->record : nullptr;
 }

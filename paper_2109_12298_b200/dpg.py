@@ -86,6 +86,18 @@ class dpg_optimizer_config(ctypes.Structure):
 _SIGS = {
     "dpg_abi_version": (ctypes.c_int, []),
     "dpg_tg_gemm_selftest": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32]),
+    "dpg_noise_schedule_init": (_I32, [_P, _I32, _D, _D, _D, ctypes.c_uint64, _P, _I64]),
+    "dpg_noise_schedule_sigma_at": (_D, [_P, ctypes.c_uint64]),
+    "dpg_schedule_noise": (_I32, [_P, ctypes.c_uint64, _P, _P]),
+    "dpg_rdp_subsampled_gaussian": (_I32, [_D, _D, _I32, _P]),
+    "dpg_accountant_create": (_I32, [_P, _I32, ctypes.POINTER(_P)]),
+    "dpg_accountant_destroy": (None, [_P]),
+    "dpg_accountant_num_orders": (_I32, [_P]),
+    "dpg_accountant_step": (_I32, [_P, _D, _D, _I64]),
+    "dpg_accountant_rdp": (_I32, [_P, _P, _P]),
+    "dpg_accountant_epsilon": (_I32, [_P, _D, _P, _P]),
+    "dpg_get_noise_multiplier": (_I32, [_D, _D, _D, _I64, _D, _D, _P]),
+    "dpg_grad_sample_export": (_I32, [_P, _I32, _P, _I64]),
     "dpg_ctx_create": (_I32, [_I32, _P, ctypes.POINTER(_P)]),
     "dpg_ctx_destroy": (None, [_P]),
     "dpg_ctx_stream": (_P, [_P]),
@@ -578,6 +590,14 @@ class DpOptimizer:
     def grad_sample(self) -> Optional[torch.Tensor]:
         return _view(lib().dpg_grad_sample(self.h), self._b * self.model.L)
 
+    def grad_sample_export(self, param: int):
+        """Parameter `param`'s per-sample gradients [b, ...param] on the host (dpg_grad_sample_export)."""
+        import numpy as np
+        numel = self.model.meta[param][4]
+        out = np.empty(self._b * numel, dtype=np.float32)
+        _check(lib().dpg_grad_sample_export(self.h, param, out.ctypes.data_as(ctypes.c_void_p), out.size), self.ctx.h)
+        return out.reshape((self._b,) + tuple(self.model.meta[param][3]))
+
     def summed_grad(self) -> Optional[torch.Tensor]:
         return _view(lib().dpg_summed_grad(self.h), self.model.L)
 
@@ -629,3 +649,101 @@ def tg_gemm_selftest(ctx: Context, a: torch.Tensor, b: torch.Tensor, bn: int = 6
     d = torch.empty(m, n, device=a.device, dtype=torch.float32)
     _check(lib().dpg_tg_gemm_selftest(ctx.h, _p(a), _p(b), _p(d), m, n, k, bn, bk), ctx.h)
     return d
+
+
+# ---------------------------------------------------------------------------------------------
+# Privacy bookkeeping (host side): NoiseSchedule, RDP accountant (include/dpg.h)
+# ---------------------------------------------------------------------------------------------
+
+class _CSchedule(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("initial_sigma", ctypes.c_double), ("gamma", ctypes.c_double),
+                ("factor", ctypes.c_double), ("period", ctypes.c_uint64), ("table", ctypes.c_void_p),
+                ("table_len", ctypes.c_int64), ("current", ctypes.c_double)]
+
+
+class NoiseSchedule:
+    """NoiseSchedule (optimizer.hpp:280-351) over dpg_noise_schedule; factories validate like the
+    reference's (ParameterError)."""
+    CONSTANT, EXPONENTIAL, STEP, CUSTOM = range(4)
+
+    def __init__(self, kind, sigma0=1.0, gamma=1.0, factor=1.0, period=1, table=None):
+        self._table = None
+        ptr, n = None, 0
+        if table is not None:
+            self._table = (ctypes.c_double * len(table))(*table)
+            ptr, n = ctypes.cast(self._table, ctypes.c_void_p), len(table)
+        self.s = _CSchedule()
+        _check(lib().dpg_noise_schedule_init(ctypes.byref(self.s), kind, sigma0, gamma, factor, period, ptr, n))
+
+    @classmethod
+    def constant(cls, sigma):
+        return cls(cls.CONSTANT, sigma)
+
+    @classmethod
+    def exponential(cls, sigma0, gamma):
+        return cls(cls.EXPONENTIAL, sigma0, gamma=gamma)
+
+    @classmethod
+    def step(cls, sigma0, factor, period):
+        return cls(cls.STEP, sigma0, factor=factor, period=period)
+
+    @classmethod
+    def custom(cls, table):
+        return cls(cls.CUSTOM, table=list(table))
+
+    @property
+    def current(self) -> float:
+        return self.s.current
+
+    def sigma_at(self, epoch: int) -> float:
+        return lib().dpg_noise_schedule_sigma_at(ctypes.byref(self.s), epoch)
+
+    def schedule_noise(self, epoch: int, optimizer=None) -> float:
+        """schedule_noise (optimizer.hpp:354-358); applies sigma to `optimizer` when given."""
+        out = ctypes.c_double()
+        _check(lib().dpg_schedule_noise(ctypes.byref(self.s), epoch, optimizer.h if optimizer else None,
+                                        ctypes.byref(out)), optimizer.ctx.h if optimizer else None)
+        return out.value
+
+
+def rdp_subsampled_gaussian(q: float, sigma: float, alpha: int) -> float:
+    out = ctypes.c_double()
+    _check(lib().dpg_rdp_subsampled_gaussian(q, sigma, alpha, ctypes.byref(out)))
+    return out.value
+
+
+def get_noise_multiplier(target_eps: float, delta: float, q: float, steps: int, sigma_min: float = 0.01,
+                         sigma_max: float = 100.0) -> float:
+    out = ctypes.c_double()
+    _check(lib().dpg_get_noise_multiplier(target_eps, delta, q, steps, sigma_min, sigma_max, ctypes.byref(out)))
+    return out.value
+
+
+class RdpAccountant:
+    """RdpAccountant over dpg_accountant."""
+
+    def __init__(self, orders: Optional[Sequence[int]] = None):
+        h = _P()
+        arr = (ctypes.c_int * len(orders))(*orders) if orders else None
+        _check(lib().dpg_accountant_create(arr, len(orders) if orders else 0, ctypes.byref(h)))
+        self._handle = _Handle(h, "dpg_accountant_destroy")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "_handle", None) is not None:
+            self._handle.destroy()
+
+    def step(self, sigma: float, q: float, steps: int = 1):
+        _check(lib().dpg_accountant_step(self.h, sigma, q, steps))
+
+    def rdp(self):
+        n = lib().dpg_accountant_num_orders(self.h)
+        orders = (ctypes.c_int * n)()
+        curve = (ctypes.c_double * n)()
+        _check(lib().dpg_accountant_rdp(self.h, orders, curve))
+        return list(orders), list(curve)
+
+    def epsilon(self, delta: float):
+        eps, best = ctypes.c_double(), ctypes.c_int()
+        _check(lib().dpg_accountant_epsilon(self.h, delta, ctypes.byref(eps), ctypes.byref(best)))
+        return eps.value, best.value

@@ -26,7 +26,9 @@ def test_tg_gemm_matches_fp64(ctx, m, n, k, bn, bk):
     ref = a.astype(np.float64) @ b.astype(np.float64).T
     got = d.cpu().numpy().astype(np.float64)
     err = np.abs(got - ref).max() / np.abs(ref).max()
-    # fp32-faithful: the fp32 product sum itself is ~sqrt(k) 2^-24 off
-    assert err < 2e-6, f"max-scaled error {err:.3e}"
+    # fp32-faithful to the parity criterion (SURVEY.md §8c, 1e-5 max-scaled): the split operands are
+    # exact to 2^-22, but the tensor core's fp32 accumulation adds ~2.5e-8 of max|D| per MMA of the
+    # chain (3 K / 8 of them: 5.3e-6 measured at K = 576)
+    assert err < 1e-5, f"max-scaled error {err:.3e}"
     # and no bias: mean signed error tiny relative to the spread
     assert abs((got - ref).mean()) < 1e-6 * np.abs(ref).max()
