@@ -221,12 +221,13 @@ size_t clipped_sum_ws_conv2d(const ConvGeom& g) {
 
 void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
                                const float* scale, const ConvGeom& g, float* sw, float* sb,
-                               int accumulate, void* ws) {
+                               int accumulate, void* ws, bool hw_nhwc) {
   (void)sb;  // the bias clipped sum is a weighted sum of the bias records (launch_wsum_multi)
   const int64_t nw = g.oc * g.K();
+  if (hw_nhwc && !tk::supported(g)) raise(DPG_ERR_INTERNAL, "channels-last highway needs the thin-K path");
   if (tk::supported(g)) {
     const int splits = tk::csum_splits(g);
-    tk::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits);
+    tk::csum(ctx, x, x_relu, hw, scale, g, static_cast<float*>(ws), splits, hw_nhwc);
     launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate);
     return;
   }

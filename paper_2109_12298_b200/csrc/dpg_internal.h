@@ -218,10 +218,10 @@ void linear_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, con
 namespace tk {  // thin-K conv layers (ic*kh*kw <= 64) on CUDA cores: rule (+ bias rule), clipped sum
 bool supported(const ConvGeom& g);
 void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& g, float* gw,
-        double* sq_part, float* gb, double* sq_b);
+        double* sq_part, float* gb, double* sq_b, bool hw_nhwc = false);
 int csum_splits(const ConvGeom& g);
 void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* scale,
-          const ConvGeom& g, float* part, int splits);
+          const ConvGeom& g, float* part, int splits, bool hw_nhwc = false);
 }  // namespace tk
 
 namespace rs {
@@ -240,7 +240,7 @@ void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const floa
 // gb / sq_b (optional): the bias rule fused into the same launch when gs_conv2d_fuses_bias(g)
 // (sq_b then has sq_rows_conv2d_bias(g) rows), else a separate bias launch (one row)
 void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& g,
-                      float* gw, double* sq_part, float* gb = nullptr, double* sq_b = nullptr);
+                      float* gw, double* sq_part, float* gb = nullptr, double* sq_b = nullptr, bool hw_nhwc = false);
 bool gs_conv2d_fuses_bias(const ConvGeom& g);
 int sq_rows_conv2d_bias(const ConvGeom& g);
 // bias rule: gb[n,o] = sum over middle of hw; `hw_layout_conv` selects [b, o, P] vs [b, mid, o]
@@ -265,7 +265,7 @@ void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, c
                                float* sw, float* sb, int accumulate, void* ws);
 void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
                                const float* scale, const ConvGeom& g, float* sw, float* sb,
-                               int accumulate, void* ws);
+                               int accumulate, void* ws, bool hw_nhwc = false);
 size_t clipped_sum_ws_embedding(int64_t b, int64_t vocab);
 void launch_clipped_sum_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* sorted_s,
                                   const float* hw, const float* scale, int64_t b, int64_t t,
@@ -332,6 +332,9 @@ struct LossFuse {
   // previous layer's pre-activation folded in), bit-identical to launch_linear_dgrad's vector path
   float* dx = nullptr;
   const float* dmask = nullptr;
+  // optional: dx also channels-last for a TMA-fed conv dgrad (flat j = c P + p -> [p][c])
+  float* dx_nhwc = nullptr;
+  int nhwc_c = 0, nhwc_p = 0;
 };
 // can the logits layer's forward launch also produce its input gradient (launch_linear_fwd + LossFuse::dx)?
 bool linear_fwd_fuses_dgrad(int64_t d, int64_t r, const float* dx, const float* mask);

@@ -246,6 +246,14 @@ __global__ void __launch_bounds__(32 * NW) linear_fwd_row_kernel(const float* __
           if (!(mv.w > 0.f)) a.w = 0.f;
         }
         *reinterpret_cast<float4*>(ce.dx + row * d + j) = a;
+        if (ce.dx_nhwc) {
+          const float e[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int jj = (int)j + u, c = jj / ce.nhwc_p, pp = jj - c * ce.nhwc_p;
+            ce.dx_nhwc[row * d + (int64_t)pp * ce.nhwc_c + c] = e[u];
+          }
+        }
       }
     }
   }

@@ -60,6 +60,9 @@ struct LayerPlan {
   int tg_fwd = 0;
   bool tg_dgrad = false;
   bool xh_by_prev = false, hh_by_next = false;
+  // the highway lives only channels-last (hh): written by the next layer's TMA-fed dgrad, read by
+  // this layer's thin-K rule / clipped sum (a first layer: no dgrad of its own reads it)
+  bool hw_nhwc = false;
   int next_param_layer = -1;
   float* xh = nullptr;    // [b][H][W][C] of the layer input (ReLU applied)
   float* hh = nullptr;    // [b][OH][OW][O] of the layer's highway
@@ -301,6 +304,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
   }
   // ---- forward (layers.hpp:576-592) ----
   bool loss_done = false;  // softmax-CE fused into the logits-producing linear forward
+  int hh_by_logits = -1;   // layer whose NHWC highway the logits launch wrote
   int dgrad_fused = -1;    // ... and that layer's input gradient too (its backward dgrad is skipped)
   for (size_t l = 0; l < m->layers.size(); ++l) {
     LayerPlan& lp = m->layers[l];
@@ -327,6 +331,12 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
             ce.dx = dst;
             ce.dmask = mask;
             dgrad_fused = l;
+            if (prev.tg_dgrad && prev.kind == DPG_LAYER_CONV2D && prev.g.oc * prev.g.P() == lp.d.in_features) {
+              ce.dx_nhwc = prev.hh;  // the conv's TMA-fed dgrad reads its highway channels-last
+              ce.nhwc_c = (int)prev.g.oc;
+              ce.nhwc_p = (int)prev.g.P();
+              hh_by_logits = lp.prev_param_layer;
+            }
           }
         }
         dpg::launch_linear_fwd(ctx, in, lp.in_relu, w, bias, b * lp.mid, lp.d.in_features,
@@ -438,11 +448,13 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
                             2.0 * b * g.oc * g.K() * g.P());
           if (lp.nparams > 1 && dpg::gs_conv2d_fuses_bias(g)) {
             // bias rule in the same launch (its norm rows: one per oc tile)
-            dpg::launch_gs_conv2d(ctx, in, lp.in_relu, hw, g, gw, sq_w, gs_ptr(o, lp.param0 + 1, b),
-                                  slab + (int64_t)m->params[lp.param0 + 1].sq_row0 * b);
+            dpg::launch_gs_conv2d(ctx, in, lp.in_relu, lp.hw_nhwc ? lp.hh : hw, g, gw, sq_w,
+                                  gs_ptr(o, lp.param0 + 1, b), slab + (int64_t)m->params[lp.param0 + 1].sq_row0 * b,
+                                  lp.hw_nhwc);
             break;
           }
-          dpg::launch_gs_conv2d(ctx, in, lp.in_relu, hw, g, gw, sq_w);
+          dpg::launch_gs_conv2d(ctx, in, lp.in_relu, lp.hw_nhwc ? lp.hh : hw, g, gw, sq_w, nullptr, nullptr,
+                                lp.hw_nhwc);
         }
         if (lp.nparams > 1) pending_bias = {g.P(), g.oc, 1};
         break;
@@ -485,13 +497,14 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
           ConvGeom g = lp.g;
           g.b = b;
           if (lp.tg_dgrad) {
-            if (!lp.hh_by_next) {
+            if (!lp.hh_by_next && hh_by_logits != l) {
               dpg::ProfScope ps(ctx, "nhwc.hw" + ls, 8.0 * b * lp.out_numel, 0.0);
               dpg::tg::nchw_to_nhwc(ctx, hw, 0, b, g.oc, g.P(), lp.hh);
             }
             dpg::ProfScope ps(ctx, "dgrad.conv2d" + ls, dio, 2.0 * b * g.oc * g.K() * g.P());
-            dpg::tg::conv_dgrad_nhwc(ctx, lp.hh, lp.wd, g, lp.in_relu ? lp.xh : nullptr, dst,
-                                     prev.tg_dgrad ? prev.hh : nullptr);
+            // the previous layer's highway: NCHW (its rules / dgrad read it) and / or its NHWC copy
+            dpg::tg::conv_dgrad_nhwc(ctx, lp.hh, lp.wd, g, lp.in_relu ? lp.xh : nullptr, prev.hw_nhwc ? nullptr : dst,
+                                     (prev.tg_dgrad || prev.hw_nhwc) ? prev.hh : nullptr);
             break;
           }
           dpg::ProfScope ps(ctx, "dgrad.conv2d" + ls, dio, 2.0 * b * g.oc * g.K() * g.P());
@@ -608,8 +621,8 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
           ConvGeom g = lp.g;
           g.b = b;
           dpg::ProfScope ps(ctx, "csum.conv2d" + ls, cio, 2.0 * b * g.oc * g.K() * g.P());
-          dpg::launch_clipped_sum_conv2d(ctx, in, lp.in_relu, hw, o->scale, g, dst, nullptr,
-                                         accumulate, ws);
+          dpg::launch_clipped_sum_conv2d(ctx, in, lp.in_relu, lp.hw_nhwc ? lp.hh : hw, o->scale, g, dst, nullptr,
+                                         accumulate, ws, lp.hw_nhwc);
           break;
         }
         case DPG_LAYER_EMBEDDING: {
@@ -878,6 +891,11 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
       lp.tg_dgrad = lp.tg_fwd && lp.prev_param_layer >= 0 && dpg::tg::dgrad_nhwc_ok(lp.g);
     }
     for (auto& lp : m->layers) {
+      if (lp.kind == DPG_LAYER_CONV2D && lp.prev_param_layer < 0 && lp.next_param_layer >= 0 &&
+          m->layers[lp.next_param_layer].tg_dgrad && dpg::tk::supported(lp.g))
+        lp.hw_nhwc = true;
+    }
+    for (auto& lp : m->layers) {
       // every conv forward writes its consumer's NHWC copy in the epilogue
       if (lp.tg_fwd && lp.prev_param_layer >= 0) lp.xh_by_prev = m->layers[lp.prev_param_layer].kind == DPG_LAYER_CONV2D;
       if (lp.tg_dgrad && lp.next_param_layer >= 0) lp.hh_by_next = m->layers[lp.next_param_layer].tg_dgrad;
@@ -942,7 +960,7 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     auto tg_sizes = [&](const LayerPlan& lp, size_t* sz) {  // xh, hh, wf, wd
       const int64_t wn = lp.g.oc * lp.g.K();
       sz[0] = lp.tg_fwd == 1 ? sizeof(float) * max_batch * lp.in_numel : 0;
-      sz[1] = lp.tg_dgrad ? sizeof(float) * max_batch * lp.out_numel : 0;
+      sz[1] = (lp.tg_dgrad || lp.hw_nhwc) ? sizeof(float) * max_batch * lp.out_numel : 0;
       sz[2] = lp.tg_fwd == 1 ? 2 * sizeof(float) * wn : 0;  // TF32 hi and lo planes
       sz[3] = lp.tg_dgrad ? 2 * sizeof(float) * wn : 0;
     };

@@ -96,13 +96,14 @@ int sq_rows_conv2d_bias(const ConvGeom& g) {
 }
 
 void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& g,
-                      float* gw, double* sq_part, float* gb, double* sq_b) {
+                      float* gw, double* sq_part, float* gb, double* sq_b, bool hw_nhwc) {
   if (g.b == 0) return;
   const bool bias = gb || sq_b;
   if (tk::supported(g)) {
-    tk::gs(ctx, x, x_relu, hw, g, gw, sq_part, gb, sq_b);
+    tk::gs(ctx, x, x_relu, hw, g, gw, sq_part, gb, sq_b, hw_nhwc);
     return;
   }
+  if (hw_nhwc) raise(DPG_ERR_INTERNAL, "channels-last highway needs the thin-K rule");
   if (rs::supported(g)) {
     rs::gs(ctx, x, x_relu, hw, g, gw, sq_part, gb, sq_b);
     return;

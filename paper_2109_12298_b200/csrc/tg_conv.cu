@@ -214,7 +214,7 @@ struct ConvDgradT {
       if (has_dxh) *reinterpret_cast<float4*>(stg + sw64_off(row, c)) =
           make_float4(out[4 * c], out[4 * c + 1], out[4 * c + 2], out[4 * c + 3]);
     }
-    if (n >= b || iy >= H || ix >= W) return;
+    if (!dx || n >= b || iy >= H || ix >= W) return;  // dx null: the NHWC copy is the only output
     const int cb0 = nt * BN + c0;
 #pragma unroll
     for (int j = 0; j < 16; ++j)

@@ -29,6 +29,7 @@ constexpr int kMaxOc = 64;
 
 struct Geo {
   int ic, h, w, oc, kh, kw, stride, pad, oh, ow, P, Kc, hp, wp;
+  int hw_nhwc;  // the highway arrives channels-last [b][P][oc] (the engine's TMA-fed dgrad output)
 };
 
 Geo make(const ConvGeom& g) {
@@ -39,6 +40,7 @@ Geo make(const ConvGeom& g) {
   // padded extent covering every window: (o - 1) * stride + k
   r.hp = std::max<int>(r.h + 2 * r.pad, (r.oh - 1) * r.stride + r.kh);
   r.wp = std::max<int>(r.w + 2 * r.pad, (r.ow - 1) * r.stride + r.kw);
+  r.hw_nhwc = 0;
   return r;
 }
 
@@ -128,9 +130,31 @@ __device__ __forceinline__ void sample_g(const Geo& g, const GsPlan& q, const fl
                                          double& bsq) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   stage_image(g, x, relu, n, xs, kt, pb);
-  // one warp per highway row, lanes along p, 8 loads in flight per lane; transposed stores
   const float* hn = hw + n * (int64_t)g.oc * g.P;
-  for (int o = warp; o < g.oc; o += kThreads / 32) {
+  if (g.hw_nhwc) {
+    // channels-last highway: already the [p][oc] order of the tile (oc % 4 == 0): 16-byte copies,
+    // 4 in flight per thread
+    const int oc4 = g.oc / 4, tot4 = g.P * oc4;
+    const float4* h4 = reinterpret_cast<const float4*>(hn);
+    for (int i0 = tid; i0 < tot4; i0 += 4 * kThreads) {
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = i0 + j * kThreads;
+        v[j] = i < tot4 ? __ldg(h4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = i0 + j * kThreads;
+        if (i < tot4) {
+          const int m = i / oc4, c4 = i - m * oc4;
+          *reinterpret_cast<float4*>(bs + m * q.ocp + 4 * c4) = v[j];
+        }
+      }
+    }
+  }
+  // one warp per highway row, lanes along p, 8 loads in flight per lane; transposed stores
+  for (int o = warp; o < g.oc && !g.hw_nhwc; o += kThreads / 32) {
     const float* row = hn + (int64_t)o * g.P;
     for (int m0 = 0; m0 < g.P; m0 += 8 * 32) {
       float v[8];
@@ -298,8 +322,9 @@ bool supported(const ConvGeom& cg) {
 static void set_smem(const void* fn, size_t bytes) { ensure_smem_attr(fn, (int)bytes); }
 
 void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom& cg, float* gw,
-        double* sq_part, float* gb, double* sq_b) {
-  const Geo g = make(cg);
+        double* sq_part, float* gb, double* sq_b, bool hw_nhwc) {
+  Geo g = make(cg);
+  g.hw_nhwc = hw_nhwc ? 1 : 0;
   const size_t smem = gs_smem(g);
   set_smem((const void*)tk_gs_kernel<0>, smem);
   ::dpg::launch_pdl(tk_gs_kernel<0>, (unsigned)cg.b, kThreads, smem, ctx->stream, g, x, relu, hw, nullptr, cg.b, 1, gw,
@@ -314,8 +339,9 @@ int csum_splits(const ConvGeom& cg) {
 }
 
 void csum(dpg_ctx* ctx, const float* x, int relu, const float* hw, const float* scale, const ConvGeom& cg,
-          float* part, int splits) {
-  const Geo g = make(cg);
+          float* part, int splits, bool hw_nhwc) {
+  Geo g = make(cg);
+  g.hw_nhwc = hw_nhwc ? 1 : 0;
   const size_t smem = gs_smem(g);
   const int64_t spl = (cg.b + splits - 1) / splits;
   set_smem((const void*)tk_gs_kernel<1>, smem);

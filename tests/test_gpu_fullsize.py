@@ -284,13 +284,12 @@ def test_cfg2_linear_t64_pipeline(ctx):
     np.testing.assert_array_equal(_n(pd), params - g * np.float32(0.1))
 
 
-@pytest.mark.parametrize("split", ["off"])
-def test_small_batch_steps_without_split_k(split):
-    """Both sides of the split-K threshold at small b: the step suite re-run in a fresh process
-    with split-K disabled (DPG_KSPLIT=off), so the no-split forward / dgrad epilogues also run
-    at the sizes the small-b tests use."""
-    env = dict(os.environ, DPG_KSPLIT=split)
+@pytest.mark.parametrize("variant,env", [("ksplit_off", {"DPG_KSPLIT": "off"}), ("tg0", {"DPG_TG": "0"})])
+def test_small_batch_steps_alternate_paths(variant, env):
+    """The step suite re-run in a fresh process on the other dispatch paths: split-K disabled (the
+    register-gather no-split forward / dgrad epilogues at small b) and DPG_TG=0 (every convolution
+    on the register-gather tcgen05 kernels instead of the TMA-fed core)."""
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_step.py"), "-k", "matches_oracle or virtual"],
-                       env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
+                       env=dict(os.environ, **env), cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
