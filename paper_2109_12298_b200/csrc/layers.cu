@@ -4,6 +4,7 @@
 // activations are stored pre-ReLU and the ReLU is applied on load (forward) or as a mask in
 // the producing dgrad epilogue (backward, layers.hpp:712-718).
 #include "conv_common.cuh"
+#include "step_common.cuh"
 #include "igemm.cuh"
 
 namespace dpg {
@@ -167,9 +168,6 @@ __global__ void __launch_bounds__(256) linear_fwd_narrow_kernel(const float* __r
 // Narrow outputs (r <= 64) with d % 4 == 0: one CTA per row, its 4 warps split the row's 16-byte
 // chunks; every lane keeps the r weight chunks of its column in flight (coalesced 128-bit loads),
 // per-row dot products are reduced warp (fixed shuffle tree) then across the 4 warps in order.
-__device__ __forceinline__ void softmax_ce_warp(const float* row, int logits_relu, const float* __restrict__ targets,
-                                                int64_t n, int64_t k, float* __restrict__ loss,
-                                                float* __restrict__ grad, DeviceErr* err);
 template <int RMAX, int NW>  // NW warps per row: 8 for long rows (e.g. 32768 features), else 4
 __global__ void __launch_bounds__(32 * NW) linear_fwd_row_kernel(const float* __restrict__ x,
                                                                        int x_relu,
@@ -503,49 +501,6 @@ void launch_embedding_fwd(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* 
   if (total == 0) return;
   ::dpg::launch_pdl(embedding_fwd_kernel, (unsigned)((total + 7) / 8), 256, 0, ctx->stream, sorted_v, sorted_s, table, total, t, dim, out);
   DPG_LAUNCH_CHECK(ctx);
-}
-
-// softmax cross-entropy (layers.hpp:894-919), in double like the reference; per-sample loss
-// and d(loss_n)/d(logits_n) = p - onehot (not divided by b). Invalid targets report
-// (stage TARGET, sample n). One warp per sample: lanes own classes, max and sum by a fixed
-// shuffle tree (the fp64 sum is associated differently from the reference's loop; the float
-// outputs agree to rounding).
-// one warp: loss and logit gradient of sample n from its k logits in `row`
-__device__ __forceinline__ void softmax_ce_warp(const float* row, int logits_relu, const float* __restrict__ targets,
-                                                int64_t n, int64_t k, float* __restrict__ loss,
-                                                float* __restrict__ grad, DeviceErr* err) {
-  const int lane = threadIdx.x & 31;
-  const double tv = (double)targets[n];
-  int64_t cls = 0;
-  if (!(tv >= 0.0) || tv != floor(tv) || tv >= (double)k) {
-    if (lane == 0)
-      report_error(err, err_key(ERR_STAGE_TARGET, 0, (uint64_t)n), (uint64_t)__float_as_uint(targets[n]));
-  } else {
-    cls = (int64_t)tv;
-  }
-  double mx = -INFINITY;
-  for (int64_t j = lane; j < k; j += 32) {
-    const double v = (double)relu_if(row[j], logits_relu);
-    mx = mx < v ? v : mx;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double t = __shfl_xor_sync(0xffffffffu, mx, o);
-    mx = mx < t ? t : mx;
-  }
-  double denom = 0.0;
-  for (int64_t j = lane; j < k; j += 32) denom += exp((double)relu_if(row[j], logits_relu) - mx);
-  denom = warp_sum(denom);
-  const double log_denom = log(denom);
-  if (loss && lane == 0)
-    loss[n] = (float)(-((double)relu_if(row[cls], logits_relu) - mx - log_denom));
-  for (int64_t j = lane; j < k; j += 32) {
-    const float lv = relu_if(row[j], logits_relu);
-    const double p = exp((double)lv - mx) / denom;
-    float gv = (float)(p - (j == cls ? 1.0 : 0.0));
-    if (logits_relu && !(row[j] > 0.f)) gv = 0.f;  // relu layer after the last linear
-    grad[n * k + j] = gv;
-  }
 }
 
 __global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict__ logits, int logits_relu,

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "dpg_internal.h"
+#include "persist.h"
 
 using dpg::ConvGeom;
 using dpg::guard;
@@ -150,6 +151,7 @@ struct dpg_model {
   float* losses[2] = {nullptr, nullptr};         // per-slot loss buffers: their D2H runs on the copy stream
   cudaEvent_t loss_read[2] = {nullptr, nullptr}; // that D2H done (the slot's next step may overwrite)
   int64_t async_calls = 0;
+  unsigned int* persist_bar = nullptr;  // grid barrier words of the persistent small-batch step
 };
 
 struct dpg_optimizer {
@@ -969,6 +971,7 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
       tg_sizes(lp, sz);
       for (size_t z : sz) total += z ? al(z) : 0;
     }
+    total += al(64);  // persist_bar
     DPG_CUDA(cudaMalloc(&m->arena, total));
     DPG_CUDA(cudaMemset(m->arena, 0, total));
     char* p = m->arena;
@@ -1002,6 +1005,7 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
         lp.xhat = reinterpret_cast<float*>(take(sizeof(float) * max_batch * lp.in_numel));
         lp.inv_std = reinterpret_cast<float*>(take(sizeof(float) * max_batch * lp.stat_blocks));
       }
+    m->persist_bar = reinterpret_cast<unsigned int*>(take(64));
     for (auto& lp : m->layers) {
       size_t sz[4];
       tg_sizes(lp, sz);
@@ -1347,6 +1351,113 @@ const float* dpg_summed_grad(const dpg_optimizer* o) { return (o && o->has_summe
 const float* dpg_grad(const dpg_optimizer* o) { return (o && o->has_grad) ? o->grad : nullptr; }
 int64_t dpg_accumulated_samples(const dpg_optimizer* o) { return o ? o->accumulated : 0; }
 
+namespace {
+
+// opt-in (DPG_PERSIST=1, read per call): measured slower than the multi-kernel step on the
+// BASELINE small config (MNIST CNN b = 64: 0.227 vs 0.074 ms per step), see DESIGN.md §4c
+bool persist_enabled() {
+  const char* e = std::getenv("DPG_PERSIST");
+  return e && e[0] == '1';
+}
+
+// Does a fresh logical batch of this model fit the persistent single-kernel step (persist.cu)?
+// Small models and batches only: the kernel's phases are plain grid-stride loops, which win over
+// the multi-kernel step only while launches, not work, bound it.
+bool persist_ok(const dpg_optimizer* o, int64_t b) {
+  const dpg_model* m = o->m;
+  if (!persist_enabled() || !o->cfg.materialise_grad_sample || o->peers.world > 1 || m->ctx->comm ||
+      m->ctx->profiling || m->out_width > 64 || b > 1024 || m->params.size() > (size_t)dpg::ps::kMaxParams)
+    return false;
+  int nl = 0;
+  double macs = 0.0;
+  for (const auto& lp : m->layers) {
+    if (lp.kind == DPG_LAYER_RELU || lp.kind == DPG_LAYER_FLATTEN) continue;
+    if (lp.kind == DPG_LAYER_LINEAR && lp.mid == 1) macs += (double)lp.out_numel * lp.d.in_features;
+    else if (lp.kind == DPG_LAYER_CONV2D) macs += (double)lp.out_numel * lp.g.K();
+    else return false;
+    if (++nl > dpg::ps::kMaxLayers) return false;
+  }
+  if (macs * b > 4.0e7) return false;  // MNIST CNN b = 64: 1.7e7
+  // a sample's input, activations and highways in shared memory
+  int64_t floats = 0;
+  for (const auto& lp : m->layers)
+    if (lp.param0 >= 0) floats += (floats == 0 ? lp.in_numel : 0) + 2 * lp.out_numel;
+  return 4 * floats <= 200 * 1024;
+}
+
+// the whole step (forward_backward + step of a fresh batch) as one cooperative launch
+void persist_step(dpg_optimizer* o, const float* x, const float* targets, int64_t b, float* loss, bool graph_mode) {
+  dpg_model* m = o->m;
+  float* P = m->p_params;
+  dpg::ps::Params p{};
+  int li = 0;
+  int64_t smem = 0;
+  for (const auto& lp : m->layers) {
+    if (lp.param0 < 0) continue;
+    dpg::ps::PLayer& L = p.L[li++];
+    L.conv = lp.kind == DPG_LAYER_CONV2D;
+    L.in_relu = lp.in_relu ? 1 : 0;
+    if (L.conv) {
+      L.C = (int)lp.g.ic; L.H = (int)lp.g.h; L.W = (int)lp.g.w; L.O = (int)lp.g.oc; L.KH = (int)lp.g.kh;
+      L.KW = (int)lp.g.kw; L.S = (int)lp.g.stride; L.PAD = (int)lp.g.pad; L.OH = (int)lp.g.oh; L.OW = (int)lp.g.ow;
+    } else {
+      L.C = (int)lp.d.in_features;
+      L.O = (int)lp.d.out_features;
+    }
+    L.in_numel = lp.in_numel;
+    L.out_numel = lp.out_numel;
+    L.in = lp.in_buf < 0 ? x : nullptr;
+    const ParamInfo& pw = m->params[lp.param0];
+    L.w = P + pw.offset;
+    L.bias = lp.nparams > 1 ? P + m->params[lp.param0 + 1].offset : nullptr;
+    L.gw = o->record + b * pw.offset;
+    L.gb = lp.nparams > 1 ? o->record + b * m->params[lp.param0 + 1].offset : nullptr;
+    L.numel_w = pw.numel;
+    L.pw = lp.param0;
+    // shared memory of one sample: the input, then per layer its output and highway
+    L.in_s = li == 1 ? 0 : p.L[li - 2].out_s;
+    if (li == 1) smem = lp.in_numel;
+    L.out_s = (int)smem;
+    L.hw_s = (int)(smem + lp.out_numel);
+    L.hw_prev_s = li == 1 ? -1 : p.L[li - 2].hw_s;
+    smem += 2 * lp.out_numel;
+  }
+  smem *= 4;
+  p.nl = li;
+  p.b = b;
+  p.out_relu = m->out_relu ? 1 : 0;
+  p.targets = targets;
+  p.loss = loss;
+  p.np = (int)m->params.size();
+  for (int q = 0; q < p.np; ++q) {
+    p.rec[q] = o->record + b * m->params[q].offset;
+    p.numel[q] = m->params[q].numel;
+    p.off[q] = m->params[q].offset;
+  }
+  p.Ltot = m->L;
+  p.c = o->cfg.max_grad_norm;
+  p.part = o->slab;
+  p.norms = o->norms;
+  p.scale = o->scale;
+  p.num_clipped = reinterpret_cast<long long*>(o->num_clipped);
+  p.summed = o->summed;
+  p.grad = o->grad;
+  p.params = P;
+  p.std_dev = o->cfg.noise_multiplier * o->cfg.max_grad_norm;
+  p.inv_e = 1.0f / (float)o->cfg.expected_batch_size;
+  p.lr = (float)o->cfg.learning_rate;
+  p.seed = o->cfg.noise_seed;
+  p.step = o->steps;
+  p.step_ptr = graph_mode ? o->step_dev : nullptr;
+  p.injected = o->injected;
+  p.err = m->ctx->dev_err;
+  p.bar = m->persist_bar;
+  dpg::ProfScope ps(m->ctx, "persist.step", 0.0, 0.0);
+  dpg::launch_persist_step(m->ctx, p, (int)smem);
+}
+
+}  // namespace
+
 dpg_status dpg_train_step(dpg_optimizer* o, const float* x, const float* targets, int64_t b,
                           float* loss, int use_graph) {
   if (!o) return DPG_ERR_PARAMETER;
@@ -1369,7 +1480,15 @@ dpg_status dpg_train_step(dpg_optimizer* o, const float* x, const float* targets
       o->pending_b = b;
       o->pending_x = x;
     };
+    const bool persist = persist_ok(o, b);
     if (!use_graph) {
+      if (persist) {
+        persist_step(o, x, targets, b, loss, false);
+        mark_done();
+        ++o->steps;
+        o->dev_step_known = false;
+        return;
+      }
       forward_backward_impl(o, x, targets, b, loss);
       o->has_grad_sample = true;
       o->pending_b = b;
@@ -1394,11 +1513,15 @@ dpg_status dpg_train_step(dpg_optimizer* o, const float* x, const float* targets
       ctx->capturing = true;
       DPG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
       try {
-        forward_backward_impl(o, x, targets, b, loss);
-        o->has_grad_sample = true;
-        o->pending_b = b;
-        o->pending_x = x;
-        step_impl(o, x, true);
+        if (persist) {
+          persist_step(o, x, targets, b, loss, true);
+        } else {
+          forward_backward_impl(o, x, targets, b, loss);
+          o->has_grad_sample = true;
+          o->pending_b = b;
+          o->pending_x = x;
+          step_impl(o, x, true);
+        }
       } catch (...) {
         cudaStreamEndCapture(ctx->stream, &graph);
         ctx->capturing = false;

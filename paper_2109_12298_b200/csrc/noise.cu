@@ -12,40 +12,9 @@
 // u2 = (y >> 11) * 2^-53 in [0, 1); element 2q gets r cos(theta), 2q+1 gets r sin(theta).
 #include <algorithm>
 
-#include "dpg_device.cuh"
+#include "step_common.cuh"
 
 namespace dpg {
-
-__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
-  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    if (r > 0) {
-      key.x += W0;
-      key.y += W1;
-    }
-    const uint32_t hi0 = __umulhi(M0, ctr.x), lo0 = M0 * ctr.x;
-    const uint32_t hi1 = __umulhi(M1, ctr.z), lo1 = M1 * ctr.z;
-    ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
-  }
-  return ctr;
-}
-
-__device__ __forceinline__ void normal_pair(uint64_t seed, uint64_t step, uint64_t q, double& z0,
-                                            double& z1) {
-  const uint4 r = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), (uint32_t)step,
-                                           (uint32_t)(step >> 32)),
-                                make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-  const uint64_t x = ((uint64_t)r.y << 32) | r.x;
-  const uint64_t y = ((uint64_t)r.w << 32) | r.z;
-  const double u1 = (double)((x >> 11) + 1) * 0x1.0p-53;
-  const double u2 = (double)(y >> 11) * 0x1.0p-53;
-  const double rad = sqrt(-2.0 * log(u1));
-  double s, c;
-  sincospi(2.0 * u2, &s, &c);
-  z0 = rad * c;
-  z1 = rad * s;
-}
 
 // Graph replays keep the Philox step on the device: every CTA reads it first, and the last CTA
 // to take a ticket (self-resetting counter) writes step + 1 for the next replay — no host-to-device

@@ -314,8 +314,10 @@ def test_nccl_allreduce_in_captured_step(ctx):
     w, params, x, y, m, o, cfg = _setup(ctx, "cifar_b512", b, noise_multiplier=1.0)
     xt, yt = _t(x), _t(y)
     loss = torch.zeros(b, device="cuda")
-    for _ in range(2):
-        o.train_step(xt, yt, loss, use_graph=True)
+    for _ in range(2):  # the multi-kernel step (train_step may take the persistent kernel at this size)
+        o.zero_grad()
+        o.forward_backward(xt, yt, loss)
+        o.step()
     ctx.sync()
     ref = m.store_params()
     c2 = dpg.Context(0)
