@@ -384,7 +384,8 @@ DPG_API dpg_status dpg_grad_sample_export(const dpg_optimizer* opt, int param, f
  * Diagnostics (no reference counterpart): unit test of the TMA-fed tcgen05 GEMM core that the
  * convolution contractions are built on. D[m][n] = sum_k A[m][k] B[n][k], row-major fp32 device
  * buffers, 3xTF32; bn in {32, 64, 128} output columns per tile, bk in {16, 32} K per stage
- * (K a multiple of 4). */
+ * (K a multiple of 4). bk = -32: b holds B transposed ([k][n] row-major) and lands as an
+ * MN-major B tile (bn in {32, 64, 96, 192}). */
 DPG_API dpg_status dpg_tg_gemm_selftest(dpg_ctx* ctx, const float* a, const float* b, float* d,
                                         int64_t m, int64_t n, int64_t k, int bn, int bk);
 

@@ -190,6 +190,11 @@ void conv_fwd_nhwc(dpg_ctx* ctx, const float* xh, const float* wf, const float* 
 void conv_dgrad_nhwc(dpg_ctx* ctx, const float* hh, const float* wd, const ConvGeom& g, const float* mask_h,
                      float* dx, float* dxh);
 void prep_weights(dpg_ctx* ctx, const TgPrepItems& items);
+// clipped sum of a conv weight: MN-major NHWC input tiles, s ⊙ highway rows in TMEM
+bool csum_nhwc_ok(const ConvGeom& g);
+int csum_nhwc_splits(const ConvGeom& g);
+void conv_csum_nhwc(dpg_ctx* ctx, const float* xh, const float* hw, const float* scale, const ConvGeom& g,
+                    float* part, int splits);
 void nchw_to_nhwc(dpg_ctx* ctx, const float* src, int relu, int64_t b, int64_t C, int64_t P, float* dst);
 }  // namespace tg
 

@@ -45,20 +45,26 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
 }
 
 // ---- D[M][N] = A[M][K] B[N][K]^T, all row-major (the core's unit test) ----
-template <int BN, int BK>
+template <int BN, int BK, bool BMN = false>
 struct Gemm2D {
-  static constexpr bool kScaleA = false, kBPreSplit = false, kCtaReduce = false;
+  static constexpr bool kScaleA = false, kBPreSplit = false, kCtaReduce = false, kBMajorMN = BMN;
   static constexpr int kStaging = 0, kEpiIn = 0;
   CUtensorMap ma, mb;
   float* d;
   int M, N, K;
   __device__ int nkb(int) const { return (K + BK - 1) / BK; }
-  __device__ uint32_t stage_bytes() const { return (uint32_t)((BM + BN) * BK * 4); }
+  __device__ uint32_t stage_bytes() const { return (uint32_t)((BM + BN) * BK * 4); }  // (MN: BN/32 boxes)
   __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t, uint32_t bar, int mt, int nt, int) const {
     tma2(sa, &ma, bar, kb * BK, mt * BM);
-    tma2(sb, &mb, bar, kb * BK, nt * BN);
+    if (BMN) {  // B^T [K][N]: one [BK][32] box per 32-wide N chunk
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tma2(sb + c * (BK * 128), &mb, bar, nt * BN + 32 * c, kb * BK);
+    } else {
+      tma2(sb, &mb, bar, kb * BK, nt * BN);
+    }
   }
   __device__ float scale(int, int, int, int) const { return 1.f; }
+  __device__ int a_rows() const { return BM; }
   __device__ bool has_epi_in() const { return false; }
   __device__ uint32_t epi_in_bytes() const { return 0; }
   __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
@@ -76,14 +82,20 @@ struct Gemm2D {
   __device__ void finish(int, int, int, double) const {}
 };
 
-template <int BN, int BK>
+template <int BN, int BK, bool BMN = false>
 void gemm2d(dpg_ctx* ctx, const float* a, const float* b, float* d, int M, int N, int K) {
   const uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N};
   const uint64_t sa[1] = {(uint64_t)K * 4}, sb[1] = {(uint64_t)K * 4};
   const uint32_t ba[2] = {BK, BM}, bb[2] = {BK, BN};
-  Gemm2D<BN, BK> p;
+  Gemm2D<BN, BK, BMN> p;
   p.ma = make_map(a, 2, da, sa, ba, nullptr, KLay<BK>::TMA_SWIZZLE);
-  p.mb = make_map(b, 2, db, sb, bb, nullptr, KLay<BK>::TMA_SWIZZLE);
+  if (BMN) {  // b holds B^T: [K][N] row-major
+    const uint64_t dt[2] = {(uint64_t)N, (uint64_t)K}, st[1] = {(uint64_t)N * 4};
+    const uint32_t bt[2] = {32, BK};
+    p.mb = make_map(b, 2, dt, st, bt, nullptr, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  } else {
+    p.mb = make_map(b, 2, db, sb, bb, nullptr, KLay<BK>::TMA_SWIZZLE);
+  }
   p.d = d; p.M = M; p.N = N; p.K = K;
   launch<BN, BK, stages_for<BN, BK>()>(ctx, p, dim3((M + BM - 1) / BM, (N + BN - 1) / BN, 1));
 }
@@ -104,7 +116,7 @@ void gemm2d(dpg_ctx* ctx, const float* a, const float* b, float* d, int M, int N
 // rows of a tile: spt whole samples (spt P <= 128)
 template <int BN, int BK>
 struct ConvFwdT {
-  static constexpr bool kScaleA = false, kBPreSplit = true, kCtaReduce = false;
+  static constexpr bool kScaleA = false, kBPreSplit = true, kCtaReduce = false, kBMajorMN = false;
   static constexpr int kStaging = 2 * 8192, kEpiIn = 0;  // NCHW [spt][16][P] | NHWC [128][16] (SW64)
   CUtensorMap ma, mb, my, myh;
   int b, O, P, kw, s, pad, spt, cpt, nk, has_yh, relu_out;
@@ -120,6 +132,7 @@ struct ConvFwdT {
     tma3(sblo, &mb, bar, kb * BK, nt * BN, 1);
   }
   __device__ float scale(int, int, int, int) const { return 1.f; }
+  __device__ int a_rows() const { return BM; }
   __device__ bool has_epi_in() const { return false; }
   __device__ uint32_t epi_in_bytes() const { return 0; }
   __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
@@ -160,7 +173,7 @@ struct ConvFwdT {
 // NHWC result leaves as a TMA store with the class's stride; the NCHW result is stored directly.
 template <int BN, int BK>
 struct ConvDgradT {
-  static constexpr bool kScaleA = false, kBPreSplit = true, kCtaReduce = false;
+  static constexpr bool kScaleA = false, kBPreSplit = true, kCtaReduce = false, kBMajorMN = false;
   static constexpr int kStaging = 8192, kEpiIn = 8192;  // NHWC [spt][QH][QW][16] (SW64) out / mask in
   CUtensorMap ma, mb, mdxh, mmask;
   int b, C, H, W, kh, kw, s, pad, QH, QW, spt, ocb, has_mask, has_dxh;
@@ -187,6 +200,7 @@ struct ConvDgradT {
     tma3(sblo, &mb, bar, ob * BK, brow, 1);
   }
   __device__ float scale(int, int, int, int) const { return 1.f; }
+  __device__ int a_rows() const { return BM; }
   __device__ bool has_epi_in() const { return has_mask != 0; }
   __device__ uint32_t epi_in_bytes() const { return (uint32_t)(spt * QH * QW * 16 * 4); }
   __device__ void epi_load(int mt, int nt, int z, int c0, uint32_t dst, uint32_t bar) const {
@@ -225,6 +239,63 @@ struct ConvDgradT {
     const int py = z / s, px = z - py * s;
     tma_st4(&mdxh, stg, nt * BN + c0, px, py, mt * spt);
   }
+  __device__ void finish(int, int, int, double) const {}
+};
+
+// ---- clipped sum of a conv weight (clip_and_sum pass 2 as (s ⊙ B)^T A, optimizer.hpp:99-114):
+//   S_z[o][c kk + t] = sum over the split's samples n and positions p of
+//                      s_n B[n, o, p] X~[n, p, (t, c)]
+// M = output channels: the K-major rows s_n B[n, o, p0 .. p0 + BK) of the NCHW highway are the A
+// operand, scaled and split into TMEM by the converters (rows past O written as zeros). N = (tap,
+// channel) in tap-major order: per 32-channel chunk of a tap, one NHWC box of the layer input
+// (ReLU applied by its producer) lands as an MN-major [BK positions][32 channels] tile (32-byte-atom
+// swizzle) — the implicit im2col with no transposition. K = (sample, position) of the split, one
+// sample per K block (P % BK == 0). Partials [split][O][C kk] in the reference's k order, combined
+// in split order by the split-K reduce. Chains are bounded like the register-gather kernel's
+// (<= 512 products per TMEM accumulator).
+template <int BN, int BK>
+struct ConvCsumT {
+  static constexpr bool kScaleA = true, kBPreSplit = false, kCtaReduce = false, kBMajorMN = true;
+  static constexpr int kStaging = 0, kEpiIn = 0;
+  CUtensorMap ma, mb;
+  int b, O, C, khw, kw, s, pad, OW, G, kpb, spl;
+  uint32_t bytes;
+  const float* svec;
+  float* part;  // [splits][O][C khw]
+  __device__ int a_rows() const { return O; }
+  __device__ int nkb(int z) const {
+    const int n0 = z * spl, n1 = min(b, n0 + spl);
+    return n1 > n0 ? (n1 - n0) * kpb : 0;
+  }
+  __device__ uint32_t stage_bytes() const { return bytes; }
+  __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t, uint32_t bar, int, int nt, int z) const {
+    const int n = z * spl + kb / kpb, j = kb % kpb;
+    tma3(sa, &ma, bar, j * BK, 0, n);  // B[n, 0 .. O, p0 .. p0 + BK)
+    const int rows = BK / OW, cpc = C / 32;
+#pragma unroll 1
+    for (int i = 0; i < BN / 32; ++i) {
+      const int tl = i / cpc, cc = i - tl * cpc, t = nt * G + tl;
+      const int ki = t / kw, kj = t - ki * kw;
+      const int y0 = t < khw ? j * rows * s - pad + ki : -(1 << 20);  // past the taps: zeros
+      tma4(sb + i * (BK * 128), &mb, bar, cc * 32, kj - pad, y0, n);
+    }
+  }
+  __device__ float scale(int kb, int, int, int z) const { return __ldg(svec + z * spl + kb / kpb); }
+  __device__ bool has_epi_in() const { return false; }
+  __device__ uint32_t epi_in_bytes() const { return 0; }
+  __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
+  __device__ void epilogue(int, int nt, int z, int row, int c0, const float (&v)[16], double&, uint8_t*,
+                           const uint8_t*) const {
+    if (row >= O) return;
+    const int K = C * khw;
+    float* dst = part + ((int64_t)z * O + row) * K;
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int col = c0 + jj, tl = col / C, c = col - tl * C, t = nt * G + tl;
+      if (t < khw) dst[c * khw + t] = v[jj];
+    }
+  }
+  __device__ void epi_store(int, int, int, int, uint32_t) const {}
   __device__ void finish(int, int, int, double) const {}
 };
 
@@ -392,6 +463,56 @@ void conv_dgrad_nhwc(dpg_ctx* ctx, const float* hh, const float* wd, const ConvG
   });
 }
 
+// ---- clipped sum of a conv weight on the core ----
+bool csum_nhwc_ok(const ConvGeom& g) {
+  const int64_t P = g.P();
+  const int bk = P % 32 == 0 ? 32 : 16;
+  return (g.ic == 32 || g.ic == 64) && g.oc <= 128 && P % bk == 0 && bk % g.ow == 0 &&
+         g.ow * g.stride <= 256 && (bk / g.ow) * g.stride <= 256 && g.kh * g.kw <= 64;
+}
+int csum_nhwc_splits(const ConvGeom& g) {
+  // chains of <= 512 products per TMEM accumulator (tc_conv.cu kCsumChain), and >= one tile per SM
+  const int64_t P = g.P();
+  const int G = 3, ntn = (int)((g.kh * g.kw + G - 1) / G);
+  const int64_t spl_chain = std::max<int64_t>(1, 512 / P);
+  const int64_t want = (kNumSMs + ntn - 1) / ntn;
+  const int64_t spl = std::min<int64_t>(spl_chain, std::max<int64_t>(1, (g.b + want - 1) / want));
+  return (int)((g.b + spl - 1) / spl);
+}
+
+void conv_csum_nhwc(dpg_ctx* ctx, const float* xh, const float* hw, const float* scale, const ConvGeom& g,
+                    float* part, int splits) {
+  const int b = (int)g.b, P = (int)g.P(), C = (int)g.ic, khw = (int)(g.kh * g.kw);
+  const int bk = P % 32 == 0 ? 32 : 16;
+  constexpr int G = 3;  // taps per N tile
+  auto go = [&](auto BNc, auto BKc) {
+    constexpr int BN = decltype(BNc)::value, BK = decltype(BKc)::value;
+    using Pr = ConvCsumT<BN, BK>;
+    Pr p;
+    {  // A: highway NCHW [b][O][P], K-major rows of BK positions
+      const uint64_t dims[3] = {(uint64_t)P, (uint64_t)g.oc, (uint64_t)b};
+      const uint64_t str[2] = {(uint64_t)P * 4, (uint64_t)(g.oc * P * 4)};
+      const uint32_t box[3] = {(uint32_t)BK, (uint32_t)g.oc, 1};
+      p.ma = make_map(hw, 3, dims, str, box, nullptr, KLay<BK>::TMA_SWIZZLE);
+    }
+    // B: the layer input NHWC, 32-channel boxes of BK / OW output rows walked with the stride
+    p.mb = nhwc_map(xh, b, (int)g.h, (int)g.w, C, 32, (int)g.ow, BK / (int)g.ow, 1, (int)g.stride,
+                    CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    p.b = b; p.O = (int)g.oc; p.C = C; p.khw = khw; p.kw = (int)g.kw; p.s = (int)g.stride; p.pad = (int)g.pad;
+    p.OW = (int)g.ow; p.G = G; p.kpb = P / BK; p.spl = (b + splits - 1) / splits;
+    p.bytes = (uint32_t)(((int)g.oc + BN) * BK * 4);
+    p.svec = scale; p.part = part;
+    launch<BN, BK, stages_for<BN, BK>()>(ctx, p, dim3(1, (unsigned)((khw + G - 1) / G), (unsigned)splits));
+  };
+  if (C == 32) {
+    if (bk == 32) go(std::integral_constant<int, 96>{}, std::integral_constant<int, 32>{});
+    else go(std::integral_constant<int, 96>{}, std::integral_constant<int, 16>{});
+  } else {
+    if (bk == 32) go(std::integral_constant<int, 192>{}, std::integral_constant<int, 32>{});
+    else go(std::integral_constant<int, 192>{}, std::integral_constant<int, 16>{});
+  }
+}
+
 void prep_weights(dpg_ctx* ctx, const TgPrepItems& items) {
   if (items.count == 0) return;
   ::dpg::launch_pdl(prep_weights_kernel, dim3(2 * kNumSMs / items.count + 1, (unsigned)items.count), 256, 0,
@@ -427,7 +548,16 @@ dpg_status dpg_tg_gemm_selftest(dpg_ctx* ctx, const float* a, const float* b, fl
     if (m <= 0 || n <= 0 || k <= 0 || (k * 4) % 16 != 0 || m >= (1 << 30) || n >= (1 << 30) || k >= (1 << 30))
       raise(DPG_ERR_DIMENSION, "tg_gemm_selftest: extents must be positive, K a multiple of 4");
     const int M = (int)m, N = (int)n, K = (int)k;
-    if (bk == 32) {
+    if (bk == -32) {  // B given transposed ([K][N] row-major): the MN-major B path
+      if (n % 4 != 0) raise(DPG_ERR_DIMENSION, "tg_gemm_selftest: MN-major B needs N a multiple of 4");
+      switch (bn) {
+        case 32: dpg::tg::gemm2d<32, 32, true>(ctx, a, b, d, M, N, K); break;
+        case 64: dpg::tg::gemm2d<64, 32, true>(ctx, a, b, d, M, N, K); break;
+        case 96: dpg::tg::gemm2d<96, 32, true>(ctx, a, b, d, M, N, K); break;
+        case 192: dpg::tg::gemm2d<192, 32, true>(ctx, a, b, d, M, N, K); break;
+        default: raise(DPG_ERR_PARAMETER, "tg_gemm_selftest: bn must be 32, 64, 96 or 192 with bk -32");
+      }
+    } else if (bk == 32) {
       switch (bn) {
         case 32: dpg::tg::gemm2d<32, 32>(ctx, a, b, d, M, N, K); break;
         case 64: dpg::tg::gemm2d<64, 32>(ctx, a, b, d, M, N, K); break;

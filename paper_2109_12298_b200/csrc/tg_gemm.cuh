@@ -156,9 +156,18 @@ struct KLay {
   }
 };
 
-// kind::tf32: D f32, A/B tf32, both K-major, M = 128, N = n
-__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// kind::tf32: D f32, A/B tf32, A K-major, B K-major (or MN-major: bit 16), M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_tf32(int n, bool b_mn = false) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+// MN-major tile of tf32 (32-bit MN-major operands need the 32-byte-atom swizzle:
+// SWIZZLE_128B_BASE32B, UMMA layout 1; TMA's CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 128-byte rows of
+// 32 N values, one row per K, 4-row atoms; lbo = byte stride between 32-wide N chunks, sbo = byte
+// stride between 4-row K groups (CuTe's Layout_MN_SW128_32B_Atom)
+__device__ __forceinline__ uint64_t desc_mn128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)1 << 61);
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
@@ -263,6 +272,9 @@ struct Tiles {
 // Prob interface (all __device__ const members; the Prob is a __grid_constant__ kernel parameter,
 // so tensor maps it holds are addressable by TMA):
 //   static constexpr bool kScaleA;     converters multiply the A tile by scale(...)
+//   int a_rows() const;                A rows that hold data (the converters write zeros past them)
+//   static constexpr bool kBMajorMN;   B lands MN-major: per 32-wide N chunk one SWIZZLE_128B box of
+//                                      [BK K rows][32 N] (chunks BK x 128 B apart); else K-major
 //   static constexpr bool kBPreSplit;  issue() loads B_hi and B_lo (both TF32-rounded in global);
 //                                      otherwise converters split the landed B in place
 //   static constexpr bool kCtaReduce;  per-tile reduction of the epilogue's acc -> finish()
@@ -348,7 +360,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(BN);
+      constexpr uint32_t idesc = idesc_tf32(BN, Prob::kBMajorMN);
       int it = 0, j = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
         int mt, nt, z;
@@ -366,11 +378,19 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
           const uint32_t ahi = tmem + tA(s), alo = ahi + BK;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t off = kk * 32;  // 8 tf32 = 32 B along the swizzled row
             const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32_ts(acc, alo + kk * 8, Lay::desc(sB(s) + off), idesc, acc0);
-            mma_tf32_ts(acc, ahi + kk * 8, Lay::desc(sBlo(s) + off), idesc, 1u);
-            mma_tf32_ts(acc, ahi + kk * 8, Lay::desc(sB(s) + off), idesc, 1u);
+            uint64_t bhi, blo;
+            if constexpr (Prob::kBMajorMN) {  // B as [BK rows][BN] in 32-wide N chunks of BK rows
+              bhi = desc_mn128(sB(s) + kk * 1024, BK * 128, 512);
+              blo = desc_mn128(sBlo(s) + kk * 1024, BK * 128, 512);
+            } else {
+              const uint32_t off = kk * 32;  // 8 tf32 = 32 B along the swizzled row
+              bhi = Lay::desc(sB(s) + off);
+              blo = Lay::desc(sBlo(s) + off);
+            }
+            mma_tf32_ts(acc, alo + kk * 8, bhi, idesc, acc0);
+            mma_tf32_ts(acc, ahi + kk * 8, blo, idesc, 1u);
+            mma_tf32_ts(acc, ahi + kk * 8, bhi, idesc, 1u);
           }
           mma_commit(empty(s));
         }
@@ -399,9 +419,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
 #pragma unroll
         for (int h = 0; h < BK / 16; ++h) {  // 16 columns (4 chunks) at a time
           uint32_t hi[16], lo[16];
+          const bool zero_row = r >= p.a_rows();  // rows past the operand: zeros (no stale data)
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             float4 v = *reinterpret_cast<const float4*>(arow + (((4 * h + c) ^ sw) << 4));
+            if (zero_row) v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (Prob::kScaleA) {
               v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
             }

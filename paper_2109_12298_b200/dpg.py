@@ -645,7 +645,7 @@ class DpOptimizer:
 def tg_gemm_selftest(ctx: Context, a: torch.Tensor, b: torch.Tensor, bn: int = 64, bk: int = 32) -> torch.Tensor:
     """D = A B^T through the TMA-fed tcgen05 GEMM core (dpg_tg_gemm_selftest; diagnostics)."""
     m, k = a.shape
-    n = b.shape[0]
+    n = b.shape[1] if bk < 0 else b.shape[0]  # bk < 0: b is B transposed, [k][n]
     d = torch.empty(m, n, device=a.device, dtype=torch.float32)
     _check(lib().dpg_tg_gemm_selftest(ctx.h, _p(a), _p(b), _p(d), m, n, k, bn, bk), ctx.h)
     return d

@@ -14,14 +14,17 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("m,n,k,bn,bk", [
     (128, 64, 32, 64, 32), (300, 100, 200, 64, 32), (300, 100, 200, 32, 16), (257, 130, 576, 128, 32),
-    (1000, 32, 64, 32, 32), (64, 64, 16, 64, 16)])
+    (1000, 32, 64, 32, 32), (64, 64, 16, 64, 16),
+    # MN-major B (the clipped sums' NHWC input tiles): chunks of 32 along N, ragged N and K
+    (256, 96, 64, 96, -32), (300, 192, 288, 192, -32), (128, 64, 32, 64, -32), (200, 100, 100, 96, -32)])
 def test_tg_gemm_matches_fp64(ctx, m, n, k, bn, bk):
     import torch
     from paper_2109_12298_b200 import dpg
     rng = np.random.default_rng(m + n + k)
     a = rng.standard_normal((m, k)).astype(np.float32)
     b = rng.standard_normal((n, k)).astype(np.float32)
-    d = dpg.tg_gemm_selftest(ctx, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), bn, bk)
+    bt = np.ascontiguousarray(b.T) if bk < 0 else b  # bk < 0: B lands MN-major from [k][n]
+    d = dpg.tg_gemm_selftest(ctx, torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda(), bn, bk)
     ctx.sync()
     ref = a.astype(np.float64) @ b.astype(np.float64).T
     got = d.cpu().numpy().astype(np.float64)
