@@ -115,6 +115,17 @@ DPG_API int64_t dpg_ctx_kernel_launches(const dpg_ctx* ctx);
 DPG_API dpg_status dpg_ctx_set_profiling(dpg_ctx* ctx, int on);
 DPG_API const char* dpg_ctx_profile_read(dpg_ctx* ctx);
 
+/* Graph timeline: while on, the stage scopes of a step captured by dpg_train_step become CUDA
+ * event-record nodes on the stream (main or branch) that runs each stage, so a replay shows the
+ * step's real overlap. Turning it on (or off) clears the records; steps captured before keep no
+ * records. dpg_ctx_timeline_read synchronises the device and returns, for the last replay, one
+ * line per stage scope in capture order:
+ *   "<stage> <start_ms_from_graph_start> <duration_ms> <kernels>\n"
+ * The record nodes split programmatic-dependent launch edges at stage boundaries, so the step
+ * runs slightly slower than without them (a diagnostic, not a bench number). */
+DPG_API dpg_status dpg_ctx_set_timeline(dpg_ctx* ctx, int on);
+DPG_API const char* dpg_ctx_timeline_read(dpg_ctx* ctx);
+
 /* NCCL: one communicator per context for the sample-sharded step.
  * dpg_nccl_unique_id fills 128 bytes on rank 0; every rank then calls dpg_ctx_init_comm. */
 DPG_API dpg_status dpg_nccl_unique_id(unsigned char id[128]);
@@ -388,6 +399,10 @@ DPG_API dpg_status dpg_grad_sample_export(const dpg_optimizer* opt, int param, f
  * MN-major B tile (bn in {32, 64, 96, 192}). */
 DPG_API dpg_status dpg_tg_gemm_selftest(dpg_ctx* ctx, const float* a, const float* b, float* d,
                                         int64_t m, int64_t n, int64_t k, int bn, int bk);
+/* The same with the K blocks split over a thread-block cluster of ck CTAs (1, 2, 4) whose
+ * partials are summed through distributed shared memory (bk 32, K-major B, bn 32 or 64). */
+DPG_API dpg_status dpg_tg_gemm_selftest_split(dpg_ctx* ctx, const float* a, const float* b, float* d,
+                                              int64_t m, int64_t n, int64_t k, int bn, int ck);
 
 #ifdef __cplusplus
 }

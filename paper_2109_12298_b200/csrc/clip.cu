@@ -85,9 +85,14 @@ void launch_clip_factors(dpg_ctx* ctx, const double* slab, const int32_t* row_pa
 constexpr int kColWarps = 16;
 constexpr int kColBatch = 16;
 
-template <class V, class C>
+struct IdOut {
+  __device__ __forceinline__ int64_t operator()(int64_t j) const { return j; }
+};
+
+template <class V, class C, class OI = IdOut>
 __device__ __forceinline__ void colsum_body(const V& v, const C& c, int64_t nz, int64_t ncol,
-                                            int64_t j0, float* __restrict__ out, int accumulate) {
+                                            int64_t j0, float* __restrict__ out, int accumulate,
+                                            OI oi = IdOut{}) {
   __shared__ float part[kColWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t j = j0 + lane;
@@ -113,7 +118,8 @@ __device__ __forceinline__ void colsum_body(const V& v, const C& c, int64_t nz, 
     float t = part[0][lane];
 #pragma unroll
     for (int w = 1; w < kColWarps; ++w) t += part[w][lane];
-    out[j] = accumulate ? out[j] + t : t;
+    const int64_t jo = oi(j);
+    out[jo] = accumulate ? out[jo] + t : t;
   }
 }
 
@@ -141,6 +147,24 @@ static void launch_splitk_reduce(dpg_ctx* ctx, const float* part, int splits, in
   ::dpg::launch_pdl(splitk_reduce_kernel, (unsigned)((n + 31) / 32), 32 * kColWarps, 0, ctx->stream, 
       PartV{part, n}, splits, n, out, accumulate);
   DPG_LAUNCH_CHECK(ctx);
+}
+
+// partials of the TMA-fed conv clipped sum are [split][o][(tap, channel)]: the column of the
+// reference's k order (channel-major, layers.hpp:290-324) is c * khw + t
+struct TapMajorOut {
+  int C, khw;
+  int64_t K;
+  __device__ __forceinline__ int64_t operator()(int64_t j) const {
+    const int64_t o = j / K, r = j - o * K, t = r / C, c = r - t * C;
+    return o * K + c * khw + t;
+  }
+};
+
+__global__ void __launch_bounds__(32 * kColWarps) splitk_reduce_tap_kernel(PartV v, int splits, int64_t n,
+                                                                           float* out, int accumulate,
+                                                                           TapMajorOut oi) {
+  pdl_wait();
+  colsum_body(v, OneC{}, splits, n, (int64_t)blockIdx.x * 32, out, accumulate, oi);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -214,16 +238,27 @@ void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, c
 // Conv weight: S[oc, k] = sum_{n, p} (scale_n * B[n, oc, p]) * X~[n, k, p] — the conv weight
 // gradient of the clip-scaled highway; split-K over samples.
 // ------------------------------------------------------------------------------------------
-size_t clipped_sum_ws_conv2d(const ConvGeom& g) {
+size_t clipped_sum_ws_conv2d(const ConvGeom& g, bool nhwc_in) {
+  if (nhwc_in) return sizeof(float) * (size_t)tg::csum_nhwc_splits(g) * (size_t)(g.oc * g.K());
   if (tk::supported(g)) return sizeof(float) * (size_t)tk::csum_splits(g) * (size_t)(g.oc * g.K());
   return sizeof(float) * (size_t)tc::csum_conv_splits(g) * (size_t)(g.oc * g.K());
 }
 
 void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
                                const float* scale, const ConvGeom& g, float* sw, float* sb,
-                               int accumulate, void* ws, bool hw_nhwc) {
+                               int accumulate, void* ws, bool hw_nhwc, const float* xh) {
   (void)sb;  // the bias clipped sum is a weighted sum of the bias records (launch_wsum_multi)
   const int64_t nw = g.oc * g.K();
+  if (xh) {  // the layer input's NHWC copy exists: the TMA-fed core (tg_conv.cu ConvCsumT)
+    if (hw_nhwc || !tg::csum_nhwc_ok(g)) raise(DPG_ERR_INTERNAL, "NHWC clipped sum: unsupported geometry");
+    const int splits = tg::csum_nhwc_splits(g);
+    tg::conv_csum_nhwc(ctx, xh, hw, scale, g, static_cast<float*>(ws), splits);
+    ::dpg::launch_pdl(splitk_reduce_tap_kernel, (unsigned)((nw + 31) / 32), 32 * kColWarps, 0, ctx->stream,
+                      PartV{static_cast<float*>(ws), nw}, splits, nw, sw, accumulate,
+                      TapMajorOut{(int)g.ic, (int)(g.kh * g.kw), g.K()});
+    DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
   if (hw_nhwc && !tk::supported(g)) raise(DPG_ERR_INTERNAL, "channels-last highway needs the thin-K path");
   if (tk::supported(g)) {
     const int splits = tk::csum_splits(g);

@@ -84,6 +84,18 @@ static cudaEvent_t pooled_event(dpg_ctx* ctx) {
 
 ProfScope::ProfScope(dpg_ctx* c, std::string name, double bytes, double flops)
     : ctx(c), on(c->profiling && !c->capturing) {
+  if (c->timeline && c->capturing) {  // an event-record node pair inside the captured step
+    tl = true;
+    rec.name = std::move(name);
+    rec.bytes = bytes;
+    rec.flops = flops;
+    rec.a = pooled_event(ctx);
+    rec.b = pooled_event(ctx);
+    rec.kernels = ctx->launches;
+    rec.seq = (int64_t)ctx->tl_recs.size();
+    DPG_CUDA(cudaEventRecordWithFlags(rec.a, ctx->stream, cudaEventRecordExternal));
+    return;
+  }
   if (!on) return;
   rec.name = std::move(name);
   rec.bytes = bytes;
@@ -96,6 +108,12 @@ ProfScope::ProfScope(dpg_ctx* c, std::string name, double bytes, double flops)
 }
 
 ProfScope::~ProfScope() {
+  if (tl) {
+    rec.kernels = ctx->launches - rec.kernels;
+    cudaEventRecordWithFlags(rec.b, ctx->stream, cudaEventRecordExternal);
+    ctx->tl_recs.push_back(rec);
+    return;
+  }
   if (!on) return;
   rec.kernels = ctx->launches - rec.kernels;
   cudaEventRecord(rec.b, ctx->stream);
@@ -202,6 +220,39 @@ dpg_status dpg_ctx_set_profiling(dpg_ctx* ctx, int on) {
       ctx->prof_seq = 0;
     }
   });
+}
+
+dpg_status dpg_ctx_set_timeline(dpg_ctx* ctx, int on) {
+  if (!ctx) return DPG_ERR_PARAMETER;
+  return guard(ctx, [&] {
+    if (ctx->capturing) dpg::raise(DPG_ERR_LIFECYCLE, "set_timeline during a graph capture");
+    ctx->timeline = on != 0;
+    for (auto& r : ctx->tl_recs) {
+      ctx->event_pool.push_back(r.a);
+      ctx->event_pool.push_back(r.b);
+    }
+    ctx->tl_recs.clear();
+    if (on && !ctx->tl_start) DPG_CUDA(cudaEventCreate(&ctx->tl_start));
+  });
+}
+
+const char* dpg_ctx_timeline_read(dpg_ctx* ctx) {
+  if (!ctx) return "";
+  const dpg_status st = guard(ctx, [&] {
+    DPG_CUDA(cudaDeviceSynchronize());
+    std::string out;
+    char line[512];
+    for (auto& r : ctx->tl_recs) {
+      float t0 = 0.f, dt = 0.f;
+      DPG_CUDA(cudaEventElapsedTime(&t0, ctx->tl_start, r.a));
+      DPG_CUDA(cudaEventElapsedTime(&dt, r.a, r.b));
+      std::snprintf(line, sizeof line, "%s %.6f %.6f %lld\n", r.name.c_str(), t0, dt, (long long)r.kernels);
+      out += line;
+    }
+    ctx->prof_text = out;
+  });
+  if (st != DPG_OK) return "";
+  return ctx->prof_text.c_str();
 }
 
 const char* dpg_ctx_profile_read(dpg_ctx* ctx) {

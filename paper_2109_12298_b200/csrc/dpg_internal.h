@@ -99,6 +99,12 @@ struct dpg_ctx {
   };
   int64_t prof_seq = 0;
   bool profiling = false;
+  // graph timeline (dpg_ctx_set_timeline): the stage scopes of a captured step become event-record
+  // nodes on whichever stream (main or branch) runs them; after a replay each stage's start and
+  // duration are read relative to the graph's first node, so the step's real overlap is visible
+  bool timeline = false;
+  cudaEvent_t tl_start = nullptr;
+  std::vector<ProfRec> tl_recs;
   std::vector<ProfRec> prof_pending;
   std::map<std::string, ProfAgg> prof_agg;
   std::vector<cudaEvent_t> event_pool;
@@ -126,6 +132,7 @@ inline void count_launch(dpg_ctx* ctx) { ++ctx->launches; }
 struct ProfScope {
   dpg_ctx* ctx;
   bool on;
+  bool tl = false;  // timeline record (inside a capture)
   dpg_ctx::ProfRec rec;
   ProfScope(dpg_ctx* c, std::string name, double bytes, double flops);
   ~ProfScope();
@@ -264,13 +271,13 @@ void launch_sq_reduce(dpg_ctx* ctx, const double* part, int rows, int64_t b, dou
 void launch_clip_factors(dpg_ctx* ctx, const double* slab, const int32_t* row_param, int rows,
                          int64_t b, double c, double* norms, float* scale, int64_t* num_clipped);
 size_t clipped_sum_ws_linear(int64_t b, int64_t mid, int64_t d, int64_t r);
-size_t clipped_sum_ws_conv2d(const ConvGeom& g);
+size_t clipped_sum_ws_conv2d(const ConvGeom& g, bool nhwc_in = false);
 void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw,
                                const float* scale, int64_t b, int64_t mid, int64_t d, int64_t r,
                                float* sw, float* sb, int accumulate, void* ws);
 void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
                                const float* scale, const ConvGeom& g, float* sw, float* sb,
-                               int accumulate, void* ws, bool hw_nhwc = false);
+                               int accumulate, void* ws, bool hw_nhwc = false, const float* xh = nullptr);
 size_t clipped_sum_ws_embedding(int64_t b, int64_t vocab);
 void launch_clipped_sum_embedding(dpg_ctx* ctx, const int32_t* sorted_v, const int32_t* sorted_s,
                                   const float* hw, const float* scale, int64_t b, int64_t t,

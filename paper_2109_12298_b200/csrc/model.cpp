@@ -61,6 +61,7 @@ struct LayerPlan {
   int tg_fwd = 0;
   bool tg_dgrad = false;
   bool xh_by_prev = false, hh_by_next = false;
+  bool tg_csum = false;  // clipped sum on the TMA core from xh (tg_conv.cu ConvCsumT)
   // the highway lives only channels-last (hh): written by the next layer's TMA-fed dgrad, read by
   // this layer's thin-K rule / clipped sum (a first layer: no dgrad of its own reads it)
   bool hw_nhwc = false;
@@ -70,6 +71,13 @@ struct LayerPlan {
   float* wf = nullptr;    // [2][O][kh][kw][C] (TF32 hi, lo)
   float* wd = nullptr;    // [2][kh][kw][C][O]
 };
+
+// DPG_TG_CSUM=1: conv clipped sums on the TMA-fed core (read when a model is planned; opt-in:
+// measured slower on the CIFAR step, DESIGN.md §6 negative results)
+bool tg_csum_enabled() {
+  const char* e = std::getenv("DPG_TG_CSUM");
+  return e && e[0] == '1';
+}
 
 bool tg_enabled() {
   static const bool on = [] {
@@ -430,7 +438,9 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
       });
     };
     struct { int64_t mid, r, conv; } pending_bias{0, 0, -1};  // a separate bias rule, forked below
-    on_branch(m, rb, [&] {
+    // the first parametric layer has no input gradient: once the last dgrad is issued the caller's
+    // stream is idle, so its rule runs there (a branch may still be busy with the rule before it)
+    on_branch(m, lp.prev_param_layer < 0 ? -1 : rb, [&] {
     switch (lp.kind) {
       case DPG_LAYER_LINEAR: {
         {
@@ -560,9 +570,11 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
     }
   }
   // stream plan for the per-layer (s ⊙ B)^T A launches: greedy, largest first, onto the least
-  // loaded of aux 0 / aux 1 / the caller's stream (estimated cost ~ launch + flops); the record
-  // weighted sums (one launch) take the caller's stream
-  double load[3] = {0.0, 0.0, 1.0};
+  // loaded of aux 0 / aux 1 / the caller's stream, then the record weighted sums (one launch)
+  // onto the least loaded. Estimated cost: a convolution's clipped sum is latency-bound at the
+  // step's sizes (conv2..conv4 of CIFAR take 59-72 us in the graph timeline whatever their
+  // flops), so a fixed part dominates; linear and embedding sums are short.
+  double load[3] = {0.0, 0.0, 0.0};
   std::vector<int> stream_of(m->layers.size(), 2);
   {
     std::vector<std::pair<double, int>> cost;
@@ -573,7 +585,7 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       if (lp.kind == DPG_LAYER_CONV2D) fl = 2.0 * b * lp.g.oc * lp.g.K() * lp.g.P();
       if (lp.kind == DPG_LAYER_LINEAR) fl = 2.0 * b * lp.mid * lp.d.in_features * lp.d.out_features;
       if (lp.kind == DPG_LAYER_EMBEDDING) fl = 8.0 * b * lp.out_numel;
-      cost.push_back({1.0 + 25.0 * fl / 1e9, (int)l});
+      cost.push_back({(lp.kind == DPG_LAYER_CONV2D ? 20.0 : 2.0) + 5.0 * fl / 1e9, (int)l});
     }
     std::sort(cost.begin(), cost.end(), [](const auto& a, const auto& c) { return a.first > c.first; });
     for (auto& [c, l] : cost) {
@@ -582,6 +594,7 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       stream_of[l] = s;
     }
   }
+  const int record_stream = (int)(std::min_element(load, load + 3) - load);
   int rr_branch = 0;
   for (size_t l = 0; l < m->layers.size(); ++l) {
     LayerPlan& lp = m->layers[l];
@@ -624,7 +637,7 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
           g.b = b;
           dpg::ProfScope ps(ctx, "csum.conv2d" + ls, cio, 2.0 * b * g.oc * g.K() * g.P());
           dpg::launch_clipped_sum_conv2d(ctx, in, lp.in_relu, lp.hw_nhwc ? lp.hh : hw, o->scale, g, dst, nullptr,
-                                         accumulate, ws, lp.hw_nhwc);
+                                         accumulate, ws, lp.hw_nhwc, lp.tg_csum ? lp.xh : nullptr);
           break;
         }
         case DPG_LAYER_EMBEDDING: {
@@ -641,19 +654,21 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
   // record-based clipped sums (biases, normalisation affines, small weights): weighted column sums
   // of the per-sample records, all in one launch
   if (!o->cfg.clipped_sum_from_record) {
-    dpg::WsumItems items{};
-    double bytes = 0;
-    for (auto& pi : m->params) {
-      if (!from_record[&pi - &m->params[0]]) continue;
-      if (items.count == 16) {
-        dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
-        items.count = 0;
+    on_branch(m, record_stream < dpg_model::kAux ? record_stream : -1, [&] {
+      dpg::WsumItems items{};
+      double bytes = 0;
+      for (auto& pi : m->params) {
+        if (!from_record[&pi - &m->params[0]]) continue;
+        if (items.count == 16) {
+          dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+          items.count = 0;
+        }
+        items.item[items.count++] = {gs_ptr(o, (int)(&pi - &m->params[0]), b), o->summed + pi.offset, pi.numel};
+        bytes += 4.0 * (b * pi.numel + 2 * pi.numel);
       }
-      items.item[items.count++] = {gs_ptr(o, (int)(&pi - &m->params[0]), b), o->summed + pi.offset, pi.numel};
-      bytes += 4.0 * (b * pi.numel + 2 * pi.numel);
-    }
-    dpg::ProfScope ps(ctx, "csum.record[all]", bytes, 0.0);
-    dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+      dpg::ProfScope ps(ctx, "csum.record[all]", bytes, 0.0);
+      dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+    });
   }
   join_branches(m);
   o->has_summed = true;
@@ -897,6 +912,8 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
           m->layers[lp.next_param_layer].tg_dgrad && dpg::tk::supported(lp.g))
         lp.hw_nhwc = true;
     }
+    for (auto& lp : m->layers)
+      lp.tg_csum = lp.tg_fwd == 1 && !lp.hw_nhwc && dpg::tg::csum_nhwc_ok(lp.g) && tg_csum_enabled();
     for (auto& lp : m->layers) {
       // every conv forward writes its consumer's NHWC copy in the epilogue
       if (lp.tg_fwd && lp.prev_param_layer >= 0) lp.xh_by_prev = m->layers[lp.prev_param_layer].kind == DPG_LAYER_CONV2D;
@@ -938,7 +955,7 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
         ConvGeom g = lp.g;
         for (int64_t bb = 1;; bb = std::min(bb * 2, max_batch)) {
           g.b = bb;
-          cs = std::max(cs, dpg::clipped_sum_ws_conv2d(g));
+          cs = std::max(cs, dpg::clipped_sum_ws_conv2d(g, lp.tg_csum));
           ws = std::max(ws, dpg::conv_fwd_ws_bytes(g));
           ws = std::max(ws, dpg::conv_dgrad_ws_bytes(g));
           if (bb == max_batch) break;
@@ -1512,6 +1529,7 @@ dpg_status dpg_train_step(dpg_optimizer* o, const float* x, const float* targets
       const int64_t before = ctx->launches;
       ctx->capturing = true;
       DPG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      if (ctx->timeline) DPG_CUDA(cudaEventRecordWithFlags(ctx->tl_start, ctx->stream, cudaEventRecordExternal));
       try {
         if (persist) {
           persist_step(o, x, targets, b, loss, true);

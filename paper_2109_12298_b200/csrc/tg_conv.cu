@@ -1,6 +1,9 @@
 // tg_conv.cu — the TMA-fed tcgen05 contractions (tg_gemm.cuh): tensor-map construction and the
 // plain row-major GEMM the core is unit-tested through (dpg_tg_gemm_selftest).
+#include <map>
 #include <mutex>
+#include <string>
+#include <tuple>
 
 #include "tg_gemm.cuh"
 
@@ -25,6 +28,32 @@ EncodeTiledFn encoder() {
   return fn;
 }
 }  // namespace
+
+int max_active_clusters(const void* fn, int smem, int ck, int threads) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int>, int> memo;
+  int dev = 0;
+  DPG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = memo.find({dev, fn, ck});
+  if (it != memo.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ck * kNumSMs);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ck;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  DPG_CUDA(cudaOccupancyMaxActiveClusters(&n, fn, &cfg));
+  if (n <= 0) raise(DPG_ERR_INTERNAL, "cluster split-K: no cluster of " + std::to_string(ck) + " fits");
+  memo[{dev, fn, ck}] = n;
+  return n;
+}
 
 CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                      const uint32_t* box, const uint32_t* estr, CUtensorMapSwizzle swz) {
@@ -68,8 +97,11 @@ struct Gemm2D {
   __device__ bool has_epi_in() const { return false; }
   __device__ uint32_t epi_in_bytes() const { return 0; }
   __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
+  __device__ uint64_t pre_epilogue(int, int, int, int) const { return 0; }
+  static constexpr bool kEpiConst = false;
+  __device__ void epi_const(int, int, int, int, float*) const {}
   __device__ void epilogue(int mt, int nt, int, int row, int c0, const float (&v)[16], double&, uint8_t*,
-                           const uint8_t*) const {
+                           const uint8_t*, uint64_t, const float*) const {
     const int m = mt * BM + row;
     if (m >= M) return;
 #pragma unroll
@@ -82,8 +114,19 @@ struct Gemm2D {
   __device__ void finish(int, int, int, double) const {}
 };
 
+// launch with split-K over clusters of ck CTAs (1, 2 or 4)
+template <int BN, int BK, class Pr>
+void launch_ck(dpg_ctx* ctx, const Pr& p, dim3 grid, int ck) {
+  constexpr int STG = Pr::kStaging, EIN = Pr::kEpiIn;
+  switch (ck) {
+    case 4: launch<BN, BK, stages_for<BN, BK, STG, EIN, red_bytes(4)>(), Pr, 4>(ctx, p, grid); break;
+    case 2: launch<BN, BK, stages_for<BN, BK, STG, EIN, red_bytes(2)>(), Pr, 2>(ctx, p, grid); break;
+    default: launch<BN, BK, stages_for<BN, BK, STG, EIN>(), Pr, 1>(ctx, p, grid); break;
+  }
+}
+
 template <int BN, int BK, bool BMN = false>
-void gemm2d(dpg_ctx* ctx, const float* a, const float* b, float* d, int M, int N, int K) {
+void gemm2d(dpg_ctx* ctx, const float* a, const float* b, float* d, int M, int N, int K, int ck = 1) {
   const uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N};
   const uint64_t sa[1] = {(uint64_t)K * 4}, sb[1] = {(uint64_t)K * 4};
   const uint32_t ba[2] = {BK, BM}, bb[2] = {BK, BN};
@@ -97,7 +140,9 @@ void gemm2d(dpg_ctx* ctx, const float* a, const float* b, float* d, int M, int N
     p.mb = make_map(b, 2, db, sb, bb, nullptr, KLay<BK>::TMA_SWIZZLE);
   }
   p.d = d; p.M = M; p.N = N; p.K = K;
-  launch<BN, BK, stages_for<BN, BK>()>(ctx, p, dim3((M + BM - 1) / BM, (N + BN - 1) / BN, 1));
+  const dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, 1);
+  if constexpr (!BMN && BN <= 64) launch_ck<BN, BK>(ctx, p, grid, ck);
+  else launch<BN, BK, stages_for<BN, BK>()>(ctx, p, grid);
 }
 
 // =============================================================================================
@@ -117,11 +162,13 @@ void gemm2d(dpg_ctx* ctx, const float* a, const float* b, float* d, int M, int N
 template <int BN, int BK>
 struct ConvFwdT {
   static constexpr bool kScaleA = false, kBPreSplit = true, kCtaReduce = false, kBMajorMN = false;
-  static constexpr int kStaging = 2 * 8192, kEpiIn = 0;  // NCHW [spt][16][P] | NHWC [128][16] (SW64)
-  CUtensorMap ma, mb, my, myh;
-  int b, O, P, kw, s, pad, spt, cpt, nk, has_yh, relu_out;
+  static constexpr int kStaging = 0, kEpiIn = 0;
+  CUtensorMap ma, mb;
+  int b, O, P, kw, s, pad, spt, cpt, nk, relu_out;
   uint32_t bytes;
   const float* bias;
+  float* y;   // NCHW [b][O][P]
+  float* yh;  // NHWC [b][P][O] of the consumer's input (ReLU applied when relu_out) or null
   __device__ int nkb(int) const { return nk; }
   __device__ uint32_t stage_bytes() const { return bytes; }
   __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t sblo, uint32_t bar, int mt, int nt, int) const {
@@ -136,31 +183,38 @@ struct ConvFwdT {
   __device__ bool has_epi_in() const { return false; }
   __device__ uint32_t epi_in_bytes() const { return 0; }
   __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
-  __device__ void epilogue(int, int nt, int, int row, int c0, const float (&v)[16], double&, uint8_t* stg,
-                           const uint8_t*) const {
-    if (row >= spt * P) return;
+  __device__ uint64_t pre_epilogue(int, int, int, int) const { return 0; }
+  // the bias of the tile's BN output channels, loaded while the tile's MMAs run
+  static constexpr bool kEpiConst = true;
+  __device__ void epi_const(int, int nt, int, int row, float* cst) const {
+    if (row < BN) cst[row] = (bias && nt * BN + row < O) ? __ldg(bias + nt * BN + row) : 0.f;
+  }
+  // direct stores: a warp's rows are consecutive positions, so each NCHW store instruction covers
+  // whole 16-byte .. 128-byte position runs, and each thread writes its NHWC row's 16 channels as
+  // four 16-byte stores (TMA stores of small-P boxes were request-bound: 16-byte NCHW rows)
+  __device__ void epilogue(int mt, int nt, int, int row, int c0, const float (&v)[16], double&, uint8_t*,
+                           const uint8_t*, uint64_t, const float* cst) const {
     const int r = row / P, pp = row - r * P;
-    const int o0 = nt * BN + c0;
+    const int n = mt * spt + r, o0 = nt * BN + c0;
+    if (row >= spt * P || n >= b || o0 >= O) return;  // O % 4 == 0; a chunk may straddle O
     float out[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) out[j] = v[j] + ((bias && o0 + j < O) ? __ldg(bias + o0 + j) : 0.f);
-    float* nchw = reinterpret_cast<float*>(stg) + r * 16 * P + pp;  // [spt][16][P]
+    for (int j = 0; j < 16; ++j) out[j] = v[j] + cst[c0 + j];
+    float* yp = y + ((int64_t)n * O + o0) * P + pp;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) nchw[j * P] = out[j];
-    if (has_yh) {
-      uint8_t* nhwc = stg + 8192;
+    for (int j = 0; j < 16; ++j)
+      if (o0 + j < O) yp[(int64_t)j * P] = out[j];
+    if (yh) {
+      float* hp = yh + ((int64_t)n * P + pp) * O + o0;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        *reinterpret_cast<float4*>(nhwc + sw64_off(row, c)) =
-            make_float4(relu_if(out[4 * c], relu_out), relu_if(out[4 * c + 1], relu_out),
-                        relu_if(out[4 * c + 2], relu_out), relu_if(out[4 * c + 3], relu_out));
+        if (o0 + 4 * c < O)
+          *reinterpret_cast<float4*>(hp + 4 * c) =
+              make_float4(relu_if(out[4 * c], relu_out), relu_if(out[4 * c + 1], relu_out),
+                          relu_if(out[4 * c + 2], relu_out), relu_if(out[4 * c + 3], relu_out));
     }
   }
-  __device__ void epi_store(int mt, int nt, int, int c0, uint32_t stg) const {
-    const int o0 = nt * BN + c0;
-    tma_st3(&my, stg, 0, o0, mt * spt);
-    if (has_yh) tma_st2(&myh, stg + 8192, o0, mt * spt * P);
-  }
+  __device__ void epi_store(int, int, int, int, uint32_t) const {}
   __device__ void finish(int, int, int, double) const {}
 };
 
@@ -174,11 +228,13 @@ struct ConvFwdT {
 template <int BN, int BK>
 struct ConvDgradT {
   static constexpr bool kScaleA = false, kBPreSplit = true, kCtaReduce = false, kBMajorMN = false;
-  static constexpr int kStaging = 8192, kEpiIn = 8192;  // NHWC [spt][QH][QW][16] (SW64) out / mask in
-  CUtensorMap ma, mb, mdxh, mmask;
-  int b, C, H, W, kh, kw, s, pad, QH, QW, spt, ocb, has_mask, has_dxh;
+  static constexpr int kStaging = 0, kEpiIn = 0;
+  CUtensorMap ma, mb;
+  int b, C, H, W, kh, kw, s, pad, QH, QW, spt, ocb;
   uint32_t bytes;
-  float* dx;  // NCHW [b][C][H][W]
+  const float* mask_h;  // NHWC [b][H][W][C] layer input (ReLU mask of the input gradient) or null
+  float* dxh;           // NHWC [b][H][W][C] input gradient or null
+  float* dx;            // NCHW [b][C][H][W] input gradient or null
   __device__ int first_tap(int ph) const { return (ph + pad) % s; }
   __device__ int taps(int k0, int kdim) const { return k0 < kdim ? (kdim - k0 + s - 1) / s : 0; }
   __device__ int nkb(int z) const {
@@ -201,44 +257,76 @@ struct ConvDgradT {
   }
   __device__ float scale(int, int, int, int) const { return 1.f; }
   __device__ int a_rows() const { return BM; }
-  __device__ bool has_epi_in() const { return has_mask != 0; }
-  __device__ uint32_t epi_in_bytes() const { return (uint32_t)(spt * QH * QW * 16 * 4); }
-  __device__ void epi_load(int mt, int nt, int z, int c0, uint32_t dst, uint32_t bar) const {
-    const int py = z / s, px = z - py * s;
-    tma4(dst, &mmask, bar, nt * BN + c0, px, py, mt * spt);
-  }
-  __device__ void epilogue(int mt, int nt, int z, int row, int c0, const float (&v)[16], double&, uint8_t* stg,
-                           const uint8_t* in) const {
+  __device__ bool has_epi_in() const { return false; }
+  __device__ uint32_t epi_in_bytes() const { return 0; }
+  __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
+  // the input pixel of an epilogue row (false: padding row of the tile)
+  __device__ bool pixel(int mt, int z, int row, int64_t& pix, int& n, int& iy, int& ix) const {
     const int q = QH * QW;
-    if (row >= spt * q) return;
+    if (row >= spt * q) return false;
     const int r = row / q, rr = row - r * q;
-    const int n = mt * spt + r;
+    n = mt * spt + r;
     const int qy = rr / QW, qx = rr - qy * QW;
     const int py = z / s, px = z - py * s;
-    const int iy = s * qy + py, ix = s * qx + px;
+    iy = s * qy + py;
+    ix = s * qx + px;
+    if (n >= b || iy >= H || ix >= W) return false;
+    pix = ((int64_t)n * H + iy) * W + ix;
+    return true;
+  }
+  static constexpr bool kEpiConst = false;
+  __device__ void epi_const(int, int, int, int, float*) const {}
+  // ReLU mask of the tile's first 64 channels as bits, from the NHWC input copy (one thread reads
+  // its pixel's contiguous channels; the loads overlap the tile's MMAs)
+  __device__ uint64_t pre_epilogue(int mt, int nt, int z, int row) const {
+    int64_t pix;
+    int n, iy, ix;
+    if (!mask_h || !pixel(mt, z, row, pix, n, iy, ix)) return 0;
+    const float4* src = reinterpret_cast<const float4*>(mask_h + pix * C + nt * BN);
+    constexpr int NV = (BN < 64 ? BN : 64) / 4;
+    float4 m[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) m[i] = __ldg(src + i);
+    uint64_t bits = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      bits |= (uint64_t)((m[i].x > 0.f) | (m[i].y > 0.f) << 1 | (m[i].z > 0.f) << 2 | (m[i].w > 0.f) << 3) << (4 * i);
+    return bits;
+  }
+  __device__ void epilogue(int mt, int nt, int z, int row, int c0, const float (&v)[16], double&, uint8_t*,
+                           const uint8_t*, uint64_t pre, const float*) const {
+    int64_t pix;
+    int n, iy, ix;
+    if (!pixel(mt, z, row, pix, n, iy, ix)) return;
+    const int cb0 = nt * BN + c0;
+    if (cb0 >= C) return;  // C % 16 == 0: a chunk is inside or past the channels
+    uint32_t mbits = 0xFFFFu;
+    if (mask_h) {
+      if (c0 < 64) {
+        mbits = (uint32_t)(pre >> c0) & 0xFFFFu;
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(mask_h + pix * C + cb0);
+        mbits = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 m = __ldg(src + c);
+          mbits |= ((m.x > 0.f) | (m.y > 0.f) << 1 | (m.z > 0.f) << 2 | (m.w > 0.f) << 3) << (4 * c);
+        }
+      }
+    }
     float out[16];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      float4 m = make_float4(1.f, 1.f, 1.f, 1.f);
-      if (has_mask) m = *reinterpret_cast<const float4*>(in + sw64_off(row, c));
-      out[4 * c] = m.x > 0.f ? v[4 * c] : 0.f;
-      out[4 * c + 1] = m.y > 0.f ? v[4 * c + 1] : 0.f;
-      out[4 * c + 2] = m.z > 0.f ? v[4 * c + 2] : 0.f;
-      out[4 * c + 3] = m.w > 0.f ? v[4 * c + 3] : 0.f;
-      if (has_dxh) *reinterpret_cast<float4*>(stg + sw64_off(row, c)) =
-          make_float4(out[4 * c], out[4 * c + 1], out[4 * c + 2], out[4 * c + 3]);
-    }
-    if (!dx || n >= b || iy >= H || ix >= W) return;  // dx null: the NHWC copy is the only output
-    const int cb0 = nt * BN + c0;
+    for (int j = 0; j < 16; ++j) out[j] = (mbits >> j) & 1u ? v[j] : 0.f;
+    if (dxh) {
+      float4* d = reinterpret_cast<float4*>(dxh + pix * C + cb0);
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (cb0 + j < C) dx[(((int64_t)n * C + cb0 + j) * H + iy) * W + ix] = out[j];
+      for (int c = 0; c < 4; ++c) d[c] = make_float4(out[4 * c], out[4 * c + 1], out[4 * c + 2], out[4 * c + 3]);
+    }
+    if (!dx) return;  // dx null: the NHWC copy is the only output
+#pragma unroll
+    for (int j = 0; j < 16; ++j) dx[(((int64_t)n * C + cb0 + j) * H + iy) * W + ix] = out[j];
   }
-  __device__ void epi_store(int mt, int nt, int z, int c0, uint32_t stg) const {
-    if (!has_dxh) return;
-    const int py = z / s, px = z - py * s;
-    tma_st4(&mdxh, stg, nt * BN + c0, px, py, mt * spt);
-  }
+  __device__ void epi_store(int, int, int, int, uint32_t) const {}
   __device__ void finish(int, int, int, double) const {}
 };
 
@@ -250,8 +338,9 @@ struct ConvDgradT {
 // channel) in tap-major order: per 32-channel chunk of a tap, one NHWC box of the layer input
 // (ReLU applied by its producer) lands as an MN-major [BK positions][32 channels] tile (32-byte-atom
 // swizzle) — the implicit im2col with no transposition. K = (sample, position) of the split, one
-// sample per K block (P % BK == 0). Partials [split][O][C kk] in the reference's k order, combined
-// in split order by the split-K reduce. Chains are bounded like the register-gather kernel's
+// sample per K block (P % BK == 0). Partials [split][O][(tap, channel)], 16-float row pieces per
+// epilogue thread; the split-K reduce combines them in a fixed order and writes the reference's
+// k order (clip.cu TapMajorOut). Chains are bounded like the register-gather kernel's
 // (<= 512 products per TMEM accumulator).
 template <int BN, int BK>
 struct ConvCsumT {
@@ -284,16 +373,16 @@ struct ConvCsumT {
   __device__ bool has_epi_in() const { return false; }
   __device__ uint32_t epi_in_bytes() const { return 0; }
   __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
+  __device__ uint64_t pre_epilogue(int, int, int, int) const { return 0; }
+  static constexpr bool kEpiConst = false;
+  __device__ void epi_const(int, int, int, int, float*) const {}
   __device__ void epilogue(int, int nt, int z, int row, int c0, const float (&v)[16], double&, uint8_t*,
-                           const uint8_t*) const {
-    if (row >= O) return;
-    const int K = C * khw;
-    float* dst = part + ((int64_t)z * O + row) * K;
+                           const uint8_t*, uint64_t, const float*) const {
+    const int K = C * khw, col = nt * G * C + c0;  // tap-major column: (tap, channel)
+    if (row >= O || col >= K) return;
+    float4* dst = reinterpret_cast<float4*>(part + ((int64_t)z * O + row) * K + col);
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj) {
-      const int col = c0 + jj, tl = col / C, c = col - tl * C, t = nt * G + tl;
-      if (t < khw) dst[c * khw + t] = v[jj];
-    }
+    for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   }
   __device__ void epi_store(int, int, int, int, uint32_t) const {}
   __device__ void finish(int, int, int, double) const {}
@@ -363,10 +452,37 @@ CUtensorMap split_rows_map(const float* base, int64_t rows, int64_t k, int bk, i
   return make_map(base, 3, dims, str, box, nullptr, swz);
 }
 // output columns per tile: the widest of 128 / 64 / 32 that still gives >= one CTA per SM
-int pick_bn(int n, int64_t mtiles) {
-  for (int bn : {128, 64, 32})
-    if (bn <= ((n + 15) / 16) * 16 + 15 && mtiles * ((n + bn - 1) / bn) >= kNumSMs) return bn;
-  return 32;
+// Output tile width and cluster split-K of a conv launch with `slices` M tiles (x parity classes)
+// and nkb K blocks per tile. Estimated time in K-block units: waves x (K blocks per CTA x the MMA
+// cost at that N + the epilogue's chunks), the cluster split adding the partial exchange. A
+// persistent CTA runs its tiles back to back, so waves = ceil(tiles / co-resident clusters).
+// The cluster split is opt-in (DPG_TG_CK=2 or 4 allows it): measured, it does not pay on the
+// CIFAR step (negative results).
+void pick_tile(int n, int64_t slices, int nkb, int& bn_out, int& ck_out) {
+  static const int ck_max = [] {
+    const char* e = std::getenv("DPG_TG_CK");
+    return e ? std::max(1, std::min(4, std::atoi(e))) : 1;
+  }();
+  double best = 1e30;
+  bn_out = 32;
+  ck_out = 1;
+  for (int bn : {128, 64, 32}) {
+    if (bn > ((n + 15) / 16) * 16 + 15) continue;
+    const int64_t tiles = slices * ((n + bn - 1) / bn);
+    for (int ck : {1, 2, 4}) {
+      if (ck > ck_max || (ck > 1 && (bn > 64 || nkb < 2 * ck))) continue;
+      const int64_t slots = kNumSMs / ck;
+      const int64_t waves = (tiles + slots - 1) / slots;
+      const double mma = bn <= 64 ? 1.0 : 1.3;
+      const double epi = 0.15 * (bn / 16) * (ck > 1 ? 2.0 : 1.0);
+      const double t = (double)waves * ((double)((nkb + ck - 1) / ck) * mma + epi);
+      if (t < best - 1e-9) {
+        best = t;
+        bn_out = bn;
+        ck_out = ck;
+      }
+    }
+  }
 }
 template <class F>
 void with_bn(int bn, F&& f) {
@@ -398,7 +514,8 @@ void conv_fwd_nhwc(dpg_ctx* ctx, const float* xh, const float* wf, const float* 
   const int spt = BM / P;
   const int64_t mtiles = (b + spt - 1) / spt;
   const int bk = g.ic % 32 == 0 ? 32 : 16;
-  const int bn = pick_bn((int)g.oc, mtiles);
+  int bn, ck;
+  pick_tile((int)g.oc, mtiles, (int)(g.kh * g.kw * (g.ic / bk)), bn, ck);
   with_bk(bk, [&](auto BKc) {
     constexpr int BK = decltype(BKc)::value;
     with_bn(bn, [&](auto BNc) {
@@ -408,25 +525,15 @@ void conv_fwd_nhwc(dpg_ctx* ctx, const float* xh, const float* wf, const float* 
       p.ma = nhwc_map(xh, b, (int)g.h, (int)g.w, (int)g.ic, BK, (int)g.ow, (int)g.oh, spt, (int)g.stride,
                       KLay<BK>::TMA_SWIZZLE);
       p.mb = split_rows_map(wf, g.oc, g.K(), BK, BN, KLay<BK>::TMA_SWIZZLE);
-      {  // NCHW y [b][O][P]: box (P, 16 channels, spt samples)
-        const uint64_t dims[3] = {(uint64_t)P, (uint64_t)g.oc, (uint64_t)b};
-        const uint64_t str[2] = {(uint64_t)P * 4, (uint64_t)(g.oc * P * 4)};
-        const uint32_t box[3] = {(uint32_t)P, 16, (uint32_t)spt};
-        p.my = make_map(y, 3, dims, str, box, nullptr, CU_TENSOR_MAP_SWIZZLE_NONE);
-      }
-      p.has_yh = yh != nullptr;
-      if (yh) {  // NHWC yh [b P][O]: box (16 channels, spt P rows), 64-byte swizzled staging rows
-        const uint64_t dims[2] = {(uint64_t)g.oc, (uint64_t)b * P};
-        const uint64_t str[1] = {(uint64_t)g.oc * 4};
-        const uint32_t box[2] = {16, (uint32_t)(spt * P)};
-        p.myh = make_map(yh, 2, dims, str, box, nullptr, CU_TENSOR_MAP_SWIZZLE_64B);
-      }
+      p.y = y;
+      p.yh = yh;
       p.b = b; p.O = (int)g.oc; p.P = P; p.kw = (int)g.kw; p.s = (int)g.stride; p.pad = (int)g.pad;
       p.spt = spt; p.cpt = (int)g.ic / BK; p.nk = (int)(g.kh * g.kw) * p.cpt; p.relu_out = relu_out;
       p.bytes = (uint32_t)((spt * P + 2 * BN) * BK * 4);
       p.bias = bias;
-      launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn>()>(
-          ctx, p, dim3((unsigned)mtiles, (unsigned)((g.oc + BN - 1) / BN), 1));
+      const dim3 grid((unsigned)mtiles, (unsigned)((g.oc + BN - 1) / BN), 1);
+      if constexpr (BN <= 64) launch_ck<BN, BK>(ctx, p, grid, ck);
+      else launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn>()>(ctx, p, grid);
     });
   });
 }
@@ -438,7 +545,8 @@ void conv_dgrad_nhwc(dpg_ctx* ctx, const float* hh, const float* wd, const ConvG
   const int spt = BM / (QH * QW);
   const int64_t mtiles = (b + spt - 1) / spt;
   const int bk = g.oc % 32 == 0 ? 32 : 16;
-  const int bn = pick_bn((int)g.ic, mtiles * s * s);
+  int bn, ck;  // K blocks per tile: at most ceil(kh / s) ceil(kw / s) taps x the channel blocks
+  pick_tile((int)g.ic, mtiles * s * s, (int)(((g.kh + s - 1) / s) * ((g.kw + s - 1) / s) * (g.oc / bk)), bn, ck);
   with_bk(bk, [&](auto BKc) {
     constexpr int BK = decltype(BKc)::value;
     with_bn(bn, [&](auto BNc) {
@@ -448,17 +556,15 @@ void conv_dgrad_nhwc(dpg_ctx* ctx, const float* hh, const float* wd, const ConvG
       // unit-stride boxes over the highway (NHWC [b][OH][OW][O])
       p.ma = nhwc_map(hh, b, (int)g.oh, (int)g.ow, (int)g.oc, BK, QW, QH, spt, 1, KLay<BK>::TMA_SWIZZLE);
       p.mb = split_rows_map(wd, g.kh * g.kw * g.ic, g.oc, BK, BN, KLay<BK>::TMA_SWIZZLE);
-      p.has_mask = mask_h != nullptr;
-      p.has_dxh = dxh != nullptr;
-      // 16-channel boxes of the input-side NHWC tensors, the class grid walked with stride s
-      if (mask_h) p.mmask = nhwc_map(mask_h, b, (int)g.h, (int)g.w, (int)g.ic, 16, QW, QH, spt, s, CU_TENSOR_MAP_SWIZZLE_64B);
-      if (dxh) p.mdxh = nhwc_map(dxh, b, (int)g.h, (int)g.w, (int)g.ic, 16, QW, QH, spt, s, CU_TENSOR_MAP_SWIZZLE_64B);
+      p.mask_h = mask_h;
+      p.dxh = dxh;
       p.b = b; p.C = (int)g.ic; p.H = (int)g.h; p.W = (int)g.w; p.kh = (int)g.kh; p.kw = (int)g.kw;
       p.s = s; p.pad = (int)g.pad; p.QH = QH; p.QW = QW; p.spt = spt; p.ocb = (int)g.oc / BK;
       p.bytes = (uint32_t)((spt * QH * QW + 2 * BN) * BK * 4);
       p.dx = dx;
-      launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn>()>(
-          ctx, p, dim3((unsigned)mtiles, (unsigned)((g.ic + BN - 1) / BN), (unsigned)(s * s)));
+      const dim3 grid((unsigned)mtiles, (unsigned)((g.ic + BN - 1) / BN), (unsigned)(s * s));
+      if constexpr (BN <= 64) launch_ck<BN, BK>(ctx, p, grid, ck);
+      else launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn>()>(ctx, p, grid);
     });
   });
 }
@@ -475,8 +581,10 @@ int csum_nhwc_splits(const ConvGeom& g) {
   const int64_t P = g.P();
   const int G = 3, ntn = (int)((g.kh * g.kw + G - 1) / G);
   const int64_t spl_chain = std::max<int64_t>(1, 512 / P);
-  const int64_t want = (kNumSMs + ntn - 1) / ntn;
-  const int64_t spl = std::min<int64_t>(spl_chain, std::max<int64_t>(1, (g.b + want - 1) / want));
+  // about two tiles per SM: the persistent CTAs overlap one tile's epilogue with the next's loads
+  const int64_t want = (2 * kNumSMs + ntn - 1) / ntn;
+  int64_t spl = std::min<int64_t>(spl_chain, std::max<int64_t>(1, (g.b + want - 1) / want));
+  if (const char* e = std::getenv("DPG_TG_CSUM_SPL")) spl = std::min<int64_t>(spl_chain, std::max(1, std::atoi(e)));
   return (int)((g.b + spl - 1) / spl);
 }
 
@@ -534,12 +642,27 @@ void nchw_to_nhwc(dpg_ctx* ctx, const float* src, int relu, int64_t b, int64_t C
 #ifdef DPG_TG_TRACE
 // trace builds only (tools/tg_trace_step.py): read the traced launch's timeline
 extern "C" __attribute__((visibility("default"))) void dpg_tg_trace_read(unsigned long long* out) {
-  cudaMemcpyFromSymbol(out, dpg::tg::g_tg_trace, sizeof(unsigned long long) * 8 * 256);
+  cudaMemcpyFromSymbol(out, dpg::tg::g_tg_trace, sizeof(unsigned long long) * 10 * 256);
 }
 #endif
 
 using dpg::guard;
 using dpg::raise;
+
+dpg_status dpg_tg_gemm_selftest_split(dpg_ctx* ctx, const float* a, const float* b, float* d, int64_t m,
+                                      int64_t n, int64_t k, int bn, int ck) {
+  return guard(ctx, [&] {
+    if (!ctx) raise(DPG_ERR_PARAMETER, "null context");
+    if (m <= 0 || n <= 0 || k <= 0 || (k * 4) % 16 != 0 || m >= (1 << 30) || n >= (1 << 30) || k >= (1 << 30))
+      raise(DPG_ERR_DIMENSION, "tg_gemm_selftest_split: extents must be positive, K a multiple of 4");
+    if (ck != 1 && ck != 2 && ck != 4) raise(DPG_ERR_PARAMETER, "tg_gemm_selftest_split: ck must be 1, 2 or 4");
+    switch (bn) {
+      case 32: dpg::tg::gemm2d<32, 32>(ctx, a, b, d, (int)m, (int)n, (int)k, ck); break;
+      case 64: dpg::tg::gemm2d<64, 32>(ctx, a, b, d, (int)m, (int)n, (int)k, ck); break;
+      default: raise(DPG_ERR_PARAMETER, "tg_gemm_selftest_split: bn must be 32 or 64");
+    }
+  });
+}
 
 dpg_status dpg_tg_gemm_selftest(dpg_ctx* ctx, const float* a, const float* b, float* d, int64_t m, int64_t n,
                                 int64_t k, int bn, int bk) {

@@ -40,6 +40,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "dpg_device.cuh"
 
@@ -52,10 +54,10 @@ constexpr int kConvThreads = 128;
 // Timeline trace of CTA 0 (tools/micro/tg_trace.cu builds with -DDPG_TG_TRACE): globaltimer
 // stamps per role and iteration into g_tg_trace[event][iteration].
 #ifdef DPG_TG_TRACE
-__device__ unsigned long long g_tg_trace[8][256];
+__device__ unsigned long long g_tg_trace[10][256];
 __device__ int g_tg_trace_on;  // set by the host for the one launch it traces
 __device__ __forceinline__ void tg_trace(int ev, int i) {
-  if (g_tg_trace_on && blockIdx.x == 0 && i < 256) {
+  if (g_tg_trace_on == (int)blockIdx.x + 1 && i < 256) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_tg_trace[ev][i] = t;
@@ -85,6 +87,50 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     if (done) return;
     if (n == (1u << 30)) __trap();
   }
+}
+// cluster-scope wait: the arrivals came from other CTAs of the cluster (release.cluster)
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  for (uint32_t n = 0;; ++n) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    if (done) return;
+    if (n == (1u << 30)) __trap();
+  }
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// the shared::cluster address of this CTA's shared address a in cluster CTA `rank`
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ float4 ld_cluster4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+// bulk copy of this CTA's shared [src, src + bytes) into another cluster CTA's shared memory,
+// completing `bytes` transactions on that CTA's mbarrier (both addresses shared::cluster)
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "r"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -229,15 +275,17 @@ __device__ __forceinline__ void split16(uint8_t* hi, uint8_t* lo, float s) {
   *reinterpret_cast<uint4*>(lo) = l;
 }
 
-template <int BN, int BK, int ST, int STG, int EIN>
+template <int BN, int BK, int ST, int STG, int EIN, int RED = 0>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE = A_BYTES + 2 * B_BYTES;  // A (raw), B, B_lo
   static constexpr int STG_OFF = ST * STAGE;           // 2 epilogue staging buffers of STG bytes
   static constexpr int EIN_OFF = STG_OFF + 2 * STG;     // 2 epilogue input buffers of EIN bytes
-  static constexpr int BAR_OFF = EIN_OFF + 2 * EIN;
-  static constexpr int BARS = (3 * ST + 6) * 8;
+  static constexpr int RED_OFF = EIN_OFF + 2 * EIN;    // split-K: peers' partial chunks (leader)
+  static constexpr int CST_OFF = RED_OFF + RED;        // 2 x 256 per-tile epilogue constants
+  static constexpr int BAR_OFF = CST_OFF + 2 * 1024;
+  static constexpr int BARS = (3 * ST + 10) * 8;
   static constexpr int TOTAL = BAR_OFF + BARS + 16 + 1024;  // + alignment slack
 };
 
@@ -247,15 +295,19 @@ constexpr int tmem_stage_cap() {
   return (512 - 2 * BN) / (2 * BK);
 }
 // deepest ring (<= 6 stages) that fits the 227 KB a CTA may use and the 512 TMEM columns
-template <int BN, int BK, int STG = 0, int EIN = 0>
+template <int BN, int BK, int STG = 0, int EIN = 0, int RED = 0>
 constexpr int stages_for() {
   constexpr int st = Smem<BN, BK, 1, STG, EIN>::STAGE;
-  constexpr int fixed = 2 * STG + 2 * EIN + 4096;
+  constexpr int fixed = 2 * STG + 2 * EIN + RED + 2048 + 4096;
   constexpr int lim = 227 * 1024 - fixed;
   constexpr int by_smem = (6 * st <= lim) ? 6 : (5 * st <= lim) ? 5 : (4 * st <= lim) ? 4 : (3 * st <= lim) ? 3 : 2;
   return by_smem < tmem_stage_cap<BN, BK>() ? by_smem : tmem_stage_cap<BN, BK>();
 }
 constexpr uint32_t kTmemCols = 512;
+// split-K over a cluster of CK CTAs: two chunk buffers of [128 rows][16] fp32 per peer
+// staging buffers of a peer's outgoing chunks, read by rank 0 through distributed shared memory
+constexpr int kRedChunk = BM * 16 * 4;
+constexpr int red_bytes(int ck) { return ck > 1 ? 2 * kRedChunk : 0; }
 
 // Tile space of a launch: mt fastest, then nt, then z.
 struct Tiles {
@@ -288,15 +340,28 @@ struct Tiles {
 //   bool has_epi_in() const;           this launch loads epilogue inputs (kEpiIn > 0)
 //   uint32_t epi_in_bytes() const;     bytes one epi_load moves (<= kEpiIn)
 //   void epi_load(int mt, int nt, int z, int c0, uint32_t dst, uint32_t bar) const;   kEpiIn bytes
+//   uint64_t pre_epilogue(int mt, int nt, int z, int row) const;   per-thread tile state, fetched
+//                                      before the accumulator is ready (e.g. a ReLU mask as bits)
+//   static constexpr bool kEpiConst;   epi_const(mt, nt, z, row, float* cst) fills <= 256 per-tile
+//                                      constants in shared memory (e.g. the bias of the tile's
+//                                      columns) before the accumulator is ready; epilogue reads cst
 //   void epilogue(int mt, int nt, int z, int row, int c0, const float (&v)[16], double& acc,
-//                 uint8_t* stage, const uint8_t* in) const;   row < 128, columns c0 .. c0+15
+//                 uint8_t* stage, const uint8_t* in, uint64_t pre, const float* cst) const;
+//                                      row < 128, columns c0 .. c0+15
 //   void epi_store(int mt, int nt, int z, int c0, uint32_t stage) const;   one thread (kStaging)
 //   void finish(int mt, int nt, int z, double acc_sum) const;               (kCtaReduce)
 constexpr int kThreads2 = 320;
-template <int BN, int BK, int ST, class Prob>
+//
+// Split-K over a thread-block cluster (CK > 1): the CK CTAs of a cluster own one tile at a time,
+// CTA rank r running K blocks [r nkb / CK, (r + 1) nkb / CK) into its own TMEM accumulator. Per
+// 16-column chunk the peers store their partial through distributed shared memory into the rank-0
+// CTA's reduction buffer (st.shared::cluster, then a remote mbarrier arrive); rank 0 adds them in
+// rank order (deterministic), frees the buffer with a remote arrive per peer, and runs the epilogue.
+template <int BN, int BK, int ST, class Prob, int CK = 1>
 __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant__ Prob p, const Tiles tiles) {
   constexpr int STG = Prob::kStaging, EIN = Prob::kEpiIn;
-  using S = Smem<BN, BK, ST, STG, EIN>;
+  static_assert(CK == 1 || (EIN == 0 && !Prob::kCtaReduce), "cluster split-K: plain epilogues only");
+  using S = Smem<BN, BK, ST, STG, EIN, red_bytes(CK)>;
   using Lay = KLay<BK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
@@ -308,6 +373,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
   auto tfull = [&](int a) { return bar0 + 8u * (3 * ST + a); };
   auto tempty = [&](int a) { return bar0 + 8u * (3 * ST + 2 + a); };
   auto ein = [&](int a) { return bar0 + 8u * (3 * ST + 4 + a); };
+  auto red_full = [&](int a) { return bar0 + 8u * (3 * ST + 6 + a); };   // rank 0: peers' chunks landed
+  auto red_empty = [&](int a) { return bar0 + 8u * (3 * ST + 8 + a); };  // peers: rank 0 read them
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::BAR_OFF + S::BARS);
   auto sA = [&](int s) { return sbase + s * S::STAGE; };
   auto sB = [&](int s) { return sbase + s * S::STAGE + S::A_BYTES; };
@@ -317,6 +384,15 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = tiles.count();
+  const int crank = CK > 1 ? (int)cluster_rank() : 0;
+  const int t_first = CK > 1 ? (int)blockIdx.x / CK : (int)blockIdx.x;
+  const int t_step = CK > 1 ? (int)gridDim.x / CK : (int)gridDim.x;
+  // this CTA's K blocks of a tile of slice z: [kb0, kb0 + nk)
+  auto krange = [&](int z, int& kb0, int& nk) {
+    const int n = p.nkb(z);
+    kb0 = CK > 1 ? n * crank / CK : 0;
+    nk = CK > 1 ? n * (crank + 1) / CK - kb0 : n;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -328,6 +404,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
       mbar_init(tfull(a), 1);
       mbar_init(tempty(a), kConvThreads);
       mbar_init(ein(a), 1);
+      mbar_init(red_full(a), CK - 1);  // one remote arrive per peer and chunk
+      mbar_init(red_empty(a), 1);      // one remote arrive from rank 0 per use
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -338,6 +416,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CK > 1) cluster_sync_all();  // every CTA's barriers exist before remote arrives
   tc_fence_after();
   pdl_wait();  // barrier init and TMEM allocation overlap the previous kernel's tail
   const uint32_t tmem = *tmem_slot;
@@ -345,16 +424,17 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = t_first; t < ntiles; t += t_step) {
         int mt, nt, z;
         tiles.at(t, mt, nt, z);
-        const int nkb = p.nkb(z);
+        int kb0, nkb;
+        krange(z, kb0, nkb);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % ST;
           if (it >= ST) mbar_wait(empty(s), ((it / ST) - 1) & 1);
           tg_trace(0, it);
           mbar_expect_tx(full(s), p.stage_bytes());
-          p.issue(kb, sA(s), sB(s), sBlo(s), full(s), mt, nt, z);
+          p.issue(kb0 + kb, sA(s), sB(s), sBlo(s), full(s), mt, nt, z);
         }
       }
     }
@@ -362,10 +442,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(BN, Prob::kBMajorMN);
       int it = 0, j = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      for (int t = t_first; t < ntiles; t += t_step, ++j) {
         int mt, nt, z;
         tiles.at(t, mt, nt, z);
-        const int nkb = p.nkb(z);
+        int kb0, nkb;
+        krange(z, kb0, nkb);
         const int a = j & 1;
         if (j >= 2) mbar_wait(tempty(a), ((j >> 1) - 1) & 1);
         tc_fence_after();
@@ -404,16 +485,17 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
     const int r = 32 * q + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * q) << 16);
     int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int t = t_first; t < ntiles; t += t_step) {
       int mt, nt, z;
       tiles.at(t, mt, nt, z);
-      const int nkb = p.nkb(z);
+      int kb0, nkb;
+      krange(z, kb0, nkb);
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         const int s = it % ST;
         mbar_wait(full(s), (it / ST) & 1);
         if (tc == 0) tg_trace(1, it);
         float sc = 1.f;
-        if (Prob::kScaleA) sc = p.scale(kb, mt, nt, z);
+        if (Prob::kScaleA) sc = p.scale(kb0 + kb, mt, nt, z);
         const uint8_t* arow = smem + s * S::STAGE + r * Lay::ROW;
         const int sw = Lay::ROW == 128 ? (r & 7) : ((r >> 1) & 3);
 #pragma unroll
@@ -456,20 +538,27 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
     const int row = 32 * q + lane;
     const bool leader = warp == 6 && lane == 0;
     int j = 0, g = 0;  // tile and chunk counters of this CTA
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+    for (int t = t_first; t < ntiles; t += t_step, ++j) {
       int mt, nt, z;
       tiles.at(t, mt, nt, z);
-      const int nkb = p.nkb(z);
+      int kb0, nkb;
+      krange(z, kb0, nkb);
       const int a = j & 1;
       const bool epi_in = EIN > 0 && p.has_epi_in();
       if (epi_in && leader) {  // epilogue inputs of the tile's first chunk
         mbar_expect_tx(ein(g & 1), p.epi_in_bytes());
         p.epi_load(mt, nt, z, 0, sbase + S::EIN_OFF + (g & 1) * EIN, ein(g & 1));
       }
+      const uint64_t pre = crank == 0 ? p.pre_epilogue(mt, nt, z, row) : 0;  // overlaps the tile's MMAs
+      float* cst = reinterpret_cast<float*>(smem + S::CST_OFF + a * 1024);
+      if constexpr (Prob::kEpiConst) {
+        if (crank == 0) p.epi_const(mt, nt, z, row, cst);
+      }
       mbar_wait(tfull(a), (j >> 1) & 1);
+      if constexpr (Prob::kEpiConst) asm volatile("bar.sync 1, 128;" ::: "memory");  // constants written
       if (row == 0) tg_trace(4, j);
       tc_fence_after();
-      if (t + (int)gridDim.x >= ntiles) pdl_trigger();  // last tile: the next kernel may launch
+      if (t + t_step >= ntiles) pdl_trigger();  // last tile: the next kernel may launch
       double acc = 0.0;
       float v[16];
 #pragma unroll 1
@@ -489,13 +578,46 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
           tc_fence_before();
           mbar_arrive(tempty(a));
         }
+        if constexpr (CK > 1) {  // split-K partials: rank 0 pulls the peers' chunks, adds in rank order
+          const int bb = g & 1;
+          const uint32_t send = sbase + S::RED_OFF + bb * kRedChunk + row * 64;  // [2][128][16]
+          if (crank != 0) {
+            // peer: stage the chunk in local shared memory, then tell rank 0 it is there
+            if (g >= 2) mbar_wait_cluster(red_empty(bb), ((g >> 1) - 1) & 1);  // rank 0 read it
+            float4* st4 = reinterpret_cast<float4*>(smem + (send - sbase));
+#pragma unroll
+            for (int c = 0; c < 4; ++c) st4[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (leader) mbar_arrive_remote(mapa(red_full(bb), 0));
+            if (row == 0) tg_trace(8, j * 8 + c0 / 16);
+            continue;  // the epilogue is rank 0's
+          }
+          mbar_wait_cluster(red_full(bb), (g >> 1) & 1);
+          if (row == 0) tg_trace(8, j * 8 + c0 / 16);
+          float4 w[CK - 1][4];
+#pragma unroll
+          for (int r = 1; r < CK; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) w[r - 1][c] = ld_cluster4(mapa(send + 16 * c, (uint32_t)r));
+#pragma unroll
+          for (int r = 1; r < CK; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              v[4 * c] += w[r - 1][c].x; v[4 * c + 1] += w[r - 1][c].y;
+              v[4 * c + 2] += w[r - 1][c].z; v[4 * c + 3] += w[r - 1][c].w;
+            }
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // every row read: the peers may refill
+          if (leader)
+#pragma unroll
+            for (int r = 1; r < CK; ++r) mbar_arrive_remote(mapa(red_empty(bb), (uint32_t)r));
+        }
         const uint8_t* in = nullptr;
         if (epi_in) {
           mbar_wait(ein(g & 1), (g >> 1) & 1);
           in = smem + S::EIN_OFF + (g & 1) * EIN;
         }
         uint8_t* stg = STG > 0 ? smem + S::STG_OFF + (g & 1) * STG : nullptr;
-        p.epilogue(mt, nt, z, row, c0, v, acc, stg, in);
+        p.epilogue(mt, nt, z, row, c0, v, acc, stg, in, pre, cst);
         if (STG > 0) {
           fence_proxy_async();
           if (leader) bulk_wait_read<0>();  // the previous chunk's stores have read their buffer
@@ -518,10 +640,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
         if (q == 0 && lane == 0) p.finish(mt, nt, z, red[a][0] + red[a][1] + red[a][2] + red[a][3]);
       }
     }
-    if (STG > 0 && leader) bulk_wait_all();
+    if ((STG > 0 || CK > 1) && leader) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CK > 1) cluster_sync_all();  // no CTA leaves while a peer may still address it
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
@@ -538,23 +661,51 @@ inline int& trace_launch_count() {
 }
 #endif
 
+// clusters of `ck` CTAs of fn (smem bytes each) that fit the GPU at once (cached per device)
+int max_active_clusters(const void* fn, int smem, int ck, int threads);
+
 // grid: the tile space (m tiles, n tiles, slices); the launch is persistent, min(tiles, #SMs) CTAs
-template <int BN, int BK, int ST, class Prob>
+// (CK > 1: min(tiles, co-resident clusters) clusters of CK CTAs)
+template <int BN, int BK, int ST, class Prob, int CK = 1>
 void launch(dpg_ctx* ctx, const Prob& p, dim3 grid) {
-  const int smem = Smem<BN, BK, ST, Prob::kStaging, Prob::kEpiIn>::TOTAL;
-  ensure_smem_attr(reinterpret_cast<const void*>(tg_kernel<BN, BK, ST, Prob>), smem);
+  const int smem = Smem<BN, BK, ST, Prob::kStaging, Prob::kEpiIn, red_bytes(CK)>::TOTAL;
+  const void* fn = reinterpret_cast<const void*>(tg_kernel<BN, BK, ST, Prob, CK>);
+  ensure_smem_attr(fn, smem);
   const Tiles tiles{(int)grid.x, (int)grid.y, (int)grid.z};
   const int64_t nt = (int64_t)grid.x * grid.y * grid.z;
-  const unsigned ctas = (unsigned)std::min<int64_t>(nt, kNumSMs);
+  const int64_t slots = CK > 1 ? max_active_clusters(fn, smem, CK, kThreads2) : kNumSMs;
+  const unsigned ctas = (unsigned)(std::min<int64_t>(nt, std::max<int64_t>(slots, 1)) * CK);
+  if (std::getenv("DPG_TG_VERBOSE"))
+    std::fprintf(stderr, "tg launch BN=%d BK=%d ST=%d CK=%d tiles=%lld slots=%lld ctas=%u smem=%d\n", BN, BK, ST, CK,
+                 (long long)nt, (long long)slots, ctas, smem);
 #ifdef DPG_TG_TRACE
   {  // trace only the DPG_TG_TRACE_AT-th TMA-fed launch of the process
     const int at = std::getenv("DPG_TG_TRACE_AT") ? std::atoi(std::getenv("DPG_TG_TRACE_AT")) : -1;
-    const int on = trace_launch_count()++ == at ? 1 : 0;
+    const char* cta = std::getenv("DPG_TG_TRACE_CTA");  // the traced CTA (default 0)
+    const int on = trace_launch_count()++ == at ? 1 + (cta ? std::atoi(cta) : 0) : 0;
     cudaMemcpyToSymbolAsync(g_tg_trace_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
   }
 #endif
-  ::dpg::launch_pdl(tg_kernel<BN, BK, ST, Prob>, dim3(ctas), kThreads2, smem, ctx->stream, p, tiles);
+  if constexpr (CK == 1) {
+    ::dpg::launch_pdl(tg_kernel<BN, BK, ST, Prob>, dim3(ctas), kThreads2, smem, ctx->stream, p, tiles);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kThreads2);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CK;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    (void)cudaLaunchKernelEx(&cfg, tg_kernel<BN, BK, ST, Prob, CK>, p, tiles);
+  }
   DPG_LAUNCH_CHECK(ctx);
 }
 

@@ -86,6 +86,7 @@ class dpg_optimizer_config(ctypes.Structure):
 _SIGS = {
     "dpg_abi_version": (ctypes.c_int, []),
     "dpg_tg_gemm_selftest": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32]),
+    "dpg_tg_gemm_selftest_split": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32]),
     "dpg_noise_schedule_init": (_I32, [_P, _I32, _D, _D, _D, ctypes.c_uint64, _P, _I64]),
     "dpg_noise_schedule_sigma_at": (_D, [_P, ctypes.c_uint64]),
     "dpg_schedule_noise": (_I32, [_P, ctypes.c_uint64, _P, _P]),
@@ -106,6 +107,8 @@ _SIGS = {
     "dpg_ctx_kernel_launches": (_I64, [_P]),
     "dpg_ctx_set_profiling": (_I32, [_P, _I32]),
     "dpg_ctx_profile_read": (ctypes.c_char_p, [_P]),
+    "dpg_ctx_set_timeline": (_I32, [_P, _I32]),
+    "dpg_ctx_timeline_read": (ctypes.c_char_p, [_P]),
     "dpg_nccl_unique_id": (_I32, [ctypes.c_char_p]),
     "dpg_ctx_init_comm": (_I32, [_P, _I32, _I32, ctypes.c_char_p]),
     "dpg_allreduce_sum": (_I32, [_P, _P, _I64]),
@@ -262,6 +265,19 @@ class Context:
             name, ms, cnt, by, fl, kern, seq = line.split()
             out[name] = {"ms": float(ms), "count": int(cnt), "bytes": float(by), "flops": float(fl),
                          "kernels": int(kern), "seq": int(seq)}
+        return out
+
+    def set_timeline(self, on: bool):
+        """Record the stage scopes of steps captured from now on as graph event nodes."""
+        _check(lib().dpg_ctx_set_timeline(self.h, int(on)), self.h)
+
+    def timeline(self):
+        """[(stage, start_ms, duration_ms, kernels)] of the last replay, in capture order."""
+        txt = lib().dpg_ctx_timeline_read(self.h).decode()
+        out = []
+        for line in txt.strip().splitlines():
+            name, t0, dt, kern = line.split()
+            out.append((name, float(t0), float(dt), int(kern)))
         return out
 
     def init_comm(self, nranks: int, rank: int, uid: bytes):
@@ -648,6 +664,15 @@ def tg_gemm_selftest(ctx: Context, a: torch.Tensor, b: torch.Tensor, bn: int = 6
     n = b.shape[1] if bk < 0 else b.shape[0]  # bk < 0: b is B transposed, [k][n]
     d = torch.empty(m, n, device=a.device, dtype=torch.float32)
     _check(lib().dpg_tg_gemm_selftest(ctx.h, _p(a), _p(b), _p(d), m, n, k, bn, bk), ctx.h)
+    return d
+
+
+def tg_gemm_selftest_split(ctx: Context, a: torch.Tensor, b: torch.Tensor, bn: int = 64, ck: int = 2) -> torch.Tensor:
+    """D = A B^T with the K blocks split over a cluster of ck CTAs (dpg_tg_gemm_selftest_split)."""
+    m, k = a.shape
+    n = b.shape[0]
+    d = torch.empty(m, n, device=a.device, dtype=torch.float32)
+    _check(lib().dpg_tg_gemm_selftest_split(ctx.h, _p(a), _p(b), _p(d), m, n, k, bn, ck), ctx.h)
     return d
 
 

@@ -35,3 +35,28 @@ def test_tg_gemm_matches_fp64(ctx, m, n, k, bn, bk):
     assert err < 1e-5, f"max-scaled error {err:.3e}"
     # and no bias: mean signed error tiny relative to the spread
     assert abs((got - ref).mean()) < 1e-6 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("m,n,k,bn,ck", [
+    (256, 64, 288, 64, 2), (300, 64, 576, 64, 4), (128, 32, 64, 32, 2),
+    # fewer K blocks (3) than cluster ranks: one rank contributes an empty accumulator
+    (1000, 64, 96, 64, 4),
+    # more tiles than co-resident clusters: the reduction buffers cycle through several phases
+    (25600, 64, 576, 64, 2), (25600, 32, 256, 32, 4)])
+def test_tg_gemm_cluster_split_k(ctx, m, n, k, bn, ck):
+    """K blocks split over a thread-block cluster, partials summed through distributed shared
+    memory in rank order (tg_gemm.cuh): fp64 parity and bitwise determinism across runs."""
+    import torch
+    from paper_2109_12298_b200 import dpg
+    rng = np.random.default_rng(7 * m + n + k + ck)
+    a = rng.standard_normal((m, k)).astype(np.float32)
+    b = rng.standard_normal((n, k)).astype(np.float32)
+    at, bt = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    d = dpg.tg_gemm_selftest_split(ctx, at, bt, bn, ck)
+    d2 = dpg.tg_gemm_selftest_split(ctx, at, bt, bn, ck)
+    ctx.sync()
+    ref = a.astype(np.float64) @ b.astype(np.float64).T
+    got = d.cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < 1e-5, f"max-scaled error {err:.3e}"
+    assert torch.equal(d, d2), "split-K result differs between runs"

@@ -31,11 +31,12 @@ xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
 o.train_step(xt, yt, use_graph=False)
 ctx.sync()
 lib = dpg.lib()
-buf = (ctypes.c_ulonglong * (8 * 256))()
+buf = (ctypes.c_ulonglong * (10 * 256))()
 lib.dpg_tg_trace_read(buf)
-tr = np.frombuffer(buf, dtype=np.uint64).reshape(8, 256).astype(np.int64)
+tr = np.frombuffer(buf, dtype=np.uint64).reshape(10, 256).astype(np.int64)
 t0 = tr[0, 0]
-print(f"launch {os.environ.get('DPG_TG_TRACE_AT')}; it: issue landed converted mma_start (ns)")
+print(f"launch {os.environ.get('DPG_TG_TRACE_AT')} cta {os.environ.get('DPG_TG_TRACE_CTA', '0')} "
+      f"(t0 = {t0 % 10**9} ns); it: issue landed converted mma_start (ns)")
 for i in range(256):
     if tr[0, i] == 0 or (i > 0 and tr[0, i] < t0):
         break
@@ -43,5 +44,7 @@ for i in range(256):
 for j in range(4):
     if tr[4, j] > 0:
         print(f"tile {j}: tfull {tr[4, j] - t0} epi_done {tr[5, j] - t0}")
-        print("   chunks (loaded, stored):", [(int(tr[6, j * 8 + c] - t0), int(tr[7, j * 8 + c] - t0))
-                                            for c in range(8) if tr[6, j * 8 + c] > 0])
+        print("   chunks (loaded, split-K exchange, stored):",
+              [(int(tr[6, j * 8 + c] - t0), int(tr[8, j * 8 + c] - t0) if tr[8, j * 8 + c] > 0 else None,
+                int(tr[7, j * 8 + c] - t0) if tr[7, j * 8 + c] >= t0 else None)
+               for c in range(8) if tr[6, j * 8 + c] > 0])
