@@ -197,6 +197,9 @@ void conv_fwd_nhwc(dpg_ctx* ctx, const float* xh, const float* wf, const float* 
 void conv_dgrad_nhwc(dpg_ctx* ctx, const float* hh, const float* wd, const ConvGeom& g, const float* mask_h,
                      float* dx, float* dxh);
 void prep_weights(dpg_ctx* ctx, const TgPrepItems& items);
+// per-sample gradient + norm partials (3 rows) of a 3x3, 32-input-channel conv weight
+bool rule_nhwc_ok(const ConvGeom& g);
+void conv_rule_nhwc(dpg_ctx* ctx, const float* xh, const float* hw, const ConvGeom& g, float* gw, double* sq);
 // clipped sum of a conv weight: MN-major NHWC input tiles, s ⊙ highway rows in TMEM
 bool csum_nhwc_ok(const ConvGeom& g);
 int csum_nhwc_splits(const ConvGeom& g);
@@ -245,14 +248,15 @@ void gs(dpg_ctx* ctx, const float* x, int relu, const float* hw, const ConvGeom&
 
 // rules.cu — per-sample gradients
 int sq_rows_linear(int64_t mid, int64_t d, int64_t r);
-int sq_rows_conv2d(const ConvGeom& g);
+int sq_rows_conv2d(const ConvGeom& g, bool nhwc_rule = false);
 int sq_rows_embedding(int64_t vocab, int64_t dim);
 void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw, int64_t b,
                       int64_t mid, int64_t d, int64_t r, float* gw, double* sq_part);
 // gb / sq_b (optional): the bias rule fused into the same launch when gs_conv2d_fuses_bias(g)
 // (sq_b then has sq_rows_conv2d_bias(g) rows), else a separate bias launch (one row)
 void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& g,
-                      float* gw, double* sq_part, float* gb = nullptr, double* sq_b = nullptr, bool hw_nhwc = false);
+                      float* gw, double* sq_part, float* gb = nullptr, double* sq_b = nullptr, bool hw_nhwc = false,
+                      const float* xh = nullptr);
 bool gs_conv2d_fuses_bias(const ConvGeom& g);
 int sq_rows_conv2d_bias(const ConvGeom& g);
 // bias rule: gb[n,o] = sum over middle of hw; `hw_layout_conv` selects [b, o, P] vs [b, mid, o]

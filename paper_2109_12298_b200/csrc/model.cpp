@@ -62,6 +62,7 @@ struct LayerPlan {
   bool tg_dgrad = false;
   bool xh_by_prev = false, hh_by_next = false;
   bool tg_csum = false;  // clipped sum on the TMA core from xh (tg_conv.cu ConvCsumT)
+  bool tg_rule = false;  // per-sample rule on the TMA core from xh (tg_conv.cu ConvRuleT)
   // the highway lives only channels-last (hh): written by the next layer's TMA-fed dgrad, read by
   // this layer's thin-K rule / clipped sum (a first layer: no dgrad of its own reads it)
   bool hw_nhwc = false;
@@ -76,6 +77,13 @@ struct LayerPlan {
 // measured slower on the CIFAR step, DESIGN.md §6 negative results)
 bool tg_csum_enabled() {
   const char* e = std::getenv("DPG_TG_CSUM");
+  return e && e[0] == '1';
+}
+
+// DPG_TG_RULE=1: the 3x3 / 32-channel per-sample conv rule on the TMA-fed core (read when a model
+// is planned; opt-in: measured no faster than the register-gather rule)
+bool tg_rule_enabled() {
+  const char* e = std::getenv("DPG_TG_RULE");
   return e && e[0] == '1';
 }
 
@@ -466,7 +474,7 @@ void forward_backward_impl(dpg_optimizer* o, const float* x, const float* target
             break;
           }
           dpg::launch_gs_conv2d(ctx, in, lp.in_relu, lp.hw_nhwc ? lp.hh : hw, g, gw, sq_w, nullptr, nullptr,
-                                lp.hw_nhwc);
+                                lp.hw_nhwc, lp.tg_rule ? lp.xh : nullptr);
         }
         if (lp.nparams > 1) pending_bias = {g.P(), g.oc, 1};
         break;
@@ -914,6 +922,8 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
     }
     for (auto& lp : m->layers)
       lp.tg_csum = lp.tg_fwd == 1 && !lp.hw_nhwc && dpg::tg::csum_nhwc_ok(lp.g) && tg_csum_enabled();
+    for (auto& lp : m->layers)
+      lp.tg_rule = lp.tg_fwd == 1 && !lp.hw_nhwc && dpg::tg::rule_nhwc_ok(lp.g) && tg_rule_enabled();
     for (auto& lp : m->layers) {
       // every conv forward writes its consumer's NHWC copy in the epilogue
       if (lp.tg_fwd && lp.prev_param_layer >= 0) lp.xh_by_prev = m->layers[lp.prev_param_layer].kind == DPG_LAYER_CONV2D;
@@ -929,7 +939,7 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
         if (pi.is_bias && lp.kind == DPG_LAYER_CONV2D) r = dpg::sq_rows_conv2d_bias(lp.g);
         if (!pi.is_bias) {
           if (lp.kind == DPG_LAYER_LINEAR) r = dpg::sq_rows_linear(lp.mid, lp.d.in_features, lp.d.out_features);
-          else if (lp.kind == DPG_LAYER_CONV2D) r = dpg::sq_rows_conv2d(lp.g);
+          else if (lp.kind == DPG_LAYER_CONV2D) r = dpg::sq_rows_conv2d(lp.g, lp.tg_rule);
           else r = dpg::sq_rows_embedding(lp.d.vocab_size, lp.d.embedding_dim);
         }
         pi.sq_row0 = rows;

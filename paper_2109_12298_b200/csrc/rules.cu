@@ -80,7 +80,8 @@ void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const floa
 // Conv2d: G[n, oc, k] = sum_p B[n, oc, p] * X~[n, k, p], X~ = im2col(x) gathered on the fly
 // (layers.hpp:290-324 index map: k = (c*kh + ki)*kw + kj, p = oy*ow + ox).
 // ------------------------------------------------------------------------------------------
-int sq_rows_conv2d(const ConvGeom& g) {
+int sq_rows_conv2d(const ConvGeom& g, bool nhwc_rule) {
+  if (nhwc_rule) return 3;  // tg_conv.cu ConvRuleT: one partial per three-tap tile
   if (tk::supported(g)) return 1;
   if (rs::supported(g)) return rs::gs_rows(g);
   return tc::gs_conv_rows(g);
@@ -96,9 +97,15 @@ int sq_rows_conv2d_bias(const ConvGeom& g) {
 }
 
 void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw, const ConvGeom& g,
-                      float* gw, double* sq_part, float* gb, double* sq_b, bool hw_nhwc) {
+                      float* gw, double* sq_part, float* gb, double* sq_b, bool hw_nhwc, const float* xh) {
   if (g.b == 0) return;
   const bool bias = gb || sq_b;
+  if (xh) {  // the layer input's NHWC copy exists: the TMA-fed core (tg_conv.cu ConvRuleT)
+    if (hw_nhwc || !tg::rule_nhwc_ok(g)) raise(DPG_ERR_INTERNAL, "NHWC conv rule: unsupported geometry");
+    if (bias) launch_gs_bias(ctx, hw, g.b, g.P(), g.oc, true, gb, sq_b);
+    tg::conv_rule_nhwc(ctx, xh, hw, g, gw, sq_part);
+    return;
+  }
   if (tk::supported(g)) {
     tk::gs(ctx, x, x_relu, hw, g, gw, sq_part, gb, sq_b, hw_nhwc);
     return;

@@ -388,6 +388,71 @@ struct ConvCsumT {
   __device__ void finish(int, int, int, double) const {}
 };
 
+// ---- per-sample gradient of a 3x3 conv weight with 32 input channels (grad_sample.hpp conv2d
+// rule: G_n[o][c kk + t] = sum_p B[n, o, p] X~[n, p, (t, c)], layers.hpp:290-324 k order), its
+// squared norm (clip_and_sum pass 1) and the materialised record:
+// one sample per tile group — three tiles of three taps x 32 channels (N = 96, MN-major NHWC
+// input boxes as in ConvCsumT) and the sample's highway rows as the A operand (M = output
+// channels). A CTA keeps the three tiles of a sample (blocked schedule) and stages their
+// columns in the reference's k order in shared memory (row pitch K + 1: conflict-free), then
+// writes the sample's [O][K] record contiguously; the norm is one partial per tile.
+template <int BK>
+struct ConvRuleT {
+  static constexpr int BN = 96, G = 3, NTN = 3, KK = 9, C = 32, K = C * KK, KP = K + 1, OMAX = 64;
+  static constexpr bool kScaleA = false, kBPreSplit = false, kCtaReduce = true, kBMajorMN = true;
+  static constexpr int kStaging = 0, kEpiIn = 0;
+  static constexpr int kTileStg = OMAX * KP * 4, kTileBlock = NTN;
+  CUtensorMap ma, mb;
+  int b, O, kw, s, pad, OW, kpb;
+  uint32_t bytes;
+  float* gw;      // record [b][O][K] or null (norms only)
+  double* sq;     // norm partials [NTN][b]
+  __device__ int a_rows() const { return O; }
+  __device__ int nkb(int) const { return kpb; }
+  __device__ uint32_t stage_bytes() const { return bytes; }
+  __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t, uint32_t bar, int, int nt, int n) const {
+    tma3(sa, &ma, bar, kb * BK, 0, n);  // B[n, 0 .. O, p0 .. p0 + BK)
+    const int rows = BK / OW;
+#pragma unroll
+    for (int tl = 0; tl < G; ++tl) {
+      const int t = nt * G + tl, ki = t / kw, kj = t - ki * kw;
+      tma4(sb + tl * (BK * 128), &mb, bar, 0, kj - pad, kb * rows * s - pad + ki, n);
+    }
+  }
+  __device__ float scale(int, int, int, int) const { return 1.f; }
+  __device__ bool has_epi_in() const { return false; }
+  __device__ uint32_t epi_in_bytes() const { return 0; }
+  __device__ void epi_load(int, int, int, int, uint32_t, uint32_t) const {}
+  __device__ uint64_t pre_epilogue(int, int, int, int) const { return 0; }
+  static constexpr bool kEpiConst = false;
+  __device__ void epi_const(int, int, int, int, float*) const {}
+  __device__ void epilogue(int, int nt, int, int row, int c0, const float (&v)[16], double& acc, uint8_t* stg,
+                           const uint8_t*, uint64_t, const float*) const {
+    if (row >= O) return;
+    const int t = nt * G + c0 / C, cb = c0 % C;  // a chunk is 16 channels of one tap
+    float* dst = reinterpret_cast<float*>(stg) + row * KP + cb * KK + t;
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      dst[jj * KK] = v[jj];
+      acc += (double)v[jj] * (double)v[jj];
+    }
+  }
+  __device__ void epi_store(int, int, int, int, uint32_t) const {}
+  __device__ void finish(int, int nt, int n, double sum) const {
+    if (sq) sq[(int64_t)nt * b + n] = sum;
+  }
+  __device__ void tile_done(int, int nt, int n, int row, uint8_t* stg) const {
+    if (nt != NTN - 1 || !gw) return;
+    const float* src = reinterpret_cast<const float*>(stg);
+    float4* dst = reinterpret_cast<float4*>(gw + (int64_t)n * O * K);
+    for (int i4 = row; i4 < O * K / 4; i4 += 128) {  // K % 4 == 0: a float4 never straddles rows
+      const int o = (4 * i4) / K, k = 4 * i4 - o * K;
+      const float* s4 = src + o * KP + k;
+      dst[i4] = make_float4(s4[0], s4[1], s4[2], s4[3]);
+    }
+  }
+};
+
 // ---- helper kernels ----
 // per-step weight layouts of one conv layer, TF32-split: wf[h][o][(ki kw + kj) C + c] and
 // wd[h][((ki kw + kj) C + c) O + o], h = 0: rna_tf32(w), h = 1: rna_tf32(w - hi)
@@ -567,6 +632,33 @@ void conv_dgrad_nhwc(dpg_ctx* ctx, const float* hh, const float* wd, const ConvG
       else launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn>()>(ctx, p, grid);
     });
   });
+}
+
+// ---- per-sample gradient + norm of a conv weight on the core ----
+bool rule_nhwc_ok(const ConvGeom& g) {
+  const int64_t P = g.P();
+  return g.ic == 32 && g.kh == 3 && g.kw == 3 && g.oc <= 64 && P % 32 == 0 && 32 % g.ow == 0 &&
+         g.ow * g.stride <= 256 && (32 / g.ow) * g.stride <= 256;
+}
+
+void conv_rule_nhwc(dpg_ctx* ctx, const float* xh, const float* hw, const ConvGeom& g, float* gw, double* sq) {
+  constexpr int BK = 32;
+  using Pr = ConvRuleT<BK>;
+  const int b = (int)g.b, P = (int)g.P();
+  Pr p;
+  {  // A: highway NCHW [b][O][P], K-major rows of BK positions
+    const uint64_t dims[3] = {(uint64_t)P, (uint64_t)g.oc, (uint64_t)b};
+    const uint64_t str[2] = {(uint64_t)P * 4, (uint64_t)(g.oc * P * 4)};
+    const uint32_t box[3] = {(uint32_t)BK, (uint32_t)g.oc, 1};
+    p.ma = make_map(hw, 3, dims, str, box, nullptr, KLay<BK>::TMA_SWIZZLE);
+  }
+  p.mb = nhwc_map(xh, b, (int)g.h, (int)g.w, 32, 32, (int)g.ow, BK / (int)g.ow, 1, (int)g.stride,
+                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  p.b = b; p.O = (int)g.oc; p.kw = (int)g.kw; p.s = (int)g.stride; p.pad = (int)g.pad; p.OW = (int)g.ow;
+  p.kpb = P / BK;
+  p.bytes = (uint32_t)(((int)g.oc + Pr::BN) * BK * 4);
+  p.gw = gw; p.sq = sq;
+  launch<Pr::BN, BK, stages_for<Pr::BN, BK, 0, 0, Pr::kTileStg>()>(ctx, p, dim3(1, Pr::NTN, (unsigned)b));
 }
 
 // ---- clipped sum of a conv weight on the core ----

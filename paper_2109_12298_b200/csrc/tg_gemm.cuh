@@ -40,6 +40,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -226,6 +227,16 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
+// issue only: the registers are valid after tcgen05.wait::ld (tmem_ld_wait)
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -350,6 +361,23 @@ struct Tiles {
 //                                      row < 128, columns c0 .. c0+15
 //   void epi_store(int mt, int nt, int z, int c0, uint32_t stage) const;   one thread (kStaging)
 //   void finish(int mt, int nt, int z, double acc_sum) const;               (kCtaReduce)
+// Optional Prob members (default 0 when absent):
+//   static constexpr int kTileStg;     bytes of a per-CTA tile staging area: passed to epilogue() as
+//                                      `stage`, then tile_done(mt, nt, z, row, stage) runs on all 128
+//                                      epilogue threads after the tile's last chunk (between two
+//                                      epilogue barriers), e.g. to store a re-ordered tile coalesced
+//   static constexpr int kTileBlock;   > 0: blocked persistent schedule — CTA i walks a contiguous
+//                                      range of tiles whose bounds are multiples of kTileBlock, so a
+//                                      group of kTileBlock consecutive tiles stays on one CTA
+template <class P, class = void>
+struct TileStg : std::integral_constant<int, 0> {};
+template <class P>
+struct TileStg<P, std::void_t<decltype(P::kTileStg)>> : std::integral_constant<int, P::kTileStg> {};
+template <class P, class = void>
+struct TileBlock : std::integral_constant<int, 0> {};
+template <class P>
+struct TileBlock<P, std::void_t<decltype(P::kTileBlock)>> : std::integral_constant<int, P::kTileBlock> {};
+
 constexpr int kThreads2 = 320;
 //
 // Split-K over a thread-block cluster (CK > 1): the CK CTAs of a cluster own one tile at a time,
@@ -361,7 +389,9 @@ template <int BN, int BK, int ST, class Prob, int CK = 1>
 __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant__ Prob p, const Tiles tiles) {
   constexpr int STG = Prob::kStaging, EIN = Prob::kEpiIn;
   static_assert(CK == 1 || (EIN == 0 && !Prob::kCtaReduce), "cluster split-K: plain epilogues only");
-  using S = Smem<BN, BK, ST, STG, EIN, red_bytes(CK)>;
+  constexpr int TST = TileStg<Prob>::value, TBL = TileBlock<Prob>::value;
+  static_assert(TBL == 0 || CK == 1, "blocked tile schedule: no cluster split");
+  using S = Smem<BN, BK, ST, STG, EIN, red_bytes(CK) + TST>;
   using Lay = KLay<BK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
@@ -385,8 +415,15 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = tiles.count();
   const int crank = CK > 1 ? (int)cluster_rank() : 0;
-  const int t_first = CK > 1 ? (int)blockIdx.x / CK : (int)blockIdx.x;
-  const int t_step = CK > 1 ? (int)gridDim.x / CK : (int)gridDim.x;
+  int t_first = CK > 1 ? (int)blockIdx.x / CK : (int)blockIdx.x;
+  int t_step = CK > 1 ? (int)gridDim.x / CK : (int)gridDim.x;
+  int t_end = ntiles;
+  if constexpr (TBL > 0) {  // contiguous, kTileBlock-aligned range of tiles per CTA
+    const int groups = (ntiles + TBL - 1) / TBL;
+    t_first = (int)((int64_t)groups * blockIdx.x / gridDim.x) * TBL;
+    t_end = std::min(ntiles, (int)((int64_t)groups * (blockIdx.x + 1) / gridDim.x) * TBL);
+    t_step = 1;
+  }
   // this CTA's K blocks of a tile of slice z: [kb0, kb0 + nk)
   auto krange = [&](int z, int& kb0, int& nk) {
     const int n = p.nkb(z);
@@ -424,7 +461,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
-      for (int t = t_first; t < ntiles; t += t_step) {
+      for (int t = t_first; t < t_end; t += t_step) {
         int mt, nt, z;
         tiles.at(t, mt, nt, z);
         int kb0, nkb;
@@ -442,7 +479,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(BN, Prob::kBMajorMN);
       int it = 0, j = 0;
-      for (int t = t_first; t < ntiles; t += t_step, ++j) {
+      for (int t = t_first; t < t_end; t += t_step, ++j) {
         int mt, nt, z;
         tiles.at(t, mt, nt, z);
         int kb0, nkb;
@@ -485,7 +522,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
     const int r = 32 * q + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * q) << 16);
     int it = 0;
-    for (int t = t_first; t < ntiles; t += t_step) {
+    for (int t = t_first; t < t_end; t += t_step) {
       int mt, nt, z;
       tiles.at(t, mt, nt, z);
       int kb0, nkb;
@@ -538,7 +575,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
     const int row = 32 * q + lane;
     const bool leader = warp == 6 && lane == 0;
     int j = 0, g = 0;  // tile and chunk counters of this CTA
-    for (int t = t_first; t < ntiles; t += t_step, ++j) {
+    for (int t = t_first; t < t_end; t += t_step, ++j) {
       int mt, nt, z;
       tiles.at(t, mt, nt, z);
       int kb0, nkb;
@@ -558,9 +595,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
       if constexpr (Prob::kEpiConst) asm volatile("bar.sync 1, 128;" ::: "memory");  // constants written
       if (row == 0) tg_trace(4, j);
       tc_fence_after();
-      if (t + t_step >= ntiles) pdl_trigger();  // last tile: the next kernel may launch
+      if (t + t_step >= t_end) pdl_trigger();  // last tile: the next kernel may launch
       double acc = 0.0;
       float v[16];
+      uint32_t vn[16];  // the next chunk, in flight from TMEM while this one is processed
+      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16, ++g) {
         if (epi_in && leader && c0 + 16 < BN) {  // prefetch the next chunk's inputs
@@ -568,13 +607,17 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
           p.epi_load(mt, nt, z, c0 + 16, sbase + S::EIN_OFF + ((g + 1) & 1) * EIN, ein((g + 1) & 1));
         }
         if (nkb > 0) {
-          tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), v);
+          if (c0 == 0) tmem_ld16_async(trow, vn);
+          tmem_ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(vn[jj]);
+          if (c0 + 16 < BN) tmem_ld16_async(trow + (uint32_t)(c0 + 16), vn);
         } else {
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
         }
         if (row == 0) tg_trace(6, j * 8 + c0 / 16);
-        if (c0 + 16 >= BN) {  // every TMEM read of this buffer is done: release it to the MMA warp
+        if (c0 + 16 >= BN) {  // every TMEM read of this buffer is done (waited): release it
           tc_fence_before();
           mbar_arrive(tempty(a));
         }
@@ -616,7 +659,9 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
           mbar_wait(ein(g & 1), (g >> 1) & 1);
           in = smem + S::EIN_OFF + (g & 1) * EIN;
         }
-        uint8_t* stg = STG > 0 ? smem + S::STG_OFF + (g & 1) * STG : nullptr;
+        uint8_t* stg = STG > 0   ? smem + S::STG_OFF + (g & 1) * STG
+                       : TST > 0 ? smem + S::RED_OFF + red_bytes(CK)
+                                 : nullptr;
         p.epilogue(mt, nt, z, row, c0, v, acc, stg, in, pre, cst);
         if (STG > 0) {
           fence_proxy_async();
@@ -638,6 +683,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
         if (lane == 0) red[a][q] = acc;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (q == 0 && lane == 0) p.finish(mt, nt, z, red[a][0] + red[a][1] + red[a][2] + red[a][3]);
+      }
+      if constexpr (TST > 0) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // every chunk of the tile is staged
+        p.tile_done(mt, nt, z, row, smem + S::RED_OFF + red_bytes(CK));
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free for the next tile
       }
     }
     if ((STG > 0 || CK > 1) && leader) bulk_wait_all();
@@ -668,7 +718,7 @@ int max_active_clusters(const void* fn, int smem, int ck, int threads);
 // (CK > 1: min(tiles, co-resident clusters) clusters of CK CTAs)
 template <int BN, int BK, int ST, class Prob, int CK = 1>
 void launch(dpg_ctx* ctx, const Prob& p, dim3 grid) {
-  const int smem = Smem<BN, BK, ST, Prob::kStaging, Prob::kEpiIn, red_bytes(CK)>::TOTAL;
+  const int smem = Smem<BN, BK, ST, Prob::kStaging, Prob::kEpiIn, red_bytes(CK) + TileStg<Prob>::value>::TOTAL;
   const void* fn = reinterpret_cast<const void*>(tg_kernel<BN, BK, ST, Prob, CK>);
   ensure_smem_attr(fn, smem);
   const Tiles tiles{(int)grid.x, (int)grid.y, (int)grid.z};

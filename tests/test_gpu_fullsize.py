@@ -285,12 +285,13 @@ def test_cfg2_linear_t64_pipeline(ctx):
 
 
 @pytest.mark.parametrize("variant,env", [("ksplit_off", {"DPG_KSPLIT": "off"}), ("tg0", {"DPG_TG": "0"}),
-                                         ("tg_opt_in", {"DPG_TG_CK": "4", "DPG_TG_CSUM": "1"})])
+                                         ("tg_opt_in", {"DPG_TG_CK": "4", "DPG_TG_CSUM": "1", "DPG_TG_RULE": "1"})])
 def test_small_batch_steps_alternate_paths(variant, env):
     """The step suite re-run in a fresh process on the other dispatch paths: split-K disabled (the
     register-gather no-split forward / dgrad epilogues at small b), DPG_TG=0 (every convolution
     on the register-gather tcgen05 kernels instead of the TMA-fed core), and the TMA core's opt-in
-    paths (cluster split-K of the small-M convolutions, clipped sums on the core)."""
+    paths (cluster split-K of the small-M convolutions, clipped sums and the conv2 rule on the
+    core)."""
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_step.py"), "-k", "matches_oracle or virtual"],
                        env=dict(os.environ, **env), cwd=ROOT, capture_output=True, text=True, timeout=900)
