@@ -21,9 +21,99 @@ size_t conv_dgrad_ws_bytes(const ConvGeom& g) {
   return tc::dgrad_supported(g) ? tc::dgrad_ws_bytes(g) : 0;
 }
 
+// Thin first layers (K = ic kh kw <= KMAX, e.g. an RGB or greyscale image) on the CUDA cores: the
+// contraction is 27-64 deep, so a tensor-core tile would be mostly padding and the launch is
+// bound by its stores. Thread = output pixel: its K input values (zero padding, ReLU on load)
+// in registers, the transposed weights [k][oc] and the bias in shared memory (broadcast float4
+// reads), OC fp32 accumulators (bias first, then k ascending — layers.hpp:432-467's sum
+// order per output), then the NCHW output (one coalesced store per channel) and the consumer's
+// NHWC copy (OC contiguous floats per pixel, ReLU applied when relu_out).
+template <int OC, int IC, int KH, int KW>
+__global__ void __launch_bounds__(256) conv_fwd_thin_kernel(const float* __restrict__ x, int x_relu,
+                                                            const float* __restrict__ w,
+                                                            const float* __restrict__ bias, ConvGeom g,
+                                                            float* __restrict__ y, float* __restrict__ yh,
+                                                            int relu_out) {
+  constexpr int K = IC * KH * KW;
+  __shared__ __align__(16) float wt[K][OC];
+  __shared__ __align__(16) float bs[OC];
+  pdl_wait();
+  for (int i = threadIdx.x; i < OC * K; i += blockDim.x) {
+    const int o = i / K, k = i - o * K;
+    wt[k][o] = __ldg(w + i);
+  }
+  for (int i = threadIdx.x; i < OC; i += blockDim.x) bs[i] = bias ? __ldg(bias + i) : 0.f;
+  __syncthreads();
+  const int P = (int)(g.oh * g.ow), pblocks = (P + 255) / 256;
+  const int items = (int)g.b * pblocks;
+  // persistent: the weights are staged once per CTA, then (sample, 256-pixel block) items
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+  const int n = it / pblocks, p = (it - n * pblocks) * 256 + threadIdx.x;
+  if (p >= P) continue;
+  const int oy = p / (int)g.ow, ox = p - oy * (int)g.ow;
+  const int H = (int)g.h, W = (int)g.w;
+  const int iy0 = oy * (int)g.stride - (int)g.pad, ix0 = ox * (int)g.stride - (int)g.pad;
+  const float* xn = x + (int64_t)n * IC * H * W;
+  float in[K];
+#pragma unroll
+  for (int c = 0; c < IC; ++c)
+#pragma unroll
+    for (int ki = 0; ki < KH; ++ki)
+#pragma unroll
+      for (int kj = 0; kj < KW; ++kj) {
+        const int iy = iy0 + ki, ix = ix0 + kj;
+        const bool ok = iy >= 0 && iy < H && ix >= 0 && ix < W;
+        const float v = ok ? __ldg(xn + ((int64_t)c * H + iy) * W + ix) : 0.f;
+        in[(c * KH + ki) * KW + kj] = x_relu ? fmaxf(v, 0.f) : v;
+      }
+  float acc[OC];
+#pragma unroll
+  for (int o = 0; o < OC; o += 4) {
+    const float4 b4 = *reinterpret_cast<const float4*>(&bs[o]);
+    acc[o] = b4.x; acc[o + 1] = b4.y; acc[o + 2] = b4.z; acc[o + 3] = b4.w;
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int o = 0; o < OC; o += 4) {
+      const float4 w4 = *reinterpret_cast<const float4*>(&wt[k][o]);
+      acc[o] = fmaf(in[k], w4.x, acc[o]);
+      acc[o + 1] = fmaf(in[k], w4.y, acc[o + 1]);
+      acc[o + 2] = fmaf(in[k], w4.z, acc[o + 2]);
+      acc[o + 3] = fmaf(in[k], w4.w, acc[o + 3]);
+    }
+  float* yn = y + (int64_t)n * OC * P + p;
+#pragma unroll
+  for (int o = 0; o < OC; ++o) yn[(int64_t)o * P] = acc[o];
+  if (yh) {
+    float4* hp = reinterpret_cast<float4*>(yh + ((int64_t)n * P + p) * OC);
+#pragma unroll
+    for (int o = 0; o < OC; o += 4)
+      hp[o / 4] = make_float4(relu_if(acc[o], relu_out), relu_if(acc[o + 1], relu_out),
+                              relu_if(acc[o + 2], relu_out), relu_if(acc[o + 3], relu_out));
+  }
+  }
+}
+
+template <int OC, int IC, int KH, int KW>
+static void launch_fwd_thin(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
+                            const ConvGeom& g, float* y, float* yh, int relu_out) {
+  const int64_t items = g.b * ((g.P() + 255) / 256);
+  const unsigned grid = (unsigned)std::min<int64_t>(items, 2 * kNumSMs);
+  ::dpg::launch_pdl(conv_fwd_thin_kernel<OC, IC, KH, KW>, dim3(grid), 256, 0, ctx->stream, x, x_relu, w, bias, g,
+                    y, yh, relu_out);
+  DPG_LAUNCH_CHECK(ctx);
+}
+
 void launch_conv2d_fwd(dpg_ctx* ctx, const float* x, int x_relu, const float* w, const float* bias,
                        const ConvGeom& g, float* y, void* ws, float* yh, int relu_out) {
   if (g.b == 0) return;
+  if (g.b < 65536 && g.P() < (1 << 30)) {
+    if (g.oc == 32 && g.ic == 3 && g.kh == 3 && g.kw == 3)
+      return launch_fwd_thin<32, 3, 3, 3>(ctx, x, x_relu, w, bias, g, y, yh, relu_out);
+    if (g.oc == 16 && g.ic == 1 && g.kh == 8 && g.kw == 8)
+      return launch_fwd_thin<16, 1, 8, 8>(ctx, x, x_relu, w, bias, g, y, yh, relu_out);
+  }
   tc::conv_fwd(ctx, x, x_relu, w, bias, g, y, ws, yh, relu_out);
 }
 
