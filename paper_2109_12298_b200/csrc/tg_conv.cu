@@ -104,9 +104,16 @@ struct Gemm2D {
                            const uint8_t*, uint64_t, const float*) const {
     const int m = mt * BM + row;
     if (m >= M) return;
+    const int n0 = nt * BN + c0;
+    if (N % 4 == 0 && n0 + 16 <= N) {  // 16-byte stores
+      float4* dp = reinterpret_cast<float4*>(d + (int64_t)m * N + n0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dp[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const int n = nt * BN + c0 + j;
+      const int n = n0 + j;
       if (n < N) d[(int64_t)m * N + n] = v[j];
     }
   }
