@@ -124,11 +124,11 @@ struct Gemm2D {
 // launch with split-K over clusters of ck CTAs (1, 2 or 4)
 template <int BN, int BK, class Pr>
 void launch_ck(dpg_ctx* ctx, const Pr& p, dim3 grid, int ck) {
-  constexpr int STG = Pr::kStaging, EIN = Pr::kEpiIn;
+  constexpr int STG = Pr::kStaging, EIN = Pr::kEpiIn, AW = acc_width<Pr, BN>();
   switch (ck) {
-    case 4: launch<BN, BK, stages_for<BN, BK, STG, EIN, red_bytes(4)>(), Pr, 4>(ctx, p, grid); break;
-    case 2: launch<BN, BK, stages_for<BN, BK, STG, EIN, red_bytes(2)>(), Pr, 2>(ctx, p, grid); break;
-    default: launch<BN, BK, stages_for<BN, BK, STG, EIN>(), Pr, 1>(ctx, p, grid); break;
+    case 4: launch<BN, BK, stages_for<BN, BK, STG, EIN, red_bytes(4), AW>(), Pr, 4>(ctx, p, grid); break;
+    case 2: launch<BN, BK, stages_for<BN, BK, STG, EIN, red_bytes(2), AW>(), Pr, 2>(ctx, p, grid); break;
+    default: launch<BN, BK, stages_for<BN, BK, STG, EIN, 0, AW>(), Pr, 1>(ctx, p, grid); break;
   }
 }
 
@@ -605,7 +605,7 @@ void conv_fwd_nhwc(dpg_ctx* ctx, const float* xh, const float* wf, const float* 
       p.bias = bias;
       const dim3 grid((unsigned)mtiles, (unsigned)((g.oc + BN - 1) / BN), 1);
       if constexpr (BN <= 64) launch_ck<BN, BK>(ctx, p, grid, ck);
-      else launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn>()>(ctx, p, grid);
+      else launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn, 0, acc_width<Pr, BN>()>()>(ctx, p, grid);
     });
   });
 }
@@ -636,7 +636,7 @@ void conv_dgrad_nhwc(dpg_ctx* ctx, const float* hh, const float* wd, const ConvG
       p.dx = dx;
       const dim3 grid((unsigned)mtiles, (unsigned)((g.ic + BN - 1) / BN), (unsigned)(s * s));
       if constexpr (BN <= 64) launch_ck<BN, BK>(ctx, p, grid, ck);
-      else launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn>()>(ctx, p, grid);
+      else launch<BN, BK, stages_for<BN, BK, Pr::kStaging, Pr::kEpiIn, 0, acc_width<Pr, BN>()>()>(ctx, p, grid);
     });
   });
 }

@@ -300,19 +300,33 @@ struct Smem {
   static constexpr int TOTAL = BAR_OFF + BARS + 16 + 1024;  // + alignment slack
 };
 
-// TMEM: two accumulator buffers of BN columns, then per stage A_hi and A_lo (BK columns each)
-template <int BN, int BK>
+// TMEM: two accumulator buffers of AW columns (AW = BN, or 2 BN with paired B below), then per
+// stage A_hi and A_lo (BK columns each)
+template <int AW, int BK>
 constexpr int tmem_stage_cap() {
-  return (512 - 2 * BN) / (2 * BK);
+  return (512 - 2 * AW) / (2 * BK);
 }
 // deepest ring (<= 6 stages) that fits the 227 KB a CTA may use and the 512 TMEM columns
-template <int BN, int BK, int STG = 0, int EIN = 0, int RED = 0>
+template <int BN, int BK, int STG = 0, int EIN = 0, int RED = 0, int AW = BN>
 constexpr int stages_for() {
   constexpr int st = Smem<BN, BK, 1, STG, EIN>::STAGE;
   constexpr int fixed = 2 * STG + 2 * EIN + RED + 2048 + 4096;
   constexpr int lim = 227 * 1024 - fixed;
   constexpr int by_smem = (6 * st <= lim) ? 6 : (5 * st <= lim) ? 5 : (4 * st <= lim) ? 4 : (3 * st <= lim) ? 3 : 2;
-  return by_smem < tmem_stage_cap<BN, BK>() ? by_smem : tmem_stage_cap<BN, BK>();
+  return by_smem < tmem_stage_cap<AW, BK>() ? by_smem : tmem_stage_cap<AW, BK>();
+}
+// Paired B (pre-split operands): B_hi and B_lo land as adjacent row blocks, so one MMA of N = 2 BN
+// computes A_hi B_hi (columns [0, BN)) and A_hi B_lo ([BN, 2 BN)) and a second of N = BN adds
+// A_lo B_hi into [0, BN): two MMAs per K = 8 slice instead of three. An M = 128 MMA costs the same
+// 52 cycles for every N <= 64 (tools/micro/mma_rate.cu), so for the step's N = 32-64 tiles the
+// wider one is free. The epilogue adds the two column blocks.
+template <class Prob, int BN>
+constexpr bool pair_b() {
+  return Prob::kBPreSplit && !Prob::kBMajorMN && BN <= 64;  // 4 BN accumulator columns + A stages
+}
+template <class Prob, int BN>
+constexpr int acc_width() {
+  return pair_b<Prob, BN>() ? 2 * BN : BN;
 }
 constexpr uint32_t kTmemCols = 512;
 // split-K over a cluster of CK CTAs: two chunk buffers of [128 rows][16] fp32 per peer
@@ -410,7 +424,10 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
   auto sB = [&](int s) { return sbase + s * S::STAGE + S::A_BYTES; };
   auto sBlo = [&](int s) { return sbase + s * S::STAGE + S::A_BYTES + S::B_BYTES; };
   // TMEM columns of stage s's A_hi / A_lo (after the two accumulator buffers)
-  auto tA = [&](int s) { return (uint32_t)(2 * BN + s * 2 * BK); };
+  constexpr bool PAIR = pair_b<Prob, BN>();
+  constexpr int AW = acc_width<Prob, BN>();
+  static_assert(ST >= 2 && 2 * AW + ST * 2 * BK <= 512, "TMEM: accumulators + A stages exceed 512 columns");
+  auto tA = [&](int s) { return (uint32_t)(2 * AW + s * 2 * BK); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = tiles.count();
@@ -441,8 +458,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
       mbar_init(tfull(a), 1);
       mbar_init(tempty(a), kConvThreads);
       mbar_init(ein(a), 1);
-      mbar_init(red_full(a), CK - 1);  // one remote arrive per peer and chunk
-      mbar_init(red_empty(a), 1);      // one remote arrive from rank 0 per use
+      mbar_init(red_full(a), (CK - 1) * kConvThreads);  // every peer epilogue thread, per chunk
+      mbar_init(red_empty(a), kConvThreads);            // every rank-0 epilogue thread, per use
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -478,6 +495,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(BN, Prob::kBMajorMN);
+      constexpr uint32_t idesc2 = idesc_tf32(PAIR ? 2 * BN : BN, Prob::kBMajorMN);
       int it = 0, j = 0;
       for (int t = t_first; t < t_end; t += t_step, ++j) {
         int mt, nt, z;
@@ -487,7 +505,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
         const int a = j & 1;
         if (j >= 2) mbar_wait(tempty(a), ((j >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t acc = tmem + (uint32_t)(a * BN);
+        const uint32_t acc = tmem + (uint32_t)(a * AW);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % ST;
           mbar_wait(conv(s), (it / ST) & 1);
@@ -506,9 +524,14 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
               bhi = Lay::desc(sB(s) + off);
               blo = Lay::desc(sBlo(s) + off);
             }
-            mma_tf32_ts(acc, alo + kk * 8, bhi, idesc, acc0);
-            mma_tf32_ts(acc, ahi + kk * 8, blo, idesc, 1u);
-            mma_tf32_ts(acc, ahi + kk * 8, bhi, idesc, 1u);
+            if constexpr (PAIR) {  // [A_hi B_hi | A_hi B_lo], then A_lo B_hi into the first block
+              mma_tf32_ts(acc, ahi + kk * 8, bhi, idesc2, acc0);
+              mma_tf32_ts(acc, alo + kk * 8, bhi, idesc, 1u);
+            } else {
+              mma_tf32_ts(acc, alo + kk * 8, bhi, idesc, acc0);
+              mma_tf32_ts(acc, ahi + kk * 8, blo, idesc, 1u);
+              mma_tf32_ts(acc, ahi + kk * 8, bhi, idesc, 1u);
+            }
           }
           mma_commit(empty(s));
         }
@@ -599,7 +622,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
       double acc = 0.0;
       float v[16];
       uint32_t vn[16];  // the next chunk, in flight from TMEM while this one is processed
-      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN);
+      uint32_t vm[16];  // paired B: the A_hi B_lo block of the same columns
+      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * AW);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16, ++g) {
         if (epi_in && leader && c0 + 16 < BN) {  // prefetch the next chunk's inputs
@@ -607,11 +631,18 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
           p.epi_load(mt, nt, z, c0 + 16, sbase + S::EIN_OFF + ((g + 1) & 1) * EIN, ein((g + 1) & 1));
         }
         if (nkb > 0) {
-          if (c0 == 0) tmem_ld16_async(trow, vn);
+          if (c0 == 0) {
+            tmem_ld16_async(trow, vn);
+            if constexpr (PAIR) tmem_ld16_async(trow + (uint32_t)BN, vm);
+          }
           tmem_ld_wait();
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(vn[jj]);
-          if (c0 + 16 < BN) tmem_ld16_async(trow + (uint32_t)(c0 + 16), vn);
+          for (int jj = 0; jj < 16; ++jj)
+            v[jj] = PAIR ? __uint_as_float(vn[jj]) + __uint_as_float(vm[jj]) : __uint_as_float(vn[jj]);
+          if (c0 + 16 < BN) {
+            tmem_ld16_async(trow + (uint32_t)(c0 + 16), vn);
+            if constexpr (PAIR) tmem_ld16_async(trow + (uint32_t)(BN + c0 + 16), vm);
+          }
         } else {
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
@@ -630,8 +661,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
             float4* st4 = reinterpret_cast<float4*>(smem + (send - sbase));
 #pragma unroll
             for (int c = 0; c < 4; ++c) st4[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (leader) mbar_arrive_remote(mapa(red_full(bb), 0));
+            mbar_arrive_remote(mapa(red_full(bb), 0));  // per thread: releases its own row
             if (row == 0) tg_trace(8, j * 8 + c0 / 16);
             continue;  // the epilogue is rank 0's
           }
@@ -649,10 +679,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
               v[4 * c] += w[r - 1][c].x; v[4 * c + 1] += w[r - 1][c].y;
               v[4 * c + 2] += w[r - 1][c].z; v[4 * c + 3] += w[r - 1][c].w;
             }
-          asm volatile("bar.sync 1, 128;" ::: "memory");  // every row read: the peers may refill
-          if (leader)
 #pragma unroll
-            for (int r = 1; r < CK; ++r) mbar_arrive_remote(mapa(red_empty(bb), (uint32_t)r));
+          for (int r = 1; r < CK; ++r) mbar_arrive_remote(mapa(red_empty(bb), (uint32_t)r));  // row read
         }
         const uint8_t* in = nullptr;
         if (epi_in) {
