@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for k in 5 6; do
-DPG_LIB=libdpg_trace.so DPG_TG_TRACE_AT=$k timeout 120 python tools/tg_trace_step.py 2>&1 | tail -22
+for c in 0 100; do
+DPG_TG_RESB=1 DPG_LIB=libdpg_trace.so DPG_TG_TRACE_AT=5 DPG_TG_TRACE_CTA=$c timeout 120 python tools/tg_trace_step.py 2>&1 | tail -46
 done
