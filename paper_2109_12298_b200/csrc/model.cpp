@@ -603,7 +603,31 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
     }
   }
   const int record_stream = (int)(std::min_element(load, load + 3) - load);
+  // record-based clipped sums (biases, normalisation affines, small weights): weighted column sums
+  // of the per-sample records, all in one launch
+  auto record_sums = [&] {
+    if (!o->cfg.clipped_sum_from_record) {
+      on_branch(m, record_stream < dpg_model::kAux ? record_stream : -1, [&] {
+        dpg::WsumItems items{};
+        double bytes = 0;
+        for (auto& pi : m->params) {
+          if (!from_record[&pi - &m->params[0]]) continue;
+          if (items.count == 16) {
+            dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+            items.count = 0;
+          }
+          items.item[items.count++] = {gs_ptr(o, (int)(&pi - &m->params[0]), b), o->summed + pi.offset, pi.numel};
+          bytes += 4.0 * (b * pi.numel + 2 * pi.numel);
+        }
+        dpg::ProfScope ps(ctx, "csum.record[all]", bytes, 0.0);
+        dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
+      });
+    }
+  };
+  // pass 0 forks the branches' launches, pass 1 enqueues the caller's stream's: a fork waits for
+  // everything already on the caller's stream, so its long sums must come last
   int rr_branch = 0;
+  for (int pass = 0; pass < 2; ++pass) {
   for (size_t l = 0; l < m->layers.size(); ++l) {
     LayerPlan& lp = m->layers[l];
     if (lp.param0 < 0) continue;
@@ -615,6 +639,7 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       const std::string ls = "[" + std::to_string(l) + "]";
       if (from_record[p] && !o->cfg.clipped_sum_from_record) continue;  // done above
       if (o->cfg.clipped_sum_from_record) {
+        if (pass == 1) continue;
         // the reference's pass 2 over the stored per-sample gradients (exact order), one launch
         // per parameter, round-robin over the three streams
         on_branch(m, (rr_branch % 3) < dpg_model::kAux ? rr_branch % 3 : -1, [&] {
@@ -630,6 +655,7 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       const double cio = 4.0 * (b * (lp.in_numel + lp.out_numel) + 2 * pi.numel);
       void* ws = m->csum_ws[l];
       const int br = stream_of[l];
+      if ((br < dpg_model::kAux) != (pass == 0)) continue;
       on_branch(m, br < dpg_model::kAux ? br : -1, [&] {
       switch (lp.kind) {
         case DPG_LAYER_LINEAR: {
@@ -659,25 +685,9 @@ void fold_impl(dpg_optimizer* o, int64_t b, const float* x) {
       });
     }
   }
-  // record-based clipped sums (biases, normalisation affines, small weights): weighted column sums
-  // of the per-sample records, all in one launch
-  if (!o->cfg.clipped_sum_from_record) {
-    on_branch(m, record_stream < dpg_model::kAux ? record_stream : -1, [&] {
-      dpg::WsumItems items{};
-      double bytes = 0;
-      for (auto& pi : m->params) {
-        if (!from_record[&pi - &m->params[0]]) continue;
-        if (items.count == 16) {
-          dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
-          items.count = 0;
-        }
-        items.item[items.count++] = {gs_ptr(o, (int)(&pi - &m->params[0]), b), o->summed + pi.offset, pi.numel};
-        bytes += 4.0 * (b * pi.numel + 2 * pi.numel);
-      }
-      dpg::ProfScope ps(ctx, "csum.record[all]", bytes, 0.0);
-      dpg::launch_wsum_multi(ctx, items, o->scale, b, accumulate);
-    });
+  if (pass == 0 && record_stream < dpg_model::kAux) record_sums();
   }
+  if (record_stream >= dpg_model::kAux) record_sums();
   join_branches(m);
   o->has_summed = true;
   o->accumulated += b;
