@@ -333,3 +333,37 @@ def test_nccl_allreduce_in_captured_step(ctx):
     c2.allreduce_sum(buf)
     c2.sync()
     assert torch.equal(buf, torch.arange(10, dtype=torch.float32, device="cuda"))
+
+
+def test_graph_timeline_records_every_stage_and_keeps_the_result():
+    """dpg_ctx_set_timeline: the stage scopes of a captured step become event nodes; a replay
+    yields a start / duration per stage (non-negative, inside the step, branches overlapping the
+    main chain) and the step's result is bit-identical to the graph without the nodes."""
+    import torch
+    from paper_2109_12298_b200 import dpg
+    b = 32
+    results = []
+    for timeline in (False, True):
+        ctx = dpg.Context(0)
+        ctx.set_timeline(timeline)
+        w, params, x, y, m, o, cfg = _setup(ctx, "cifar_b512", b, noise_multiplier=1.0)
+        xt, yt = _t(x), _t(y)
+        for _ in range(3):
+            o.train_step(xt, yt, use_graph=True)
+        ctx.sync()
+        results.append(m.store_params())
+        if timeline:
+            tl = ctx.timeline()
+            names = [r[0] for r in tl]
+            for stage in ("fwd.conv2d[0]", "dgrad.conv2d[2]", "gs.conv2d[2]", "clip_factors",
+                          "csum.conv2d[2]", "noise_update"):
+                assert stage in names, (stage, names)
+            assert all(t0 >= 0.0 and dt >= 0.0 for _, t0, dt, _ in tl)
+            span = max(t0 + dt for _, t0, dt, _ in tl)
+            assert 0.0 < span < 50.0, span  # ms
+            by = {r[0]: r for r in tl}
+            # causal order on the main chain; a rule branch overlaps the dgrad chain
+            assert by["clip_factors"][1] >= by["fwd.conv2d[0]"][1] + by["fwd.conv2d[0]"][2]
+            assert by["noise_update"][1] >= by["clip_factors"][1]
+            assert by["gs.conv2d[4]"][1] < by["dgrad.conv2d[2]"][1] + by["dgrad.conv2d[2]"][2]
+    assert np.array_equal(results[0], results[1]), "timeline nodes must not change the step"
