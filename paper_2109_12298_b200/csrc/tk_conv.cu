@@ -8,7 +8,8 @@
 // — summed over P positions: the tensor-core pipeline's per-stage cost (gather + hi/lo split +
 // smem stores for 16 K) buys ~1/4 useful rows, so the rule and the clipped sum run as direct
 // contractions from shared memory instead (measured, CIFAR conv1 b=512: rule + bias rule
-// 28 + 12 -> 31 us, clipped sum 52 -> 34 us). The forward stays on tcgen05 (20 us vs 27 us). One CTA
+// 28 + 12 -> 31 us, clipped sum 52 -> 34 us); the forward runs on CUDA cores too (layers.cu
+// conv_fwd_thin_kernel, compile-time shaped: 30 -> 23 us against the register-gather tcgen05 kernel). One CTA
 // stages one sample's zero-padded image (ReLU applied) once; every im2col element is then a
 // shared-memory read at (window origin of p) + (tap offset of k), no bounds checks.
 //
