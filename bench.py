@@ -776,6 +776,27 @@ def main():
                          "floor_ms_full": full / (hbm * 1e6)},
                 "stages_ms": {k: round(v["ms"], 5) for k, v in sorted(stages.items(), key=lambda kv: -kv[1]["ms"])},
                 "eager_stage_sum_ms": eager_step_ms}
+    # graph-time stage durations: the same step captured with event-record nodes around every
+    # stage (dpg_ctx_set_timeline), replayed, each stage's duration as it overlaps in the graph
+    if world == 1:
+        tctx = dpg.Context(local)
+        tctx.set_timeline(True)
+        tm = dpg.Model(tctx, w.layers, w.in_shape, max_batch=b)
+        tm.load_params(params)
+        to = dpg.DpOptimizer(tm, noise_multiplier=args.sigma, max_grad_norm=args.max_grad_norm,
+                             learning_rate=0.1, expected_batch_size=float(gb), noise_seed=3,
+                             materialise_grad_sample=materialise)
+        for _ in range(5):
+            to.train_step(xt, yt, loss)
+        tl = tctx.timeline()
+        span = max(t0 + dt for _, t0, dt, _ in tl) if tl else 0.0
+        roofline["graph_stages_ms"] = {nm: round(dt, 5) for nm, t0, dt, _ in sorted(tl, key=lambda r: -r[2])}
+        roofline["graph_timeline"] = {
+            "span_ms": round(span, 5),
+            "note": "one replay with an event-record node around every stage (PDL edges split at "
+                    "stage boundaries, so the span exceeds ms_per_step); durations include the "
+                    "overlap with concurrent branches; profiles/r02_timeline_cifar_b512.txt charts it"}
+        del to, tm, tctx
 
     # ---- strong scaling, BASELINE configs[4]: global batch 4096 split over the ranks ----
     strong = None
