@@ -215,7 +215,9 @@ void launch_wsum_multi(dpg_ctx* ctx, const WsumItems& items, const float* scale,
 // Linear weight, mid > 1: split-K GEMM over (n, t).
 size_t clipped_sum_ws_linear(int64_t b, int64_t mid, int64_t d, int64_t r) {
   if (mid == 1) return 0;
-  return sizeof(float) * (size_t)tc::csum_linear_splits(b, mid, d, r) * (size_t)(r * d);
+  int splits = tc::csum_linear_splits(b, mid, d, r);
+  if (tg::lin_shape_ok(b, mid, d, r)) splits = std::max(splits, tg::lin_csum_splits(b, mid, d, r));
+  return sizeof(float) * (size_t)splits * (size_t)(r * d);
 }
 
 void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const float* hw,
@@ -227,6 +229,12 @@ void launch_clipped_sum_linear(dpg_ctx* ctx, const float* acts, int acts_relu, c
     OuterV v{acts, hw, d, r, acts_relu};
     ::dpg::launch_pdl(wsum_outer_kernel, (unsigned)((r * d + 31) / 32), 32 * kColWarps, 0, ctx->stream, v, scale, b, sw, accumulate);
     DPG_LAUNCH_CHECK(ctx);
+    return;
+  }
+  if (tg::lin_ok(acts, hw, ws, b, mid, d, r)) {  // TMA-fed core, partials [split][o][i] as below
+    const int splits = tg::lin_csum_splits(b, mid, d, r);
+    tg::lin_csum(ctx, acts, acts_relu, hw, scale, b, mid, d, r, static_cast<float*>(ws), splits);
+    launch_splitk_reduce(ctx, static_cast<float*>(ws), splits, r * d, sw, accumulate);
     return;
   }
   const int splits = tc::csum_linear_splits(b, mid, d, r);

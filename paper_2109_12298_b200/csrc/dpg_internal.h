@@ -206,6 +206,14 @@ int csum_nhwc_splits(const ConvGeom& g);
 void conv_csum_nhwc(dpg_ctx* ctx, const float* xh, const float* hw, const float* scale, const ConvGeom& g,
                     float* part, int splits);
 void nchw_to_nhwc(dpg_ctx* ctx, const float* src, int relu, int64_t b, int64_t C, int64_t P, float* dst);
+// T > 1 linear rule / clipped sum on the core (tg_linear.cu); DPG_TG=0 or DPG_TG_LIN=0: off
+bool lin_shape_ok(int64_t b, int64_t mid, int64_t d, int64_t r);
+bool lin_ok(const void* acts, const void* hw, const void* out, int64_t b, int64_t mid, int64_t d, int64_t r);
+void lin_rule(dpg_ctx* ctx, const float* acts, int relu, const float* hw, int64_t b, int64_t mid, int64_t d,
+              int64_t r, float* gw, double* sq_part);
+int lin_csum_splits(int64_t b, int64_t mid, int64_t d, int64_t r);
+void lin_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, const float* scale, int64_t b,
+              int64_t mid, int64_t d, int64_t r, float* part, int splits);
 }  // namespace tg
 
 namespace tc {

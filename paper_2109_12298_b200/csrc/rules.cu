@@ -73,6 +73,10 @@ void launch_gs_linear(dpg_ctx* ctx, const float* acts, int acts_relu, const floa
     DPG_LAUNCH_CHECK(ctx);
     return;
   }
+  if (tg::lin_ok(acts, hw, gw, b, mid, d, r)) {  // TMA-fed core (same norm-row order)
+    tg::lin_rule(ctx, acts, acts_relu, hw, b, mid, d, r, gw, sq_part);
+    return;
+  }
   tc::linear_gs(ctx, acts, acts_relu, hw, b, mid, d, r, gw, sq_part);
 }
 

@@ -50,7 +50,6 @@ namespace dpg {
 namespace tg {
 
 constexpr int BM = 128;          // UMMA M: TMEM lanes = tile rows
-constexpr int kConvThreads = 128;
 
 // Timeline trace of CTA 0 (tools/micro/tg_trace.cu builds with -DDPG_TG_TRACE): globaltimer
 // stamps per role and iteration into g_tg_trace[event][iteration].
@@ -391,8 +390,36 @@ template <class P, class = void>
 struct TileBlock : std::integral_constant<int, 0> {};
 template <class P>
 struct TileBlock<P, std::void_t<decltype(P::kTileBlock)>> : std::integral_constant<int, P::kTileBlock> {};
+//   static constexpr bool kAMajorMN;   A lands M-major: one unswizzled [BK K rows][BM] box (row pitch
+//                                      BM x 4 bytes); the converter thread of tile row r reads column r
+//                                      (a warp reads one 128-byte run per K row: conflict-free) and
+//                                      applies ReLU first when a_relu() (e.g. the T > 1 linear rule's
+//                                      [n][t][i] activations, i contiguous)
+//   static constexpr bool kCoopStore;  with kStaging: after the chunk is staged and the epilogue
+//                                      barrier, all 128 epilogue threads run coop_store(mt, nt, z,
+//                                      c0, row, stage) (e.g. 512-byte STG.128 runs) instead of the
+//                                      leader's TMA store
+template <class P, class = void>
+struct CoopStore : std::false_type {};
+template <class P>
+struct CoopStore<P, std::void_t<decltype(P::kCoopStore)>> : std::integral_constant<bool, P::kCoopStore> {};
+template <class P, class = void>
+struct AMajorMN : std::false_type {};
+template <class P>
+struct AMajorMN<P, std::void_t<decltype(P::kAMajorMN)>> : std::integral_constant<bool, P::kAMajorMN> {};
 
-constexpr int kThreads2 = 320;
+//   static constexpr int kConvWarps;   converter warps, 4 (default) or 8 (two per TMEM lane quarter,
+//                                      splitting the A columns; for operands both split on the fly)
+template <class P, class = void>
+struct ConvWarps : std::integral_constant<int, 4> {};
+template <class P>
+struct ConvWarps<P, std::void_t<decltype(P::kConvWarps)>> : std::integral_constant<int, P::kConvWarps> {};
+// producer + MMA warps, the converters, 4 epilogue warps
+template <class P>
+constexpr int threads_of() {
+  return 64 + 32 * ConvWarps<P>::value + 128;
+}
+constexpr int kEpiThreads = 128;
 //
 // Split-K over a thread-block cluster (CK > 1): the CK CTAs of a cluster own one tile at a time,
 // CTA rank r running K blocks [r nkb / CK, (r + 1) nkb / CK) into its own TMEM accumulator. Per
@@ -400,10 +427,12 @@ constexpr int kThreads2 = 320;
 // CTA's reduction buffer (st.shared::cluster, then a remote mbarrier arrive); rank 0 adds them in
 // rank order (deterministic), frees the buffer with a remote arrive per peer, and runs the epilogue.
 template <int BN, int BK, int ST, class Prob, int CK = 1>
-__global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant__ Prob p, const Tiles tiles) {
+__global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_constant__ Prob p, const Tiles tiles) {
   constexpr int STG = Prob::kStaging, EIN = Prob::kEpiIn;
   static_assert(CK == 1 || (EIN == 0 && !Prob::kCtaReduce), "cluster split-K: plain epilogues only");
   constexpr int TST = TileStg<Prob>::value, TBL = TileBlock<Prob>::value;
+  constexpr int CW = ConvWarps<Prob>::value, kCvt = 32 * CW;
+  static_assert(CW == 4 || CW == 8, "converter warps: 4 or 8");
   static_assert(TBL == 0 || CK == 1, "blocked tile schedule: no cluster split");
   using S = Smem<BN, BK, ST, STG, EIN, red_bytes(CK) + TST>;
   using Lay = KLay<BK>;
@@ -451,15 +480,15 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(conv(s), kConvThreads);
+      mbar_init(conv(s), kCvt);
       mbar_init(empty(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), kConvThreads);
+      mbar_init(tempty(a), kEpiThreads);
       mbar_init(ein(a), 1);
-      mbar_init(red_full(a), (CK - 1) * kConvThreads);  // every peer epilogue thread, per chunk
-      mbar_init(red_empty(a), kConvThreads);            // every rank-0 epilogue thread, per use
+      mbar_init(red_full(a), (CK - 1) * kEpiThreads);  // every peer epilogue thread, per chunk
+      mbar_init(red_empty(a), kEpiThreads);            // every rank-0 epilogue thread, per use
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -538,10 +567,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
         mma_commit(tfull(a));
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 2 + CW) {
     // converters. A: thread = row 32 (w % 4) + lane of the tile (its TMEM lane)
     const int tc = threadIdx.x - 64;
     const int q = warp & 3;
+    const int h0 = (warp - 2) >> 2;  // 8 converter warps: two per lane quarter, alternate 16-column halves
     const int r = 32 * q + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * q) << 16);
     int it = 0;
@@ -556,10 +586,28 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
         if (tc == 0) tg_trace(1, it);
         float sc = 1.f;
         if (Prob::kScaleA) sc = p.scale(kb0 + kb, mt, nt, z);
+        if constexpr (AMajorMN<Prob>::value) {  // [BK][BM] box: this thread's column r
+          const float* acol = reinterpret_cast<const float*>(smem + s * S::STAGE) + r;
+          const bool relu = p.a_relu();
+#pragma unroll
+          for (int h = h0; h < BK / 16; h += CW / 4) {
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              float e = acol[(16 * h + u) * BM];
+              if (relu) e = e > 0.f ? e : 0.f;
+              if (Prob::kScaleA) e *= sc;
+              hi[u] = rna_tf32(__float_as_uint(e));
+              lo[u] = rna_tf32(__float_as_uint(e - __uint_as_float(hi[u])));
+            }
+            tmem_st16(lane_addr + tA(s) + 16 * h, hi);
+            tmem_st16(lane_addr + tA(s) + BK + 16 * h, lo);
+          }
+        }
         const uint8_t* arow = smem + s * S::STAGE + r * Lay::ROW;
         const int sw = Lay::ROW == 128 ? (r & 7) : ((r >> 1) & 3);
 #pragma unroll
-        for (int h = 0; h < BK / 16; ++h) {  // 16 columns (4 chunks) at a time
+        for (int h = h0; h < (AMajorMN<Prob>::value ? 0 : BK / 16); h += CW / 4) {  // 16 columns (4 chunks) at a time
           uint32_t hi[16], lo[16];
           const bool zero_row = r >= p.a_rows();  // rows past the operand: zeros (no stale data)
 #pragma unroll
@@ -582,7 +630,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
         if (!Prob::kBPreSplit) {
           uint8_t* b = smem + s * S::STAGE + S::A_BYTES;
 #pragma unroll 4
-          for (int i = tc * 16; i < S::B_BYTES; i += kConvThreads * 16) split16<false>(b + i, b + S::B_BYTES + i, 1.f);
+          for (int i = tc * 16; i < S::B_BYTES; i += kCvt * 16) split16<false>(b + i, b + S::B_BYTES + i, 1.f);
           fence_proxy_async();
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -596,7 +644,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
     // outputs staged in shared memory go out as TMA bulk stores issued by one thread
     const int q = warp & 3;
     const int row = 32 * q + lane;
-    const bool leader = warp == 6 && lane == 0;
+    const bool leader = warp == 2 + CW && lane == 0;
     int j = 0, g = 0;  // tile and chunk counters of this CTA
     for (int t = t_first; t < t_end; t += t_step, ++j) {
       int mt, nt, z;
@@ -691,7 +739,12 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
                        : TST > 0 ? smem + S::RED_OFF + red_bytes(CK)
                                  : nullptr;
         p.epilogue(mt, nt, z, row, c0, v, acc, stg, in, pre, cst);
-        if (STG > 0) {
+        if constexpr (STG > 0 && CoopStore<Prob>::value) {
+          // the chunk is staged: every epilogue thread stores a slice of it; the same buffer is
+          // rewritten two chunks later, after the next chunk's barrier (its reads are done)
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          p.coop_store(mt, nt, z, c0, row, stg);
+        } else if (STG > 0) {
           fence_proxy_async();
           if (leader) bulk_wait_read<0>();  // the previous chunk's stores have read their buffer
           asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -718,7 +771,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tg_kernel(const __grid_constant_
         asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free for the next tile
       }
     }
-    if ((STG > 0 || CK > 1) && leader) bulk_wait_all();
+    if (((STG > 0 && !CoopStore<Prob>::value) || CK > 1) && leader) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -751,7 +804,7 @@ void launch(dpg_ctx* ctx, const Prob& p, dim3 grid) {
   ensure_smem_attr(fn, smem);
   const Tiles tiles{(int)grid.x, (int)grid.y, (int)grid.z};
   const int64_t nt = (int64_t)grid.x * grid.y * grid.z;
-  const int64_t slots = CK > 1 ? max_active_clusters(fn, smem, CK, kThreads2) : kNumSMs;
+  const int64_t slots = CK > 1 ? max_active_clusters(fn, smem, CK, threads_of<Prob>()) : kNumSMs;
   const unsigned ctas = (unsigned)(std::min<int64_t>(nt, std::max<int64_t>(slots, 1)) * CK);
   if (std::getenv("DPG_TG_VERBOSE"))
     std::fprintf(stderr, "tg launch BN=%d BK=%d ST=%d CK=%d tiles=%lld slots=%lld ctas=%u smem=%d\n", BN, BK, ST, CK,
@@ -766,11 +819,11 @@ void launch(dpg_ctx* ctx, const Prob& p, dim3 grid) {
   }
 #endif
   if constexpr (CK == 1) {
-    ::dpg::launch_pdl(tg_kernel<BN, BK, ST, Prob>, dim3(ctas), kThreads2, smem, ctx->stream, p, tiles);
+    ::dpg::launch_pdl(tg_kernel<BN, BK, ST, Prob>, dim3(ctas), threads_of<Prob>(), smem, ctx->stream, p, tiles);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ctas);
-    cfg.blockDim = dim3(kThreads2);
+    cfg.blockDim = dim3(threads_of<Prob>());
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
     cudaLaunchAttribute attr[2];
