@@ -142,8 +142,70 @@ __global__ void __launch_bounds__(32 * kColWarps) splitk_reduce_kernel(PartV v, 
   colsum_body(v, OneC{}, splits, n, (int64_t)blockIdx.x * 32, out, accumulate);
 }
 
+// Split-K partials, 16-byte columns: a CTA owns 128 x 4 consecutive columns (one float4 per lane);
+// its 8 warps take contiguous z ranges (kColBatch loads in flight per thread) and the warp partials
+// are added in warp order — deterministic, and 4x the bytes per load of colsum_body, which left
+// the wide reduces (e.g. 37 splits x 262,144 columns) latency-bound at ~1 TB/s.
+constexpr int kRed4Warps = 8;
+template <class OI>
+__global__ void __launch_bounds__(32 * kRed4Warps) splitk_reduce4_kernel(const float* __restrict__ part, int splits,
+                                                                         int64_t n, float* __restrict__ out,
+                                                                         int accumulate, OI oi) {
+  pdl_wait();
+  __shared__ float4 red[kRed4Warps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = ((int64_t)blockIdx.x * 32 + lane) * 4;
+  const int z0 = (int)((int64_t)splits * warp / kRed4Warps), z1 = (int)((int64_t)splits * (warp + 1) / kRed4Warps);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j < n) {
+    const float4* p = reinterpret_cast<const float4*>(part + j);
+    const int64_t zs = n / 4;
+    int z = z0;
+    for (; z + kColBatch <= z1; z += kColBatch) {
+      float4 v[kColBatch];
+#pragma unroll
+      for (int u = 0; u < kColBatch; ++u) v[u] = __ldg(p + (z + u) * zs);
+#pragma unroll
+      for (int u = 0; u < kColBatch; ++u) {
+        acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+      }
+    }
+    for (; z < z1; ++z) {
+      const float4 v = __ldg(p + z * zs);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && j < n) {
+    float4 t = red[0][lane];
+#pragma unroll
+    for (int w = 1; w < kRed4Warps; ++w) {
+      const float4 v = red[w][lane];
+      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+    }
+    const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t jo = oi(j + e);
+      out[jo] = accumulate ? out[jo] + tv[e] : tv[e];
+    }
+  }
+}
+
+template <class OI>
+static bool launch_splitk_reduce4(dpg_ctx* ctx, const float* part, int splits, int64_t n, float* out,
+                                  int accumulate, OI oi) {
+  if (n % 4 != 0 || (reinterpret_cast<uintptr_t>(part) & 15) != 0) return false;
+  ::dpg::launch_pdl(splitk_reduce4_kernel<OI>, (unsigned)((n / 4 + 31) / 32), 32 * kRed4Warps, 0, ctx->stream, part,
+                    splits, n, out, accumulate, oi);
+  DPG_LAUNCH_CHECK(ctx);
+  return true;
+}
+
 static void launch_splitk_reduce(dpg_ctx* ctx, const float* part, int splits, int64_t n, float* out,
                                  int accumulate) {
+  if (launch_splitk_reduce4(ctx, part, splits, n, out, accumulate, IdOut{})) return;
   ::dpg::launch_pdl(splitk_reduce_kernel, (unsigned)((n + 31) / 32), 32 * kColWarps, 0, ctx->stream, 
       PartV{part, n}, splits, n, out, accumulate);
   DPG_LAUNCH_CHECK(ctx);
@@ -261,6 +323,9 @@ void launch_clipped_sum_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const f
     if (hw_nhwc || !tg::csum_nhwc_ok(g)) raise(DPG_ERR_INTERNAL, "NHWC clipped sum: unsupported geometry");
     const int splits = tg::csum_nhwc_splits(g);
     tg::conv_csum_nhwc(ctx, xh, hw, scale, g, static_cast<float*>(ws), splits);
+    if (launch_splitk_reduce4(ctx, static_cast<float*>(ws), splits, nw, sw, accumulate,
+                              TapMajorOut{(int)g.ic, (int)(g.kh * g.kw), g.K()}))
+      return;
     ::dpg::launch_pdl(splitk_reduce_tap_kernel, (unsigned)((nw + 31) / 32), 32 * kColWarps, 0, ctx->stream,
                       PartV{static_cast<float*>(ws), nw}, splits, nw, sw, accumulate,
                       TapMajorOut{(int)g.ic, (int)(g.kh * g.kw), g.K()});
@@ -561,22 +626,29 @@ __global__ void weighted_sum_kernel(const float* __restrict__ g, const float* __
 // Narrow parameters (a few thousand columns): the record is staged through shared memory in
 // 64-sample chunks loaded by the whole CTA (every load in flight at once), then each thread
 // sums its column over the chunk in sample order — same order and roundings as above.
-constexpr int kWsCols = 128, kWsChunk = 64;
+constexpr int kWsCols = 32, kWsChunk = 128;
 __global__ void __launch_bounds__(256) weighted_sum_narrow_kernel(const float* __restrict__ g,
                                                                   const float* __restrict__ scale, int64_t b,
                                                                   int64_t numel, float* __restrict__ summed,
                                                                   int accumulate) {
   pdl_wait();
-  __shared__ float tile[kWsChunk][kWsCols];
+  __shared__ float tile[kWsChunk][kWsCols + 1];
   __shared__ float sc[kWsChunk];
   const int64_t j0 = (int64_t)blockIdx.x * kWsCols;
   const int tid = threadIdx.x;
   float acc = 0.f;
   for (int64_t n0 = 0; n0 < b; n0 += kWsChunk) {
     const int nn = (int)(b - n0 < kWsChunk ? b - n0 : kWsChunk);
-    for (int i = tid; i < kWsChunk * kWsCols; i += 256) {
-      const int q = i / kWsCols, c = i - q * kWsCols;
-      tile[q][c] = (q < nn && j0 + c < numel) ? __ldg(g + (n0 + q) * numel + j0 + c) : 0.f;
+    {  // lane = column, warp w = samples w, w + 8, ...: 16 coalesced loads in flight per thread
+      const int c = tid & 31, q0 = tid >> 5;
+      float v[kWsChunk / 8];
+#pragma unroll
+      for (int u = 0; u < kWsChunk / 8; ++u) {
+        const int q = q0 + 8 * u;
+        v[u] = (q < nn && j0 + c < numel) ? __ldg(g + (n0 + q) * numel + j0 + c) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kWsChunk / 8; ++u) tile[q0 + 8 * u][c] = v[u];
     }
     if (tid < kWsChunk) sc[tid] = tid < nn ? __ldg(scale + n0 + tid) : 0.f;
     __syncthreads();

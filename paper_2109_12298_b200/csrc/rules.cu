@@ -213,6 +213,32 @@ __global__ void __launch_bounds__(256, 4) gs_bias_kernel(const float* __restrict
         sq += (double)v * v;
       }
     }
+  } else if (r % 4 == 0 && (reinterpret_cast<uintptr_t>(hw) & 15) == 0) {
+    // 4 consecutive outputs per thread: 16 float4 loads in flight, each column summed in order
+    for (int64_t o = 4 * (int64_t)threadIdx.x; o < r; o += 4 * 256) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const float* col = hw + n * mid * r + o;
+      int64_t m = 0;
+      for (; m + 16 <= mid; m += 16) {
+        float4 v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(col + (m + u) * r));
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          a0 += (double)v[u].x; a1 += (double)v[u].y; a2 += (double)v[u].z; a3 += (double)v[u].w;
+        }
+      }
+      for (; m < mid; ++m) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(col + m * r));
+        a0 += (double)v.x; a1 += (double)v.y; a2 += (double)v.z; a3 += (double)v.w;
+      }
+      const float f[4] = {(float)a0, (float)a1, (float)a2, (float)a3};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (gb) gb[n * r + o + e] = f[e];
+        sq += (double)f[e] * f[e];
+      }
+    }
   } else {
     for (int64_t o = threadIdx.x; o < r; o += 256) {
       double acc = 0.0;
