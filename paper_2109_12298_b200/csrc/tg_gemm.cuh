@@ -395,10 +395,11 @@ struct TileBlock<P, std::void_t<decltype(P::kTileBlock)>> : std::integral_consta
 //                                      (a warp reads one 128-byte run per K row: conflict-free) and
 //                                      applies ReLU first when a_relu() (e.g. the T > 1 linear rule's
 //                                      [n][t][i] activations, i contiguous)
-//   static constexpr bool kCoopStore;  with kStaging: after the chunk is staged and the epilogue
-//                                      barrier, all 128 epilogue threads run coop_store(mt, nt, z,
-//                                      c0, row, stage) (e.g. 512-byte STG.128 runs) instead of the
-//                                      leader's TMA store
+//   static constexpr bool kCoopStore;  with kStaging: warp-local stores instead of the leader's TMA
+//                                      store — each epilogue warp stages its 32 rows of the chunk,
+//                                      syncs itself (no CTA barrier, so warps do not wait on each
+//                                      other) and runs coop_store(mt, nt, z, c0, row, stage) over
+//                                      its own rows (e.g. STG.128 of 128-byte row segments)
 template <class P, class = void>
 struct CoopStore : std::false_type {};
 template <class P>
@@ -740,10 +741,11 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
                                  : nullptr;
         p.epilogue(mt, nt, z, row, c0, v, acc, stg, in, pre, cst);
         if constexpr (STG > 0 && CoopStore<Prob>::value) {
-          // the chunk is staged: every epilogue thread stores a slice of it; the same buffer is
-          // rewritten two chunks later, after the next chunk's barrier (its reads are done)
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          // this warp's rows are staged; the warp alone reads them back and stores them (the
+          // buffer is rewritten by the same warp two chunks later, after these reads)
+          __syncwarp();
           p.coop_store(mt, nt, z, c0, row, stg);
+          __syncwarp();
         } else if (STG > 0) {
           fence_proxy_async();
           if (leader) bulk_wait_read<0>();  // the previous chunk's stores have read their buffer

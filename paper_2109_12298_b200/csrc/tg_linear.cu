@@ -60,14 +60,17 @@ struct LinBase {
     for (int j = 0; j < 16; ++j) st[j * BM + row] = v[j];
   }
   __device__ void epi_store(int, int, int, int, uint32_t) const {}
-  // 16 rows of 32 float4: thread t stores float4 t + 128 k (k < 4), so warp instruction = one o row
+  // this warp's [16 o][32 i] block (rows 32 q .. 32 q + 31 of every staged o row): lane l stores
+  // o = l / 8 + 4 k, i = 32 q + 4 (l % 8): one STG.128 covers four 128-byte row segments
   __device__ void coop_store(int mt, int nt, int z, int c0, int row, const uint8_t* stage) const {
     if (!out) return;
     const float4* st = reinterpret_cast<const float4*>(stage);
+    const int q = row >> 5, l = row & 31;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int f = row + 128 * k, ol = f >> 5, i = mt * BM + 4 * (f & 31), o = nt * kLinBN + c0 + ol;
-      const float4 v = st[f];
+      const int ol = (l >> 3) + 4 * k, il = 32 * q + 4 * (l & 7);
+      const int i = mt * BM + il, o = nt * kLinBN + c0 + ol;
+      const float4 v = st[(ol * BM + il) >> 2];
       if (o < r && i < d) {
         float* p = out + ((int64_t)z * r + o) * d + i;
         if (stream) st_stream4(p, v);
