@@ -74,10 +74,21 @@ struct LayerPlan {
 };
 
 // DPG_TG_CSUM=1: conv clipped sums on the TMA-fed core (read when a model is planned; opt-in:
-// measured slower on the CIFAR step, DESIGN.md §6 negative results)
-bool tg_csum_enabled() {
+// measured slower on the CIFAR step, DESIGN.md §6 negative results); DPG_TG_CSUM=L<i>,<j>,...:
+// only the conv layers of those model indices
+bool tg_csum_enabled(size_t layer) {
   const char* e = std::getenv("DPG_TG_CSUM");
-  return e && e[0] == '1';
+  if (!e) return false;
+  if (e[0] == '1') return true;
+  if (e[0] != 'L') return false;
+  for (const char* p = e + 1; *p;) {
+    char* end = nullptr;
+    const long v = std::strtol(p, &end, 10);
+    if (end == p) break;
+    if (v == (long)layer) return true;
+    p = *end == ',' ? end + 1 : end;
+  }
+  return false;
 }
 
 // DPG_TG_RULE=1: the 3x3 / 32-channel per-sample conv rule on the TMA-fed core (read when a model
@@ -930,8 +941,10 @@ dpg_status dpg_model_create(dpg_ctx* ctx, const dpg_layer_desc* layers, int nlay
           m->layers[lp.next_param_layer].tg_dgrad && dpg::tk::supported(lp.g))
         lp.hw_nhwc = true;
     }
-    for (auto& lp : m->layers)
-      lp.tg_csum = lp.tg_fwd == 1 && !lp.hw_nhwc && dpg::tg::csum_nhwc_ok(lp.g) && tg_csum_enabled();
+    for (size_t l = 0; l < m->layers.size(); ++l) {
+      LayerPlan& lp = m->layers[l];
+      lp.tg_csum = lp.tg_fwd == 1 && !lp.hw_nhwc && dpg::tg::csum_nhwc_ok(lp.g) && tg_csum_enabled(l);
+    }
     for (auto& lp : m->layers)
       lp.tg_rule = lp.tg_fwd == 1 && !lp.hw_nhwc && dpg::tg::rule_nhwc_ok(lp.g) && tg_rule_enabled();
     for (auto& lp : m->layers) {

@@ -1,0 +1,121 @@
+"""The T > 1 linear rule and clipped sum on the TMA-fed core (tg_linear.cu) on both sides of every
+shape rule the core has: BK = 16 (T <= 16) and 32, K blocks past T (zero fill of the 3-D tensor
+map), d and r not multiples of the 128-wide tile, several tiles per sample, the norms-only rule,
+the clipped sum's `accumulate` flag and split counts, and the fallbacks (misaligned operands, and
+DPG_TG_LIN=0 in a fresh process) onto the register-gather kernels.
+
+Reference: per_sample_rule_linear grad_sample.hpp:53-59 (batched_outer tensor.hpp:303-338), the
+clipped sum optimizer.hpp:99-114. Tolerance as tests/test_gpu_rules.py: max-scaled error vs the
+fp64 oracle <= 1e-5 and within 50x the reference's own fp32 error + 5e-6.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import maxscaled_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# b, T, d, r
+SHAPES = [
+    (3, 7, 36, 44),      # BK = 16, one partial K block, d / r below one tile
+    (2, 20, 132, 260),   # BK = 32, a partial second K block, 2 x 3 tiles with ragged edges
+    (2, 100, 64, 128),   # four K blocks, the last partial
+    (5, 64, 512, 512),   # cfg2's per-sample shape
+    (40, 16, 96, 80),    # BK = 16 exactly, many samples (clipped-sum splits)
+]
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def _n(t):
+    return t.detach().cpu().numpy()
+
+
+def _check(got, ref32, ref64, name):
+    e_gpu = maxscaled_err(got, ref64)
+    e_ref = maxscaled_err(ref32, ref64)
+    assert e_gpu <= TOL, f"{name}: gpu vs fp64 {e_gpu:.3e} > {TOL}"
+    assert e_gpu <= 50 * e_ref + 5e-6, f"{name}: gpu {e_gpu:.3e} vs reference fp32 {e_ref:.3e}"
+
+
+def _inputs(b, t, d, r, seed):
+    g = np.random.default_rng(seed)
+    return g.standard_normal((b, t, d)).astype(np.float32), g.standard_normal((b, t, r)).astype(np.float32)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_tg_linear_rule(ctx, oracle_r, shape):
+    from paper_2109_12298_b200 import dpg
+    b, t, d, r = shape
+    a, h = _inputs(b, t, d, r, sum(shape))
+    gw, gb, sw, sb = dpg.per_sample_rule_linear(ctx, _t(a), _t(h))
+    rw32, rb32 = oracle_r.rule_linear(a, h)
+    rw64, _ = oracle_r.rule_linear(a.astype(np.float64), h.astype(np.float64))
+    _check(_n(gw), rw32, rw64, f"rule {shape}")
+    assert np.array_equal(_n(gb), rb32), "bias: sequential double sum, bit-exact"
+    gwn = _n(gw).astype(np.float64)
+    np.testing.assert_allclose(_n(sw), (gwn ** 2).reshape(b, -1).sum(1), rtol=1e-10)
+    # norms only: the same fused norm without the record
+    _, _, sw2, sb2 = dpg.per_sample_rule_linear(ctx, _t(a), _t(h), grad=False)
+    assert np.array_equal(_n(sw), _n(sw2)) and np.array_equal(_n(sb), _n(sb2))
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_tg_linear_clipped_sum(ctx, oracle_r, shape):
+    import torch
+    from paper_2109_12298_b200 import dpg
+    b, t, d, r = shape
+    a, h = _inputs(b, t, d, r, 7 * sum(shape))
+    sc = np.random.default_rng(b).uniform(0.1, 1.0, size=b).astype(np.float32)
+    sw, sb = dpg.clipped_sum_linear(ctx, _t(a), _t(h), _t(sc))
+    ref64 = np.einsum("n,nto,nti->oi", sc.astype(np.float64), h.astype(np.float64), a.astype(np.float64))
+    gw32, _ = oracle_r.rule_linear(a, h)
+    ref32 = np.zeros((r, d), np.float32)
+    for n in range(b):
+        ref32 = (ref32 + np.float32(sc[n]) * gw32[n]).astype(np.float32)
+    _check(_n(sw), ref32, ref64, f"clipped sum {shape}")
+    # accumulate: out += the same sum (virtual steps, optimizer.hpp:240-254)
+    base = torch.full((r, d), 0.25, device="cuda")
+    dpg.clipped_sum_linear(ctx, _t(a), _t(h), _t(sc), out_w=base, out_b=torch.zeros(r, device="cuda"),
+                           accumulate=True)
+    _check(_n(base) - 0.25, ref32, ref64, f"clipped sum accumulate {shape}")
+
+
+def test_tg_linear_misaligned_falls_back(ctx, oracle_r):
+    """A 4-byte-offset operand cannot be a TMA tensor map: the register-gather kernel takes it and
+    gives the same records within tolerance."""
+    import torch
+    from paper_2109_12298_b200 import dpg
+    b, t, d, r = 3, 20, 64, 48
+    a, h = _inputs(b, t, d, r, 11)
+    buf = torch.empty(a.size + 1, device="cuda")
+    buf[1:] = _t(a).reshape(-1)
+    a_off = buf[1:].view(b, t, d)  # 4 bytes past a 256-byte allocation: not 16-byte aligned
+    assert a_off.data_ptr() % 16 != 0
+    gw, _, sw, _ = dpg.per_sample_rule_linear(ctx, a_off, _t(h))
+    gw_al, _, sw_al, _ = dpg.per_sample_rule_linear(ctx, _t(a), _t(h))
+    rw32, _ = oracle_r.rule_linear(a, h)
+    rw64, _ = oracle_r.rule_linear(a.astype(np.float64), h.astype(np.float64))
+    _check(_n(gw), rw32, rw64, "misaligned rule")
+    assert maxscaled_err(_n(gw), _n(gw_al).astype(np.float64)) <= 2e-6
+    np.testing.assert_allclose(_n(sw), _n(sw_al), rtol=1e-5)
+
+
+def test_tg_linear_disabled_path():
+    """DPG_TG_LIN=0 (read once per process): the linear rule / clipped-sum tests on the
+    register-gather kernels, in a fresh process."""
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_tg_linear.py"), "-k", "rule or clipped_sum"],
+                       env=dict(os.environ, DPG_TG_LIN="0"), cwd=ROOT, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
