@@ -301,18 +301,18 @@ struct Smem {
 
 // TMEM: two accumulator buffers of AW columns (AW = BN, or 2 BN with paired B below), then per
 // stage A_hi and A_lo (BK columns each)
-template <int AW, int BK>
+template <int AW, int BK, int NACC = 2>
 constexpr int tmem_stage_cap() {
-  return (512 - 2 * AW) / (2 * BK);
+  return (512 - NACC * AW) / (2 * BK);
 }
 // deepest ring (<= 6 stages) that fits the 227 KB a CTA may use and the 512 TMEM columns
-template <int BN, int BK, int STG = 0, int EIN = 0, int RED = 0, int AW = BN>
+template <int BN, int BK, int STG = 0, int EIN = 0, int RED = 0, int AW = BN, int NACC = 2>
 constexpr int stages_for() {
   constexpr int st = Smem<BN, BK, 1, STG, EIN>::STAGE;
   constexpr int fixed = 2 * STG + 2 * EIN + RED + 2048 + 4096;
   constexpr int lim = 227 * 1024 - fixed;
   constexpr int by_smem = (6 * st <= lim) ? 6 : (5 * st <= lim) ? 5 : (4 * st <= lim) ? 4 : (3 * st <= lim) ? 3 : 2;
-  return by_smem < tmem_stage_cap<AW, BK>() ? by_smem : tmem_stage_cap<AW, BK>();
+  return by_smem < tmem_stage_cap<AW, BK, NACC>() ? by_smem : tmem_stage_cap<AW, BK, NACC>();
 }
 // Paired B (pre-split operands): B_hi and B_lo land as adjacent row blocks, so one MMA of N = 2 BN
 // computes A_hi B_hi (columns [0, BN)) and A_hi B_lo ([BN, 2 BN)) and a second of N = BN adds
@@ -404,6 +404,13 @@ template <class P, class = void>
 struct CoopStore : std::false_type {};
 template <class P>
 struct CoopStore<P, std::void_t<decltype(P::kCoopStore)>> : std::integral_constant<bool, P::kCoopStore> {};
+//   static constexpr int kAccBufs;     TMEM accumulator buffers, 2 (default: a tile's epilogue overlaps
+//                                      the next tile's MMAs) or 1 (a 256-column tile; the next tile's
+//                                      MMAs wait for the epilogue's TMEM reads)
+template <class P, class = void>
+struct AccBufs : std::integral_constant<int, 2> {};
+template <class P>
+struct AccBufs<P, std::void_t<decltype(P::kAccBufs)>> : std::integral_constant<int, P::kAccBufs> {};
 template <class P, class = void>
 struct AMajorMN : std::false_type {};
 template <class P>
@@ -456,8 +463,10 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
   // TMEM columns of stage s's A_hi / A_lo (after the two accumulator buffers)
   constexpr bool PAIR = pair_b<Prob, BN>();
   constexpr int AW = acc_width<Prob, BN>();
-  static_assert(ST >= 2 && 2 * AW + ST * 2 * BK <= 512, "TMEM: accumulators + A stages exceed 512 columns");
-  auto tA = [&](int s) { return (uint32_t)(2 * AW + s * 2 * BK); };
+  constexpr int NACC = AccBufs<Prob>::value;
+  static_assert(NACC == 1 || NACC == 2, "one or two accumulator buffers");
+  static_assert(ST >= 2 && NACC * AW + ST * 2 * BK <= 512, "TMEM: accumulators + A stages exceed 512 columns");
+  auto tA = [&](int s) { return (uint32_t)(NACC * AW + s * 2 * BK); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = tiles.count();
@@ -532,8 +541,8 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
         tiles.at(t, mt, nt, z);
         int kb0, nkb;
         krange(z, kb0, nkb);
-        const int a = j & 1;
-        if (j >= 2) mbar_wait(tempty(a), ((j >> 1) - 1) & 1);
+        const int a = j % NACC;
+        if (j >= NACC) mbar_wait(tempty(a), ((j / NACC) - 1) & 1);
         tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(a * AW);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -652,7 +661,7 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
       tiles.at(t, mt, nt, z);
       int kb0, nkb;
       krange(z, kb0, nkb);
-      const int a = j & 1;
+      const int a = j % NACC;
       const bool epi_in = EIN > 0 && p.has_epi_in();
       if (epi_in && leader) {  // epilogue inputs of the tile's first chunk
         mbar_expect_tx(ein(g & 1), p.epi_in_bytes());
@@ -663,7 +672,7 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
       if constexpr (Prob::kEpiConst) {
         if (crank == 0) p.epi_const(mt, nt, z, row, cst);
       }
-      mbar_wait(tfull(a), (j >> 1) & 1);
+      mbar_wait(tfull(a), (j / NACC) & 1);
       if constexpr (Prob::kEpiConst) asm volatile("bar.sync 1, 128;" ::: "memory");  // constants written
       if (row == 0) tg_trace(4, j);
       tc_fence_after();
@@ -763,9 +772,10 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
       if (Prob::kCtaReduce) {
         __shared__ double red[2][4];
         acc = warp_sum(acc);
-        if (lane == 0) red[a][q] = acc;
+        const int rb = j & 1;  // alternate per tile (also with one accumulator buffer)
+        if (lane == 0) red[rb][q] = acc;
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (q == 0 && lane == 0) p.finish(mt, nt, z, red[a][0] + red[a][1] + red[a][2] + red[a][3]);
+        if (q == 0 && lane == 0) p.finish(mt, nt, z, red[rb][0] + red[rb][1] + red[rb][2] + red[rb][3]);
       }
       if constexpr (TST > 0) {
         asm volatile("bar.sync 1, 128;" ::: "memory");  // every chunk of the tile is staged

@@ -22,10 +22,10 @@ namespace dpg {
 namespace tg {
 
 namespace {
-constexpr int kLinBN = 128;
+constexpr int kLinBN = 128;  // clipped sum tile width; the rule takes 256 where r allows (below)
 
-// one K block = BK time steps of one sample
-template <int BK>
+// one K block = BK time steps of one sample; tiles of 128 i x BN o
+template <int BK, int BN>
 struct LinBase {
   static constexpr bool kBPreSplit = false, kBMajorMN = true, kAMajorMN = true, kEpiConst = false;
   // both operands split on the fly: two converter warps per TMEM lane quarter
@@ -41,11 +41,11 @@ struct LinBase {
   int d, r, T, b, relu;
   __device__ bool a_relu() const { return relu != 0; }
   __device__ int a_rows() const { return BM; }
-  __device__ uint32_t stage_bytes() const { return (uint32_t)((BM + kLinBN) * BK * 4); }
+  __device__ uint32_t stage_bytes() const { return (uint32_t)((BM + BN) * BK * 4); }
   __device__ void load(int n, int tb, uint32_t sa, uint32_t sb, uint32_t bar, int mt, int nt) const {
     tma3(sa, &ma, bar, mt * BM, tb * BK, n);
 #pragma unroll
-    for (int c = 0; c < kLinBN / 32; ++c) tma3(sb + c * (BK * 128), &mb, bar, nt * kLinBN + 32 * c, tb * BK, n);
+    for (int c = 0; c < BN / 32; ++c) tma3(sb + c * (BK * 128), &mb, bar, nt * BN + 32 * c, tb * BK, n);
   }
   __device__ bool has_epi_in() const { return false; }
   __device__ uint32_t epi_in_bytes() const { return 0; }
@@ -53,7 +53,7 @@ struct LinBase {
   __device__ uint64_t pre_epilogue(int, int, int, int) const { return 0; }
   __device__ void epi_const(int, int, int, int, float*) const {}
   // the chunk's 16 columns, transposed through shared memory: stage[j][row] (consecutive rows,
-  // conflict-free); out-of-range i / o are clipped by the TMA store
+  // conflict-free)
   __device__ static void stage16(uint8_t* stage, int row, const float (&v)[16]) {
     float* st = reinterpret_cast<float*>(stage);
 #pragma unroll
@@ -69,7 +69,7 @@ struct LinBase {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int ol = (l >> 3) + 4 * k, il = 32 * q + 4 * (l & 7);
-      const int i = mt * BM + il, o = nt * kLinBN + c0 + ol;
+      const int i = mt * BM + il, o = nt * BN + c0 + ol;
       const float4 v = st[(ol * BM + il) >> 2];
       if (o < r && i < d) {
         float* p = out + ((int64_t)z * r + o) * d + i;
@@ -80,12 +80,16 @@ struct LinBase {
   }
 };
 
-// per-sample rule: slice z = sample n; fused squared norm per (tile, sample)
-template <int BK>
-struct LinRuleT : LinBase<BK> {
+// per-sample rule: slice z = sample n; fused squared norm per (tile, sample). BN = 256: one
+// accumulator buffer of 256 columns (the 128 columns of a second would leave no room for the A
+// stages), so the tile's epilogue and the next tile's MMAs alternate — the epilogue's TMEM reads
+// then run without concurrent MMAs, and A is loaded and converted once per 256 outputs
+template <int BK, int BN>
+struct LinRuleT : LinBase<BK, BN> {
   static constexpr bool kScaleA = false, kCtaReduce = true;
+  static constexpr int kAccBufs = BN > 128 ? 1 : 2;
   double* sq;
-  int mtiles;
+  int mtiles, nrows128;  // norm slab rows are per 128-wide n tile (tc::gs_linear_rows)
   __device__ int nkb(int) const { return (this->T + BK - 1) / BK; }
   __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t, uint32_t bar, int mt, int nt, int z) const {
     this->load(z, kb, sa, sb, bar, mt, nt);
@@ -105,15 +109,20 @@ struct LinRuleT : LinBase<BK> {
     }
     acc += (a0 + a1) + (a2 + a3);
   }
-  // norm row = n tile * m tiles + m tile (tc::gs_linear_rows' order)
+  // norm row = 128-wide n tile * m tiles + m tile (tc::gs_linear_rows' order); a 256-wide tile
+  // puts its sum in its first row and zero in its second
   __device__ void finish(int mt, int nt, int z, double s) const {
-    if (sq) sq[(int64_t)(nt * mtiles + mt) * this->b + z] = s;
+    if (!sq) return;
+    constexpr int R = BN / 128;
+#pragma unroll
+    for (int h = 0; h < R; ++h)
+      if (nt * R + h < nrows128) sq[(int64_t)((nt * R + h) * mtiles + mt) * this->b + z] = h == 0 ? s : 0.0;
   }
 };
 
 // clipped sum: slice z = samples [z spl, z spl + spl); partial [z][o][i]
 template <int BK>
-struct LinCsumT : LinBase<BK> {
+struct LinCsumT : LinBase<BK, kLinBN> {
   static constexpr bool kScaleA = true, kCtaReduce = false;
   const float* svec;
   int spl, kpt;
@@ -154,6 +163,15 @@ void set_maps(Pr& p, const float* acts, const float* hw, int64_t b, int64_t mid,
 constexpr int64_t kChain = 512;
 }  // namespace
 
+// DPG_TG_LIN_BN=128: the rule on 128-wide double-buffered tiles only (A/B)
+int lin_rule_bn() {
+  static const int bn = [] {
+    const char* e = std::getenv("DPG_TG_LIN_BN");
+    return e && std::atoi(e) == 128 ? 128 : 256;
+  }();
+  return bn;
+}
+
 bool lin_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("DPG_TG");
@@ -175,17 +193,26 @@ bool lin_ok(const void* acts, const void* hw, const void* out, int64_t b, int64_
 
 void lin_rule(dpg_ctx* ctx, const float* acts, int relu, const float* hw, int64_t b, int64_t mid, int64_t d,
               int64_t r, float* gw, double* sq_part) {
-  const int mtiles = (int)((d + BM - 1) / BM), ntiles = (int)((r + kLinBN - 1) / kLinBN);
-  auto go = [&](auto BKc) {
-    constexpr int BK = decltype(BKc)::value;
-    LinRuleT<BK> p;
+  const int mtiles = (int)((d + BM - 1) / BM);
+  auto go = [&](auto BKc, auto BNc) {
+    constexpr int BK = decltype(BKc)::value, BN = decltype(BNc)::value;
+    using Pr = LinRuleT<BK, BN>;
+    Pr p;
     set_maps<BK>(p, acts, hw, b, mid, d, r);
-    p.relu = relu; p.sq = sq_part; p.mtiles = mtiles;
+    p.relu = relu; p.sq = sq_part; p.mtiles = mtiles; p.nrows128 = (int)((r + 127) / 128);
     p.out = gw; p.stream = true;
-    launch<kLinBN, BK, stages_for<kLinBN, BK, LinRuleT<BK>::kStaging>()>(ctx, p, dim3((unsigned)mtiles, (unsigned)ntiles, (unsigned)b));
+    const unsigned ntiles = (unsigned)((r + BN - 1) / BN);
+    launch<BN, BK, stages_for<BN, BK, Pr::kStaging, 0, 0, BN, Pr::kAccBufs>()>(ctx, p,
+                                                                              dim3((unsigned)mtiles, ntiles, (unsigned)b));
   };
-  if (pick_bk(mid) == 16) go(std::integral_constant<int, 16>{});
-  else go(std::integral_constant<int, 32>{});
+  const bool wide = r > 128 && lin_rule_bn() == 256;
+  if (pick_bk(mid) == 16) {
+    if (wide) go(std::integral_constant<int, 16>{}, std::integral_constant<int, 256>{});
+    else go(std::integral_constant<int, 16>{}, std::integral_constant<int, 128>{});
+  } else {
+    if (wide) go(std::integral_constant<int, 32>{}, std::integral_constant<int, 256>{});
+    else go(std::integral_constant<int, 32>{}, std::integral_constant<int, 128>{});
+  }
 }
 
 // samples per split: chains <= kChain products; minimise (waves of the persistent grid x K blocks

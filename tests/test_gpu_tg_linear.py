@@ -111,11 +111,12 @@ def test_tg_linear_misaligned_falls_back(ctx, oracle_r):
     np.testing.assert_allclose(_n(sw), _n(sw_al), rtol=1e-5)
 
 
-def test_tg_linear_disabled_path():
-    """DPG_TG_LIN=0 (read once per process): the linear rule / clipped-sum tests on the
-    register-gather kernels, in a fresh process."""
+@pytest.mark.parametrize("env", [{"DPG_TG_LIN": "0"}, {"DPG_TG_LIN_BN": "128"}])
+def test_tg_linear_alternate_paths(env):
+    """Switches read once per process, so in a fresh process: DPG_TG_LIN=0 puts the linear rule /
+    clipped sum on the register-gather kernels; DPG_TG_LIN_BN=128 keeps the rule on 128-wide
+    double-buffered tiles instead of the 256-wide single-buffered ones."""
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_tg_linear.py"), "-k", "rule or clipped_sum"],
-                       env=dict(os.environ, DPG_TG_LIN="0"), cwd=ROOT, capture_output=True, text=True,
-                       timeout=600)
+                       env=dict(os.environ, **env), cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
