@@ -1,10 +1,12 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-timeout 600 compute-sanitizer --tool racecheck --print-limit 5 --error-exitcode 99 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_tg.py -k cluster > gpurun_out/rc_cluster.log 2>&1; echo "racecheck cluster rc $?"; grep -E "ERROR SUMMARY|passed|failed" gpurun_out/rc_cluster.log | tail -2
-timeout 300 python -m pytest tests/test_gpu_tg.py -x -q 2>&1 | tail -2
-timeout 300 python tools/tg_time.py 2>&1 | tail -9
+timeout 900 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_tg.py tests/test_gpu_tg_linear.py tests/test_gpu_step.py > gpurun_out/pair_t.log 2>&1; echo "tests rc $?"; tail -2 gpurun_out/pair_t.log
+timeout 600 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_fullsize.py -k "cfg3_cifar_b512 or cfg2 or cfg1" > gpurun_out/pair_f.log 2>&1; echo "full rc $?"; tail -2 gpurun_out/pair_f.log
 for rep in 1 2; do
-timeout 300 python bench.py --steps 400 > gpurun_out/bp.json 2>gpurun_out/bp.err; tail -2 gpurun_out/bp.err; python -c "
-import json;d=json.load(open('gpurun_out/bp.json'));st=d['roofline']['stages_ms'];print(round(d['ms_per_step'],4),{k:round(v*1e3,1) for k,v in st.items() if 'fwd' in k or 'dgrad' in k})"
+for lib in libdpg.so libdpg_p0.so; do
+  DPG_LIB=$lib timeout 300 python bench.py --steps 400 > gpurun_out/pr.json 2>/dev/null; python -c "
+import json;d=json.load(open('gpurun_out/pr.json'));r=d['roofline'];print('$lib cifar',round(d['ms_per_step'],4),{k:round(v*1000,1) for k,v in r['stages_ms'].items() if k.startswith(('fwd.conv','dgrad'))})"
+done; done
+for lib in libdpg.so libdpg_p0.so; do
+  DPG_LIB=$lib timeout 300 python bench.py --workload linear_t64 --steps 100 > gpurun_out/pr.json 2>/dev/null; python -c "
+import json;d=json.load(open('gpurun_out/pr.json'));r=d['roofline'];print('$lib lin',round(d['ms_per_step'],4),{k:round(v*1000,1) for k,v in r['stages_ms'].items()})"
 done
-timeout 900 python -m pytest tests/test_gpu_step.py tests/test_gpu_fullsize.py -x -q 2>&1 | tail -2
