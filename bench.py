@@ -443,6 +443,16 @@ def run_linear_t64(args, rank, world):
     ms = per[name]
     achieved_gbs = by / (ms * 1e6)
     achieved_tf = fl / (ms * 1e9)
+    # DRAM bytes of the dominant stage from a committed ncu capture (tools/lin_traffic.py)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic_linear_t64.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        if name in tj:
+            traffic = tj[name]["traffic"]
+            traffic_src = (f"committed capture {os.path.relpath(tpath, ROOT)} ({tj.get('_source', 'ncu')}); "
+                           "not measured in this run")
     # end to end: pinned host A, B -> device, step, norms back
     Ah, Bh = A.cpu().pin_memory(), B.cpu().pin_memory()
     nh = torch.empty(b, dtype=torch.float64).pin_memory()
@@ -464,11 +474,17 @@ def run_linear_t64(args, rank, world):
                    "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
                    "l2": "no flush: the 268 MB per-sample gradient exceeds L2 every step"},
         "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved_gbs / hbm, "traffic": None,
+                     "frac": achieved_gbs / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
                      "algorithmic_bytes_per_launch": by, "launch_ms": ms,
                      "tensor": {"achieved_tflops": achieved_tf, "tf32_peak_tflops_measured": tf32,
                                 "peak_3xtf32_tflops": tf32 / 3.0, "frac_3xtf32": achieved_tf / (tf32 / 3.0)},
+                     # every contraction stage against both rooflines (the clipped sum is the
+                     # tensor-bound one: 2 b T d r flops over only 4 b T (d + r) bytes)
+                     "stages": {sn: {"ms": per[sn], "hbm_frac": sb / (per[sn] * 1e6) / hbm,
+                                     "tflops": sf / (per[sn] * 1e9),
+                                     "frac_3xtf32": sf / (per[sn] * 1e9) / (tf32 / 3.0)}
+                                for sn, _, sb, sf in st if sf > 0},
                      "stages_ms": per},
         "e2e": {"value": b * args.steps / e2e_s, "unit": "samples/s",
                 "h2d_bytes_per_step": int(A.numel() + B.numel()) * 4, "d2h_bytes_per_step": b * 8},

@@ -422,10 +422,22 @@ template <class P, class = void>
 struct ConvWarps : std::integral_constant<int, 4> {};
 template <class P>
 struct ConvWarps<P, std::void_t<decltype(P::kConvWarps)>> : std::integral_constant<int, P::kConvWarps> {};
-// producer + MMA warps, the converters, 4 epilogue warps
+//   static constexpr int kEpiWarps;    epilogue warps, 4 (default) or 8: two per TMEM lane quarter,
+//                                      taking alternate 16-column chunks (for latency-bound
+//                                      epilogues; plain or warp-local-store epilogues only)
+template <class P, class = void>
+struct EpiWarps : std::integral_constant<int, 4> {};
+template <class P>
+struct EpiWarps<P, std::void_t<decltype(P::kEpiWarps)>> : std::integral_constant<int, P::kEpiWarps> {};
+// producer + MMA warps, the converters, the epilogue warps
 template <class P>
 constexpr int threads_of() {
-  return 64 + 32 * ConvWarps<P>::value + 128;
+  return 64 + 32 * ConvWarps<P>::value + 32 * EpiWarps<P>::value;
+}
+// bytes of one epilogue staging slot: a chunk per epilogue warp group
+template <class P>
+constexpr int stg_bytes() {
+  return P::kStaging * (EpiWarps<P>::value / 4);
 }
 constexpr int kEpiThreads = 128;
 //
@@ -436,11 +448,15 @@ constexpr int kEpiThreads = 128;
 // rank order (deterministic), frees the buffer with a remote arrive per peer, and runs the epilogue.
 template <int BN, int BK, int ST, class Prob, int CK = 1>
 __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_constant__ Prob p, const Tiles tiles) {
-  constexpr int STG = Prob::kStaging, EIN = Prob::kEpiIn;
+  constexpr int STG = stg_bytes<Prob>(), EIN = Prob::kEpiIn;
+  constexpr int EW = EpiWarps<Prob>::value, EH = EW / 4;  // epilogue warps, chunk interleave
   static_assert(CK == 1 || (EIN == 0 && !Prob::kCtaReduce), "cluster split-K: plain epilogues only");
   constexpr int TST = TileStg<Prob>::value, TBL = TileBlock<Prob>::value;
   constexpr int CW = ConvWarps<Prob>::value, kCvt = 32 * CW;
   static_assert(CW == 4 || CW == 8, "converter warps: 4 or 8");
+  static_assert(EW == 4 || (EW == 8 && CK == 1 && EIN == 0 && !Prob::kEpiConst && TST == 0 &&
+                            (STG == 0 || CoopStore<Prob>::value)),
+                "8 epilogue warps: plain or warp-local-store epilogues only");
   static_assert(TBL == 0 || CK == 1, "blocked tile schedule: no cluster split");
   using S = Smem<BN, BK, ST, STG, EIN, red_bytes(CK) + TST>;
   using Lay = KLay<BK>;
@@ -495,7 +511,7 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), kEpiThreads);
+      mbar_init(tempty(a), 32 * EW);
       mbar_init(ein(a), 1);
       mbar_init(red_full(a), (CK - 1) * kEpiThreads);  // every peer epilogue thread, per chunk
       mbar_init(red_empty(a), kEpiThreads);            // every rank-0 epilogue thread, per use
@@ -655,6 +671,7 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
     const int q = warp & 3;
     const int row = 32 * q + lane;
     const bool leader = warp == 2 + CW && lane == 0;
+    const int ew = warp - (2 + CW), eh = ew >> 2;  // epilogue warp, its chunk phase
     int j = 0, g = 0;  // tile and chunk counters of this CTA
     for (int t = t_first; t < t_end; t += t_step, ++j) {
       int mt, nt, z;
@@ -683,30 +700,30 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
       uint32_t vm[16];  // paired B: the A_hi B_lo block of the same columns
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * AW);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16, ++g) {
+      for (int c0 = 16 * eh; c0 < BN; c0 += 16 * EH, ++g) {
         if (epi_in && leader && c0 + 16 < BN) {  // prefetch the next chunk's inputs
           mbar_expect_tx(ein((g + 1) & 1), p.epi_in_bytes());
           p.epi_load(mt, nt, z, c0 + 16, sbase + S::EIN_OFF + ((g + 1) & 1) * EIN, ein((g + 1) & 1));
         }
         if (nkb > 0) {
-          if (c0 == 0) {
-            tmem_ld16_async(trow, vn);
-            if constexpr (PAIR) tmem_ld16_async(trow + (uint32_t)BN, vm);
+          if (c0 == 16 * eh) {
+            tmem_ld16_async(trow + (uint32_t)c0, vn);
+            if constexpr (PAIR) tmem_ld16_async(trow + (uint32_t)(BN + c0), vm);
           }
           tmem_ld_wait();
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj)
             v[jj] = PAIR ? __uint_as_float(vn[jj]) + __uint_as_float(vm[jj]) : __uint_as_float(vn[jj]);
-          if (c0 + 16 < BN) {
-            tmem_ld16_async(trow + (uint32_t)(c0 + 16), vn);
-            if constexpr (PAIR) tmem_ld16_async(trow + (uint32_t)(BN + c0 + 16), vm);
+          if (c0 + 16 * EH < BN) {
+            tmem_ld16_async(trow + (uint32_t)(c0 + 16 * EH), vn);
+            if constexpr (PAIR) tmem_ld16_async(trow + (uint32_t)(BN + c0 + 16 * EH), vm);
           }
         } else {
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
         }
         if (row == 0) tg_trace(6, j * 8 + c0 / 16);
-        if (c0 + 16 >= BN) {  // every TMEM read of this buffer is done (waited): release it
+        if (c0 + 16 * EH >= BN) {  // every TMEM read of this buffer is done (waited): release it
           tc_fence_before();
           mbar_arrive(tempty(a));
         }
@@ -745,7 +762,7 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
           mbar_wait(ein(g & 1), (g >> 1) & 1);
           in = smem + S::EIN_OFF + (g & 1) * EIN;
         }
-        uint8_t* stg = STG > 0   ? smem + S::STG_OFF + (g & 1) * STG
+        uint8_t* stg = STG > 0   ? smem + S::STG_OFF + (g & 1) * STG + eh * Prob::kStaging
                        : TST > 0 ? smem + S::RED_OFF + red_bytes(CK)
                                  : nullptr;
         p.epilogue(mt, nt, z, row, c0, v, acc, stg, in, pre, cst);
@@ -770,12 +787,17 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
       }
       if (row == 0) tg_trace(5, j);
       if (Prob::kCtaReduce) {
-        __shared__ double red[2][4];
+        __shared__ double red[2][8];
         acc = warp_sum(acc);
         const int rb = j & 1;  // alternate per tile (also with one accumulator buffer)
-        if (lane == 0) red[rb][q] = acc;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (q == 0 && lane == 0) p.finish(mt, nt, z, red[rb][0] + red[rb][1] + red[rb][2] + red[rb][3]);
+        if (lane == 0) red[rb][eh * 4 + q] = acc;  // summed in lane-quarter order below
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+        if (ew == 0 && lane == 0) {
+          double sum = 0.0;
+#pragma unroll
+          for (int w = 0; w < EW; ++w) sum += red[rb][w];
+          p.finish(mt, nt, z, sum);
+        }
       }
       if constexpr (TST > 0) {
         asm volatile("bar.sync 1, 128;" ::: "memory");  // every chunk of the tile is staged
@@ -811,7 +833,7 @@ int max_active_clusters(const void* fn, int smem, int ck, int threads);
 // (CK > 1: min(tiles, co-resident clusters) clusters of CK CTAs)
 template <int BN, int BK, int ST, class Prob, int CK = 1>
 void launch(dpg_ctx* ctx, const Prob& p, dim3 grid) {
-  const int smem = Smem<BN, BK, ST, Prob::kStaging, Prob::kEpiIn, red_bytes(CK) + TileStg<Prob>::value>::TOTAL;
+  const int smem = Smem<BN, BK, ST, stg_bytes<Prob>(), Prob::kEpiIn, red_bytes(CK) + TileStg<Prob>::value>::TOTAL;
   const void* fn = reinterpret_cast<const void*>(tg_kernel<BN, BK, ST, Prob, CK>);
   ensure_smem_attr(fn, smem);
   const Tiles tiles{(int)grid.x, (int)grid.y, (int)grid.z};

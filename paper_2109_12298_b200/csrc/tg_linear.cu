@@ -21,6 +21,10 @@
 namespace dpg {
 namespace tg {
 
+#ifndef DPG_TG_LIN_EW
+#define DPG_TG_LIN_EW 8
+#endif
+
 namespace {
 constexpr int kLinBN = 128;  // clipped sum tile width; the rule takes 256 where r allows (below)
 
@@ -88,6 +92,9 @@ template <int BK, int BN>
 struct LinRuleT : LinBase<BK, BN> {
   static constexpr bool kScaleA = false, kCtaReduce = true;
   static constexpr int kAccBufs = BN > 128 ? 1 : 2;
+  // the epilogue's per-chunk chain (TMEM load, staging, 16-byte stores) is latency-bound: two warps
+  // per lane quarter take alternate chunks (DPG_TG_LIN_EW=4 at build time: one)
+  static constexpr int kEpiWarps = BN > 128 ? DPG_TG_LIN_EW : 4;
   double* sq;
   int mtiles, nrows128;  // norm slab rows are per 128-wide n tile (tc::gs_linear_rows)
   __device__ int nkb(int) const { return (this->T + BK - 1) / BK; }
@@ -202,7 +209,7 @@ void lin_rule(dpg_ctx* ctx, const float* acts, int relu, const float* hw, int64_
     p.relu = relu; p.sq = sq_part; p.mtiles = mtiles; p.nrows128 = (int)((r + 127) / 128);
     p.out = gw; p.stream = true;
     const unsigned ntiles = (unsigned)((r + BN - 1) / BN);
-    launch<BN, BK, stages_for<BN, BK, Pr::kStaging, 0, 0, BN, Pr::kAccBufs>()>(ctx, p,
+    launch<BN, BK, stages_for<BN, BK, stg_bytes<Pr>(), 0, 0, BN, Pr::kAccBufs>()>(ctx, p,
                                                                               dim3((unsigned)mtiles, ntiles, (unsigned)b));
   };
   const bool wide = r > 128 && lin_rule_bn() == 256;
