@@ -434,10 +434,12 @@ template <class P>
 constexpr int threads_of() {
   return 64 + 32 * ConvWarps<P>::value + 32 * EpiWarps<P>::value;
 }
-// bytes of one epilogue staging slot: a chunk per epilogue warp group
+// Smem's STG: half the epilogue staging bytes (it reserves two). Warp-local stores need one chunk
+// slot per epilogue warp group (each warp touches only its own rows, and rewrites them only
+// after its own reads); the leader's TMA stores double-buffer one slot.
 template <class P>
 constexpr int stg_bytes() {
-  return P::kStaging * (EpiWarps<P>::value / 4);
+  return CoopStore<P>::value ? P::kStaging * (EpiWarps<P>::value / 4) / 2 : P::kStaging;
 }
 constexpr int kEpiThreads = 128;
 //
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
   constexpr int TST = TileStg<Prob>::value, TBL = TileBlock<Prob>::value;
   constexpr int CW = ConvWarps<Prob>::value, kCvt = 32 * CW;
   static_assert(CW == 4 || CW == 8, "converter warps: 4 or 8");
-  static_assert(EW == 4 || (EW == 8 && CK == 1 && EIN == 0 && !Prob::kEpiConst && TST == 0 &&
+  static_assert(EW == 4 || ((EW == 8 || EW == 16) && CK == 1 && EIN == 0 && !Prob::kEpiConst && TST == 0 &&
                             (STG == 0 || CoopStore<Prob>::value)),
                 "8 epilogue warps: plain or warp-local-store epilogues only");
   static_assert(TBL == 0 || CK == 1, "blocked tile schedule: no cluster split");
@@ -762,7 +764,7 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
           mbar_wait(ein(g & 1), (g >> 1) & 1);
           in = smem + S::EIN_OFF + (g & 1) * EIN;
         }
-        uint8_t* stg = STG > 0   ? smem + S::STG_OFF + (g & 1) * STG + eh * Prob::kStaging
+        uint8_t* stg = STG > 0   ? smem + S::STG_OFF + (CoopStore<Prob>::value ? eh * Prob::kStaging : (g & 1) * STG)
                        : TST > 0 ? smem + S::RED_OFF + red_bytes(CK)
                                  : nullptr;
         p.epilogue(mt, nt, z, row, c0, v, acc, stg, in, pre, cst);
@@ -787,7 +789,7 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
       }
       if (row == 0) tg_trace(5, j);
       if (Prob::kCtaReduce) {
-        __shared__ double red[2][8];
+        __shared__ double red[2][16];
         acc = warp_sum(acc);
         const int rb = j & 1;  // alternate per tile (also with one accumulator buffer)
         if (lane == 0) red[rb][eh * 4 + q] = acc;  // summed in lane-quarter order below

@@ -22,7 +22,7 @@ namespace dpg {
 namespace tg {
 
 #ifndef DPG_TG_LIN_EW
-#define DPG_TG_LIN_EW 8
+#define DPG_TG_LIN_EW 16
 #endif
 
 namespace {
@@ -32,7 +32,8 @@ constexpr int kLinBN = 128;  // clipped sum tile width; the rule takes 256 where
 template <int BK, int BN>
 struct LinBase {
   static constexpr bool kBPreSplit = false, kBMajorMN = true, kAMajorMN = true, kEpiConst = false;
-  // both operands split on the fly: two converter warps per TMEM lane quarter
+  // both operands split on the fly: two converter warps per TMEM lane quarter (the clipped sum's
+  // stage rate depends on them; the rule trades them for epilogue warps, below)
   static constexpr int kConvWarps = 8;
   // a 16-column chunk of the tile is transposed through shared memory ([16 o][128 i]) and leaves
   // as 512-byte runs: one STG.128 per thread and column (measured: one 4-byte column store per
@@ -92,9 +93,11 @@ template <int BK, int BN>
 struct LinRuleT : LinBase<BK, BN> {
   static constexpr bool kScaleA = false, kCtaReduce = true;
   static constexpr int kAccBufs = BN > 128 ? 1 : 2;
-  // the epilogue's per-chunk chain (TMEM load, staging, 16-byte stores) is latency-bound: two warps
-  // per lane quarter take alternate chunks (DPG_TG_LIN_EW=4 at build time: one)
-  static constexpr int kEpiWarps = BN > 128 ? DPG_TG_LIN_EW : 4;
+  // the epilogue's per-chunk chain (TMEM load, staging, 16-byte stores) is latency-bound: four
+  // warps per lane quarter take interleaved chunks (DPG_TG_LIN_EW=4|8 at build time: one | two);
+  // 16 epilogue warps leave registers for 4 converter warps (704 threads)
+  static constexpr int kEpiWarps = DPG_TG_LIN_EW;
+  static constexpr int kConvWarps = DPG_TG_LIN_EW > 8 ? 4 : 8;
   double* sq;
   int mtiles, nrows128;  // norm slab rows are per 128-wide n tile (tc::gs_linear_rows)
   __device__ int nkb(int) const { return (this->T + BK - 1) / BK; }
