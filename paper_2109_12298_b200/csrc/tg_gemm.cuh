@@ -429,10 +429,15 @@ template <class P, class = void>
 struct EpiWarps : std::integral_constant<int, 4> {};
 template <class P>
 struct EpiWarps<P, std::void_t<decltype(P::kEpiWarps)>> : std::integral_constant<int, P::kEpiWarps> {};
+// epilogue warps of a launch: a cluster split-K launch keeps 4 (its exchange is per lane quarter)
+template <class P, int CK>
+constexpr int epi_warps() {
+  return CK > 1 ? 4 : EpiWarps<P>::value;
+}
 // producer + MMA warps, the converters, the epilogue warps
-template <class P>
+template <class P, int CK = 1>
 constexpr int threads_of() {
-  return 64 + 32 * ConvWarps<P>::value + 32 * EpiWarps<P>::value;
+  return 64 + 32 * ConvWarps<P>::value + 32 * epi_warps<P, CK>();
 }
 // Smem's STG: half the epilogue staging bytes (it reserves two). Warp-local stores need one chunk
 // slot per epilogue warp group (each warp touches only its own rows, and rewrites them only
@@ -449,14 +454,14 @@ constexpr int kEpiThreads = 128;
 // CTA's reduction buffer (st.shared::cluster, then a remote mbarrier arrive); rank 0 adds them in
 // rank order (deterministic), frees the buffer with a remote arrive per peer, and runs the epilogue.
 template <int BN, int BK, int ST, class Prob, int CK = 1>
-__global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_constant__ Prob p, const Tiles tiles) {
+__global__ void __launch_bounds__(threads_of<Prob, CK>(), 1) tg_kernel(const __grid_constant__ Prob p, const Tiles tiles) {
   constexpr int STG = stg_bytes<Prob>(), EIN = Prob::kEpiIn;
-  constexpr int EW = EpiWarps<Prob>::value, EH = EW / 4;  // epilogue warps, chunk interleave
+  constexpr int EW = epi_warps<Prob, CK>(), EH = EW / 4;  // epilogue warps, chunk interleave
   static_assert(CK == 1 || (EIN == 0 && !Prob::kCtaReduce), "cluster split-K: plain epilogues only");
   constexpr int TST = TileStg<Prob>::value, TBL = TileBlock<Prob>::value;
   constexpr int CW = ConvWarps<Prob>::value, kCvt = 32 * CW;
   static_assert(CW == 4 || CW == 8, "converter warps: 4 or 8");
-  static_assert(EW == 4 || ((EW == 8 || EW == 16) && CK == 1 && EIN == 0 && !Prob::kEpiConst && TST == 0 &&
+  static_assert(EW == 4 || ((EW == 8 || EW == 16) && CK == 1 && EIN == 0 && TST == 0 &&
                             (STG == 0 || CoopStore<Prob>::value)),
                 "8 epilogue warps: plain or warp-local-store epilogues only");
   static_assert(TBL == 0 || CK == 1, "blocked tile schedule: no cluster split");
@@ -692,7 +697,7 @@ __global__ void __launch_bounds__(threads_of<Prob>(), 1) tg_kernel(const __grid_
         if (crank == 0) p.epi_const(mt, nt, z, row, cst);
       }
       mbar_wait(tfull(a), (j / NACC) & 1);
-      if constexpr (Prob::kEpiConst) asm volatile("bar.sync 1, 128;" ::: "memory");  // constants written
+      if constexpr (Prob::kEpiConst) asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // constants written
       if (row == 0) tg_trace(4, j);
       tc_fence_after();
       if (t + t_step >= t_end) pdl_trigger();  // last tile: the next kernel may launch
@@ -840,7 +845,7 @@ void launch(dpg_ctx* ctx, const Prob& p, dim3 grid) {
   ensure_smem_attr(fn, smem);
   const Tiles tiles{(int)grid.x, (int)grid.y, (int)grid.z};
   const int64_t nt = (int64_t)grid.x * grid.y * grid.z;
-  const int64_t slots = CK > 1 ? max_active_clusters(fn, smem, CK, threads_of<Prob>()) : kNumSMs;
+  const int64_t slots = CK > 1 ? max_active_clusters(fn, smem, CK, threads_of<Prob, CK>()) : kNumSMs;
   const unsigned ctas = (unsigned)(std::min<int64_t>(nt, std::max<int64_t>(slots, 1)) * CK);
   if (std::getenv("DPG_TG_VERBOSE"))
     std::fprintf(stderr, "tg launch BN=%d BK=%d ST=%d CK=%d tiles=%lld slots=%lld ctas=%u smem=%d\n", BN, BK, ST, CK,
@@ -855,11 +860,11 @@ void launch(dpg_ctx* ctx, const Prob& p, dim3 grid) {
   }
 #endif
   if constexpr (CK == 1) {
-    ::dpg::launch_pdl(tg_kernel<BN, BK, ST, Prob>, dim3(ctas), threads_of<Prob>(), smem, ctx->stream, p, tiles);
+    ::dpg::launch_pdl(tg_kernel<BN, BK, ST, Prob>, dim3(ctas), threads_of<Prob, CK>(), smem, ctx->stream, p, tiles);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ctas);
-    cfg.blockDim = dim3(threads_of<Prob>());
+    cfg.blockDim = dim3(threads_of<Prob, CK>());
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
     cudaLaunchAttribute attr[2];
