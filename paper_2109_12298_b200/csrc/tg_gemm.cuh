@@ -411,6 +411,16 @@ template <class P, class = void>
 struct AccBufs : std::integral_constant<int, 2> {};
 template <class P>
 struct AccBufs<P, std::void_t<decltype(P::kAccBufs)>> : std::integral_constant<int, P::kAccBufs> {};
+//   static constexpr bool kBRawMN;     (with kAMajorMN, kBMajorMN = false, 8 converter warps, BK = 32,
+//                                      BN = 128) B lands as ONE unswizzled [BK][BN] box (N
+//                                      contiguous) in the B_lo buffer; converter warps 6-9 transpose
+//                                      it into K-major SWIZZLE_128B rows of B_hi / B_lo (thread = B
+//                                      row), warps 2-5 convert A. One 512-byte-row box instead of
+//                                      BN / 32 swizzled 128-byte-row boxes: fewer TMA requests
+template <class P, class = void>
+struct BRawMN : std::false_type {};
+template <class P>
+struct BRawMN<P, std::void_t<decltype(P::kBRawMN)>> : std::integral_constant<bool, P::kBRawMN> {};
 template <class P, class = void>
 struct AMajorMN : std::false_type {};
 template <class P>
@@ -460,6 +470,10 @@ __global__ void __launch_bounds__(threads_of<Prob, CK>(), 1) tg_kernel(const __g
   static_assert(CK == 1 || (EIN == 0 && !Prob::kCtaReduce), "cluster split-K: plain epilogues only");
   constexpr int TST = TileStg<Prob>::value, TBL = TileBlock<Prob>::value;
   constexpr int CW = ConvWarps<Prob>::value, kCvt = 32 * CW;
+  constexpr bool BRAW = BRawMN<Prob>::value;
+  static_assert(!BRAW || (AMajorMN<Prob>::value && !Prob::kBMajorMN && !Prob::kBPreSplit && CW == 8 && BK == 32 &&
+                          BN == 128),
+                "raw MN-major B: M-major A, K-major B for the MMA, 8 converter warps, BK 32, BN 128");
   static_assert(CW == 4 || CW == 8, "converter warps: 4 or 8");
   static_assert(EW == 4 || ((EW == 8 || EW == 16) && CK == 1 && EIN == 0 && TST == 0 &&
                             (STG == 0 || CoopStore<Prob>::value)),
@@ -619,11 +633,39 @@ __global__ void __launch_bounds__(threads_of<Prob, CK>(), 1) tg_kernel(const __g
         if (tc == 0) tg_trace(1, it);
         float sc = 1.f;
         if (Prob::kScaleA) sc = p.scale(kb0 + kb, mt, nt, z);
+        if constexpr (BRAW) {
+          if (h0 == 1) {
+            // B: row r of the tile is column r of the landed [BK][BN] box; read it whole (all
+            // 128 rows are read before any is rewritten: the raw box sits in the B_lo buffer),
+            // then split and write K-major SWIZZLE_128B rows (8 x 16 B, chunk c at c ^ (r & 7))
+            uint8_t* bhi = smem + s * S::STAGE + S::A_BYTES;
+            uint8_t* blo = bhi + S::B_BYTES;
+            const float* bcol = reinterpret_cast<const float*>(blo) + r;
+            float e[BK];
+#pragma unroll
+            for (int u = 0; u < BK; ++u) e[u] = bcol[u * BN];
+            asm volatile("bar.sync 2, 128;" ::: "memory");  // the 4 B warps have read the box
+#pragma unroll
+            for (int c = 0; c < BK / 4; ++c) {
+              uint4 hv, lv;
+              uint32_t* hp = reinterpret_cast<uint32_t*>(&hv);
+              uint32_t* lp = reinterpret_cast<uint32_t*>(&lv);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                hp[u] = rna_tf32(__float_as_uint(e[4 * c + u]));
+                lp[u] = rna_tf32(__float_as_uint(e[4 * c + u] - __uint_as_float(hp[u])));
+              }
+              const uint32_t off = (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4));
+              *reinterpret_cast<uint4*>(bhi + off) = hv;
+              *reinterpret_cast<uint4*>(blo + off) = lv;
+            }
+          }
+        }
         if constexpr (AMajorMN<Prob>::value) {  // [BK][BM] box: this thread's column r
           const float* acol = reinterpret_cast<const float*>(smem + s * S::STAGE) + r;
           const bool relu = p.a_relu();
 #pragma unroll
-          for (int h = h0; h < BK / 16; h += CW / 4) {
+          for (int h = BRAW ? 0 : h0; h < (BRAW && h0 == 1 ? 0 : BK / 16); h += BRAW ? 1 : CW / 4) {
             uint32_t hi[16], lo[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
@@ -660,7 +702,9 @@ __global__ void __launch_bounds__(threads_of<Prob, CK>(), 1) tg_kernel(const __g
           tmem_st16(lane_addr + tA(s) + 16 * h, hi);
           tmem_st16(lane_addr + tA(s) + BK + 16 * h, lo);
         }
-        if (!Prob::kBPreSplit) {
+        if (BRAW) {
+          fence_proxy_async();  // the transposed B rows, for the MMA's async-proxy reads
+        } else if (!Prob::kBPreSplit) {
           uint8_t* b = smem + s * S::STAGE + S::A_BYTES;
 #pragma unroll 4
           for (int i = tc * 16; i < S::B_BYTES; i += kCvt * 16) split16<false>(b + i, b + S::B_BYTES + i, 1.f);

@@ -21,6 +21,9 @@
 namespace dpg {
 namespace tg {
 
+#ifndef DPG_TG_LIN_BRAW
+#define DPG_TG_LIN_BRAW 1
+#endif
 #ifndef DPG_TG_LIN_EW
 #define DPG_TG_LIN_EW 16
 #endif
@@ -131,17 +134,28 @@ struct LinRuleT : LinBase<BK, BN> {
 };
 
 // clipped sum: slice z = samples [z spl, z spl + spl); partial [z][o][i]
+// (kBRawMN: H lands as one unswizzled [BK][128] box in the B_lo buffer and the converters
+// transpose it into K-major B_hi / B_lo rows — 1 TMA box per stage instead of 4 swizzled ones; the
+// clipped sum's stage rate is TMA-bound, ~4 ns per 128-byte request per SM)
 template <int BK>
 struct LinCsumT : LinBase<BK, kLinBN> {
   static constexpr bool kScaleA = true, kCtaReduce = false;
+  static constexpr bool kBRawMN = DPG_TG_LIN_BRAW != 0 && BK == 32, kBMajorMN = !kBRawMN;
+  CUtensorMap mh;  // kBRawMN: H as {r, T, b} box {128, BK, 1}, unswizzled
   const float* svec;
   int spl, kpt;
   __device__ int nkb(int z) const {
     const int ns = min(spl, this->b - z * spl);
     return ns > 0 ? ns * kpt : 0;
   }
-  __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t, uint32_t bar, int mt, int nt, int z) const {
-    this->load(z * spl + kb / kpt, kb % kpt, sa, sb, bar, mt, nt);
+  __device__ void issue(int kb, uint32_t sa, uint32_t sb, uint32_t sblo, uint32_t bar, int mt, int nt, int z) const {
+    const int n = z * spl + kb / kpt, tb = kb % kpt;
+    if constexpr (kBRawMN) {
+      tma3(sa, &this->ma, bar, mt * BM, tb * BK, n);
+      tma3(sblo, &mh, bar, nt * kLinBN, tb * BK, n);
+    } else {
+      this->load(n, tb, sa, sb, bar, mt, nt);
+    }
   }
   __device__ float scale(int kb, int, int, int z) const { return __ldg(svec + z * spl + kb / kpt); }
   __device__ void epilogue(int, int, int, int row, int, const float (&v)[16], double&, uint8_t* stage,
@@ -258,6 +272,12 @@ void lin_csum(dpg_ctx* ctx, const float* acts, int relu, const float* hw, const 
     LinCsumT<BK> p;
     set_maps<BK>(p, acts, hw, b, mid, d, r);
     p.relu = relu; p.svec = scale;
+    if constexpr (LinCsumT<BK>::kBRawMN) {
+      const uint64_t dh[3] = {(uint64_t)r, (uint64_t)mid, (uint64_t)b};
+      const uint64_t sh[2] = {(uint64_t)r * 4, (uint64_t)(mid * r * 4)};
+      const uint32_t bh[3] = {(uint32_t)kLinBN, (uint32_t)BK, 1};
+      p.mh = make_map(hw, 3, dh, sh, bh, nullptr, CU_TENSOR_MAP_SWIZZLE_NONE);
+    }
     p.out = part; p.stream = false;
     p.spl = (int)((b + splits - 1) / splits);
     p.kpt = (int)((mid + BK - 1) / BK);
