@@ -471,10 +471,13 @@ __global__ void __launch_bounds__(threads_of<Prob, CK>(), 1) tg_kernel(const __g
   constexpr int TST = TileStg<Prob>::value, TBL = TileBlock<Prob>::value;
   constexpr int CW = ConvWarps<Prob>::value, kCvt = 32 * CW;
   constexpr bool BRAW = BRawMN<Prob>::value;
-  static_assert(!BRAW || (AMajorMN<Prob>::value && !Prob::kBMajorMN && !Prob::kBPreSplit && CW == 8 && BK == 32 &&
+  static_assert(!BRAW || (AMajorMN<Prob>::value && !Prob::kBMajorMN && !Prob::kBPreSplit && CW >= 8 && BK == 32 &&
                           BN == 128),
-                "raw MN-major B: M-major A, K-major B for the MMA, 8 converter warps, BK 32, BN 128");
-  static_assert(CW == 4 || CW == 8, "converter warps: 4 or 8");
+                "raw MN-major B: M-major A, K-major B for the MMA, 8 or 16 converter warps, BK 32, BN 128");
+  // raw B: converter warp groups [0, CG) convert A, [CG, 2 CG) transpose B (CG = CW / 8 groups of 4
+  // warps each; with two groups per operand, each takes half of the 32 columns / K values)
+  constexpr int CG = CW / 8;
+  static_assert(CW == 4 || CW == 8 || CW == 16, "converter warps: 4, 8 or 16");
   static_assert(EW == 4 || ((EW == 8 || EW == 16) && CK == 1 && EIN == 0 && TST == 0 &&
                             (STG == 0 || CoopStore<Prob>::value)),
                 "8 epilogue warps: plain or warp-local-store epilogues only");
@@ -634,26 +637,30 @@ __global__ void __launch_bounds__(threads_of<Prob, CK>(), 1) tg_kernel(const __g
         float sc = 1.f;
         if (Prob::kScaleA) sc = p.scale(kb0 + kb, mt, nt, z);
         if constexpr (BRAW) {
-          if (h0 == 1) {
-            // B: row r of the tile is column r of the landed [BK][BN] box; read it whole (all
-            // 128 rows are read before any is rewritten: the raw box sits in the B_lo buffer),
-            // then split and write K-major SWIZZLE_128B rows (8 x 16 B, chunk c at c ^ (r & 7))
+          if (h0 >= CG) {
+            // B: row r of the tile is column r of the landed [BK][BN] box; read this group's K
+            // range of it (every B thread reads before any writes: the raw box sits in the B_lo
+            // buffer), then split and write K-major SWIZZLE_128B row chunks (16 B, chunk c at
+            // c ^ (r & 7))
+            constexpr int KB = BK / CG;  // K values per B group
+            const int k0 = (h0 - CG) * KB;
             uint8_t* bhi = smem + s * S::STAGE + S::A_BYTES;
             uint8_t* blo = bhi + S::B_BYTES;
             const float* bcol = reinterpret_cast<const float*>(blo) + r;
-            float e[BK];
+            float e[KB];
 #pragma unroll
-            for (int u = 0; u < BK; ++u) e[u] = bcol[u * BN];
-            asm volatile("bar.sync 2, 128;" ::: "memory");  // the 4 B warps have read the box
+            for (int u = 0; u < KB; ++u) e[u] = bcol[(k0 + u) * BN];
+            asm volatile("bar.sync 2, %0;" ::"n"(128 * CG) : "memory");  // every B warp has read the box
 #pragma unroll
-            for (int c = 0; c < BK / 4; ++c) {
+            for (int cc = 0; cc < KB / 4; ++cc) {
+              const int c = k0 / 4 + cc;
               uint4 hv, lv;
               uint32_t* hp = reinterpret_cast<uint32_t*>(&hv);
               uint32_t* lp = reinterpret_cast<uint32_t*>(&lv);
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                hp[u] = rna_tf32(__float_as_uint(e[4 * c + u]));
-                lp[u] = rna_tf32(__float_as_uint(e[4 * c + u] - __uint_as_float(hp[u])));
+                hp[u] = rna_tf32(__float_as_uint(e[4 * cc + u]));
+                lp[u] = rna_tf32(__float_as_uint(e[4 * cc + u] - __uint_as_float(hp[u])));
               }
               const uint32_t off = (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4));
               *reinterpret_cast<uint4*>(bhi + off) = hv;
@@ -665,7 +672,7 @@ __global__ void __launch_bounds__(threads_of<Prob, CK>(), 1) tg_kernel(const __g
           const float* acol = reinterpret_cast<const float*>(smem + s * S::STAGE) + r;
           const bool relu = p.a_relu();
 #pragma unroll
-          for (int h = BRAW ? 0 : h0; h < (BRAW && h0 == 1 ? 0 : BK / 16); h += BRAW ? 1 : CW / 4) {
+          for (int h = BRAW ? h0 : h0; h < (BRAW && h0 >= CG ? 0 : BK / 16); h += BRAW ? CG : CW / 4) {
             uint32_t hi[16], lo[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {

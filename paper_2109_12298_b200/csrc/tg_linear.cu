@@ -24,6 +24,9 @@ namespace tg {
 #ifndef DPG_TG_LIN_BRAW
 #define DPG_TG_LIN_BRAW 1
 #endif
+#ifndef DPG_TG_LIN_CSUM_CW
+#define DPG_TG_LIN_CSUM_CW 8
+#endif
 #ifndef DPG_TG_LIN_EW
 #define DPG_TG_LIN_EW 16
 #endif
@@ -142,6 +145,9 @@ struct LinCsumT : LinBase<BK, kLinBN> {
   static constexpr bool kScaleA = true, kCtaReduce = false;
   static constexpr bool kBRawMN = DPG_TG_LIN_BRAW != 0 && BK == 32, kBMajorMN = !kBRawMN;
   CUtensorMap mh;  // kBRawMN: H as {r, T, b} box {128, BK, 1}, unswizzled
+  // converter warps (DPG_TG_LIN_CSUM_CW=16 at build time: two groups per operand, measured
+  // 90 -> 94 us: the stage rate is not conversion-bound)
+  static constexpr int kConvWarps = kBRawMN ? DPG_TG_LIN_CSUM_CW : 8;
   const float* svec;
   int spl, kpt;
   __device__ int nkb(int z) const {
