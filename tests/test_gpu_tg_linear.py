@@ -120,3 +120,39 @@ def test_tg_linear_alternate_paths(env):
                         os.path.join(ROOT, "tests", "test_gpu_tg_linear.py"), "-k", "rule or clipped_sum"],
                        env=dict(os.environ, **env), cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("b,c", [(12, 1.0), (12, 50.0)])
+def test_tg_linear_in_the_engine(ctx, b, c):
+    """A sequence model through the engine: Linear on [b, T, d] (mid = T = 20 > 1, the TMA-fed rule
+    and clipped sum), ReLU, a second T > 1 Linear whose input is that ReLU's output (the
+    converters' ReLU path), flatten, the classifier. Whole step against the oracle's fp64 step:
+    record, norms, clipped sums, update (grad_sample.hpp:277-343, optimizer.hpp:62-133)."""
+    import oracle
+    from paper_2109_12298_b200 import dpg
+    from paper_2109_12298_b200.configs import LayerDesc as L, Workload, params_meta
+    layers = (L.linear(64, 96), L.relu(), L.linear(96, 32), L.relu(), L.flatten(), L.linear(20 * 32, 10))
+    w = Workload("seq_t20", layers, (20, 64), b, 10)
+    params, x, y = oracle.synth_inputs(w, b=b)
+    m = dpg.Model(ctx, layers, w.in_shape, max_batch=b)
+    m.load_params(params)
+    cfg = dict(noise_multiplier=0.0, max_grad_norm=c, learning_rate=0.1, expected_batch_size=float(b), noise_seed=3)
+    o = dpg.DpOptimizer(m, **cfg)
+    o.forward_backward(_t(x), _t(y))
+    rec = _n(o.grad_sample())
+    o.step()
+    summed = _n(o.summed_grad())
+    norms, _, _ = o.last_clip_summary()
+    p_new = m.store_params()
+    R = oracle.restatement()
+    res = {dt: R.dpsgd_step(layers, w.in_shape, params.astype(dt), x.astype(dt), y.astype(dt), 0.0, c, 0.1,
+                            float(b), noise_seed=3) for dt in (np.float32, np.float64)}
+    r32, r64 = res[np.float32], res[np.float64]
+    for (li, k, pname, shape, numel, off) in params_meta(layers):
+        sl = slice(b * off, b * (off + numel))
+        _check(rec[sl], r32["record"][sl], r64["record"][sl], f"record layer {li} {pname}")
+        _check(summed[off:off + numel], r32["summed"][off:off + numel], r64["summed"][off:off + numel],
+               f"summed layer {li} {pname}")
+    np.testing.assert_allclose(norms, r64["norms"], rtol=TOL)
+    e = maxscaled_err(p_new.astype(np.float64) - params, r64["params"] - params)
+    assert e <= TOL, f"update: {e:.3e}"
