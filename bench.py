@@ -288,6 +288,14 @@ def cpu_baseline(workload, budget_s=15.0, single_thread=True):
     return out
 
 
+def linear_t64_config(args):
+    """The cfg2 config dict, identical in both arms."""
+    from paper_2109_12298_b200.configs import LINEAR_T64 as C
+    return {"workload": "linear_t64", "batch": C["b"], "seq_len": C["t"], "in": C["d"],
+            "out": C["r"], "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
+            "l2": "no flush: the 268 MB per-sample gradient exceeds L2 every step"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -296,7 +304,7 @@ def run_reference(args, rank, world):
         line = {"metric": LINEAR_T64_METRIC, "value": cb["value"], "unit": "samples/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-                "config": {"workload": "linear_t64"}, "cpu_baseline": cb,
+                "config": linear_t64_config(args), "cpu_baseline": cb,
                 "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -470,9 +478,7 @@ def run_linear_t64(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": "linear_t64", "batch": b, "seq_len": t, "in": d, "out": r,
-                   "sigma": args.sigma, "max_grad_norm": args.max_grad_norm,
-                   "l2": "no flush: the 268 MB per-sample gradient exceeds L2 every step"},
+        "config": linear_t64_config(args),
         "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                      "frac": achieved_gbs / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
