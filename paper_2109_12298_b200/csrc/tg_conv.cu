@@ -448,11 +448,11 @@ struct ConvRuleT {
   __device__ void finish(int, int nt, int n, double sum) const {
     if (sq) sq[(int64_t)nt * b + n] = sum;
   }
-  __device__ void tile_done(int, int nt, int n, int row, uint8_t* stg) const {
+  __device__ void tile_done(int, int nt, int n, int tid, int nthreads, uint8_t* stg) const {
     if (nt != NTN - 1 || !gw) return;
     const float* src = reinterpret_cast<const float*>(stg);
     float4* dst = reinterpret_cast<float4*>(gw + (int64_t)n * O * K);
-    for (int i4 = row; i4 < O * K / 4; i4 += 128) {  // K % 4 == 0: a float4 never straddles rows
+    for (int i4 = tid; i4 < O * K / 4; i4 += nthreads) {  // K % 4 == 0: a float4 never straddles rows
       const int o = (4 * i4) / K, k = 4 * i4 - o * K;
       const float* s4 = src + o * KP + k;
       dst[i4] = make_float4(s4[0], s4[1], s4[2], s4[3]);

@@ -376,7 +376,8 @@ struct Tiles {
 //   void finish(int mt, int nt, int z, double acc_sum) const;               (kCtaReduce)
 // Optional Prob members (default 0 when absent):
 //   static constexpr int kTileStg;     bytes of a per-CTA tile staging area: passed to epilogue() as
-//                                      `stage`, then tile_done(mt, nt, z, row, stage) runs on all 128
+//                                      `stage`, then tile_done(mt, nt, z, tid, nthreads, stage) runs
+//                                      on all epilogue threads (tid < nthreads = 32 kEpiWarps)
 //                                      epilogue threads after the tile's last chunk (between two
 //                                      epilogue barriers), e.g. to store a re-ordered tile coalesced
 //   static constexpr int kTileBlock;   > 0: blocked persistent schedule — CTA i walks a contiguous
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(threads_of<Prob, CK>(), 1) tg_kernel(const __g
   // warps each; with two groups per operand, each takes half of the 32 columns / K values)
   constexpr int CG = CW / 8;
   static_assert(CW == 4 || CW == 8 || CW == 16, "converter warps: 4, 8 or 16");
-  static_assert(EW == 4 || ((EW == 8 || EW == 16) && CK == 1 && EIN == 0 && TST == 0 &&
+  static_assert(EW == 4 || ((EW == 8 || EW == 16) && CK == 1 && EIN == 0 &&
                             (STG == 0 || CoopStore<Prob>::value)),
                 "8 epilogue warps: plain or warp-local-store epilogues only");
   static_assert(TBL == 0 || CK == 1, "blocked tile schedule: no cluster split");
@@ -858,9 +859,9 @@ __global__ void __launch_bounds__(threads_of<Prob, CK>(), 1) tg_kernel(const __g
         }
       }
       if constexpr (TST > 0) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // every chunk of the tile is staged
-        p.tile_done(mt, nt, z, row, smem + S::RED_OFF + red_bytes(CK));
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free for the next tile
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // every chunk of the tile is staged
+        p.tile_done(mt, nt, z, 32 * ew + lane, 32 * EW, smem + S::RED_OFF + red_bytes(CK));
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // staging free for the next tile
       }
     }
     if (((STG > 0 && !CoopStore<Prob>::value) || CK > 1) && leader) bulk_wait_all();
