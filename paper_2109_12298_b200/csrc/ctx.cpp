@@ -6,6 +6,8 @@
 #include <mutex>
 #include <string>
 
+#include <vector>
+
 #include "dpg_internal.h"
 
 namespace dpg {
@@ -135,6 +137,22 @@ void* dpg_ctx::workspace(size_t bytes) {
   return ws;
 }
 
+const int32_t* dpg_ctx::identity_rows(int n) {
+  if (n <= iota_n) return iota;
+  if (capturing) dpg::raise(DPG_ERR_INTERNAL, "identity-row table growth during graph capture");
+  const int cap = n < 1024 ? 1024 : n;
+  std::vector<int32_t> h(cap);
+  for (int i = 0; i < cap; ++i) h[i] = i;
+  DPG_CUDA(cudaStreamSynchronize(stream));
+  if (iota) DPG_CUDA(cudaFree(iota));
+  iota = nullptr;
+  iota_n = 0;
+  DPG_CUDA(cudaMalloc(&iota, sizeof(int32_t) * cap));
+  DPG_CUDA(cudaMemcpy(iota, h.data(), sizeof(int32_t) * cap, cudaMemcpyHostToDevice));
+  iota_n = cap;
+  return iota;
+}
+
 using dpg::guard;
 
 extern "C" {
@@ -186,6 +204,7 @@ void dpg_ctx_destroy(dpg_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->iota) cudaFree(ctx->iota);
   if (ctx->dev_err) cudaFree(ctx->dev_err);
   if (ctx->clip_sync) cudaFree(ctx->clip_sync);
   if (ctx->host_err) cudaFreeHost(ctx->host_err);

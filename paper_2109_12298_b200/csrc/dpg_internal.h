@@ -70,7 +70,8 @@ struct dpg_ctx {
   int64_t launches = 0;
   dpg::DeviceErr* dev_err = nullptr;  // device
   unsigned long long* clip_sync = nullptr;
-  uint64_t comm_gen = 0;  // bumped by dpg_ctx_init_comm: captured steps of an older communicator are stale  // device [2]: clip_factors' clipped count + CTA ticket (self-resetting)
+  // device [2]: clip_factors' clipped count + CTA ticket (self-resetting) is clip_sync above
+  uint64_t comm_gen = 0;  // bumped by dpg_ctx_init_comm: captured steps of an older communicator are stale
   dpg::DeviceErr* host_err = nullptr; // pinned mirror
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -83,6 +84,11 @@ struct dpg_ctx {
 
   // scratch space for operator-ABI calls (grows outside capture only)
   void* workspace(size_t bytes);
+  // device-resident 0, 1, ..., n-1 (the identity row -> parameter map of an operator-ABI clip
+  // factors call); grows outside capture only, so a call needs no host copy and no sync
+  int32_t* iota = nullptr;
+  int iota_n = 0;
+  const int32_t* identity_rows(int n);
 
   // stage profiling (eager launches only): CUDA events on this stream around each stage,
   // with the stage's algorithmic bytes / flops

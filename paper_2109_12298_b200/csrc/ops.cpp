@@ -164,13 +164,9 @@ dpg_status dpg_clip_factors(dpg_ctx* ctx, const double* sq, int nparams, int64_t
     if (b == 0) raise(DPG_ERR_PARAMETER, "clip_and_sum on an empty batch");
     need(sq, "sq");
     need(scale, "scale");
-    std::vector<int32_t> rp(nparams);
-    for (int p = 0; p < nparams; ++p) rp[p] = p;
-    int32_t* drp = static_cast<int32_t*>(ctx->workspace(sizeof(int32_t) * (nparams > 0 ? nparams : 1)));
-    if (nparams > 0)
-      DPG_CUDA(cudaMemcpyAsync(drp, rp.data(), sizeof(int32_t) * nparams, cudaMemcpyHostToDevice, ctx->stream));
+    // row r of the slab is parameter r: a device-resident identity map (no host copy, no sync)
+    const int32_t* drp = ctx->identity_rows(nparams > 0 ? nparams : 1);
     dpg::launch_clip_factors(ctx, sq, drp, nparams, b, c, norms, scale, num_clipped);
-    DPG_CUDA(cudaStreamSynchronize(ctx->stream));  // rp is a host temporary
   });
 }
 
