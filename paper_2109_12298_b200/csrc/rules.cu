@@ -128,7 +128,7 @@ void launch_gs_conv2d(dpg_ctx* ctx, const float* x, int x_relu, const float* hw,
 // one warp per row with a fixed fp64 tree; linear layout [mid][r]: sequential in mid, coalesced
 // over o. One CTA per sample; norm partial = one row.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) gs_bias_kernel(const float* __restrict__ hw, int64_t mid,
+__global__ void __launch_bounds__(256, 4) gs_bias_kernel(const float* __restrict__ hw, int64_t mid,
                                                       int64_t r, int conv_layout,
                                                       float* __restrict__ gb,
                                                       double* __restrict__ sq_part, int64_t b) {
@@ -219,23 +219,13 @@ __global__ void __launch_bounds__(256, 2) gs_bias_kernel(const float* __restrict
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       const float* col = hw + n * mid * r + o;
       int64_t m = 0;
-      // software-pipelined batches of 8 rows: the next batch's loads are in flight while this
-      // one is summed (the sum stays sequential in the middle index)
-      if (mid >= 8) {
-        float4 v[8], nx[8];
+      for (; m + 16 <= mid; m += 16) {
+        float4 v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(col + u * r));
-        for (; m + 8 <= mid; m += 8) {
-          const bool more = m + 16 <= mid;
+        for (int u = 0; u < 16; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(col + (m + u) * r));
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            nx[u] = more ? __ldg(reinterpret_cast<const float4*>(col + (m + 8 + u) * r)) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            a0 += (double)v[u].x; a1 += (double)v[u].y; a2 += (double)v[u].z; a3 += (double)v[u].w;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = nx[u];
+        for (int u = 0; u < 16; ++u) {
+          a0 += (double)v[u].x; a1 += (double)v[u].y; a2 += (double)v[u].z; a3 += (double)v[u].w;
         }
       }
       for (; m < mid; ++m) {
