@@ -153,6 +153,32 @@ const int32_t* dpg_ctx::identity_rows(int n) {
   return iota;
 }
 
+bool dpg_ctx::can_fork() {
+  if (side) return true;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &st) != cudaSuccess) return false;
+  return st == cudaStreamCaptureStatusNone && !capturing;
+}
+
+void dpg_ctx::fork_side() {
+  if (!side) {
+    DPG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    DPG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    DPG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  main_saved = stream;
+  DPG_CUDA(cudaEventRecord(ev_fork, stream));
+  DPG_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+  stream = side;
+}
+
+void dpg_ctx::end_side() {
+  DPG_CUDA(cudaEventRecord(ev_join, side));
+  stream = main_saved;
+}
+
+void dpg_ctx::join_side() { DPG_CUDA(cudaStreamWaitEvent(stream, ev_join, 0)); }
+
 using dpg::guard;
 
 extern "C" {
@@ -205,6 +231,12 @@ void dpg_ctx_destroy(dpg_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->iota) cudaFree(ctx->iota);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_join);
+  }
   if (ctx->dev_err) cudaFree(ctx->dev_err);
   if (ctx->clip_sync) cudaFree(ctx->clip_sync);
   if (ctx->host_err) cudaFreeHost(ctx->host_err);

@@ -89,6 +89,15 @@ struct dpg_ctx {
   int32_t* iota = nullptr;
   int iota_n = 0;
   const int32_t* identity_rows(int n);
+  // a side stream for independent work inside one operator-ABI call (e.g. a bias rule beside its
+  // weight's rule): fork/join by events, so the call stays ordered on `stream` as a whole
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t main_saved = nullptr;
+  bool can_fork();   // the side stream exists, or may be created now (no capture in progress)
+  void fork_side();  // from here on, launches go to `side` (which waits for `stream`'s work so far)
+  void end_side();   // launches go to `stream` again; the side work is marked for join_side()
+  void join_side();  // `stream` waits for the side work
 
   // stage profiling (eager launches only): CUDA events on this stream around each stage,
   // with the stage's algorithmic bytes / flops

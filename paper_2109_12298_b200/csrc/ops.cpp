@@ -83,9 +83,18 @@ dpg_status dpg_grad_sample_linear(dpg_ctx* ctx, const float* acts, const float* 
     if (b == 0) return;
     const int rows = dpg::sq_rows_linear(mid, d, r);
     double* part = sq_w ? static_cast<double*>(ctx->workspace(ws_gs_linear(b, mid, d, r))) : nullptr;
+    // T > 1: the bias rule (a pass over the whole highway) runs on the side stream beside the
+    // weight rule; the call is joined before it returns
+    const bool side = (gb || sq_b) && mid > 1 && ctx->can_fork();
+    if (side) {
+      ctx->fork_side();
+      dpg::launch_gs_bias(ctx, highway, b, mid, r, false, gb, sq_b);
+      ctx->end_side();
+    }
     dpg::launch_gs_linear(ctx, acts, 0, highway, b, mid, d, r, gw, part);
     if (sq_w) dpg::launch_sq_reduce(ctx, part, rows, b, sq_w);
-    if (gb || sq_b) dpg::launch_gs_bias(ctx, highway, b, mid, r, false, gb, sq_b);
+    if (side) ctx->join_side();
+    else if (gb || sq_b) dpg::launch_gs_bias(ctx, highway, b, mid, r, false, gb, sq_b);
   });
 }
 
@@ -181,10 +190,20 @@ dpg_status dpg_clipped_sum_linear(dpg_ctx* ctx, const float* acts, const float* 
     need(sw, "sw");
     if (b <= 0) raise(DPG_ERR_PARAMETER, "clip_and_sum on an empty batch");
     void* ws = ctx->workspace(ws_cs_linear(b, mid, d, r));
+    // bias: weighted sum of the per-sample bias sums (bit-exact with the reference); T > 1: on the
+    // side stream, beside the weight's clipped sum (its own slice of the workspace)
+    const bool side = sb && mid > 1 && ctx->can_fork();
+    float* gb = sb ? reinterpret_cast<float*>(static_cast<char*>(ws) + dpg::clipped_sum_ws_linear(b, mid, d, r)) : nullptr;
+    if (side) {
+      ctx->fork_side();
+      dpg::launch_gs_bias(ctx, highway, b, mid, r, false, gb, nullptr);
+      dpg::launch_weighted_sum_materialised(ctx, gb, scale, b, r, sb, accumulate);
+      ctx->end_side();
+    }
     dpg::launch_clipped_sum_linear(ctx, acts, 0, highway, scale, b, mid, d, r, sw, sb, accumulate, ws);
-    if (sb) {
-      // bias: weighted sum of the per-sample bias sums (bit-exact with the reference)
-      float* gb = reinterpret_cast<float*>(static_cast<char*>(ws) + dpg::clipped_sum_ws_linear(b, mid, d, r));
+    if (side) {
+      ctx->join_side();
+    } else if (sb) {
       dpg::launch_gs_bias(ctx, highway, b, mid, r, false, gb, nullptr);
       dpg::launch_weighted_sum_materialised(ctx, gb, scale, b, r, sb, accumulate);
     }
