@@ -156,3 +156,40 @@ def test_tg_linear_in_the_engine(ctx, b, c):
     np.testing.assert_allclose(norms, r64["norms"], rtol=TOL)
     e = maxscaled_err(p_new.astype(np.float64) - params, r64["params"] - params)
     assert e <= TOL, f"update: {e:.3e}"
+
+
+def test_tg_linear_operator_calls_in_a_captured_graph():
+    """The T > 1 linear operator calls fork their bias work onto the context's side stream and
+    join it back: captured into a CUDA graph on the context's stream and replayed,
+    they give the eager results bit for bit (rule + norms, bias rule, clipped sums)."""
+    import torch
+    from paper_2109_12298_b200 import dpg
+    s = torch.cuda.Stream()
+    ctx = dpg.Context(0, stream=s)
+    b, t, d, r = 6, 20, 64, 96
+    a, h = _inputs(b, t, d, r, 5)
+    A, H = _t(a), _t(h)
+    sc = _t(np.random.default_rng(1).uniform(0.1, 1.0, size=b).astype(np.float32))
+    gw, gb, sw, sb = (torch.zeros((b, r, d), device="cuda"), torch.zeros((b, r), device="cuda"),
+                      torch.zeros(b, dtype=torch.float64, device="cuda"), torch.zeros(b, dtype=torch.float64, device="cuda"))
+    cw, cb = torch.zeros((r, d), device="cuda"), torch.zeros(r, device="cuda")
+    lib, P = dpg.lib(), dpg._p
+
+    def calls():
+        dpg._check(lib.dpg_grad_sample_linear(ctx.h, P(A), P(H), b, t, d, r, P(gw), P(gb), P(sw), P(sb)), ctx.h)
+        dpg._check(lib.dpg_clipped_sum_linear(ctx.h, P(A), P(H), P(sc), b, t, d, r, P(cw), P(cb), 0), ctx.h)
+
+    with torch.cuda.stream(s):
+        calls()  # eager: creates the side stream and the workspaces
+    ctx.sync()
+    eager = [x.clone() for x in (gw, gb, sw, sb, cw, cb)]
+    for x in (gw, gb, sw, sb, cw, cb):
+        x.zero_()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        calls()
+    g.replay()
+    torch.cuda.synchronize()
+    for x, e, name in zip((gw, gb, sw, sb, cw, cb), eager, ("gw", "gb", "sq_w", "sq_b", "sum_w", "sum_b")):
+        assert torch.equal(x, e), f"graph replay differs from the eager call: {name}"
